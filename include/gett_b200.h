@@ -1,0 +1,184 @@
+/*
+ * gett_b200.h — C ABI of the B200-native xGETT (arXiv 2410.06770).
+ *
+ * One binary tensor contraction, C += contract(A, B), over strided views of
+ * flat buffers, with the argument order of the thesis's xGETT
+ * and the semantics of the reference Python package:
+ *
+ *   gett_dgett / gett_sgett   replace  gett.kernel.dgett / sgett
+ *                             (/root/reference/pkg/src/gett/kernel.py:158-184,
+ *                              via _gett kernel.py:124-155)
+ *   gett_validate             replaces gett.plan.validate (plan.py:162-234)
+ *                             plus the phase-2 output footprint check
+ *                             (kernel.py:149-153, plan.py:237-241)
+ *   gett_derive_output_extents replaces plan.derive_output_extents (plan.py:119-127)
+ *   gett_zero_view_{d,s}      replaces gett.kernel.zero_view (kernel.py:111-113)
+ *
+ * Conventions
+ *   - A view is (rank, ext[rank], inc[rank]) over a buffer of `len` elements,
+ *     its coordinate (0,...,0) at element `offset` (the reference's offset_x
+ *     keywords, README.md:56-59).  Increments may be negative or zero.
+ *   - PERM maps free index -> output position (plan.py:10-12); free indices
+ *     are A's free dims ascending, then B's (plan.py:113-116).
+ *   - C is accumulated: C += A·B (kernel.py:76).  Output extents are derived.
+ *   - Value problems are returned as coded errors, in the reference's order
+ *     (plan.py:179-232), with C untouched and no kernel launched.
+ *   - Structural problems that the reference raises as TypeError/ValueError
+ *     (kernel.py:132-140, layout.py:71-84, plan.py:62-72) are the caller's
+ *     (the Python shim's) job; in C the array lengths are implied by the
+ *     ranks, except perm_len and inc_c_len, which the reference validates
+ *     as values (PermLengthWrong, IncCLengthWrong).
+ *
+ * Return value: number of validation errors (>= 0; 0 = the contraction ran),
+ * or a negative GETT_E_* status (CUDA failure, bad argument, out of memory).
+ * err_codes[i] / err_info[6*i .. 6*i+5] receive the first max_errs errors.
+ *
+ * Host entry points (gett_dgett, gett_sgett, gett_zero_view_*) take HOST
+ * buffers, copy the addressed spans to the device, run on the current CUDA
+ * device and copy C's span back before returning (synchronous, like the
+ * reference).  *_device entry points take DEVICE pointers and are
+ * stream-ordered on `stream` (a cudaStream_t; NULL = legacy default stream).
+ */
+#ifndef GETT_B200_H_
+#define GETT_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* validation error codes: gett.plan.ErrorCode (plan.py:23-32) */
+enum gett_error_code {
+  GETT_EXTENT_MISMATCH = 1,
+  GETT_CONT_INDEX_OUT_OF_RANGE = 2,
+  GETT_CONT_INDEX_DUPLICATE = 3,
+  GETT_PERM_LENGTH_WRONG = 4,
+  GETT_PERM_NOT_BIJECTION = 5,
+  GETT_INC_C_LENGTH_WRONG = 6,
+  GETT_OUTPUT_WRITE_ALIASING = 7,
+  GETT_FOOTPRINT_OUT_OF_BOUNDS = 8,
+  GETT_NEGATIVE_EXTENT = 9
+};
+
+/* err_info layout per error (6 x int64), used to rebuild the reference's
+ * messages:
+ *   NEGATIVE_EXTENT          [tensor(0=A,1=B,2=C), dim, extent, 0, 0, 0]
+ *   CONT_INDEX_OUT_OF_RANGE  [tensor, k, d, rank, 0, 0]
+ *   CONT_INDEX_DUPLICATE     [tensor, k, d, 0, 0, 0]
+ *   EXTENT_MISMATCH          [-1, k, ext_a, dim_a, ext_b, dim_b]
+ *   PERM_LENGTH_WRONG        [-1, perm_len, rank_c, 0, 0, 0]
+ *   PERM_NOT_BIJECTION       [-1, rank_c, 0, 0, 0, 0]
+ *   INC_C_LENGTH_WRONG       [-1, inc_c_len, rank_c, 0, 0, 0]
+ *   OUTPUT_WRITE_ALIASING    [2, dim, extent, 0, 0, 0]
+ *   FOOTPRINT_OUT_OF_BOUNDS  [tensor, lowest offset, highest offset, buffer len, 0, 0]
+ */
+#define GETT_ERR_INFO_WORDS 6
+
+/* negative status codes */
+#define GETT_E_CUDA (-1)
+#define GETT_E_INVALID_ARG (-2)
+#define GETT_E_NOMEM (-3)
+#define GETT_E_UNSUPPORTED (-4)
+
+/* ---- xGETT, host buffers (synchronous drop-in) ---- */
+int gett_dgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+               int64_t offset_a, int64_t len_a,
+               int rank_b, const int64_t* ext_b, const int64_t* inc_b, const double* b,
+               int64_t offset_b, int64_t len_b,
+               int conts, const int64_t* cont_a, const int64_t* cont_b,
+               int perm_len, const int64_t* perm,
+               int inc_c_len, const int64_t* inc_c, double* c, int64_t offset_c, int64_t len_c,
+               int32_t* err_codes, int64_t* err_info, int max_errs);
+
+int gett_sgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+               int64_t offset_a, int64_t len_a,
+               int rank_b, const int64_t* ext_b, const int64_t* inc_b, const float* b,
+               int64_t offset_b, int64_t len_b,
+               int conts, const int64_t* cont_a, const int64_t* cont_b,
+               int perm_len, const int64_t* perm,
+               int inc_c_len, const int64_t* inc_c, float* c, int64_t offset_c, int64_t len_c,
+               int32_t* err_codes, int64_t* err_info, int max_errs);
+
+/* ---- xGETT, device buffers (stream-ordered; zero-copy) ---- */
+int gett_dgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+                      int64_t offset_a, int64_t len_a,
+                      int rank_b, const int64_t* ext_b, const int64_t* inc_b, const double* b,
+                      int64_t offset_b, int64_t len_b,
+                      int conts, const int64_t* cont_a, const int64_t* cont_b,
+                      int perm_len, const int64_t* perm,
+                      int inc_c_len, const int64_t* inc_c, double* c, int64_t offset_c,
+                      int64_t len_c, void* stream,
+                      int32_t* err_codes, int64_t* err_info, int max_errs);
+
+int gett_sgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+                      int64_t offset_a, int64_t len_a,
+                      int rank_b, const int64_t* ext_b, const int64_t* inc_b, const float* b,
+                      int64_t offset_b, int64_t len_b,
+                      int conts, const int64_t* cont_a, const int64_t* cont_b,
+                      int perm_len, const int64_t* perm,
+                      int inc_c_len, const int64_t* inc_c, float* c, int64_t offset_c,
+                      int64_t len_c, void* stream,
+                      int32_t* err_codes, int64_t* err_info, int max_errs);
+
+/* ---- planning helpers ---- */
+/* Validation only.  c_mode selects how the output view takes part:
+ *   GETT_CHECK_C_NONE     plan.validate(a, b, spec, inc_c)           (plan.py:162-234)
+ *   GETT_CHECK_C_DERIVED  xGETT's two phases: the C view (derived extents, inc_c,
+ *                         offset_c, len_c) is footprint-checked only when
+ *                         everything else is clean                    (kernel.py:146-153)
+ *   GETT_CHECK_C_EXPLICIT plan.validate(..., c_view) with the explicit view
+ *                         (rank_cv, ext_cv, inc_cv, offset_c, len_c)  (plan.py:179-232) */
+#define GETT_CHECK_C_NONE 0
+#define GETT_CHECK_C_DERIVED 1
+#define GETT_CHECK_C_EXPLICIT 2
+int gett_validate(int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
+                  int64_t len_a,
+                  int rank_b, const int64_t* ext_b, const int64_t* inc_b, int64_t offset_b,
+                  int64_t len_b,
+                  int conts, const int64_t* cont_a, const int64_t* cont_b,
+                  int perm_len, const int64_t* perm, int inc_c_len, const int64_t* inc_c,
+                  int c_mode, int rank_cv, const int64_t* ext_cv, const int64_t* inc_cv,
+                  int64_t offset_c, int64_t len_c,
+                  int32_t* err_codes, int64_t* err_info, int max_errs);
+
+/* ext_c[perm[i]] = extent of free index i; requires a valid spec.
+ * Returns rank_c, or GETT_E_INVALID_ARG. */
+int gett_derive_output_extents(int rank_a, const int64_t* ext_a, int rank_b, const int64_t* ext_b,
+                               int conts, const int64_t* cont_a, const int64_t* cont_b,
+                               const int64_t* perm, int64_t* ext_c_out);
+
+/* ---- zero_view: set every addressed element to 0, nothing else ---- */
+int gett_zero_view_d(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
+                     int64_t len, double* buf);
+int gett_zero_view_s(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
+                     int64_t len, float* buf);
+int gett_zero_view_d_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
+                            int64_t len, double* buf, void* stream);
+int gett_zero_view_s_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
+                            int64_t len, float* buf, void* stream);
+
+/* ---- runtime control ---- */
+/* Kernel selection: "auto" (default), "ref" (reference-order kernel, bitwise
+ * equal to the reference on all data), "tiled" (tensor-core / register-tiled
+ * kernel), "serial" (one GPU thread, literal reference loop).  Also set by
+ * the environment variable GETT_KERNEL.  Returns 0 or GETT_E_INVALID_ARG. */
+int gett_set_kernel(const char* name);
+/* Force the split-K factor of the tiled kernel (0 = automatic). */
+int gett_set_split_k(int split);
+/* Name of the kernel the last call launched ("none" if none). */
+const char* gett_last_kernel(void);
+/* Text of the last CUDA / internal failure. */
+const char* gett_last_error(void);
+/* Number of kernels launched by this library since load (evidence counter). */
+int64_t gett_launch_count(void);
+/* Release cached device buffers and plans. */
+void gett_release_caches(void);
+/* ABI version: major*100 + minor. */
+int gett_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* GETT_B200_H_ */

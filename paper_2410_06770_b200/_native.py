@@ -1,0 +1,124 @@
+"""ctypes binding of libgett_b200.so — the C ABI declared in include/gett_b200.h.
+
+There is no Python or CPU fallback: if the library is missing this module
+raises at import, and any CUDA failure inside a call is raised as
+GettRuntimeError.  Only plain pointers and sizes cross the boundary.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgett_b200.so")
+
+# every symbol include/gett_b200.h declares (checked by tests/test_abi.py)
+EXPORTS = (
+    "gett_dgett", "gett_sgett", "gett_dgett_device", "gett_sgett_device",
+    "gett_validate", "gett_derive_output_extents",
+    "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
+    "gett_set_kernel", "gett_set_split_k", "gett_last_kernel", "gett_last_error",
+    "gett_launch_count", "gett_release_caches", "gett_abi_version",
+)
+
+ERR_INFO_WORDS = 6
+E_CUDA, E_INVALID_ARG, E_NOMEM, E_UNSUPPORTED = -1, -2, -3, -4
+
+
+class GettRuntimeError(RuntimeError):
+    """A CUDA or internal failure reported by the native library."""
+
+
+def _load():
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(
+            f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'` "
+            "(there is no CPU fallback)")
+    lib = ctypes.CDLL(LIB_PATH)
+    i64p = ctypes.POINTER(ctypes.c_int64)
+    i32p = ctypes.POINTER(ctypes.c_int32)
+    vp = ctypes.c_void_p
+    gett_args = [ctypes.c_int, i64p, i64p, vp, ctypes.c_int64, ctypes.c_int64,
+                 ctypes.c_int, i64p, i64p, vp, ctypes.c_int64, ctypes.c_int64,
+                 ctypes.c_int, i64p, i64p, ctypes.c_int, i64p,
+                 ctypes.c_int, i64p, vp, ctypes.c_int64, ctypes.c_int64]
+    for name in ("gett_dgett", "gett_sgett"):
+        f = getattr(lib, name)
+        f.restype = ctypes.c_int
+        f.argtypes = gett_args + [i32p, i64p, ctypes.c_int]
+    for name in ("gett_dgett_device", "gett_sgett_device"):
+        f = getattr(lib, name)
+        f.restype = ctypes.c_int
+        f.argtypes = gett_args + [vp, i32p, i64p, ctypes.c_int]
+    lib.gett_validate.restype = ctypes.c_int
+    lib.gett_validate.argtypes = [
+        ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        ctypes.c_int, i64p, i64p, ctypes.c_int, i64p, ctypes.c_int, i64p,
+        ctypes.c_int, ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        i32p, i64p, ctypes.c_int]
+    lib.gett_derive_output_extents.restype = ctypes.c_int
+    lib.gett_derive_output_extents.argtypes = [ctypes.c_int, i64p, ctypes.c_int, i64p,
+                                               ctypes.c_int, i64p, i64p, i64p, i64p]
+    for name, dev in (("gett_zero_view_d", False), ("gett_zero_view_s", False),
+                      ("gett_zero_view_d_device", True), ("gett_zero_view_s_device", True)):
+        f = getattr(lib, name)
+        f.restype = ctypes.c_int
+        f.argtypes = [ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64, vp] + ([vp] if dev else [])
+    lib.gett_set_kernel.restype = ctypes.c_int
+    lib.gett_set_kernel.argtypes = [ctypes.c_char_p]
+    lib.gett_set_split_k.restype = ctypes.c_int
+    lib.gett_set_split_k.argtypes = [ctypes.c_int]
+    lib.gett_last_kernel.restype = ctypes.c_char_p
+    lib.gett_last_kernel.argtypes = []
+    lib.gett_last_error.restype = ctypes.c_char_p
+    lib.gett_last_error.argtypes = []
+    lib.gett_launch_count.restype = ctypes.c_int64
+    lib.gett_launch_count.argtypes = []
+    lib.gett_release_caches.restype = None
+    lib.gett_release_caches.argtypes = []
+    lib.gett_abi_version.restype = ctypes.c_int
+    lib.gett_abi_version.argtypes = []
+    return lib
+
+
+LIB = _load()
+
+
+def i64(seq):
+    """A ctypes int64 array holding seq (length >= 1 so the pointer is valid)."""
+    seq = [int(x) for x in seq]
+    return (ctypes.c_int64 * max(1, len(seq)))(*seq)
+
+
+def check(rc: int, what: str) -> int:
+    """Raise for negative native status codes; pass error counts through."""
+    if rc >= 0:
+        return rc
+    msg = LIB.gett_last_error().decode(errors="replace")
+    kind = {E_CUDA: "CUDA failure", E_INVALID_ARG: "invalid argument", E_NOMEM: "out of device memory",
+            E_UNSUPPORTED: "unsupported descriptor"}.get(rc, f"status {rc}")
+    raise GettRuntimeError(f"{what}: {kind}: {msg}")
+
+
+def set_kernel(name: str) -> None:
+    """Select the kernel family: auto | ref | tiled | serial (see gett_b200.h)."""
+    if LIB.gett_set_kernel(name.encode()) != 0:
+        raise ValueError(f"unknown kernel {name!r}")
+
+
+def set_split_k(split: int) -> None:
+    if LIB.gett_set_split_k(int(split)) != 0:
+        raise ValueError(f"bad split {split}")
+
+
+def last_kernel() -> str:
+    return LIB.gett_last_kernel().decode()
+
+
+def launch_count() -> int:
+    return int(LIB.gett_launch_count())
+
+
+def release_caches() -> None:
+    LIB.gett_release_caches()

@@ -1,0 +1,630 @@
+// Runtime and C ABI of the B200 xGETT (include/gett_b200.h).
+//
+// Call path (mirrors kernel.py:124-155 _gett):
+//   validate (planner.cpp, reference codes/order) -> return errors, C untouched
+//   -> empty iteration space: return, nothing written (kernel.py:93-94)
+//   -> plan (cached: folded M/N/K groups + device offset tables)
+//   -> kernel choice: serial (aliasing C), ref-order, or tiled (DMMA / FFMA)
+//   -> host path only: H2D of the addressed spans before, D2H of C's span after.
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <list>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/gett_b200.h"
+#include "device.cuh"
+#include "kernels.hpp"
+#include "planner.hpp"
+
+namespace gett {
+namespace {
+
+enum class Mode { Auto, Ref, Tiled, Serial };
+
+std::mutex g_mu;
+Mode g_mode = Mode::Auto;
+int g_split = 0;
+bool g_env_read = false;
+thread_local std::string t_last_error;
+thread_local const char* t_last_kernel = "none";
+int64_t g_launches = 0;
+
+void read_env() {
+  if (g_env_read) return;
+  g_env_read = true;
+  const char* k = std::getenv("GETT_KERNEL");
+  if (k) gett_set_kernel(k);
+  const char* s = std::getenv("GETT_SPLIT_K");
+  if (s) g_split = std::atoi(s);
+}
+
+int cuda_fail(cudaError_t e, const char* what) {
+  t_last_error = std::string(what) + ": " + cudaGetErrorString(e);
+  return GETT_E_CUDA;
+}
+
+#define CK(expr)                                       \
+  do {                                                 \
+    cudaError_t e_ = (expr);                           \
+    if (e_ != cudaSuccess) return cuda_fail(e_, #expr); \
+  } while (0)
+
+// Device-resident plan: offset tables for the groups.
+struct DevPlan {
+  Plan plan;
+  int device = -1;
+  int64_t* d_tab = nullptr;
+  GroupDev gm{}, gn{}, gk{};
+  int64_t* kref_a = nullptr;
+  int64_t* kref_b = nullptr;
+  int64_t* serial_tab = nullptr;
+  int serial_nf = 0, serial_nc = 0;
+  // residues used by the vector-load checks: every table entry divisible by 2 / 4
+  bool am_even2 = false, am_even4 = false, ak_even2 = false, ak_even4 = false;
+  bool bn_even2 = false, bn_even4 = false, bk_even2 = false, bk_even4 = false;
+  ~DevPlan() {
+    if (d_tab) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      cudaSetDevice(device);
+      cudaFree(d_tab);
+      cudaSetDevice(cur);
+    }
+  }
+};
+
+struct PlanCache {
+  std::list<std::string> lru;
+  std::unordered_map<std::string, std::pair<std::shared_ptr<DevPlan>, std::list<std::string>::iterator>> map;
+  static constexpr size_t kCap = 512;
+};
+PlanCache g_plans;
+
+struct Scratch {
+  void* p = nullptr;
+  size_t bytes = 0;
+};
+struct DevState {
+  cudaStream_t stream = nullptr;
+  Scratch a, b, c, ws;
+};
+std::unordered_map<int, DevState> g_dev;
+
+int ensure(Scratch& s, size_t bytes) {
+  if (bytes <= s.bytes) return 0;
+  if (s.p) cudaFree(s.p);
+  s.p = nullptr;
+  s.bytes = 0;
+  size_t want = bytes + bytes / 8 + 256;
+  cudaError_t e = cudaMalloc(&s.p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    t_last_error = std::string("cudaMalloc scratch: ") + cudaGetErrorString(e);
+    return GETT_E_NOMEM;
+  }
+  s.bytes = want;
+  return 0;
+}
+
+bool all_div(const std::vector<int64_t>& v, int64_t d) {
+  for (int64_t x : v)
+    if (x % d) return false;
+  return true;
+}
+
+GroupDev to_dev(const Group& g, const int64_t* t0, const int64_t* t1) {
+  GroupDev d;
+  d.G = (int32_t)g.G;
+  d.e_in = FastDiv::make((int32_t)g.e_in);
+  d.s_in[0] = g.s_in[0];
+  d.s_in[1] = g.s_in[1];
+  d.T[0] = t0;
+  d.T[1] = t1;
+  return d;
+}
+
+// restatement of _plan_tables (plan.py:258-289) for the serial kernel
+std::vector<int64_t> serial_table(const View& a, const View& b, const Spec& s, int* nf, int* nc) {
+  int rank_c = a.rank + b.rank - 2 * s.conts;
+  std::vector<int64_t> out_inc(rank_c), src_inc(rank_c), from_a(rank_c), ext_free(rank_c);
+  int i = 0;
+  auto contracted = [](const int64_t* idx, int n, int d) {
+    for (int k = 0; k < n; ++k)
+      if (idx[k] == d) return true;
+    return false;
+  };
+  for (int d = 0; d < a.rank; ++d) {
+    if (contracted(s.cont_a, s.conts, d)) continue;
+    int64_t q = s.perm[i++];
+    ext_free[q] = a.ext[d]; src_inc[q] = a.inc[d]; out_inc[q] = s.inc_c[q]; from_a[q] = 1;
+  }
+  for (int d = 0; d < b.rank; ++d) {
+    if (contracted(s.cont_b, s.conts, d)) continue;
+    int64_t q = s.perm[i++];
+    ext_free[q] = b.ext[d]; src_inc[q] = b.inc[d]; out_inc[q] = s.inc_c[q]; from_a[q] = 0;
+  }
+  std::vector<int64_t> t;
+  t.insert(t.end(), out_inc.begin(), out_inc.end());
+  t.insert(t.end(), src_inc.begin(), src_inc.end());
+  t.insert(t.end(), from_a.begin(), from_a.end());
+  t.insert(t.end(), ext_free.begin(), ext_free.end());
+  for (int k = 0; k < s.conts; ++k) t.push_back(a.inc[s.cont_a[k]]);
+  for (int k = 0; k < s.conts; ++k) t.push_back(b.inc[s.cont_b[k]]);
+  for (int k = 0; k < s.conts; ++k) t.push_back(a.ext[s.cont_a[k]]);
+  *nf = rank_c;
+  *nc = s.conts;
+  return t;
+}
+
+int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t off_c,
+             int64_t len_c, std::shared_ptr<DevPlan>* out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::string key = plan_key(dtype, a, b, s, off_c) + "#" + std::to_string(dev);
+  auto it = g_plans.map.find(key);
+  if (it != g_plans.map.end()) {
+    g_plans.lru.splice(g_plans.lru.begin(), g_plans.lru, it->second.second);
+    *out = it->second.first;
+    return 0;
+  }
+  auto dp = std::make_shared<DevPlan>();
+  dp->plan = build_plan(a, b, s, off_c, len_c);
+  dp->device = dev;
+  const Plan& p = dp->plan;
+  if (p.gm.G >= (1LL << 31) || p.gn.G >= (1LL << 31) || p.gk.G >= (1LL << 31) ||
+      p.rank_c > 64 || s.conts > 64) {
+    t_last_error = "group extent >= 2^31 or rank > 64 is not supported";
+    return GETT_E_UNSUPPORTED;
+  }
+  std::vector<int64_t> host;
+  std::vector<size_t> offs;
+  auto push = [&](const std::vector<int64_t>& v) {
+    offs.push_back(host.size());
+    host.insert(host.end(), v.begin(), v.end());
+  };
+  push(p.gm.T[0]); push(p.gm.T[1]);
+  push(p.gn.T[0]); push(p.gn.T[1]);
+  push(p.gk.T[0]); push(p.gk.T[1]);
+  push(p.gk_ref.T[0]); push(p.gk_ref.T[1]);
+  push(serial_table(a, b, s, &dp->serial_nf, &dp->serial_nc));
+  CK(cudaMalloc(&dp->d_tab, host.size() * sizeof(int64_t)));
+  CK(cudaMemcpy(dp->d_tab, host.data(), host.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  int64_t* t = dp->d_tab;
+  dp->gm = to_dev(p.gm, t + offs[0], t + offs[1]);
+  dp->gn = to_dev(p.gn, t + offs[2], t + offs[3]);
+  dp->gk = to_dev(p.gk, t + offs[4], t + offs[5]);
+  dp->kref_a = t + offs[6];
+  dp->kref_b = t + offs[7];
+  dp->serial_tab = t + offs[8];
+  dp->am_even2 = all_div(p.gm.T[0], 2); dp->am_even4 = all_div(p.gm.T[0], 4);
+  dp->ak_even2 = all_div(p.gk.T[0], 2); dp->ak_even4 = all_div(p.gk.T[0], 4);
+  dp->bn_even2 = all_div(p.gn.T[0], 2); dp->bn_even4 = all_div(p.gn.T[0], 4);
+  dp->bk_even2 = all_div(p.gk.T[1], 2); dp->bk_even4 = all_div(p.gk.T[1], 4);
+  g_plans.lru.push_front(key);
+  g_plans.map[key] = {dp, g_plans.lru.begin()};
+  if (g_plans.map.size() > PlanCache::kCap) {
+    std::string last = g_plans.lru.back();
+    g_plans.lru.pop_back();
+    g_plans.map.erase(last);
+  }
+  *out = dp;
+  return 0;
+}
+
+// zero_view: the view folded as a single group (second tensor unused)
+int get_view_plan(int rank, const int64_t* ext, const int64_t* inc, std::shared_ptr<DevPlan>* out) {
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::string key = "zero|";
+  for (int d = 0; d < rank; ++d) key += std::to_string(ext[d]) + "," + std::to_string(inc[d]) + ";";
+  key += "#" + std::to_string(dev);
+  auto it = g_plans.map.find(key);
+  if (it != g_plans.map.end()) {
+    g_plans.lru.splice(g_plans.lru.begin(), g_plans.lru, it->second.second);
+    *out = it->second.first;
+    return 0;
+  }
+  auto dp = std::make_shared<DevPlan>();
+  dp->device = dev;
+  dp->plan.gm = fold_view(rank, ext, inc);
+  if (dp->plan.gm.G >= (1LL << 31)) {
+    t_last_error = "zero_view larger than 2^31 elements";
+    return GETT_E_UNSUPPORTED;
+  }
+  const std::vector<int64_t>& T = dp->plan.gm.T[0];
+  CK(cudaMalloc(&dp->d_tab, T.size() * sizeof(int64_t)));
+  CK(cudaMemcpy(dp->d_tab, T.data(), T.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+  dp->gm = to_dev(dp->plan.gm, dp->d_tab, dp->d_tab);
+  g_plans.lru.push_front(key);
+  g_plans.map[key] = {dp, g_plans.lru.begin()};
+  *out = dp;
+  return 0;
+}
+
+inline int64_t iabs(int64_t x) { return x < 0 ? -x : x; }
+
+// 16-byte vector loads along the fast dimension are legal when the fast
+// group's inner mode is unit-stride with extent divisible by V, every other
+// offset contribution is divisible by V, and the base is 16-byte aligned.
+bool vec_ok(const GroupDev& fast, bool fast_tab_div, const GroupDev& slow, bool slow_tab_div,
+            int V, const void* base) {
+  if (fast.s_in[0] != 1 || fast.e_in.d % V != 0 || !fast_tab_div) return false;
+  if (!(slow.e_in.d == 1 || slow.s_in[0] % V == 0) || !slow_tab_div) return false;
+  return ((uintptr_t)base % 16) == 0;
+}
+
+template <typename T>
+int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, DevState& ds) {
+  const Plan& p = dp.plan;
+  const T* A = p.swapped ? b : a;  // kernel roles A' / B'
+  const T* B = p.swapped ? a : b;
+  Mode mode = g_mode;
+  if (p.c_may_alias) mode = Mode::Serial;
+  const int64_t M = p.gm.G, N = p.gn.G, K = p.gk.G;
+  if (mode == Mode::Auto) {
+    if (K <= 8 || M * N * K <= (1LL << 18)) mode = Mode::Ref;
+    else mode = Mode::Tiled;
+  }
+  if (mode == Mode::Serial) {
+    SerialParams<T> sp;
+    sp.A = a; sp.B = b; sp.C = c;
+    if (!dp.serial_tab) {
+      t_last_error = "serial kernel requires an aliasing plan";
+      return GETT_E_UNSUPPORTED;
+    }
+    sp.num_free = dp.serial_nf;
+    sp.num_cont = dp.serial_nc;
+    sp.size_free = p.size_free;
+    sp.size_cont = p.size_cont;
+    sp.tab = dp.serial_tab;
+    CK(launch_serial<T>(sp, stream));
+    t_last_kernel = sizeof(T) == 8 ? "dgett_serial" : "sgett_serial";
+    ++g_launches;
+    return 0;
+  }
+  if (mode == Mode::Ref) {
+    RefParams<T> rp;
+    rp.A = A; rp.B = B; rp.C = c;
+    rp.gm = dp.gm; rp.gn = dp.gn;
+    rp.M = (int32_t)M; rp.N = (int32_t)N;
+    rp.k_inner = (int32_t)p.gk_ref.e_in;
+    rp.k_sa = p.gk_ref.s_in[0];
+    rp.k_sb = p.gk_ref.s_in[1];
+    rp.k_outer = (int32_t)p.gk_ref.T[0].size();
+    rp.kta = dp.kref_a;
+    rp.ktb = dp.kref_b;
+    CK(launch_ref<T>(rp, stream));
+    t_last_kernel = sizeof(T) == 8 ? "dgett_ref_order" : "sgett_ref_order";
+    ++g_launches;
+    return 0;
+  }
+  // tiled
+  TiledParams<T> tp;
+  tp.A = A; tp.B = B; tp.C = c;
+  tp.gm = dp.gm; tp.gn = dp.gn; tp.gk = dp.gk;
+  tp.M = (int32_t)M; tp.N = (int32_t)N; tp.K = (int32_t)K;
+  const int BM = tiled_bm(), BN = tiled_bn(), BK = tiled_bk();
+  tp.tiles_m = (int32_t)((M + BM - 1) / BM);
+  tp.tiles_n = (int32_t)((N + BN - 1) / BN);
+  int64_t tiles = (int64_t)tp.tiles_m * tp.tiles_n;
+  int64_t kblocks = (K + BK - 1) / BK;
+  int64_t splits = 1;
+  if (g_split > 0) splits = g_split;
+  else if (tiles < 148 && kblocks >= 8) {
+    splits = (2 * 148) / tiles;
+    if (splits > kblocks / 4) splits = kblocks / 4;
+    if (splits < 1) splits = 1;
+  }
+  if (splits > kblocks) splits = kblocks;
+  int64_t kchunk = ((kblocks + splits - 1) / splits) * BK;
+  splits = (K + kchunk - 1) / kchunk;
+  tp.k_chunk = (int32_t)kchunk;
+  tp.splits = (int32_t)splits;
+  tp.ws = nullptr;
+  if (splits > 1) {
+    int rc = ensure(ds.ws, (size_t)splits * M * N * sizeof(T));
+    if (rc) return rc;
+    tp.ws = (T*)ds.ws.p;
+  }
+  // gather directions and vector widths
+  bool a_kf = dp.gk.e_in.d > 1 && (dp.gm.e_in.d == 1 || iabs(dp.gk.s_in[0]) < iabs(dp.gm.s_in[0]));
+  bool b_kf = dp.gk.e_in.d > 1 && (dp.gn.e_in.d == 1 || iabs(dp.gk.s_in[1]) < iabs(dp.gn.s_in[0]));
+  const int V = (int)(16 / sizeof(T));
+  bool a_vec, b_vec;
+  {
+    GroupDev gkA = dp.gk;  // view gk from A''s side for the check
+    GroupDev gkB = dp.gk;
+    gkB.s_in[0] = dp.gk.s_in[1];
+    bool akd = V == 2 ? dp.ak_even2 : dp.ak_even4;
+    bool amd = V == 2 ? dp.am_even2 : dp.am_even4;
+    bool bkd = V == 2 ? dp.bk_even2 : dp.bk_even4;
+    bool bnd = V == 2 ? dp.bn_even2 : dp.bn_even4;
+    a_vec = a_kf ? vec_ok(gkA, akd, dp.gm, amd, V, A) : vec_ok(dp.gm, amd, gkA, akd, V, A);
+    b_vec = b_kf ? vec_ok(gkB, bkd, dp.gn, bnd, V, B) : vec_ok(dp.gn, bnd, gkB, bkd, V, B);
+  }
+  CK(launch_tiled<T>(tp, a_kf, b_kf, a_vec, b_vec, stream));
+  g_launches += splits > 1 ? 2 : 1;
+  t_last_kernel = sizeof(T) == 8 ? (splits > 1 ? "dgett_dmma_splitk" : "dgett_dmma")
+                                 : (splits > 1 ? "sgett_ffma_splitk" : "sgett_ffma");
+  return 0;
+}
+
+int fill_errors(const std::vector<Error>& errs, int32_t* codes, int64_t* info, int max_errs) {
+  int n = (int)errs.size();
+  for (int i = 0; i < n && i < max_errs; ++i) {
+    if (codes) codes[i] = errs[i].code;
+    if (info)
+      for (int w = 0; w < GETT_ERR_INFO_WORDS; ++w) info[i * GETT_ERR_INFO_WORDS + w] = errs[i].info[w];
+  }
+  return n;
+}
+
+DevState& dev_state(int* dev_out) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  *dev_out = dev;
+  DevState& ds = g_dev[dev];
+  if (!ds.stream) cudaStreamCreateWithFlags(&ds.stream, cudaStreamNonBlocking);
+  return ds;
+}
+
+template <typename T>
+int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a, const T* a,
+              int64_t off_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+              const int64_t* inc_b, const T* b, int64_t off_b, int64_t len_b, int conts,
+              const int64_t* cont_a, const int64_t* cont_b, int perm_len, const int64_t* perm,
+              int inc_c_len, const int64_t* inc_c, T* c, int64_t off_c, int64_t len_c,
+              cudaStream_t stream, int32_t* codes, int64_t* info, int max_errs) {
+  if (rank_a < 0 || rank_b < 0 || conts < 0 || perm_len < 0 || inc_c_len < 0 || off_a < 0 ||
+      off_b < 0 || off_c < 0 || len_a < 0 || len_b < 0 || len_c < 0) {
+    t_last_error = "negative rank/count/offset/length";
+    return GETT_E_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(g_mu);
+  read_env();
+  t_last_kernel = "none";
+  View va{rank_a, ext_a, inc_a, off_a, len_a};
+  View vb{rank_b, ext_b, inc_b, off_b, len_b};
+  Spec sp{conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c};
+  View vc{0, nullptr, nullptr, off_c, len_c};
+  std::vector<Error> errs = validate(va, vb, sp, CMode::Derived, vc);
+  if (!errs.empty()) return fill_errors(errs, codes, info, max_errs);
+  // empty iteration space: nothing is written (kernel.py:93-94)
+  for (int d = 0; d < rank_a; ++d)
+    if (ext_a[d] == 0) return 0;
+  for (int d = 0; d < rank_b; ++d)
+    if (ext_b[d] == 0) return 0;
+  std::shared_ptr<DevPlan> dp;
+  int rc = get_plan(sizeof(T) == 8 ? 'd' : 's', va, vb, sp, off_c, len_c, &dp);
+  if (rc) return rc;
+  const Plan& p = dp->plan;
+  int dev;
+  DevState& ds = dev_state(&dev);
+  if (!host) {
+    return run_device<T>(*dp, a + off_a, b + off_b, c + off_c, stream, ds);
+  }
+  // host buffers: copy the addressed spans in, run, copy C's span back
+  size_t na = (size_t)(p.span_hi[0] - p.span_lo[0] + 1);
+  size_t nb = (size_t)(p.span_hi[1] - p.span_lo[1] + 1);
+  size_t nc = (size_t)(p.span_hi[2] - p.span_lo[2] + 1);
+  if ((rc = ensure(ds.a, na * sizeof(T))) || (rc = ensure(ds.b, nb * sizeof(T))) ||
+      (rc = ensure(ds.c, nc * sizeof(T))))
+    return rc;
+  T* da = (T*)ds.a.p;
+  T* db = (T*)ds.b.p;
+  T* dc = (T*)ds.c.p;
+  cudaStream_t s = ds.stream;
+  CK(cudaMemcpyAsync(da, a + p.span_lo[0], na * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(db, b + p.span_lo[1], nb * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc, c + p.span_lo[2], nc * sizeof(T), cudaMemcpyHostToDevice, s));
+  rc = run_device<T>(*dp, da + (off_a - p.span_lo[0]), db + (off_b - p.span_lo[1]),
+                     dc + (off_c - p.span_lo[2]), s, ds);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c + p.span_lo[2], dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+template <typename T>
+int zero_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64_t off,
+              int64_t len, T* buf, cudaStream_t stream) {
+  if (rank < 0 || rank > 64 || off < 0 || len < 0) {
+    t_last_error = "bad zero_view descriptor";
+    return GETT_E_INVALID_ARG;
+  }
+  // view_offsets (layout.py:128-140) addresses nothing when an extent is
+  // zero, and nothing when one is negative (np.arange of a negative count)
+  for (int d = 0; d < rank; ++d)
+    if (ext[d] <= 0) return 0;
+  int64_t lo, hi;
+  footprint(rank, ext, inc, &lo, &hi);
+  if (off + lo < 0 || off + hi >= len) {
+    t_last_error = "view footprint outside the buffer";
+    return GETT_E_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(g_mu);
+  std::shared_ptr<DevPlan> dp;
+  int rc = get_view_plan(rank, ext, inc, &dp);
+  if (rc) return rc;
+  int dev;
+  DevState& ds = dev_state(&dev);
+  if (!host) {
+    CK(launch_zero<T>(buf + off, dp->gm, stream));
+    ++g_launches;
+    return 0;
+  }
+  size_t n = (size_t)(hi - lo + 1);
+  if ((rc = ensure(ds.c, n * sizeof(T)))) return rc;
+  T* d = (T*)ds.c.p;
+  cudaStream_t s = ds.stream;
+  CK(cudaMemcpyAsync(d, buf + off + lo, n * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(launch_zero<T>(d - lo, dp->gm, s));
+  ++g_launches;
+  CK(cudaMemcpyAsync(buf + off + lo, d, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
+}  // namespace
+}  // namespace gett
+
+using namespace gett;
+
+extern "C" {
+
+int gett_dgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+               int64_t offset_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+               const int64_t* inc_b, const double* b, int64_t offset_b, int64_t len_b, int conts,
+               const int64_t* cont_a, const int64_t* cont_b, int perm_len, const int64_t* perm,
+               int inc_c_len, const int64_t* inc_c, double* c, int64_t offset_c, int64_t len_c,
+               int32_t* err_codes, int64_t* err_info, int max_errs) {
+  return gett_impl<double>(true, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b, inc_b, b,
+                           offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len,
+                           inc_c, c, offset_c, len_c, nullptr, err_codes, err_info, max_errs);
+}
+
+int gett_sgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+               int64_t offset_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+               const int64_t* inc_b, const float* b, int64_t offset_b, int64_t len_b, int conts,
+               const int64_t* cont_a, const int64_t* cont_b, int perm_len, const int64_t* perm,
+               int inc_c_len, const int64_t* inc_c, float* c, int64_t offset_c, int64_t len_c,
+               int32_t* err_codes, int64_t* err_info, int max_errs) {
+  return gett_impl<float>(true, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b, inc_b, b,
+                          offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c,
+                          c, offset_c, len_c, nullptr, err_codes, err_info, max_errs);
+}
+
+int gett_dgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+                      int64_t offset_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+                      const int64_t* inc_b, const double* b, int64_t offset_b, int64_t len_b,
+                      int conts, const int64_t* cont_a, const int64_t* cont_b, int perm_len,
+                      const int64_t* perm, int inc_c_len, const int64_t* inc_c, double* c,
+                      int64_t offset_c, int64_t len_c, void* stream, int32_t* err_codes,
+                      int64_t* err_info, int max_errs) {
+  return gett_impl<double>(false, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b, inc_b,
+                           b, offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len,
+                           inc_c, c, offset_c, len_c, (cudaStream_t)stream, err_codes, err_info,
+                           max_errs);
+}
+
+int gett_sgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+                      int64_t offset_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+                      const int64_t* inc_b, const float* b, int64_t offset_b, int64_t len_b,
+                      int conts, const int64_t* cont_a, const int64_t* cont_b, int perm_len,
+                      const int64_t* perm, int inc_c_len, const int64_t* inc_c, float* c,
+                      int64_t offset_c, int64_t len_c, void* stream, int32_t* err_codes,
+                      int64_t* err_info, int max_errs) {
+  return gett_impl<float>(false, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b, inc_b, b,
+                          offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c,
+                          c, offset_c, len_c, (cudaStream_t)stream, err_codes, err_info, max_errs);
+}
+
+int gett_validate(int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
+                  int64_t len_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,
+                  int64_t offset_b, int64_t len_b, int conts, const int64_t* cont_a,
+                  const int64_t* cont_b, int perm_len, const int64_t* perm, int inc_c_len,
+                  const int64_t* inc_c, int c_mode, int rank_cv, const int64_t* ext_cv,
+                  const int64_t* inc_cv, int64_t offset_c, int64_t len_c, int32_t* err_codes,
+                  int64_t* err_info, int max_errs) {
+  if (rank_a < 0 || rank_b < 0 || conts < 0 || perm_len < 0 || inc_c_len < 0 || c_mode < 0 ||
+      c_mode > 2 || (c_mode == 2 && rank_cv < 0)) {
+    t_last_error = "bad validate arguments";
+    return GETT_E_INVALID_ARG;
+  }
+  View va{rank_a, ext_a, inc_a, offset_a, len_a};
+  View vb{rank_b, ext_b, inc_b, offset_b, len_b};
+  Spec sp{conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c};
+  View vc{c_mode == 2 ? rank_cv : 0, ext_cv, inc_cv, offset_c, len_c};
+  std::vector<Error> errs = validate(va, vb, sp, (CMode)c_mode, vc);
+  return fill_errors(errs, err_codes, err_info, max_errs);
+}
+
+int gett_derive_output_extents(int rank_a, const int64_t* ext_a, int rank_b, const int64_t* ext_b,
+                               int conts, const int64_t* cont_a, const int64_t* cont_b,
+                               const int64_t* perm, int64_t* ext_c_out) {
+  int rank_c = rank_a + rank_b - 2 * conts;
+  if (rank_c < 0) return GETT_E_INVALID_ARG;
+  int i = 0;
+  auto contracted = [](const int64_t* idx, int n, int d) {
+    for (int k = 0; k < n; ++k)
+      if (idx[k] == d) return true;
+    return false;
+  };
+  for (int d = 0; d < rank_a; ++d)
+    if (!contracted(cont_a, conts, d)) {
+      if (perm[i] < 0 || perm[i] >= rank_c) return GETT_E_INVALID_ARG;
+      ext_c_out[perm[i++]] = ext_a[d];
+    }
+  for (int d = 0; d < rank_b; ++d)
+    if (!contracted(cont_b, conts, d)) {
+      if (perm[i] < 0 || perm[i] >= rank_c) return GETT_E_INVALID_ARG;
+      ext_c_out[perm[i++]] = ext_b[d];
+    }
+  return rank_c;
+}
+
+int gett_zero_view_d(int rank, const int64_t* ext, const int64_t* inc, int64_t offset, int64_t len,
+                     double* buf) {
+  return zero_impl<double>(true, rank, ext, inc, offset, len, buf, nullptr);
+}
+int gett_zero_view_s(int rank, const int64_t* ext, const int64_t* inc, int64_t offset, int64_t len,
+                     float* buf) {
+  return zero_impl<float>(true, rank, ext, inc, offset, len, buf, nullptr);
+}
+int gett_zero_view_d_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
+                            int64_t len, double* buf, void* stream) {
+  return zero_impl<double>(false, rank, ext, inc, offset, len, buf, (cudaStream_t)stream);
+}
+int gett_zero_view_s_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
+                            int64_t len, float* buf, void* stream) {
+  return zero_impl<float>(false, rank, ext, inc, offset, len, buf, (cudaStream_t)stream);
+}
+
+int gett_set_kernel(const char* name) {
+  if (!name) return GETT_E_INVALID_ARG;
+  if (!strcmp(name, "auto")) g_mode = Mode::Auto;
+  else if (!strcmp(name, "ref")) g_mode = Mode::Ref;
+  else if (!strcmp(name, "tiled")) g_mode = Mode::Tiled;
+  else if (!strcmp(name, "serial")) g_mode = Mode::Serial;
+  else return GETT_E_INVALID_ARG;
+  return 0;
+}
+
+int gett_set_split_k(int split) {
+  if (split < 0) return GETT_E_INVALID_ARG;
+  g_split = split;
+  return 0;
+}
+
+const char* gett_last_kernel(void) { return t_last_kernel; }
+const char* gett_last_error(void) { return t_last_error.c_str(); }
+int64_t gett_launch_count(void) { return g_launches; }
+
+void gett_release_caches(void) {
+  std::lock_guard<std::mutex> lock(g_mu);
+  g_plans.map.clear();
+  g_plans.lru.clear();
+  for (auto& kv : g_dev) {
+    int cur;
+    cudaGetDevice(&cur);
+    cudaSetDevice(kv.first);
+    for (Scratch* s : {&kv.second.a, &kv.second.b, &kv.second.c, &kv.second.ws})
+      if (s->p) {
+        cudaFree(s->p);
+        s->p = nullptr;
+        s->bytes = 0;
+      }
+    cudaSetDevice(cur);
+  }
+}
+
+int gett_abi_version(void) { return 100; }
+
+}  // extern "C"

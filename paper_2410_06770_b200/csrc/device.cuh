@@ -1,0 +1,122 @@
+// Device-side types shared by the xGETT kernels (sm_100a).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gett {
+
+// Division by a runtime-invariant positive int32 with one mul.hi + shift
+// (round-up reciprocal; valid for 0 <= n < 2^31, 1 <= d < 2^31).
+struct FastDiv {
+  int32_t d;
+  uint32_t mul;
+  uint32_t shr;
+
+  __host__ static FastDiv make(int32_t d) {
+    FastDiv f;
+    f.d = d;
+    if (d == 1) {
+      f.mul = 0;
+      f.shr = 0;
+    } else {
+      uint32_t l = 0;
+      while ((1ull << l) < (uint64_t)d) ++l;  // ceil(log2 d)
+      uint32_t p = 31 + l;
+      f.mul = (uint32_t)(((1ull << p) + (uint64_t)d - 1) / (uint64_t)d);
+      f.shr = p - 32;
+    }
+    return f;
+  }
+
+  __device__ __forceinline__ void divmod(int32_t n, int32_t& q, int32_t& r) const {
+    q = (d == 1) ? n : (int32_t)(__umulhi((uint32_t)n, mul) >> shr);
+    r = n - q * d;
+  }
+};
+
+// One folded mode group on the device: element g of the group sits at
+//   T[t][g / e_in] + (g % e_in) * s_in[t]   in tensor t.
+struct GroupDev {
+  int32_t G;
+  FastDiv e_in;
+  int64_t s_in[2];
+  const int64_t* T[2];
+
+  __device__ __forceinline__ int64_t off(int t, int32_t g) const {
+    int32_t q, r;
+    e_in.divmod(g, q, r);
+    return __ldg(T[t] + q) + (int64_t)r * s_in[t];
+  }
+  __device__ __forceinline__ void off2(int32_t g, int64_t& o0, int64_t& o1) const {
+    int32_t q, r;
+    e_in.divmod(g, q, r);
+    o0 = __ldg(T[0] + q) + (int64_t)r * s_in[0];
+    o1 = __ldg(T[1] + q) + (int64_t)r * s_in[1];
+  }
+};
+
+// Tiled GETT launch parameters.  Roles are the kernel's: A' (rows m) and B'
+// (columns n); gm = (A', C), gn = (B', C), gk = (A', B').
+template <typename T>
+struct TiledParams {
+  const T* A;
+  const T* B;
+  T* C;
+  GroupDev gm, gn, gk;
+  int32_t M, N, K;
+  int32_t tiles_m, tiles_n;
+  int32_t splits;   // split-K factor (1 = fused C += acc epilogue)
+  int32_t k_chunk;  // K per split, a multiple of the k-block
+  T* ws;            // [splits][M][N] partial tiles when splits > 1
+};
+
+// Reference-order kernel parameters: one thread per output, K in the
+// reference order (pair 0 fastest) with unfused multiply then add.
+template <typename T>
+struct RefParams {
+  const T* A;
+  const T* B;
+  T* C;
+  GroupDev gm, gn;      // as in TiledParams
+  int32_t M, N;
+  int32_t k_inner;      // reference-order K: inner affine extent ...
+  int64_t k_sa, k_sb;   // ... and its strides in A', B'
+  int32_t k_outer;      // outer table length
+  const int64_t* kta;   // outer offsets in A'
+  const int64_t* ktb;   // outer offsets in B'
+};
+
+// Serial kernel: the literal reference loop (kernel.py:48-78) on one thread,
+// used when distinct output coordinates may address the same C element.
+template <typename T>
+struct SerialParams {
+  const T* A;
+  const T* B;
+  T* C;
+  int32_t num_free, num_cont;
+  int64_t size_free, size_cont;
+  const int64_t* tab;  // [out_inc | src_inc | from_a | ext_free] x num_free,
+                       // [inc_ca | inc_cb | ext_cont] x num_cont
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void cp_async_8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(smem_u32(dst)), "l"(src));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace gett

@@ -1,0 +1,514 @@
+// sm_100a kernels for the B200 xGETT.
+//
+//   gett_tiled_kernel<double>  DGETT: gathers strided M/K and K/N tiles straight
+//       from HBM into shared memory (cp.async, 16 B vectors where the planner
+//       proved contiguity), FP64 DMMA (mma.sync m8n8k4 -> DMMA.8x8x4; on
+//       sm_100a FP64 has no tcgen05 kind and DMMA reaches the FP64 pipe peak,
+//       profiles/peaks_r01.jsonl), fused epilogue C += acc through the C
+//       offset tables.  Replaces the hot loop kernel.py:48-78.
+//   gett_tiled_kernel<float>   SGETT: same gathers, register-tiled FFMA.
+//   gett_ref_kernel            one thread per output, K in reference order,
+//       unfused mul then add: bitwise equal to the reference on all data.
+//   gett_serial_kernel         the literal reference loop on one thread (used
+//       only when output coordinates may alias, which the reference permits).
+//   gett_splitk_reduce_kernel  deterministic ordered sum of split-K partials,
+//       then C += sum.
+//   gett_zero_kernel           zero_view (kernel.py:111-113) on the device.
+//
+// Signed zeros: tiles accumulate from -0.0 and K-tail padding contributes
+// (-0.0)*(+0.0) = -0.0, the additive identity, so C + acc reproduces the
+// reference's sequential signed-zero outcomes.
+#include <cstdio>
+
+#include "device.cuh"
+#include "kernels.hpp"
+
+namespace gett {
+namespace tiled {
+
+constexpr int BM = 128;
+constexpr int BN = 128;
+constexpr int BK = 16;
+constexpr int THREADS = 256;
+constexpr int STAGES = 4;
+constexpr int PAD = 4;
+constexpr int GROUP_M = 8;
+constexpr int ROWS = 128;  // BM == BN
+constexpr int KF_PITCH = BK + PAD;    // [row][k] layout
+constexpr int RF_PITCH = ROWS + PAD;  // [k][row] layout
+constexpr int STAGE_ELEMS =
+    ROWS * KF_PITCH > BK * RF_PITCH ? ROWS * KF_PITCH : BK * RF_PITCH;
+
+template <typename T>
+constexpr size_t smem_bytes() {
+  return (size_t)STAGES * 2 * STAGE_ELEMS * sizeof(T);
+}
+
+// Loads one operand's ROWS x BK tile per stage.
+//   GKF:  gmem fast along k (else along rows)
+//   VEC:  16-byte copies along the fast dimension (planner-proven)
+//   SKF:  smem layout [row][k] (else [k][row])
+//   IS_A: K-tail pad value -0.0 (A') or +0.0 (B')
+template <typename T, bool GKF, bool VEC, bool SKF, bool IS_A>
+struct Loader {
+  static constexpr int V = VEC ? (int)(16 / sizeof(T)) : 1;
+  static constexpr int FAST = GKF ? BK : ROWS;        // extent of the fast dim
+  static constexpr int CPL = FAST / V;                // chunks per line
+  static constexpr int LSTEP = THREADS / CPL;         // lines per pass
+  static constexpr int SLOW = GKF ? ROWS : BK;        // extent of the slow dim
+  static constexpr int PER = SLOW / LSTEP;            // passes per thread
+  static_assert(THREADS % CPL == 0 && SLOW % LSTEP == 0, "loader mapping");
+
+  int fast0;                  // this thread's offset along the fast dim
+  int line0;                  // first line (slow dim) of this thread
+  int64_t roff[GKF ? PER : 1];
+  bool rok[GKF ? PER : 1];
+
+  __device__ __forceinline__ void setup(const GroupDev& g, int row0, int nrows) {
+    const int t = threadIdx.x;
+    fast0 = (t % CPL) * V;
+    line0 = t / CPL;
+    if (GKF) {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        int r = row0 + line0 + i * LSTEP;
+        rok[i] = r < nrows;
+        roff[i] = rok[i] ? g.off(0, r) : 0;
+      }
+    } else {
+      int r = row0 + fast0;
+      rok[0] = r < nrows;
+      roff[0] = rok[0] ? g.off(0, r) : 0;
+    }
+  }
+
+  __device__ __forceinline__ void store_pad(T* s, int r, int k, T v) {
+    if (SKF) s[r * KF_PITCH + k] = v;
+    else s[k * RF_PITCH + r] = v;
+  }
+
+  __device__ __forceinline__ void copy(T* s, int r, int k, const T* src) {
+    T* dst = SKF ? (s + r * KF_PITCH + k) : (s + k * RF_PITCH + r);
+    if (V == 1) {
+      if (sizeof(T) == 8) cp_async_8(dst, src);
+      else cp_async_4(dst, src);
+    } else {
+      cp_async_16(dst, src);
+    }
+  }
+
+  // kt: index of this operand in gk (0 = A', 1 = B')
+  __device__ __forceinline__ void load(T* s, const T* base, const GroupDev& gk, int kt, int k0,
+                                       int kend) {
+    const T kpad = IS_A ? T(-0.0) : T(0.0);
+    if (GKF) {
+      int k = k0 + fast0;
+      bool kok = k < kend;
+      int64_t ko = kok ? gk.off(kt, k) : 0;
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        int r = line0 + i * LSTEP;
+        if (kok && rok[i]) {
+          copy(s, r, fast0, base + roff[i] + ko);
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) store_pad(s, r, fast0 + v, kok ? T(0) : kpad);
+        }
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < PER; ++i) {
+        int kk = line0 + i * LSTEP;
+        int k = k0 + kk;
+        bool kok = k < kend;
+        if (kok && rok[0]) {
+          copy(s, fast0, kk, base + roff[0] + gk.off(kt, k));
+        } else {
+#pragma unroll
+          for (int v = 0; v < V; ++v) store_pad(s, fast0 + v, kk, kok ? T(0) : kpad);
+        }
+      }
+    }
+  }
+};
+
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+__device__ __forceinline__ void tile_coords(int tiles_m, int tiles_n, int tile, int& tm, int& tn) {
+  int per_group = GROUP_M * tiles_n;
+  int group = tile / per_group;
+  int first_m = group * GROUP_M;
+  int gsize = min(tiles_m - first_m, GROUP_M);
+  int in_group = tile % per_group;
+  tm = first_m + in_group % gsize;
+  tn = in_group / gsize;
+}
+
+// T = double: DMMA core, warps 2 (M) x 4 (N), warp tile 64 x 32.
+// T = float : FFMA core, 16 x 16 threads, thread tile 8 x 8 (rows ty*4+i,
+//             64+ty*4+i; cols tx*4+j, 64+tx*4+j).
+template <typename T, bool AKF, bool BKF, bool AVEC, bool BVEC>
+__global__ void __launch_bounds__(THREADS, 1) gett_tiled_kernel(const __grid_constant__ TiledParams<T> p) {
+  constexpr bool IS_D = sizeof(T) == 8;
+  // smem layouts: DMMA follows the gmem fast dimension; FFMA always [k][row]
+  constexpr bool ASKF = IS_D ? AKF : false;
+  constexpr bool BSKF = IS_D ? BKF : false;
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  T* smem = reinterpret_cast<T*>(smem_raw);
+
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int tile = blockIdx.x % ntiles;
+  const int split = blockIdx.x / ntiles;
+  int tm, tn;
+  tile_coords(p.tiles_m, p.tiles_n, tile, tm, tn);
+  const int m0 = tm * BM, n0 = tn * BN;
+  const int kbeg = split * p.k_chunk;
+  const int kend = min(p.K, kbeg + p.k_chunk);
+  const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
+
+  Loader<T, AKF, AVEC, ASKF, true> la;
+  Loader<T, BKF, BVEC, BSKF, false> lb;
+  la.setup(p.gm, m0, p.M);
+  lb.setup(p.gn, n0, p.N);
+
+  auto sA = [&](int st) { return smem + (size_t)st * 2 * STAGE_ELEMS; };
+  auto sB = [&](int st) { return smem + (size_t)st * 2 * STAGE_ELEMS + STAGE_ELEMS; };
+
+#pragma unroll
+  for (int st = 0; st < STAGES - 1; ++st) {
+    if (st < nkb) {
+      la.load(sA(st), p.A, p.gk, 0, kbeg + st * BK, kend);
+      lb.load(sB(st), p.B, p.gk, 1, kbeg + st * BK, kend);
+    }
+    cp_async_commit();
+  }
+
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
+
+  if constexpr (IS_D) {
+    const int wm0 = (warp >> 2) * 64;
+    const int wn0 = (warp & 3) * 32;
+    double acc[8][4][2];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = -0.0;
+
+    for (int kb = 0; kb < nkb; ++kb) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        int nk = kb + STAGES - 1;
+        if (nk < nkb) {
+          la.load(sA(nk % STAGES), p.A, p.gk, 0, kbeg + nk * BK, kend);
+          lb.load(sB(nk % STAGES), p.B, p.gk, 1, kbeg + nk * BK, kend);
+        }
+        cp_async_commit();
+      }
+      const double* As = sA(kb % STAGES);
+      const double* Bs = sB(kb % STAGES);
+#pragma unroll
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int kk = ks * 4 + (lane & 3);
+        double a[8], b[4];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          int r = wm0 + i * 8 + (lane >> 2);
+          a[i] = ASKF ? As[r * KF_PITCH + kk] : As[kk * RF_PITCH + r];
+        }
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          int c = wn0 + j * 8 + (lane >> 2);
+          b[j] = BSKF ? Bs[c * KF_PITCH + kk] : Bs[kk * RF_PITCH + c];
+        }
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
+      }
+    }
+    cp_async_wait<0>();
+
+    // epilogue: acc[i][j][e] is C'(m0+wm0+i*8+lane/4, n0+wn0+j*8+2*(lane%4)+e)
+    int64_t coff[8];
+    bool cok[8];
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        int n = n0 + wn0 + j * 8 + 2 * (lane & 3) + e;
+        cok[j * 2 + e] = n < p.N;
+        coff[j * 2 + e] = (n < p.N) ? (p.splits == 1 ? p.gn.off(1, n) : (int64_t)n) : 0;
+      }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int m = m0 + wm0 + i * 8 + (lane >> 2);
+      if (m >= p.M) continue;
+      if (p.splits == 1) {
+        int64_t ro = p.gm.off(1, m);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (cok[j * 2 + e]) {
+              double* c = p.C + ro + coff[j * 2 + e];
+              *c = *c + acc[i][j][e];
+            }
+      } else {
+        double* w = p.ws + ((int64_t)split * p.M + m) * p.N;
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (cok[j * 2 + e]) w[coff[j * 2 + e]] = acc[i][j][e];
+      }
+    }
+  } else {
+    const int tx = threadIdx.x & 15;
+    const int ty = threadIdx.x >> 4;
+    float acc[8][8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[i][j] = -0.0f;
+
+    for (int kb = 0; kb < nkb; ++kb) {
+      cp_async_wait<STAGES - 2>();
+      __syncthreads();
+      {
+        int nk = kb + STAGES - 1;
+        if (nk < nkb) {
+          la.load(sA(nk % STAGES), p.A, p.gk, 0, kbeg + nk * BK, kend);
+          lb.load(sB(nk % STAGES), p.B, p.gk, 1, kbeg + nk * BK, kend);
+        }
+        cp_async_commit();
+      }
+      const float* As = sA(kb % STAGES);
+      const float* Bs = sB(kb % STAGES);
+#pragma unroll
+      for (int kk = 0; kk < BK; ++kk) {
+        float4 a0 = *reinterpret_cast<const float4*>(As + kk * RF_PITCH + ty * 4);
+        float4 a1 = *reinterpret_cast<const float4*>(As + kk * RF_PITCH + 64 + ty * 4);
+        float4 b0 = *reinterpret_cast<const float4*>(Bs + kk * RF_PITCH + tx * 4);
+        float4 b1 = *reinterpret_cast<const float4*>(Bs + kk * RF_PITCH + 64 + tx * 4);
+        float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+        float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+        for (int i = 0; i < 8; ++i)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+      }
+    }
+    cp_async_wait<0>();
+
+    int64_t coff[8];
+    bool cok[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      int n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + j - 4);
+      cok[j] = n < p.N;
+      coff[j] = (n < p.N) ? (p.splits == 1 ? p.gn.off(1, n) : (int64_t)n) : 0;
+    }
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      int m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + i - 4);
+      if (m >= p.M) continue;
+      if (p.splits == 1) {
+        int64_t ro = p.gm.off(1, m);
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (cok[j]) {
+            float* c = p.C + ro + coff[j];
+            *c = *c + acc[i][j];
+          }
+      } else {
+        float* w = p.ws + ((int64_t)split * p.M + m) * p.N;
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (cok[j]) w[coff[j]] = acc[i][j];
+      }
+    }
+  }
+}
+
+}  // namespace tiled
+
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ double mul_rn(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double add_rn(double a, double b) { return __dadd_rn(a, b); }
+__device__ __forceinline__ float mul_rn(float a, float b) { return __fmul_rn(a, b); }
+__device__ __forceinline__ float add_rn(float a, float b) { return __fadd_rn(a, b); }
+
+template <typename T>
+__global__ void __launch_bounds__(256) gett_ref_kernel(const __grid_constant__ RefParams<T> p) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.M * p.N) return;
+  int32_t n = (int32_t)(idx % p.N);
+  int32_t m = (int32_t)(idx / p.N);
+  int64_t fa, ca, fb, cb;
+  p.gm.off2(m, fa, ca);
+  p.gn.off2(n, fb, cb);
+  T* c = p.C + ca + cb;
+  T acc = *c;
+  const T* A = p.A + fa;
+  const T* B = p.B + fb;
+  for (int32_t q = 0; q < p.k_outer; ++q) {
+    const T* a = A + __ldg(p.kta + q);
+    const T* b = B + __ldg(p.ktb + q);
+    for (int32_t r = 0; r < p.k_inner; ++r)
+      acc = add_rn(acc, mul_rn(__ldg(a + (int64_t)r * p.k_sa), __ldg(b + (int64_t)r * p.k_sb)));
+  }
+  *c = acc;
+}
+
+// kernel.py:48-78 verbatim on one thread (odometer order, c read each MAC)
+template <typename T>
+__global__ void gett_serial_kernel(const __grid_constant__ SerialParams<T> p) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const int nf = p.num_free, nc = p.num_cont;
+  const int64_t* out_inc = p.tab;
+  const int64_t* src_inc = p.tab + nf;
+  const int64_t* from_a = p.tab + 2 * nf;
+  const int64_t* ext_free = p.tab + 3 * nf;
+  const int64_t* inc_ca = p.tab + 4 * nf;
+  const int64_t* inc_cb = p.tab + 4 * nf + nc;
+  const int64_t* ext_cont = p.tab + 4 * nf + 2 * nc;
+  int64_t cf[64], cc[64];
+  for (int j = 0; j < nf; ++j) cf[j] = 0;
+  for (int64_t f = 0; f < p.size_free; ++f) {
+    int64_t ic = 0, ia0 = 0, ib0 = 0;
+    for (int j = 0; j < nf; ++j) {
+      ic += out_inc[j] * cf[j];
+      if (from_a[j]) ia0 += src_inc[j] * cf[j];
+      else ib0 += src_inc[j] * cf[j];
+    }
+    for (int k = 0; k < nc; ++k) cc[k] = 0;
+    for (int64_t q = 0; q < p.size_cont; ++q) {
+      int64_t ia = ia0, ib = ib0;
+      for (int k = 0; k < nc; ++k) {
+        ia += inc_ca[k] * cc[k];
+        ib += inc_cb[k] * cc[k];
+      }
+      volatile T* c = p.C + ic;
+      *c = add_rn(*c, mul_rn(p.A[ia], p.B[ib]));
+      for (int k = 0; k < nc; ++k) {
+        cc[k] = (cc[k] + 1) % ext_cont[k];
+        if (cc[k] != 0) break;
+      }
+    }
+    for (int j = 0; j < nf; ++j) {
+      cf[j] = (cf[j] + 1) % ext_free[j];
+      if (cf[j] != 0) break;
+    }
+  }
+}
+
+// C[m, n] += sum_s ws[s][m][n], s ascending, sum started at -0.0
+template <typename T>
+__global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_constant__ TiledParams<T> p) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  int64_t mn = (int64_t)p.M * p.N;
+  if (idx >= mn) return;
+  int32_t n = (int32_t)(idx % p.N);
+  int32_t m = (int32_t)(idx / p.N);
+  T s = T(-0.0);
+  for (int sp = 0; sp < p.splits; ++sp) s = s + p.ws[sp * mn + idx];
+  T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
+  *c = *c + s;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) gett_zero_kernel(T* base, const __grid_constant__ GroupDev g) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < g.G; i += stride)
+    base[g.off(0, (int32_t)i)] = T(0);
+}
+
+// ---------------------------------------------------------------------------
+// launchers
+
+namespace {
+template <typename T, bool AKF, bool BKF, bool AV, bool BV>
+cudaError_t launch_t(const TiledParams<T>& p, cudaStream_t s) {
+  auto k = tiled::gett_tiled_kernel<T, AKF, BKF, AV, BV>;
+  constexpr size_t smem = tiled::smem_bytes<T>();
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((unsigned)(p.tiles_m * p.tiles_n * p.splits));
+  k<<<grid, tiled::THREADS, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T, bool AKF, bool BKF>
+cudaError_t launch_v(const TiledParams<T>& p, bool av, bool bv, cudaStream_t s) {
+  if (av && bv) return launch_t<T, AKF, BKF, true, true>(p, s);
+  if (av) return launch_t<T, AKF, BKF, true, false>(p, s);
+  if (bv) return launch_t<T, AKF, BKF, false, true>(p, s);
+  return launch_t<T, AKF, BKF, false, false>(p, s);
+}
+}  // namespace
+
+template <typename T>
+cudaError_t launch_tiled(const TiledParams<T>& p, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
+                         cudaStream_t s) {
+  if (sizeof(T) == 4) {  // FFMA core keeps [k][row] smem: k-fast gathers are scalar
+    if (a_kf) a_vec = false;
+    if (b_kf) b_vec = false;
+  }
+  cudaError_t e;
+  if (a_kf && b_kf) e = launch_v<T, true, true>(p, a_vec, b_vec, s);
+  else if (a_kf) e = launch_v<T, true, false>(p, a_vec, b_vec, s);
+  else if (b_kf) e = launch_v<T, false, true>(p, a_vec, b_vec, s);
+  else e = launch_v<T, false, false>(p, a_vec, b_vec, s);
+  if (e != cudaSuccess || p.splits == 1) return e;
+  int64_t mn = (int64_t)p.M * p.N;
+  gett_splitk_reduce_kernel<T><<<(unsigned)((mn + 255) / 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_ref(const RefParams<T>& p, cudaStream_t s) {
+  int64_t n = (int64_t)p.M * p.N;
+  gett_ref_kernel<T><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s) {
+  gett_serial_kernel<T><<<1, 1, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
+cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s) {
+  int64_t blocks = (g.G + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  gett_zero_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(base, g);
+  return cudaGetLastError();
+}
+
+int tiled_bm() { return tiled::BM; }
+int tiled_bn() { return tiled::BN; }
+int tiled_bk() { return tiled::BK; }
+
+template cudaError_t launch_tiled<double>(const TiledParams<double>&, bool, bool, bool, bool, cudaStream_t);
+template cudaError_t launch_tiled<float>(const TiledParams<float>&, bool, bool, bool, bool, cudaStream_t);
+template cudaError_t launch_ref<double>(const RefParams<double>&, cudaStream_t);
+template cudaError_t launch_ref<float>(const RefParams<float>&, cudaStream_t);
+template cudaError_t launch_serial<double>(const SerialParams<double>&, cudaStream_t);
+template cudaError_t launch_serial<float>(const SerialParams<float>&, cudaStream_t);
+template cudaError_t launch_zero<double>(double*, const GroupDev&, cudaStream_t);
+template cudaError_t launch_zero<float>(float*, const GroupDev&, cudaStream_t);
+
+}  // namespace gett

@@ -1,0 +1,24 @@
+// Host-side launchers for the xGETT kernels (kernels.cu).
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include "device.cuh"
+
+namespace gett {
+
+template <typename T>
+cudaError_t launch_tiled(const TiledParams<T>& p, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
+                         cudaStream_t s);
+template <typename T>
+cudaError_t launch_ref(const RefParams<T>& p, cudaStream_t s);
+template <typename T>
+cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s);
+template <typename T>
+cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
+
+int tiled_bm();
+int tiled_bn();
+int tiled_bk();
+
+}  // namespace gett

@@ -1,0 +1,142 @@
+"""xGETT entry points — the drop-in for gett.kernel (host numpy buffers).
+
+``sgett`` / ``dgett`` keep the reference signature, keyword offsets, raises
+and return values (/root/reference/pkg/src/gett/kernel.py:124-184):
+
+* TypeError unless c is an ndarray; a, b go through np.asarray; every buffer
+  must be 1-D with exactly the entry point's dtype (kernel.py:132-140).
+* ValueError for structural problems (TensorView / ContractionSpec).
+* Value problems come back as the reference's ValidationError list, in the
+  reference's order, with c untouched (kernel.py:146-153).
+* Otherwise C += contract(A, B) runs on the GPU and [] is returned.
+
+The call crosses the C ABI (include/gett_b200.h) with plain pointers; the
+native side validates, plans, copies the addressed spans to the device,
+launches the sm_100a kernel and copies C's span back.  There is no CPU path.
+"""
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _native
+from .layout import TensorView
+from .plan import ContractionSpec, decode_errors, error_capacity
+
+_PREFIX_DTYPE = {
+    "s": np.dtype(np.float32),
+    "d": np.dtype(np.float64),
+}
+_ENTRY = {"s": "gett_sgett", "d": "gett_dgett"}
+
+
+def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm,
+          inc_c, c, offset_a, offset_b, offset_c):
+    dtype = _PREFIX_DTYPE[prefix]
+    if not isinstance(c, np.ndarray):
+        raise TypeError("c must be a numpy array (results are written in place)")
+    a = np.asarray(a)
+    b = np.asarray(b)
+    for name, buf in (("a", a), ("b", b), ("c", c)):
+        if buf.ndim != 1:
+            raise TypeError(f"{name} must be a flat 1-D buffer, got shape {buf.shape}")
+        if buf.dtype != dtype:
+            raise TypeError(f"{name} has dtype {buf.dtype}, this entry point needs {dtype}")
+    a_view = TensorView(rank_a, ext_a, inc_a, offset_a, a.shape[0])
+    b_view = TensorView(rank_b, ext_b, inc_b, offset_b, b.shape[0])
+    spec = ContractionSpec(conts, cont_a, cont_b, perm)
+    inc_c = tuple(int(i) for i in inc_c)
+    a = np.ascontiguousarray(a)
+    b = np.ascontiguousarray(b)
+    cw = c if c.flags.c_contiguous else np.ascontiguousarray(c)
+    empty = a_view.is_empty or b_view.is_empty
+    if not c.flags.writeable and not empty:
+        # the reference fails at its first store into c; fail before any work
+        from .plan import validate
+        errs = validate(a_view, b_view, spec, inc_c)
+        if errs:
+            return errs
+        raise ValueError("assignment destination is read-only")
+    cap = error_capacity(a_view.rank, b_view.rank, spec.conts)
+    codes = (ctypes.c_int32 * cap)()
+    info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
+    rc = getattr(_native.LIB, _ENTRY[prefix])(
+        a_view.rank, _native.i64(a_view.extents), _native.i64(a_view.increments), a.ctypes.data,
+        a_view.base_offset, a_view.buffer_len,
+        b_view.rank, _native.i64(b_view.extents), _native.i64(b_view.increments), b.ctypes.data,
+        b_view.base_offset, b_view.buffer_len,
+        spec.conts, _native.i64(spec.cont_a), _native.i64(spec.cont_b),
+        len(spec.perm), _native.i64(spec.perm), len(inc_c), _native.i64(inc_c),
+        cw.ctypes.data, int(offset_c), cw.shape[0], codes, info, cap)
+    n = _native.check(rc, prefix + "gett")
+    if n:
+        return decode_errors(min(n, cap), codes, info, a_view.rank, a_view.extents, b_view.rank,
+                             b_view.extents, spec, inc_c)
+    if cw is not c:
+        c[...] = cw
+    return []
+
+
+def sgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+          conts, cont_a, cont_b, perm, inc_c, c,
+          offset_a=0, offset_b=0, offset_c=0):
+    """32-bit real contraction; see dgett for the parameter contract."""
+    return _gett("s", rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
+
+
+def dgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+          conts, cont_a, cont_b, perm, inc_c, c,
+          offset_a=0, offset_b=0, offset_c=0):
+    """64-bit real binary tensor contraction, accumulating into c.
+
+    Arguments follow the xGETT interface order: A's rank,
+    extents, increments and buffer; the same for B; the pair count, paired
+    dimensions of A and of B, the free-index -> output-position permutation;
+    the output increments and buffer.  offset_* locate each view's first used
+    element.  Returns [] when the contraction ran, else the validation error
+    list (c untouched).  C is accumulated: clear the view first (zero_view)
+    for a plain contraction.
+    """
+    return _gett("d", rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
+
+
+def zero_view(view: TensorView, buf: np.ndarray) -> None:
+    """Set every element addressed by the view to zero, touching nothing else
+    (kernel.py:111-113), on the GPU."""
+    if not isinstance(buf, np.ndarray) or buf.ndim != 1:
+        raise TypeError("buf must be a flat 1-D numpy array")
+    prefix = dtype_prefix(buf.dtype)
+    if view.is_empty or any(e < 0 for e in view.extents):
+        return
+    lo = hi = 0
+    for e, i in zip(view.extents, view.increments):
+        span = i * (e - 1)
+        lo, hi = (lo + span, hi) if span < 0 else (lo, hi + span)
+    if view.base_offset + lo < 0 or view.base_offset + hi >= buf.shape[0]:
+        raise IndexError(f"view addresses offsets {view.base_offset + lo}..{view.base_offset + hi} "
+                         f"outside a buffer of {buf.shape[0]} elements")
+    if not buf.flags.writeable:
+        raise ValueError("assignment destination is read-only")
+    w = buf if buf.flags.c_contiguous else np.ascontiguousarray(buf)
+    f = _native.LIB.gett_zero_view_d if prefix == "d" else _native.LIB.gett_zero_view_s
+    _native.check(f(view.rank, _native.i64(view.extents), _native.i64(view.increments),
+                    view.base_offset, w.shape[0], w.ctypes.data), "zero_view")
+    if w is not buf:
+        buf[...] = w
+
+
+def dtype_prefix(dtype) -> str:
+    """The s/d tag for a numpy element type."""
+    dtype = np.dtype(dtype)
+    for prefix, dt in _PREFIX_DTYPE.items():
+        if dt == dtype:
+            return prefix
+    raise TypeError(f"no entry point for dtype {dtype}")
+
+
+def gett_for_dtype(dtype):
+    """The entry point matching a numpy dtype."""
+    return globals()[dtype_prefix(dtype) + "gett"]

@@ -1,0 +1,27 @@
+import os
+import sys
+
+import pytest
+
+ROOT = os.path.abspath(os.path.join(os.path.dirname(__file__), ".."))
+if ROOT not in sys.path:
+    sys.path.insert(0, ROOT)
+
+
+def pytest_configure(config):
+    config.addinivalue_line("markers", "gpu: needs a CUDA GPU (B200); run with -m gpu")
+    config.addinivalue_line("markers", "slow: long-running parity case")
+
+
+@pytest.fixture
+def kernel_mode():
+    """Set the native kernel family for one test, restoring auto after."""
+    from paper_2410_06770_b200 import set_kernel, set_split_k
+
+    def use(name, split=0):
+        set_kernel(name)
+        set_split_k(split)
+
+    yield use
+    set_kernel("auto")
+    set_split_k(0)

@@ -1,0 +1,135 @@
+"""CPU tests of the drop-in boundary: the C ABI library loads, exports every
+symbol include/gett_b200.h declares, and reproduces the reference's
+validation behaviour (codes, order, messages, raises) through the C ABI —
+none of which needs a GPU, because validation and the empty-space early
+return happen before any CUDA call (kernel.py:146-153, :93-94)."""
+import ctypes
+import os
+import re
+
+import numpy as np
+import pytest
+
+import paper_2410_06770_b200 as g
+from paper_2410_06770_b200 import _native
+from tests.golden_util import load_validation, load_zero_view
+
+HEADER = os.path.join(os.path.dirname(__file__), "..", "include", "gett_b200.h")
+
+
+def header_symbols():
+    text = open(HEADER).read()
+    text = re.sub(r"/\*.*?\*/", "", text, flags=re.S)
+    return sorted(set(re.findall(r"\b(gett_\w+)\s*\(", text)))
+
+
+def test_library_exports_every_declared_symbol():
+    syms = header_symbols()
+    assert len(syms) >= 17
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for s in syms:
+        assert hasattr(lib, s), s
+    assert set(syms) == set(_native.EXPORTS)
+
+
+def test_abi_version():
+    assert _native.LIB.gett_abi_version() == 100
+
+
+@pytest.mark.parametrize("case", load_validation(), ids=lambda c: c["label"])
+def test_validation_through_abi_matches_reference(case):
+    args, kw = case["args"], case["kw"]
+    c = args[13]
+    c[:] = 7.0
+    if "raises" in case:
+        with pytest.raises({"TypeError": TypeError, "ValueError": ValueError}[case["raises"]]):
+            g.dgett(*args, **kw)
+        return
+    if not case["errors"]:
+        pytest.skip("valid call: needs the GPU (tests/test_gpu_parity.py)")
+    errs = g.dgett(*args, **kw)
+    assert [(e.code.value, e.message) for e in errs] == [tuple(e) for e in case["errors"]]
+    assert np.all(c == 7.0), "C must be untouched when validation fails"
+
+
+def test_validate_with_explicit_c_view():
+    a, b = g.TensorView.contiguous((2, 3)), g.TensorView.contiguous((3, 4))
+    spec = g.ContractionSpec(1, (1,), (0,), (0, 1))
+    assert g.validate(a, b, spec, (1, 2)) == []
+    assert g.validate(a, b, spec, (1, 2), g.TensorView.contiguous((2, 4))) == []
+    small = g.TensorView(2, (2, 4), (1, 2), 0, 7)
+    errs = g.validate(a, b, spec, (1, 2), small)
+    assert [e.code for e in errs] == [g.ErrorCode.FootprintOutOfBounds]
+    assert "C addresses" in errs[0].message
+    neg = g.TensorView(1, (-1,), (1,), 0, 4)
+    errs = g.validate(a, b, spec, (1, 2), neg)
+    assert errs[0].code == g.ErrorCode.NegativeExtent and errs[0].message.startswith("C ")
+
+
+def test_messages_match_reference_text():
+    a, b = g.TensorView.contiguous((2, 3)), g.TensorView.contiguous((4, 4))
+    errs = g.validate(a, b, g.ContractionSpec(1, (1,), (0,), (0, 1)), (1, 2))
+    assert "pair 0" in str(errs[0])
+    fa = g.TensorView(1, (5,), (1,), 0, 4)
+    errs = g.validate(fa, g.TensorView.contiguous((5,)), g.ContractionSpec(1, (0,), (0,), ()), ())
+    assert "A" in str([e for e in errs if e.code == g.ErrorCode.FootprintOutOfBounds][0])
+
+
+def test_type_and_structure_raises():
+    a = np.zeros(1, dtype=np.float32)
+    with pytest.raises(TypeError):
+        g.dgett(0, (), (), a, 0, (), (), a, 0, (), (), (), (), a)
+    a = np.zeros(2)
+    with pytest.raises(ValueError):
+        g.dgett(2, (2,), (1,), a, 1, (2,), (1,), a, 0, (), (), (0, 1), (1, 2), a)
+    with pytest.raises(TypeError):
+        g.dgett(1, (2,), (1,), a, 1, (2,), (1,), a, 1, (0,), (0,), (), (), [0.0])
+    with pytest.raises(TypeError):
+        g.dgett(1, (2,), (1,), np.zeros((2, 1)), 1, (2,), (1,), a, 1, (0,), (0,), (), (), np.zeros(1))
+    with pytest.raises(ValueError):
+        g.ContractionSpec(2, (0,), (0, 1), ())
+    with pytest.raises(ValueError):
+        g.ContractionSpec(-1, (), (), ())
+
+
+def test_empty_iteration_writes_nothing_without_device():
+    c = np.full(4, 3.0)
+    errs = g.dgett(1, (0,), (1,), np.array([1.0]), 1, (1,), (1,), np.array([2.0]),
+                   0, (), (), (0, 1), (1, 1), c)
+    assert errs == [] and np.all(c == 3.0)
+
+
+def test_derive_output_extents():
+    a, b = g.TensorView.contiguous((2, 3)), g.TensorView.contiguous((3, 4))
+    assert g.derive_output_extents(a, b, g.ContractionSpec(1, (1,), (0,), (1, 0))) == (4, 2)
+    c5a = g.TensorView.contiguous((48, 24, 32, 16, 40))
+    c5b = g.TensorView.contiguous((40, 32, 24, 96))
+    assert g.derive_output_extents(c5a, c5b, g.ContractionSpec(3, (1, 2, 4), (2, 1, 0), (1, 2, 0))) == (96, 48, 16)
+
+
+def test_fastdiv_formula():
+    """The device FastDiv (csrc/device.cuh): q = umulhi(n, mul) >> shr with
+    mul = ceil(2^(31+l) / d), l = ceil(log2 d), exact for n < 2^31."""
+    rng = np.random.default_rng(0)
+    ds = [1, 2, 3, 5, 7, 24, 40, 96, 127, 128, 129, 768, 4096, 5184, 65536, 1 << 20, (1 << 31) - 1]
+    ds += [int(x) for x in rng.integers(1, 1 << 31, 200)]
+    for d in ds:
+        if d == 1:
+            continue
+        l = (d - 1).bit_length()
+        p = 31 + l
+        mul = ((1 << p) + d - 1) // d
+        assert mul < (1 << 32)
+        shr = p - 32
+        ns = [0, 1, d - 1, d, d + 1, (1 << 31) - 1] + [int(x) for x in rng.integers(0, 1 << 31, 200)]
+        for n in ns:
+            assert ((n * mul) >> 32) >> shr == n // d, (n, d)
+
+
+def test_zero_view_golden_cpu_checks():
+    # structure of the fixture; device results are checked in test_gpu_parity.py
+    cases = load_zero_view()
+    assert len(cases) == 6
+    empty = [c for c in cases if 0 in c["ext"] or any(e < 0 for e in c["ext"])]
+    for c in empty:
+        assert c["result"] == list(np.arange(1, c["n"] + 1, dtype=float))

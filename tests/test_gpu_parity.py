@@ -1,0 +1,301 @@
+"""GPU parity: the sm_100a kernels, called through the C ABI (dgett/sgett host
+entry points and the zero-copy device entry points), against the reference's
+golden outputs and the CPU oracle.
+
+Bars (north_star / SURVEY §8d):
+  * ref-order kernel: BITWISE equal to the reference on every golden case.
+  * tiled kernels: BITWISE on integer data (exact sums); otherwise
+    err_K = max|C - C_ref| / (|K|·max|A|·max|B|) <= 1e-12 (f64) / 1e-5 (f32),
+    and for SGETT the error vs an fp64 oracle within 2x the reference's own.
+  * nothing outside the C view changes (testkit.py:568-573).
+"""
+import numpy as np
+import pytest
+
+import paper_2410_06770_b200 as g
+from oracle import oracle
+from tests.golden_util import (load_configs, load_suite, load_zero_view, sliced_workload,
+                               view_offsets)
+
+pytestmark = pytest.mark.gpu
+
+SUITE = load_suite()
+TOL_K = {"d": 1e-12, "s": 1e-5}
+
+
+def run(entry, pos, kw):
+    errs = entry(*pos, **kw)
+    assert errs == [], errs
+
+
+def k_norm_err(got, want, w_or_k, amax=1.0, bmax=1.0):
+    k = max(1, w_or_k)
+    d = np.max(np.abs(got.astype(np.float64) - want.astype(np.float64))) if got.size else 0.0
+    return d / (k * max(amax, 1e-300) * max(bmax, 1e-300))
+
+
+# ---------------------------------------------------------------------------
+# known answers (restating the reference's test_kernel.py cases)
+
+MODES = ["auto", "ref", "tiled"]
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_known_answers(mode, kernel_mode):
+    kernel_mode(mode)
+    dg = g.dgett
+    a, b, c = np.array([1.0, 2, 3]), np.array([4.0, 5, 6]), np.zeros(1)
+    assert dg(1, (3,), (1,), a, 1, (3,), (1,), b, 1, (0,), (0,), (), (), c) == [] and c[0] == 32.0
+    eye, m, c = np.eye(3).ravel(order="F"), np.arange(9, dtype=np.float64), np.zeros(9)
+    assert dg(2, (3, 3), (1, 3), eye, 2, (3, 3), (1, 3), m, 1, (1,), (0,), (0, 1), (1, 3), c) == []
+    assert np.array_equal(c, m)
+    c = np.zeros(4)
+    assert dg(1, (2,), (1,), np.array([1.0, 2]), 1, (2,), (1,), np.array([3.0, 4]), 0, (), (), (0, 1), (1, 2), c) == []
+    assert c.tolist() == [3.0, 6.0, 4.0, 8.0]
+    b6, c = np.arange(6, dtype=np.float64), np.zeros(6)
+    assert dg(0, (), (), np.array([2.5]), 2, (2, 3), (1, 2), b6, 0, (), (), (0, 1), (1, 2), c) == []
+    assert np.array_equal(c, 2.5 * b6)
+    a, b, c = np.array([1.0, 2, 3]), np.array([1.0, 2, 3]), np.zeros(1)
+    assert dg(1, (3,), (-1,), a, 1, (3,), (1,), b, 1, (0,), (0,), (), (), c, offset_a=2) == [] and c[0] == 10
+    c = np.full(16, 9.0)
+    assert dg(1, (2,), (1,), np.array([1.0, 2]), 1, (2,), (1,), np.array([3.0, 4]), 0, (), (), (0, 1), (1, 4), c, offset_c=5) == []
+    assert [c[5], c[6], c[9], c[10]] == [12, 15, 13, 17]
+    assert all(c[i] == 9.0 for i in set(range(16)) - {5, 6, 9, 10})
+    c = np.zeros(4)
+    assert dg(2, (2, 2), (0, 1), np.array([5.0, 7]), 1, (2,), (1,), np.array([1.0, 1]), 1, (1,), (0,), (0,), (1,), c[:2]) == []
+    assert c[:2].tolist() == [12.0, 12.0]
+    cs = np.zeros(1, np.float32)
+    assert g.sgett(1, (3,), (1,), np.array([1, 2, 3], np.float32), 1, (3,), (1,), np.array([4, 5, 6], np.float32),
+                   1, (0,), (0,), (), (), cs) == [] and cs[0] == np.float32(32)
+
+
+@pytest.mark.parametrize("mode", MODES)
+def test_accumulation_and_gemm(mode, kernel_mode):
+    kernel_mode(mode)
+    rng = np.random.default_rng(5)
+    for m, k, n in [(1, 1, 1), (5, 3, 2), (33, 65, 17), (129, 40, 131), (256, 300, 64)]:
+        A = rng.integers(-4, 5, (m, k)).astype(np.float64)
+        B = rng.integers(-4, 5, (k, n)).astype(np.float64)
+        c = np.zeros(m * n)
+        args = (2, (m, k), (1, m), A.ravel(order="F"), 2, (k, n), (1, k), B.ravel(order="F"),
+                1, (1,), (0,), (0, 1), (1, m), c)
+        assert g.dgett(*args) == []
+        assert np.array_equal(c.reshape((m, n), order="F"), A @ B)
+        assert g.dgett(*args) == []
+        assert np.array_equal(c.reshape((m, n), order="F"), 2 * (A @ B))
+
+
+def test_kernel_selection_evidence(kernel_mode):
+    c = np.zeros(128 * 128)
+    A = np.ones(128 * 512)
+    kernel_mode("tiled")
+    g.dgett(2, (128, 512), (512, 1), A, 2, (512, 128), (128, 1), A, 1, (1,), (0,), (0, 1), (128, 1), c)
+    assert g.last_kernel().startswith("dgett_dmma")
+    kernel_mode("ref")
+    g.dgett(2, (128, 512), (512, 1), A, 2, (512, 128), (128, 1), A, 1, (1,), (0,), (0, 1), (128, 1), c)
+    assert g.last_kernel() == "dgett_ref_order"
+    n0 = g.launch_count()
+    g.dgett(2, (128, 512), (512, 1), A, 2, (512, 128), (128, 1), A, 1, (1,), (0,), (0, 1), (128, 1), c)
+    assert g.launch_count() == n0 + 1
+
+
+# ---------------------------------------------------------------------------
+# golden suite (reference-generated descriptors, reference outputs)
+
+
+def _check_suite_case(case, mode, kernel_mode):
+    kernel_mode(mode)
+    a, b, c = case.buffers()
+    before = c.copy()
+    pos, kw = case.args(a, b, c)
+    run(g.dgett if case.dtype == "d" else g.sgett, pos, kw)
+    offs = case.c_offsets()
+    got = c[offs]
+    mask = np.ones(len(c), bool)
+    mask[offs] = False
+    assert c[mask].tobytes() == before[mask].tobytes(), "bytes outside the C view changed"
+    if mode == "ref" or case.data == "int":
+        assert got.tobytes() == case.want.tobytes(), "not bitwise equal to the reference"
+    else:
+        k = int(np.prod([case.a["ext"][d] for d in case.cont_a])) if case.conts else 1
+        assert k_norm_err(got, case.want, k) <= TOL_K[case.dtype]
+
+
+@pytest.mark.parametrize("mode", ["ref", "tiled", "auto"])
+def test_golden_suite(mode, kernel_mode):
+    failures = []
+    for case in SUITE:
+        try:
+            _check_suite_case(case, mode, kernel_mode)
+        except AssertionError as e:
+            failures.append(f"{case.id}: {e}")
+    assert not failures, f"{len(failures)} failures, first: {failures[:5]}"
+
+
+@pytest.mark.parametrize("split", [2, 3, 7])
+def test_golden_suite_forced_split_k(split, kernel_mode):
+    failures = []
+    for case in SUITE[::5]:
+        try:
+            kernel_mode("tiled", split)
+            _check_suite_case(case, "tiled", lambda m, s=split: kernel_mode(m, s))
+        except AssertionError as e:
+            failures.append(f"{case.id}: {e}")
+    assert not failures, failures[:5]
+
+
+def test_commutativity_bit_identical(kernel_mode):
+    """Swapping A and B with a rotated perm writes a bit-identical buffer
+    (testkit.py:476-495, :575-581) on the integer-data cases."""
+    kernel_mode("tiled")
+    for case in SUITE:
+        if case.data != "int":
+            continue
+        a, b, c = case.buffers()
+        pos, kw = case.args(a, b, c.copy())
+        c1 = pos[13]
+        run(g.dgett if case.dtype == "d" else g.sgett, pos, kw)
+        fa = case.a["rank"] - case.conts
+        perm = tuple(case.perm[fa:]) + tuple(case.perm[:fa])
+        c2 = c.copy()
+        pos2 = (case.b["rank"], tuple(case.b["ext"]), tuple(case.b["inc"]), b,
+                case.a["rank"], tuple(case.a["ext"]), tuple(case.a["inc"]), a,
+                case.conts, tuple(case.cont_b), tuple(case.cont_a), perm, tuple(case.c["inc"]), c2)
+        kw2 = dict(offset_a=case.b["off"], offset_b=case.a["off"], offset_c=case.c["off"])
+        run(g.dgett if case.dtype == "d" else g.sgett, pos2, kw2)
+        assert c1.tobytes() == c2.tobytes(), case.id
+
+
+# ---------------------------------------------------------------------------
+# BASELINE configs
+
+
+CONFIGS = load_configs()
+
+
+@pytest.mark.parametrize("key", sorted(CONFIGS))
+def test_config_slices_ref_bitwise(key, kernel_mode):
+    kernel_mode("ref")
+    meta, want = CONFIGS[key]
+    w = sliced_workload(meta)
+    a, b, c = w.buffers()
+    pos, kw = w.args(a, b, c)
+    run(g.dgett if w.dtype == "d" else g.sgett, pos, kw)
+    assert c[view_offsets(w.ext_c, w.inc_c, w.off_c)].tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("key", sorted(CONFIGS))
+def test_config_slices_tiled(key, kernel_mode):
+    kernel_mode("auto")
+    meta, want = CONFIGS[key]
+    w = sliced_workload(meta)
+    a, b, c = w.buffers()
+    pos, kw = w.args(a, b, c)
+    run(g.dgett if w.dtype == "d" else g.sgett, pos, kw)
+    got = c[view_offsets(w.ext_c, w.inc_c, w.off_c)]
+    assert k_norm_err(got, want, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K[w.dtype]
+
+
+@pytest.mark.parametrize("name", ["c1", "c2", "c3", "c4", "c5"])
+def test_full_config(name, kernel_mode):
+    """Full-size run: golden slices (reference) + fp64 einsum over the whole
+    output + padding untouched."""
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+
+    kernel_mode("auto")
+    w = W[name]
+    a, b, c = w.buffers()
+    c0 = c.copy()
+    pos, kw = w.args(a, b, c)
+    run(g.dgett if w.dtype == "d" else g.sgett, pos, kw)
+    offs = view_offsets(w.ext_c, w.inc_c, w.off_c)
+    mask = np.ones(len(c), bool)
+    mask[offs] = False
+    assert c[mask].tobytes() == c0[mask].tobytes()
+    amax, bmax = float(np.abs(a).max()), float(np.abs(b).max())
+    # reference golden slices
+    for key, (meta, want) in CONFIGS.items():
+        if meta["workload"] != name:
+            continue
+        ws = sliced_workload(meta)
+        got = c[view_offsets(ws.ext_c, ws.inc_c, ws.off_c)]
+        assert k_norm_err(got, want, w.size_k, amax, bmax) <= TOL_K[w.dtype], key
+    # whole output vs fp64
+    ref = oracle.einsum_check(w.ext_a, w.inc_a, a, w.off_a, w.ext_b, w.inc_b, b, w.off_b,
+                              w.conts, w.cont_a, w.cont_b, w.perm)
+    ref = ref + oracle.strided(c0, w.ext_c, w.inc_c, w.off_c).astype(np.float64)
+    got = oracle.strided(c, w.ext_c, w.inc_c, w.off_c)
+    assert k_norm_err(got, ref, w.size_k, amax, bmax) <= TOL_K[w.dtype]
+    if name == "c5":
+        # secondary gate: error vs fp64 no worse than 2x the reference's own
+        _, want = CONFIGS["c5_0"]
+        ref_flat = ref.ravel(order="F")  # view order: dimension 0 fastest
+        e_ref = np.max(np.abs(want.astype(np.float64) - ref_flat))
+        e_new = np.max(np.abs(c[offs].astype(np.float64) - ref_flat))
+        assert e_new <= 2 * e_ref, (e_new, e_ref)
+
+
+# ---------------------------------------------------------------------------
+# other entry points
+
+
+def test_device_entry_matches_host_bitwise():
+    import torch
+
+    from paper_2410_06770_b200.device import dgett_device
+    from paper_2410_06770_b200.workloads import C3
+
+    w = C3.slice_free("A", 0, 0, 8)
+    a, b, c = w.buffers()
+    ch = c.copy()
+    pos, kw = w.args(a, b, ch)
+    run(g.dgett, pos, kw)
+    ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+    pos, kw = w.args(ta, tb, tc)
+    assert dgett_device(*pos, **kw) == []
+    torch.cuda.synchronize()
+    assert tc.cpu().numpy().tobytes() == ch.tobytes()
+
+
+def test_zero_view_golden():
+    for z in load_zero_view():
+        buf = np.arange(1, z["n"] + 1, dtype=np.float64)
+        g.zero_view(g.TensorView(z["rank"], z["ext"], z["inc"], z["off"], z["n"]), buf)
+        assert buf.tolist() == z["result"]
+        bs = np.arange(1, z["n"] + 1, dtype=np.float32)
+        g.zero_view(g.TensorView(z["rank"], z["ext"], z["inc"], z["off"], z["n"]), bs)
+        assert bs.tolist() == z["result"]
+
+
+def test_aliasing_output_uses_serial_kernel_and_matches_oracle():
+    """Distinct output coordinates sharing a C element (legal: only inc 0 is
+    rejected, plan.py:220-227) — the serial kernel reproduces the sequential
+    reference order bitwise."""
+    rng = np.random.default_rng(3)
+    a = rng.uniform(-1, 1, 12)
+    b = rng.uniform(-1, 1, 20)
+    args = (2, (3, 4), (1, 3), a, 2, (4, 5), (1, 4), b, 1, (1,), (0,), (0, 1), (1, 1))
+    c = rng.uniform(-1, 1, 10)
+    want = c.copy()
+    oracle.oracle_dgett(*args, want)
+    assert g.dgett(*args, c) == []
+    assert g.last_kernel() == "dgett_serial"
+    assert c.tobytes() == want.tobytes()
+
+
+def test_signed_zero_semantics(kernel_mode):
+    for mode in ("ref", "tiled"):
+        kernel_mode(mode)
+        a = np.array([-0.0, 0.0, -4.0])
+        b = np.array([1.0, -0.0, 0.0])
+        for c0 in (0.0, -0.0):
+            c = np.array([c0])
+            want = np.array([c0])
+            oracle.oracle_dgett(1, (3,), (1,), a, 1, (3,), (1,), b, 1, (0,), (0,), (), (), want)
+            assert g.dgett(1, (3,), (1,), a, 1, (3,), (1,), b, 1, (0,), (0,), (), (), c) == []
+            assert c.tobytes() == want.tobytes(), (mode, c0)
+        # all products -0 with C = -0 stays -0
+        c = np.array([-0.0])
+        assert g.dgett(1, (3,), (1,), np.array([-0.0, -0.0, -0.0]),
+                       1, (3,), (1,), np.ones(3), 1, (0,), (0,), (), (), c) == []
+        assert np.signbit(c[0])
