@@ -411,9 +411,11 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
     return run_device<T>(*dp, a + off_a, b + off_b, c + off_c, stream, ds);
   }
   // host buffers: copy the addressed spans in, run, copy C's span back
-  size_t na = (size_t)(p.span_hi[0] - p.span_lo[0] + 1);
-  size_t nb = (size_t)(p.span_hi[1] - p.span_lo[1] + 1);
-  size_t nc = (size_t)(p.span_hi[2] - p.span_lo[2] + 1);
+  // (the plan is cached by descriptor only: spans use this call's offsets)
+  const int64_t lo_a = off_a + p.fp_lo[0], lo_b = off_b + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
+  size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
+  size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
   if ((rc = ensure(ds.a, na * sizeof(T))) || (rc = ensure(ds.b, nb * sizeof(T))) ||
       (rc = ensure(ds.c, nc * sizeof(T))))
     return rc;
@@ -421,13 +423,12 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   T* db = (T*)ds.b.p;
   T* dc = (T*)ds.c.p;
   cudaStream_t s = ds.stream;
-  CK(cudaMemcpyAsync(da, a + p.span_lo[0], na * sizeof(T), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(db, b + p.span_lo[1], nb * sizeof(T), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(dc, c + p.span_lo[2], nc * sizeof(T), cudaMemcpyHostToDevice, s));
-  rc = run_device<T>(*dp, da + (off_a - p.span_lo[0]), db + (off_b - p.span_lo[1]),
-                     dc + (off_c - p.span_lo[2]), s, ds);
+  CK(cudaMemcpyAsync(da, a + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(db, b + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc, c + lo_c, nc * sizeof(T), cudaMemcpyHostToDevice, s));
+  rc = run_device<T>(*dp, da - p.fp_lo[0], db - p.fp_lo[1], dc - p.fp_lo[2], s, ds);
   if (rc) return rc;
-  CK(cudaMemcpyAsync(c + p.span_lo[2], dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaMemcpyAsync(c + lo_c, dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   return 0;
 }

@@ -281,11 +281,11 @@ Plan build_plan(const View& a, const View& b, const Spec& s, int64_t off_c, int6
   // spans
   int64_t lo, hi;
   footprint(a.rank, a.ext, a.inc, &lo, &hi);
-  p.span_lo[0] = a.off + lo; p.span_hi[0] = a.off + hi;
+  p.fp_lo[0] = lo; p.fp_hi[0] = hi;
   footprint(b.rank, b.ext, b.inc, &lo, &hi);
-  p.span_lo[1] = b.off + lo; p.span_hi[1] = b.off + hi;
+  p.fp_lo[1] = lo; p.fp_hi[1] = hi;
   footprint(p.rank_c, p.ext_c.data(), s.inc_c, &lo, &hi);
-  p.span_lo[2] = off_c + lo; p.span_hi[2] = off_c + hi;
+  p.fp_lo[2] = lo; p.fp_hi[2] = hi;
   return p;
 }
 

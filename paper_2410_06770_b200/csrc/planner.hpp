@@ -75,8 +75,9 @@ struct Plan {
   Group gm, gn, gk;
   Group gk_ref;          // K in reference order (pair 0 fastest) over (A', B')
   bool c_may_alias = false;  // distinct output coordinates may share a C element
-  // spans (absolute element indices, inclusive) addressed in each buffer
-  int64_t span_lo[3] = {0, 0, 0}, span_hi[3] = {-1, -1, -1};
+  // footprints (lowest, highest offset relative to each view's base offset);
+  // offsets are not part of the plan, so callers add their own
+  int64_t fp_lo[3] = {0, 0, 0}, fp_hi[3] = {0, 0, 0};
 };
 
 // Build the plan for validated arguments.

@@ -283,6 +283,24 @@ def test_aliasing_output_uses_serial_kernel_and_matches_oracle():
     assert c.tobytes() == want.tobytes()
 
 
+@pytest.mark.parametrize("mode", ["tiled", "ref"])
+def test_plan_cache_is_offset_independent(mode, kernel_mode):
+    """Plans are cached by descriptor; offsets (and so copied spans) are per
+    call.  Same descriptor, different offsets, back to back."""
+    kernel_mode(mode)
+    rng = np.random.default_rng(11)
+    a = rng.integers(-4, 5, 40).astype(np.float64)
+    b = rng.integers(-4, 5, 40).astype(np.float64)
+    for off_a, off_b, off_c in [(0, 0, 0), (7, 3, 2), (30, 0, 5), (1, 31, 0)]:
+        c = rng.integers(-4, 5, 12).astype(np.float64)
+        want = c.copy()
+        args = (1, (5,), (1,), a, 1, (5,), (-1,), b, 1, (0,), (0,), (), ())
+        kw = dict(offset_a=off_a, offset_b=off_b + 4, offset_c=off_c)
+        oracle.oracle_dgett(*args, want, **kw)
+        assert g.dgett(*args, c, **kw) == []
+        assert c.tobytes() == want.tobytes(), (off_a, off_b, off_c)
+
+
 def test_signed_zero_semantics(kernel_mode):
     for mode in ("ref", "tiled"):
         kernel_mode(mode)
