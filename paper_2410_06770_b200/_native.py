@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libgett_b200.so")
+LIB_PATH = os.environ.get("GETT_LIB_PATH") or os.path.join(_HERE, "libgett_b200.so")
 
 # every symbol include/gett_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (

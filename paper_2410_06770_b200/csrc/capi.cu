@@ -310,7 +310,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   tp.A = A; tp.B = B; tp.C = c;
   tp.gm = dp.gm; tp.gn = dp.gn; tp.gk = dp.gk;
   tp.M = (int32_t)M; tp.N = (int32_t)N; tp.K = (int32_t)K;
-  const int BM = tiled_bm(), BN = tiled_bn(), BK = tiled_bk();
+  const int BM = tiled_bm(), BN = tiled_bn(), BK = tiled_bk((int)sizeof(T));
   tp.tiles_m = (int32_t)((M + BM - 1) / BM);
   tp.tiles_n = (int32_t)((N + BN - 1) / BN);
   int64_t tiles = (int64_t)tp.tiles_m * tp.tiles_n;

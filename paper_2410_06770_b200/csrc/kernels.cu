@@ -28,20 +28,42 @@ namespace tiled {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int BK = 16;
-constexpr int THREADS = 256;
-constexpr int STAGES = 4;
 constexpr int PAD = 4;
-constexpr int GROUP_M = 8;
+#ifndef GETT_GROUP_M
+#define GETT_GROUP_M 8
+#endif
+#ifndef GETT_D_BK
+#define GETT_D_BK 32
+#endif
+#ifndef GETT_D_STAGES
+#define GETT_D_STAGES 3
+#endif
+#ifndef GETT_D_THREADS
+#define GETT_D_THREADS 512
+#endif
+constexpr int GROUP_M = GETT_GROUP_M;
 constexpr int ROWS = 128;  // BM == BN
-constexpr int KF_PITCH = BK + PAD;    // [row][k] layout
-constexpr int RF_PITCH = ROWS + PAD;  // [k][row] layout
-constexpr int STAGE_ELEMS =
-    ROWS * KF_PITCH > BK * RF_PITCH ? ROWS * KF_PITCH : BK * RF_PITCH;
+
+// Per element type: k-block depth and pipeline stages.  f64: BK 32 x 3 stages
+// (216 KB smem, halves the per-k-block barrier/issue overhead of the DMMA
+// loop); f32 FFMA: BK 16 x 4 stages.
+template <typename T>
+struct Cfg {
+  static constexpr int BK = sizeof(T) == 8 ? GETT_D_BK : 16;
+  static constexpr int STAGES = sizeof(T) == 8 ? GETT_D_STAGES : 4;
+  static constexpr int THREADS = sizeof(T) == 8 ? GETT_D_THREADS : 256;
+  // DMMA warp grid: 8 warps -> 2 x 4 (warp tile 64 x 32); 16 warps -> 4 x 4 (32 x 32)
+  static constexpr int WARPS_M = THREADS / 32 / 4;
+  static constexpr int WARPS_N = 4;
+  static constexpr int KF_PITCH = BK + PAD;    // [row][k] layout (f64: 36 = 4 mod 16)
+  static constexpr int RF_PITCH = ROWS + PAD;  // [k][row] layout (132 = 4 mod 16)
+  static constexpr int STAGE_ELEMS =
+      ROWS * KF_PITCH > BK * RF_PITCH ? ROWS * KF_PITCH : BK * RF_PITCH;
+};
 
 template <typename T>
 constexpr size_t smem_bytes() {
-  return (size_t)STAGES * 2 * STAGE_ELEMS * sizeof(T);
+  return (size_t)Cfg<T>::STAGES * 2 * Cfg<T>::STAGE_ELEMS * sizeof(T);
 }
 
 // Loads one operand's ROWS x BK tile per stage.
@@ -51,9 +73,13 @@ constexpr size_t smem_bytes() {
 //   IS_A: K-tail pad value -0.0 (A') or +0.0 (B')
 template <typename T, bool GKF, bool VEC, bool SKF, bool IS_A>
 struct Loader {
+  static constexpr int BK = Cfg<T>::BK;
+  static constexpr int KF_PITCH = Cfg<T>::KF_PITCH;
+  static constexpr int RF_PITCH = Cfg<T>::RF_PITCH;
   static constexpr int V = VEC ? (int)(16 / sizeof(T)) : 1;
   static constexpr int FAST = GKF ? BK : ROWS;        // extent of the fast dim
   static constexpr int CPL = FAST / V;                // chunks per line
+  static constexpr int THREADS = Cfg<T>::THREADS;
   static constexpr int LSTEP = THREADS / CPL;         // lines per pass
   static constexpr int SLOW = GKF ? ROWS : BK;        // extent of the slow dim
   static constexpr int PER = SLOW / LSTEP;            // passes per thread
@@ -152,8 +178,13 @@ __device__ __forceinline__ void tile_coords(int tiles_m, int tiles_n, int tile, 
 // T = float : FFMA core, 16 x 16 threads, thread tile 8 x 8 (rows ty*4+i,
 //             64+ty*4+i; cols tx*4+j, 64+tx*4+j).
 template <typename T, bool AKF, bool BKF, bool AVEC, bool BVEC>
-__global__ void __launch_bounds__(THREADS, 1) gett_tiled_kernel(const __grid_constant__ TiledParams<T> p) {
+__global__ void __launch_bounds__(Cfg<T>::THREADS, 1) gett_tiled_kernel(const __grid_constant__ TiledParams<T> p) {
   constexpr bool IS_D = sizeof(T) == 8;
+  constexpr int BK = Cfg<T>::BK;
+  constexpr int STAGES = Cfg<T>::STAGES;
+  constexpr int KF_PITCH = Cfg<T>::KF_PITCH;
+  constexpr int RF_PITCH = Cfg<T>::RF_PITCH;
+  constexpr int STAGE_ELEMS = Cfg<T>::STAGE_ELEMS;
   // smem layouts: DMMA follows the gmem fast dimension; FFMA always [k][row]
   constexpr bool ASKF = IS_D ? AKF : false;
   constexpr bool BSKF = IS_D ? BKF : false;
@@ -191,54 +222,73 @@ __global__ void __launch_bounds__(THREADS, 1) gett_tiled_kernel(const __grid_con
   const int warp = threadIdx.x >> 5;
 
   if constexpr (IS_D) {
-    const int wm0 = (warp >> 2) * 64;
-    const int wn0 = (warp & 3) * 32;
-    double acc[8][4][2];
+    constexpr int WM = BM / Cfg<T>::WARPS_M, WN = BN / Cfg<T>::WARPS_N;
+    constexpr int MI = WM / 8, NJ = WN / 8;
+    const int wm0 = (warp / Cfg<T>::WARPS_N) * WM;
+    const int wn0 = (warp % Cfg<T>::WARPS_N) * WN;
+    double acc[MI][NJ][2];
 #pragma unroll
-    for (int i = 0; i < 8; ++i)
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-      for (int j = 0; j < 4; ++j) acc[i][j][0] = acc[i][j][1] = -0.0;
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = -0.0;
+
+    // fragment offsets within a stage (k-step 0); k-step ks adds 4*ks along k
+    int aoff[MI], boff[NJ];
+#pragma unroll
+    for (int i = 0; i < MI; ++i) {
+      int r = wm0 + i * 8 + (lane >> 2);
+      aoff[i] = ASKF ? r * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + r;
+    }
+#pragma unroll
+    for (int j = 0; j < NJ; ++j) {
+      int c = wn0 + j * 8 + (lane >> 2);
+      boff[j] = BSKF ? c * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + c;
+    }
+    constexpr int AKS = ASKF ? 4 : 4 * RF_PITCH;  // k-step stride in smem
+    constexpr int BKS = BSKF ? 4 : 4 * RF_PITCH;
 
     for (int kb = 0; kb < nkb; ++kb) {
       cp_async_wait<STAGES - 2>();
       __syncthreads();
-      {
-        int nk = kb + STAGES - 1;
-        if (nk < nkb) {
-          la.load(sA(nk % STAGES), p.A, p.gk, 0, kbeg + nk * BK, kend);
-          lb.load(sB(nk % STAGES), p.B, p.gk, 1, kbeg + nk * BK, kend);
-        }
-        cp_async_commit();
-      }
       const double* As = sA(kb % STAGES);
       const double* Bs = sB(kb % STAGES);
+      // register double buffer: fragments of k-step ks+1 load under the DMMAs of ks
+      double a[2][MI], b[2][NJ];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) a[0][i] = As[aoff[i]];
+#pragma unroll
+      for (int j = 0; j < NJ; ++j) b[0][j] = Bs[boff[j]];
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
-        const int kk = ks * 4 + (lane & 3);
-        double a[8], b[4];
+        const int cur = ks & 1;
+        if (ks + 1 < BK / 4) {
 #pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          int r = wm0 + i * 8 + (lane >> 2);
-          a[i] = ASKF ? As[r * KF_PITCH + kk] : As[kk * RF_PITCH + r];
+          for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[aoff[i] + (ks + 1) * AKS];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[boff[j] + (ks + 1) * BKS];
         }
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          int c = wn0 + j * 8 + (lane >> 2);
-          b[j] = BSKF ? Bs[c * KF_PITCH + kk] : Bs[kk * RF_PITCH + c];
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+        if (ks == 0) {
+          // issue the next stage's gathers while the first k-step's DMMAs drain
+          int nk = kb + STAGES - 1;
+          if (nk < nkb) {
+            la.load(sA(nk % STAGES), p.A, p.gk, 0, kbeg + nk * BK, kend);
+            lb.load(sB(nk % STAGES), p.B, p.gk, 1, kbeg + nk * BK, kend);
+          }
+          cp_async_commit();
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int j = 0; j < 4; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[i], b[j]);
       }
     }
     cp_async_wait<0>();
 
     // epilogue: acc[i][j][e] is C'(m0+wm0+i*8+lane/4, n0+wn0+j*8+2*(lane%4)+e)
-    int64_t coff[8];
-    bool cok[8];
+    int64_t coff[NJ * 2];
+    bool cok[NJ * 2];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
       for (int e = 0; e < 2; ++e) {
         int n = n0 + wn0 + j * 8 + 2 * (lane & 3) + e;
@@ -246,13 +296,13 @@ __global__ void __launch_bounds__(THREADS, 1) gett_tiled_kernel(const __grid_con
         coff[j * 2 + e] = (n < p.N) ? (p.splits == 1 ? p.gn.off(1, n) : (int64_t)n) : 0;
       }
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
+    for (int i = 0; i < MI; ++i) {
       int m = m0 + wm0 + i * 8 + (lane >> 2);
       if (m >= p.M) continue;
       if (p.splits == 1) {
         int64_t ro = p.gm.off(1, m);
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
             if (cok[j * 2 + e]) {
@@ -262,7 +312,7 @@ __global__ void __launch_bounds__(THREADS, 1) gett_tiled_kernel(const __grid_con
       } else {
         double* w = p.ws + ((int64_t)split * p.M + m) * p.N;
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
             if (cok[j * 2 + e]) w[coff[j * 2 + e]] = acc[i][j][e];
@@ -445,7 +495,7 @@ cudaError_t launch_t(const TiledParams<T>& p, cudaStream_t s) {
     configured = true;
   }
   dim3 grid((unsigned)(p.tiles_m * p.tiles_n * p.splits));
-  k<<<grid, tiled::THREADS, smem, s>>>(p);
+  k<<<grid, tiled::Cfg<T>::THREADS, smem, s>>>(p);
   return cudaGetLastError();
 }
 
@@ -500,7 +550,7 @@ cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s) {
 
 int tiled_bm() { return tiled::BM; }
 int tiled_bn() { return tiled::BN; }
-int tiled_bk() { return tiled::BK; }
+int tiled_bk(int elt_bytes) { return elt_bytes == 8 ? tiled::Cfg<double>::BK : tiled::Cfg<float>::BK; }
 
 template cudaError_t launch_tiled<double>(const TiledParams<double>&, bool, bool, bool, bool, cudaStream_t);
 template cudaError_t launch_tiled<float>(const TiledParams<float>&, bool, bool, bool, bool, cudaStream_t);

@@ -19,6 +19,6 @@ cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 
 int tiled_bm();
 int tiled_bn();
-int tiled_bk();
+int tiled_bk(int elt_bytes);
 
 }  // namespace gett

@@ -1,0 +1,51 @@
+"""Time the device-resident xGETT on the BASELINE configs for one build of the
+library (GETT_LIB_PATH selects a variant .so).  Prints one JSON line per
+config: CUDA-event ms per call (median of reps) and TFLOP/s.
+
+    GETT_LIB_PATH=build/variants/libgett_X.so python tools/tune.py c2 c3 c4 c5
+"""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.getcwd())
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_2410_06770_b200 as g  # noqa: E402
+from paper_2410_06770_b200.device import dgett_device, sgett_device  # noqa: E402
+from paper_2410_06770_b200.workloads import CONFIGS  # noqa: E402
+
+
+def main():
+    names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
+    reps = int(os.environ.get("REPS", "7"))
+    for name in names:
+        w = CONFIGS[name]
+        a, b, c = w.buffers()
+        ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+        fn = dgett_device if w.dtype == "d" else sgett_device
+        pos, kw = w.args(ta, tb, tc)
+        for _ in range(3):
+            assert fn(*pos, **kw) == []
+        torch.cuda.synchronize()
+        times = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(*pos, **kw)
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = float(np.median(times))
+        print(json.dumps({"lib": os.path.basename(os.environ.get("GETT_LIB_PATH", "default")),
+                          "config": name, "ms": round(ms, 4),
+                          "tflops": round(w.flops / ms / 1e9, 3), "kernel": g.last_kernel(),
+                          "min_ms": round(min(times), 4)}), flush=True)
+        del ta, tb, tc
+        torch.cuda.empty_cache()
+
+
+if __name__ == "__main__":
+    main()
