@@ -166,6 +166,10 @@ int gett_zero_view_s_device(int rank, const int64_t* ext, const int64_t* inc, in
 int gett_set_kernel(const char* name);
 /* Force the split-K factor of the tiled kernel (0 = automatic). */
 int gett_set_split_k(int split);
+/* Host entry points only: overlap H2D / compute / D2H by cutting C's outermost
+ * free mode into `slabs` sub-contractions (-1 = automatic for calls moving
+ * >= 64 MB, 0 = off, n >= 2 = always n slabs).  Also GETT_PIPELINE. */
+int gett_set_pipeline(int slabs);
 /* Name of the kernel the last call launched ("none" if none). */
 const char* gett_last_kernel(void);
 /* Text of the last CUDA / internal failure. */

@@ -7,7 +7,8 @@ semantics.  Python calls the native library (libgett_b200.so, C ABI in
 include/gett_b200.h); the planner and the kernels are C++/CUDA.
 """
 from . import _native
-from ._native import GettRuntimeError, last_kernel, launch_count, set_kernel, set_split_k
+from ._native import (GettRuntimeError, last_kernel, launch_count, set_kernel, set_pipeline,
+                      set_split_k)
 from .kernel import dgett, dtype_prefix, gett_for_dtype, sgett, zero_view
 from .layout import TensorView, contiguous_increments, footprint, num_elements
 from .plan import (

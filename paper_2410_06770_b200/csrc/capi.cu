@@ -31,6 +31,7 @@ enum class Mode { Auto, Ref, Tiled, Serial };
 std::mutex g_mu;
 Mode g_mode = Mode::Auto;
 int g_split = 0;
+int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
 thread_local std::string t_last_error;
 thread_local const char* t_last_kernel = "none";
@@ -43,6 +44,8 @@ void read_env() {
   if (k) gett_set_kernel(k);
   const char* s = std::getenv("GETT_SPLIT_K");
   if (s) g_split = std::atoi(s);
+  const char* pl = std::getenv("GETT_PIPELINE");
+  if (pl) g_pipeline_slabs = std::atoi(pl);
 }
 
 int cuda_fail(cudaError_t e, const char* what) {
@@ -93,7 +96,17 @@ struct Scratch {
 };
 struct DevState {
   cudaStream_t stream = nullptr;
+  cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
+  std::vector<cudaEvent_t> events;
   Scratch a, b, c, ws;
+  cudaEvent_t event(size_t i) {
+    while (events.size() <= i) {
+      cudaEvent_t e;
+      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      events.push_back(e);
+    }
+    return events[i];
+  }
 };
 std::unordered_map<int, DevState> g_dev;
 
@@ -356,6 +369,106 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   return 0;
 }
 
+constexpr int kNotPipelined = 1 << 30;
+
+// Host-buffer path with transfers overlapped: the free mode with the largest
+// C stride (outermost in C) is cut into slabs — each slab is itself an xGETT
+// on sub-views (shard.py's argument), so slab s computes while slab s+1's
+// operand/C spans are copied in and slab s-1's C span is copied out.  The
+// operand that does not own the slab mode is copied once, up front.  Slab C
+// spans must be disjoint (stride of the slab mode > span of the other C modes).
+template <typename T>
+int host_pipelined(DevPlan& full, const View& a, const View& b, const Spec& s, const T* ha,
+                   const T* hb, T* hc, int64_t off_c, int64_t len_c, DevState& ds) {
+  const Plan& p = full.plan;
+  if (g_pipeline_slabs == 0 || g_pipeline_slabs == 1 || p.c_may_alias) return kNotPipelined;
+  const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
+  const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
+  const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
+  if (g_pipeline_slabs < 0 && (na + nb + 2 * nc) * sizeof(T) < (64u << 20)) return kNotPipelined;
+  auto contracted = [](const int64_t* idx, int n, int d) {
+    for (int k = 0; k < n; ++k)
+      if (idx[k] == d) return true;
+    return false;
+  };
+  int owner = -1, dim = -1, q = -1, i = 0;
+  int64_t best = -1;
+  for (int t = 0; t < 2; ++t) {
+    const View& v = t == 0 ? a : b;
+    const int64_t* cont = t == 0 ? s.cont_a : s.cont_b;
+    for (int d = 0; d < v.rank; ++d) {
+      if (contracted(cont, s.conts, d)) continue;
+      int qq = (int)s.perm[i++];
+      if (v.ext[d] > 1 && iabs(s.inc_c[qq]) > best) {
+        best = iabs(s.inc_c[qq]);
+        owner = t; dim = d; q = qq;
+      }
+    }
+  }
+  if (owner < 0) return kNotPipelined;
+  int64_t other = 0;
+  for (int qq = 0; qq < p.rank_c; ++qq)
+    if (qq != q && p.ext_c[qq] > 0) other += iabs(s.inc_c[qq]) * (p.ext_c[qq] - 1);
+  if (iabs(s.inc_c[q]) <= other) return kNotPipelined;
+  const View& ov = owner == 0 ? a : b;
+  const int64_t E = ov.ext[dim];
+  int64_t S = g_pipeline_slabs > 1 ? g_pipeline_slabs : 8;
+  if (S > E) S = E;
+  if (S < 2) return kNotPipelined;
+
+  int rc;
+  if ((rc = ensure(ds.a, na * sizeof(T))) || (rc = ensure(ds.b, nb * sizeof(T))) ||
+      (rc = ensure(ds.c, nc * sizeof(T))))
+    return rc;
+  if (!ds.h2d) CK(cudaStreamCreateWithFlags(&ds.h2d, cudaStreamNonBlocking));
+  if (!ds.d2h) CK(cudaStreamCreateWithFlags(&ds.d2h, cudaStreamNonBlocking));
+  // device bases: base[idx] mirrors host element idx over each full span
+  const int64_t lo_a = a.off + p.fp_lo[0], lo_b = b.off + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  T* base_a = (T*)ds.a.p - lo_a;
+  T* base_b = (T*)ds.b.p - lo_b;
+  T* base_c = (T*)ds.c.p - lo_c;
+  // the non-owning operand, whole
+  if (owner == 0) CK(cudaMemcpyAsync(base_b + lo_b, hb + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
+  else CK(cudaMemcpyAsync(base_a + lo_a, ha + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
+  std::vector<int64_t> ext_o(ov.ext, ov.ext + ov.rank);
+  std::vector<int64_t> ext_c(p.ext_c);
+  for (int64_t sl = 0; sl < S; ++sl) {
+    const int64_t lo = E * sl / S, hi = E * (sl + 1) / S;
+    ext_o[dim] = hi - lo;
+    ext_c[q] = hi - lo;
+    View sa = a, sb = b;
+    if (owner == 0) { sa.ext = ext_o.data(); sa.off = a.off + lo * a.inc[dim]; }
+    else { sb.ext = ext_o.data(); sb.off = b.off + lo * b.inc[dim]; }
+    const int64_t soff_c = off_c + lo * s.inc_c[q];
+    std::shared_ptr<DevPlan> dp;
+    rc = get_plan(sizeof(T) == 8 ? 'd' : 's', sa, sb, s, soff_c, len_c, &dp);
+    if (rc) return rc;
+    int64_t flo, fhi;
+    const View& so = owner == 0 ? sa : sb;
+    footprint(so.rank, so.ext, so.inc, &flo, &fhi);
+    const int64_t olo = so.off + flo;
+    const size_t on = (size_t)(fhi - flo + 1);
+    T* obase = owner == 0 ? base_a : base_b;
+    const T* ohost = owner == 0 ? ha : hb;
+    CK(cudaMemcpyAsync(obase + olo, ohost + olo, on * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
+    footprint(p.rank_c, ext_c.data(), s.inc_c, &flo, &fhi);
+    const int64_t clo = soff_c + flo;
+    const size_t cn = (size_t)(fhi - flo + 1);
+    CK(cudaMemcpyAsync(base_c + clo, hc + clo, cn * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
+    cudaEvent_t ein = ds.event(2 * sl), eout = ds.event(2 * sl + 1);
+    CK(cudaEventRecord(ein, ds.h2d));
+    CK(cudaStreamWaitEvent(ds.stream, ein, 0));
+    rc = run_device<T>(*dp, base_a + sa.off, base_b + sb.off, base_c + soff_c, ds.stream, ds);
+    if (rc) return rc;
+    CK(cudaEventRecord(eout, ds.stream));
+    CK(cudaStreamWaitEvent(ds.d2h, eout, 0));
+    CK(cudaMemcpyAsync(hc + clo, base_c + clo, cn * sizeof(T), cudaMemcpyDeviceToHost, ds.d2h));
+  }
+  CK(cudaStreamSynchronize(ds.d2h));
+  CK(cudaStreamSynchronize(ds.stream));
+  return 0;
+}
+
 int fill_errors(const std::vector<Error>& errs, int32_t* codes, int64_t* info, int max_errs) {
   int n = (int)errs.size();
   for (int i = 0; i < n && i < max_errs; ++i) {
@@ -410,6 +523,8 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   if (!host) {
     return run_device<T>(*dp, a + off_a, b + off_b, c + off_c, stream, ds);
   }
+  rc = host_pipelined<T>(*dp, va, vb, sp, a, b, c, off_c, len_c, ds);
+  if (rc != kNotPipelined) return rc;
   // host buffers: copy the addressed spans in, run, copy C's span back
   // (the plan is cached by descriptor only: spans use this call's offsets)
   const int64_t lo_a = off_a + p.fp_lo[0], lo_b = off_b + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
@@ -601,6 +716,12 @@ int gett_set_kernel(const char* name) {
 int gett_set_split_k(int split) {
   if (split < 0) return GETT_E_INVALID_ARG;
   g_split = split;
+  return 0;
+}
+
+int gett_set_pipeline(int slabs) {
+  if (slabs < -1) return GETT_E_INVALID_ARG;
+  g_pipeline_slabs = slabs;
   return 0;
 }
 

@@ -144,6 +144,18 @@ def test_golden_suite_forced_split_k(split, kernel_mode):
     assert not failures, failures[:5]
 
 
+@pytest.mark.parametrize("slabs", [2, 3])
+def test_golden_suite_pipelined_host_path(slabs, kernel_mode):
+    """Host path with H2D/compute/D2H overlapped over C-disjoint slabs."""
+    failures = []
+    for case in SUITE:
+        try:
+            _check_suite_case(case, "tiled", lambda m: kernel_mode(m, 0, slabs))
+        except AssertionError as e:
+            failures.append(f"{case.id}: {e}")
+    assert not failures, f"{len(failures)} failures, first: {failures[:5]}"
+
+
 def test_commutativity_bit_identical(kernel_mode):
     """Swapping A and B with a rotated perm writes a bit-identical buffer
     (testkit.py:476-495, :575-581) on the integer-data cases."""

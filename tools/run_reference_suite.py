@@ -36,7 +36,11 @@ def _adapt(entry):
 _k.dgett = _adapt(_b.dgett)
 _k.sgett = _adapt(_b.sgett)
 
+_ref_zero_view = _k.zero_view
+
 def _zero_view(view, buf):
+    if buf.dtype.kind == "c":  # complex stays on the reference (not this round's path)
+        return _ref_zero_view(view, buf)
     _b.zero_view(_b.TensorView(view.rank, view.extents, view.increments, view.base_offset,
                                view.buffer_len), buf)
 _k.zero_view = _zero_view
