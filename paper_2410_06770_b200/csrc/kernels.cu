@@ -521,6 +521,11 @@ cudaError_t launch_tiled(const TiledParams<T>& p, bool a_kf, bool b_kf, bool a_v
   else if (b_kf) e = launch_v<T, false, true>(p, a_vec, b_vec, s);
   else e = launch_v<T, false, false>(p, a_vec, b_vec, s);
   if (e != cudaSuccess || p.splits == 1) return e;
+  return launch_splitk_reduce<T>(p, s);
+}
+
+template <typename T>
+cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s) {
   int64_t mn = (int64_t)p.M * p.N;
   gett_splitk_reduce_kernel<T><<<(unsigned)((mn + 255) / 256), 256, 0, s>>>(p);
   return cudaGetLastError();
@@ -554,6 +559,8 @@ int tiled_bk(int elt_bytes) { return elt_bytes == 8 ? tiled::Cfg<double>::BK : t
 
 template cudaError_t launch_tiled<double>(const TiledParams<double>&, bool, bool, bool, bool, cudaStream_t);
 template cudaError_t launch_tiled<float>(const TiledParams<float>&, bool, bool, bool, bool, cudaStream_t);
+template cudaError_t launch_splitk_reduce<double>(const TiledParams<double>&, cudaStream_t);
+template cudaError_t launch_splitk_reduce<float>(const TiledParams<float>&, cudaStream_t);
 template cudaError_t launch_ref<double>(const RefParams<double>&, cudaStream_t);
 template cudaError_t launch_ref<float>(const RefParams<float>&, cudaStream_t);
 template cudaError_t launch_serial<double>(const SerialParams<double>&, cudaStream_t);
