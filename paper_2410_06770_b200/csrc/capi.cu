@@ -68,8 +68,6 @@ struct DevPlan {
   int64_t* kref_a = nullptr;
   int64_t* kref_b = nullptr;
   int64_t* serial_tab = nullptr;
-  int64_t* ktab_a = nullptr;  // SGETT tcgen05 path: offset of every k in A' / B'
-  int64_t* ktab_b = nullptr;
   int serial_nf = 0, serial_nc = 0;
   // residues used by the vector-load checks: every table entry divisible by 2 / 4
   bool am_even2 = false, am_even4 = false, ak_even2 = false, ak_even4 = false;
@@ -209,17 +207,6 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
   push(p.gk.T[0]); push(p.gk.T[1]);
   push(p.gk_ref.T[0]); push(p.gk_ref.T[1]);
   push(serial_table(a, b, s, &dp->serial_nf, &dp->serial_nc));
-  const bool want_ktab = dtype == 's' && p.gk.G <= (1LL << 26);
-  if (want_ktab) {
-    std::vector<int64_t> ka(p.gk.G), kb(p.gk.G);
-    for (int64_t k = 0; k < p.gk.G; ++k) {
-      int64_t q = k / p.gk.e_in, r = k % p.gk.e_in;
-      ka[k] = p.gk.T[0][q] + r * p.gk.s_in[0];
-      kb[k] = p.gk.T[1][q] + r * p.gk.s_in[1];
-    }
-    push(ka);
-    push(kb);
-  }
   CK(cudaMalloc(&dp->d_tab, host.size() * sizeof(int64_t)));
   CK(cudaMemcpy(dp->d_tab, host.data(), host.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
   int64_t* t = dp->d_tab;
@@ -229,10 +216,6 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
   dp->kref_a = t + offs[6];
   dp->kref_b = t + offs[7];
   dp->serial_tab = t + offs[8];
-  if (want_ktab) {
-    dp->ktab_a = t + offs[9];
-    dp->ktab_b = t + offs[10];
-  }
   dp->am_even2 = all_div(p.gm.T[0], 2); dp->am_even4 = all_div(p.gm.T[0], 4);
   dp->ak_even2 = all_div(p.gk.T[0], 2); dp->ak_even4 = all_div(p.gk.T[0], 4);
   dp->bn_even2 = all_div(p.gn.T[0], 2); dp->bn_even4 = all_div(p.gn.T[0], 4);
@@ -341,7 +324,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   tp.gm = dp.gm; tp.gn = dp.gn; tp.gk = dp.gk;
   tp.M = (int32_t)M; tp.N = (int32_t)N; tp.K = (int32_t)K;
   // SGETT: 3xTF32 on tcgen05 unless forced to the FFMA core (or no k table)
-  const bool use_tc = sizeof(T) == 4 && mode != Mode::Ffma && dp.ktab_a != nullptr;
+  const bool use_tc = sizeof(T) == 4 && mode != Mode::Ffma;
   const int BM = use_tc ? tc_bm() : tiled_bm(), BN = use_tc ? tc_bn() : tiled_bn();
   const int BK = use_tc ? tc_bk() : tiled_bk((int)sizeof(T));
   tp.tiles_m = (int32_t)((M + BM - 1) / BM);
@@ -383,8 +366,8 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     b_vec = b_kf ? vec_ok(gkB, bkd, dp.gn, bnd, V, B) : vec_ok(dp.gn, bnd, gkB, bkd, V, B);
   }
   if (use_tc) {
-    CK(launch_sgett_tc(*reinterpret_cast<TiledParams<float>*>(&tp), dp.ktab_a, dp.ktab_b, a_kf,
-                       b_kf, a_vec, b_vec, stream));
+    CK(launch_sgett_tc(*reinterpret_cast<TiledParams<float>*>(&tp), a_kf, b_kf, a_vec, b_vec,
+                       stream));
     g_launches += splits > 1 ? 2 : 1;
     t_last_kernel = splits > 1 ? "sgett_tc3xtf32_splitk" : "sgett_tc3xtf32";
     return 0;

@@ -295,20 +295,43 @@ __global__ void __launch_bounds__(Cfg<T>::THREADS, 1) gett_tiled_kernel(const __
         cok[j * 2 + e] = n < p.N;
         coff[j * 2 + e] = (n < p.N) ? (p.splits == 1 ? p.gn.off(1, n) : (int64_t)n) : 0;
       }
+    if (p.splits == 1) {
+      // all C loads first (many in flight), then the stores: C += acc
+      int64_t ro[MI];
+      bool rok[MI];
+#pragma unroll
+      for (int i = 0; i < MI; ++i) {
+        int m = m0 + wm0 + i * 8 + (lane >> 2);
+        rok[i] = m < p.M;
+        ro[i] = rok[i] ? p.gm.off(1, m) : 0;
+      }
+      constexpr int IH = 1;  // rows per batch (bounds live registers)
+#pragma unroll
+      for (int i0 = 0; i0 < MI; i0 += IH) {
+        double cv[IH][NJ][2];
+#pragma unroll
+        for (int i = 0; i < IH; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              cv[i][j][e] = (rok[i0 + i] && cok[j * 2 + e]) ? p.C[ro[i0 + i] + coff[j * 2 + e]] : 0.0;
+#pragma unroll
+        for (int i = 0; i < IH; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j)
+#pragma unroll
+            for (int e = 0; e < 2; ++e)
+              if (rok[i0 + i] && cok[j * 2 + e])
+                p.C[ro[i0 + i] + coff[j * 2 + e]] = cv[i][j][e] + acc[i0 + i][j][e];
+      }
+    }
 #pragma unroll
     for (int i = 0; i < MI; ++i) {
       int m = m0 + wm0 + i * 8 + (lane >> 2);
       if (m >= p.M) continue;
       if (p.splits == 1) {
-        int64_t ro = p.gm.off(1, m);
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e)
-            if (cok[j * 2 + e]) {
-              double* c = p.C + ro + coff[j * 2 + e];
-              *c = *c + acc[i][j][e];
-            }
+        continue;
       } else {
         double* w = p.ws + ((int64_t)split * p.M + m) * p.N;
 #pragma unroll

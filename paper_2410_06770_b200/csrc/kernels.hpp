@@ -20,10 +20,9 @@ cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 template <typename T>
 cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s);
 
-// SGETT 3xTF32 on tcgen05 (sgett_tc.cu); ktab_*: full per-k offsets of A', B'
-cudaError_t launch_sgett_tc(const TiledParams<float>& p, const int64_t* ktab_a,
-                            const int64_t* ktab_b, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
-                            cudaStream_t s);
+// SGETT 3xTF32 on tcgen05 (sgett_tc.cu)
+cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec,
+                            bool b_vec, cudaStream_t s);
 
 int tiled_bm();
 int tiled_bn();

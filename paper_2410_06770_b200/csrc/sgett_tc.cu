@@ -1,39 +1,55 @@
 // SGETT on the 5th-generation tensor cores: 3xTF32 with tcgen05.mma + TMEM.
 //
 // Replaces the fp32 hot loop (kernel.py:48-78 for sgett) for contractions big
-// enough to tile.  Per 128x128 output tile and k-block of 32:
+// enough to tile.  Per 128x128 output tile and k-block of 16:
 //   * 128 threads gather the A' (M x K) and B' (N x K) tiles straight from the
-//     strided views (row offsets from the planner's groups, k offsets from a
-//     precomputed per-k table), split every value x = hi + lo with
-//     hi = rna_tf32(x), lo = x - hi (exact in fp32), and store hi/lo tiles in
-//     the UMMA K-major no-swizzle layout (8-row x 16-byte core matrices;
-//     LBO 128 B between k-chunks, SBO 1 KB between 8-row groups);
-//   * one thread issues, per UMMA_K=8 step, tcgen05.mma.kind::tf32 for
-//     hi*hi, hi*lo, lo*hi into one fp32 accumulator in TMEM (128 lanes x 128
-//     columns), and tcgen05.commit frees the smem stage through an mbarrier;
-//   * the gathers of k-block kb+1 are in flight while the MMAs of kb run
-//     (3-stage smem ring);
+//     strided views with cp.async (row offsets from the planner's groups, k
+//     offsets from a precomputed per-k table; 16-byte copies where the
+//     planner proved 4-k contiguity) into the UMMA K-major no-swizzle layout
+//     (8-row x 16-byte core matrices, LBO 128 B between k-chunks, SBO 512 B
+//     between 8-row groups).  GETT_TC_STAGES-1 k-blocks are in flight, which
+//     is what a latency-bound strided gather needs (SGETT c5 is HBM-bound);
+//   * when a k-block lands, each thread splits its own elements in place:
+//     hi = rna_tf32(x) (overwrites x), lo = x - hi (exact in fp32) into the lo
+//     tile, then fence.proxy.async publishes both to the tensor core;
+//   * one thread issues, per UMMA_K = 8 step, tcgen05.mma.kind::tf32 for
+//     lo*hi, hi*lo, hi*hi into one fp32 accumulator in TMEM (128 lanes x 128
+//     columns); tcgen05.commit frees the smem stage through an mbarrier;
 //   * epilogue: tcgen05.ld 32x32b (thread = row), C += acc through the C
 //     offset tables, or the split-K partial into the workspace.
-// Accuracy: the 3xTF32 product error is ~2^-22 relative per term, fp32
-// accumulation in TMEM; checked against the fp64 oracle and the reference.
+// Accuracy: 3xTF32 products are within ~2^-22 relative, fp32 accumulation in
+// TMEM; checked against the fp64 oracle and the reference (tests/).
 #include <cstdint>
 
 #include "device.cuh"
 #include "kernels.hpp"
+
+#ifndef GETT_TC_STAGES
+#define GETT_TC_STAGES 2
+#endif
+#ifndef GETT_TC_SLACK
+#define GETT_TC_SLACK 1
+#endif
 
 namespace gett {
 namespace tc {
 
 constexpr int BM = 128;
 constexpr int BN = 128;
-constexpr int BK = 32;
-constexpr int STAGES = 3;
+constexpr int BK = 16;
+constexpr int CH = BK / 4;                     // 16-byte k-chunks per row
+constexpr int STAGES = GETT_TC_STAGES;
 constexpr int THREADS = 128;
 constexpr int GROUP_M = 8;
-constexpr int TILE_BYTES = 128 * BK * 4;       // one operand part (hi or lo): 16 KB
+constexpr int LBO = 128;                       // bytes between k-chunks
+constexpr int SBO = CH * 128;                  // bytes between 8-row groups
+constexpr int TILE_BYTES = 128 * BK * 4;       // one operand part (hi or lo): 8 KB
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;    // A hi, A lo, B hi, B lo
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 1024;
+#ifndef GETT_TC_TCAP
+#define GETT_TC_TCAP 256
+#endif
+constexpr int TCAP = GETT_TC_TCAP;             // outer k-table entries staged in smem
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 2 * TCAP * 8;
 constexpr uint32_t TMEM_COLS = 128;
 
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
@@ -41,13 +57,13 @@ constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >
                            ((uint32_t)(BM >> 4) << 24);
 
 __device__ __forceinline__ uint32_t toff(int r, int c) {
-  return (uint32_t)((r >> 3) * 1024 + c * 128 + (r & 7) * 16);
+  return (uint32_t)((r >> 3) * SBO + c * LBO + (r & 7) * 16);
 }
 
-// shared-memory matrix descriptor (sm_100: version 1), no swizzle, K-major
+// shared-memory matrix descriptor (sm_100: version 1 at bit 46), no swizzle
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(128u >> 4) << 16) |
-         ((uint64_t)(1024u >> 4) << 32) | (1ull << 46);
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(LBO >> 4) << 16) |
+         ((uint64_t)(SBO >> 4) << 32) | (1ull << 46);
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
@@ -75,94 +91,109 @@ __device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, 
       : "memory");
 }
 
-__device__ __forceinline__ void tf32_split(float x, float& hi, float& lo) {
-  uint32_t h;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(x));
-  hi = __uint_as_float(h);
-  lo = x - hi;
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
 }
 
-// One operand's 128-row x 32-k gather.  GKF: gmem fast along k (thread owns
-// one 4-k chunk of 8 rows) else along rows (thread owns one row, all chunks).
+__device__ __forceinline__ void split4(float4 x, float4& h, float4& l) {
+  uint32_t t;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.x)); h.x = __uint_as_float(t); l.x = x.x - h.x;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.y)); h.y = __uint_as_float(t); l.y = x.y - h.y;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.z)); h.z = __uint_as_float(t); l.z = x.z - h.z;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.w)); h.w = __uint_as_float(t); l.w = x.w - h.w;
+}
+
+// k-group decoder for one operand: offset(k) = T[k / e_in] + (k % e_in) * s
+struct KDec {
+  const int64_t* T;
+  int64_t s;
+  FastDiv div;
+};
+
+// One operand's 128-row x BK gather with cp.async.  GKF: gmem fast along k
+// (a thread owns one 16-byte k-chunk of 4 rows) else along rows (a thread
+// owns one row, all chunks).  Units are (row, chunk) pairs.
 template <bool GKF, bool VEC>
 struct Gather {
-  float v[8][4];
-  int64_t roff[GKF ? 8 : 1];
-  bool rok[GKF ? 8 : 1];
+  static constexpr int U = GKF ? 4 : CH;  // units per thread
+  int64_t roff[GKF ? 4 : 1];
+  bool rok[GKF ? 4 : 1];
   int chunk, row0;
+
+  __device__ __forceinline__ int urow(int u) const { return GKF ? row0 + 32 * u : row0; }
+  __device__ __forceinline__ int uchunk(int u) const { return GKF ? chunk : u; }
 
   __device__ __forceinline__ void setup(const GroupDev& g, int base_row, int nrows) {
     const int t = threadIdx.x;
-    if (GKF) {
-      chunk = t & 7;
-      row0 = t >> 3;
+    chunk = GKF ? (t & (CH - 1)) : 0;
+    row0 = GKF ? t / CH : t;
 #pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        int r = base_row + row0 + 16 * i;
-        rok[i] = r < nrows;
-        roff[i] = rok[i] ? g.off(0, r) : 0;
-      }
-    } else {
-      chunk = 0;
-      row0 = t;
-      int r = base_row + t;
-      rok[0] = r < nrows;
-      roff[0] = rok[0] ? g.off(0, r) : 0;
+    for (int i = 0; i < (GKF ? 4 : 1); ++i) {
+      int r = base_row + row0 + 32 * i;
+      rok[i] = r < nrows;
+      roff[i] = rok[i] ? g.off(0, r) : 0;
     }
   }
 
-  __device__ __forceinline__ void load(const float* base, const int64_t* ktab, int k0, int kend) {
-    if (GKF) {
-      const int k = k0 + 4 * chunk;
+  // k offsets of the next k-block, loaded ahead of the copies so the table
+  // reads overlap (the cp.async issue would otherwise serialise on them)
+  static constexpr int NKO = GKF ? (VEC ? 1 : 4) : BK;
+  int64_t ko[NKO];
+  int kk0, kkend;
+
+  // k -> offset by stepping the group's (outer q, inner r) decode: one fast
+  // divmod per k-block, and an outer-table read only when r wraps (the
+  // table sits in shared memory when it fits)
+  __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
+    kk0 = k0;
+    kkend = kend;
+    const int kb = GKF ? k0 + 4 * chunk : k0;
+    int q, r;
+    kd.div.divmod(kb, q, r);
+    int64_t t = kb < kend ? kd.T[q] : 0;
+#pragma unroll
+    for (int e = 0; e < NKO; ++e) {
+      ko[e] = t + (int64_t)r * kd.s;
+      if (++r == kd.div.d) {
+        r = 0;
+        ++q;
+        t = (kb + e + 1 < kend) ? kd.T[q] : 0;
+      }
+    }
+  }
+
+  // issue the prepared k-block into the hi tile at smem address s
+  __device__ __forceinline__ void issue(uint8_t* s, const float* base) {
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int r = urow(u), c = uchunk(u);
+      const bool rv = rok[GKF ? u : 0];
+      const int64_t ro = roff[GKF ? u : 0];
+      uint8_t* dst = s + toff(r, c);
+      const int k = kk0 + 4 * c;
       if (VEC) {
-        const bool kok = k < kend;  // planner: K % 4 == 0 when VEC
-        const int64_t ko = kok ? __ldg(ktab + k) : 0;
-#pragma unroll
-        for (int i = 0; i < 8; ++i) {
-          if (kok && rok[i]) {
-            float4 x = __ldg(reinterpret_cast<const float4*>(base + roff[i] + ko));
-            v[i][0] = x.x; v[i][1] = x.y; v[i][2] = x.z; v[i][3] = x.w;
-          } else {
-            v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
-          }
-        }
+        if (rv && k < kkend) cp_async_16(dst, base + ro + ko[0]);
+        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
-        int64_t ko[4];
-        bool kok[4];
 #pragma unroll
         for (int e = 0; e < 4; ++e) {
-          kok[e] = k + e < kend;
-          ko[e] = kok[e] ? __ldg(ktab + k + e) : 0;
+          const int64_t o = GKF ? ko[e] : ko[4 * c + e];
+          if (rv && k + e < kkend) cp_async_4(dst + 4 * e, base + ro + o);
+          else *reinterpret_cast<float*>(dst + 4 * e) = 0.f;
         }
-#pragma unroll
-        for (int i = 0; i < 8; ++i)
-#pragma unroll
-          for (int e = 0; e < 4; ++e) v[i][e] = (kok[e] && rok[i]) ? __ldg(base + roff[i] + ko[e]) : 0.f;
       }
-    } else {
-#pragma unroll
-      for (int c = 0; c < 8; ++c)
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int k = k0 + 4 * c + e;
-          const bool ok = rok[0] && k < kend;
-          v[c][e] = ok ? __ldg(base + roff[0] + __ldg(ktab + k)) : 0.f;
-        }
     }
   }
 
-  // split into hi/lo and store both tiles (byte offsets hi_s / lo_s in smem)
-  __device__ __forceinline__ void store(uint8_t* hi_s, uint8_t* lo_s) {
+  // split this thread's own landed elements: hi in place, lo into lo tile
+  __device__ __forceinline__ void split(uint8_t* hi_s, uint8_t* lo_s) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int r = GKF ? row0 + 16 * i : row0;
-      const int c = GKF ? chunk : i;
+    for (int u = 0; u < U; ++u) {
+      const uint32_t o = toff(urow(u), uchunk(u));
+      float4 x = *reinterpret_cast<const float4*>(hi_s + o);
       float4 h, l;
-      tf32_split(v[i][0], h.x, l.x);
-      tf32_split(v[i][1], h.y, l.y);
-      tf32_split(v[i][2], h.z, l.z);
-      tf32_split(v[i][3], h.w, l.w);
-      const uint32_t o = toff(r, c);
+      split4(x, h, l);
       *reinterpret_cast<float4*>(hi_s + o) = h;
       *reinterpret_cast<float4*>(lo_s + o) = l;
     }
@@ -171,11 +202,11 @@ struct Gather {
 
 template <bool AKF, bool BKF, bool AVEC, bool BVEC>
 __global__ void __launch_bounds__(THREADS, 1)
-    sgett_tc_kernel(const __grid_constant__ TiledParams<float> p, const int64_t* __restrict__ ktab_a,
-                    const int64_t* __restrict__ ktab_b) {
+    sgett_tc_kernel(const __grid_constant__ TiledParams<float> p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // [STAGES] free, [STAGES] done
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // [STAGES] free, [1] done
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + STAGES + 1);
+  int64_t* ktabs = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + 256);  // [2][TCAP]
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
@@ -212,22 +243,53 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
+  // the K group's outer offset tables, staged in shared memory when small
+  const int n_outer = (p.gk.G + p.gk.e_in.d - 1) / p.gk.e_in.d;
+  KDec kda{p.gk.T[0], p.gk.s_in[0], p.gk.e_in}, kdb{p.gk.T[1], p.gk.s_in[1], p.gk.e_in};
+  if (n_outer <= TCAP) {
+    for (int i = tid; i < n_outer; i += THREADS) {
+      ktabs[i] = __ldg(p.gk.T[0] + i);
+      ktabs[TCAP + i] = __ldg(p.gk.T[1] + i);
+    }
+    __syncthreads();
+    kda.T = ktabs;
+    kdb.T = ktabs + TCAP;
+  }
   Gather<AKF, AVEC> ga;
   Gather<BKF, BVEC> gb;
   ga.setup(p.gm, m0, p.M);
   gb.setup(p.gn, n0, p.N);
-  if (nkb > 0) {
-    ga.load(p.A, ktab_a, kbeg, kend);
-    gb.load(p.B, ktab_b, kbeg, kend);
+  auto stage = [&](int s) { return smem + s * STAGE_BYTES; };
+
+  // prefetch distance: DIST k-blocks of copies in flight; the stage being
+  // refilled was read by the MMAs of k-block kb - (STAGES - DIST), issued
+  // STAGES - DIST iterations earlier, so MMA latency stays off the loop
+  constexpr int DIST = STAGES - GETT_TC_SLACK;
+#pragma unroll 1
+  for (int s = 0; s < DIST; ++s) {
+    if (s < nkb) {
+      ga.prep(kda, kbeg + s * BK, kend);
+      gb.prep(kdb, kbeg + s * BK, kend);
+      ga.issue(stage(s), p.A);
+      gb.issue(stage(s) + 2 * TILE_BYTES, p.B);
+    }
+    cp_async_commit();
   }
   const uint32_t smem_base = smem_u32(smem);
+#pragma unroll 1
   for (int kb = 0; kb < nkb; ++kb) {
     const int s = kb % STAGES;
-    const int use = kb / STAGES;
-    if (use > 0) mbar_wait(smem_u32(bars + s), (use - 1) & 1);
-    uint8_t* st = smem + s * STAGE_BYTES;
-    ga.store(st, st + TILE_BYTES);
-    gb.store(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES);
+    const int nk = kb + DIST;
+    if (nk < nkb) {  // table reads for the refill, hidden behind this k-block's work
+      ga.prep(kda, kbeg + nk * BK, kend);
+      gb.prep(kdb, kbeg + nk * BK, kend);
+    }
+    cp_async_wait<DIST - 1>();
+    uint8_t* st = stage(s);
+#ifndef GETT_TC_NO_SPLIT
+    ga.split(st, st + TILE_BYTES);
+    gb.split(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES);
+#endif
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     __syncthreads();
     if (tid == 0) {
@@ -239,24 +301,27 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint64_t al = sdesc(sb + TILE_BYTES + 256 * j);
         const uint64_t bh = sdesc(sb + 2 * TILE_BYTES + 256 * j);
         const uint64_t bl = sdesc(sb + 3 * TILE_BYTES + 256 * j);
-        mma_tf32(tmem, al, bh, (kb | j) != 0);
+        mma_tf32(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
+#ifndef GETT_TC_NO_MMA
+        mma_tf32(tmem, al, bh, 1);
         mma_tf32(tmem, ah, bl, 1);
-        mma_tf32(tmem, ah, bh, 1);
+#endif
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(bars + s))
-                   : "memory");
+      commit(smem_u32(bars + s));
     }
-    if (kb + 1 < nkb) {
-      ga.load(p.A, ktab_a, kbeg + (kb + 1) * BK, kend);
-      gb.load(p.B, ktab_b, kbeg + (kb + 1) * BK, kend);
+    // refill the stage k-block kb - SLACK used, once its MMAs are done
+    if (nk < nkb) {
+      const int ns = nk % STAGES;
+      const int prev = nk - STAGES;  // last k-block that used stage ns
+      if (prev >= 0) mbar_wait(smem_u32(bars + ns), (prev / STAGES) & 1);
+#ifndef GETT_TC_NO_LOAD
+      ga.issue(stage(ns), p.A);
+      gb.issue(stage(ns) + 2 * TILE_BYTES, p.B);
+#endif
     }
+    cp_async_commit();
   }
-  if (tid == 0) {
-    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                     smem_u32(bars + STAGES))
-                 : "memory");
-  }
+  if (tid == 0) commit(smem_u32(bars + STAGES));
   if (nkb > 0) mbar_wait(smem_u32(bars + STAGES), 0);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 
@@ -297,7 +362,7 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 
 template <bool AKF, bool BKF, bool AV, bool BV>
-cudaError_t launch4(const TiledParams<float>& p, const int64_t* ka, const int64_t* kb, cudaStream_t s) {
+cudaError_t launch4(const TiledParams<float>& p, cudaStream_t s) {
   auto k = sgett_tc_kernel<AKF, BKF, AV, BV>;
   static bool configured = false;
   if (!configured) {
@@ -305,30 +370,29 @@ cudaError_t launch4(const TiledParams<float>& p, const int64_t* ka, const int64_
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p, ka, kb);
+  k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
 template <bool AKF, bool BKF>
-cudaError_t launch2(const TiledParams<float>& p, const int64_t* ka, const int64_t* kb, bool av, bool bv,
-                    cudaStream_t s) {
-  if (av && bv) return launch4<AKF, BKF, true, true>(p, ka, kb, s);
-  if (av) return launch4<AKF, BKF, true, false>(p, ka, kb, s);
-  if (bv) return launch4<AKF, BKF, false, true>(p, ka, kb, s);
-  return launch4<AKF, BKF, false, false>(p, ka, kb, s);
+cudaError_t launch2(const TiledParams<float>& p, bool av, bool bv, cudaStream_t s) {
+  if (av && bv) return launch4<AKF, BKF, true, true>(p, s);
+  if (av) return launch4<AKF, BKF, true, false>(p, s);
+  if (bv) return launch4<AKF, BKF, false, true>(p, s);
+  return launch4<AKF, BKF, false, false>(p, s);
 }
 
 }  // namespace tc
 
-cudaError_t launch_sgett_tc(const TiledParams<float>& p, const int64_t* ktab_a, const int64_t* ktab_b,
-                            bool a_kf, bool b_kf, bool a_vec, bool b_vec, cudaStream_t s) {
+cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
+                            cudaStream_t s) {
   if (!a_kf) a_vec = false;  // vectors only along k
   if (!b_kf) b_vec = false;
   cudaError_t e;
-  if (a_kf && b_kf) e = tc::launch2<true, true>(p, ktab_a, ktab_b, a_vec, b_vec, s);
-  else if (a_kf) e = tc::launch2<true, false>(p, ktab_a, ktab_b, a_vec, b_vec, s);
-  else if (b_kf) e = tc::launch2<false, true>(p, ktab_a, ktab_b, a_vec, b_vec, s);
-  else e = tc::launch2<false, false>(p, ktab_a, ktab_b, a_vec, b_vec, s);
+  if (a_kf && b_kf) e = tc::launch2<true, true>(p, a_vec, b_vec, s);
+  else if (a_kf) e = tc::launch2<true, false>(p, a_vec, b_vec, s);
+  else if (b_kf) e = tc::launch2<false, true>(p, a_vec, b_vec, s);
+  else e = tc::launch2<false, false>(p, a_vec, b_vec, s);
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_splitk_reduce<float>(p, s);
 }

@@ -21,8 +21,19 @@ from paper_2410_06770_b200.workloads import CONFIGS  # noqa: E402
 def main():
     names = sys.argv[1:] or ["c1", "c2", "c3", "c4", "c5"]
     reps = int(os.environ.get("REPS", "7"))
+    from dataclasses import replace
+
+    extra = {
+        # contiguous fp32 GEMM 4096^3 (row-major A[m,k], B[k,n]) as a tensor-core sanity point
+        "sgemm": replace(CONFIGS["c2"], name="sgemm", dtype="s", ext_a=(4096, 4096),
+                         inc_a=(4096, 1), len_a=4096 * 4096, ext_b=(4096, 4096), inc_b=(4096, 1),
+                         len_b=4096 * 4096, inc_c=(4096, 1), len_c=4096 * 4096),
+        "dgemm": replace(CONFIGS["c2"], name="dgemm", ext_a=(4096, 4096), inc_a=(4096, 1),
+                         len_a=4096 * 4096, ext_b=(4096, 4096), inc_b=(4096, 1),
+                         len_b=4096 * 4096, inc_c=(4096, 1), len_c=4096 * 4096),
+    }
     for name in names:
-        w = CONFIGS[name]
+        w = extra[name] if name in extra else CONFIGS[name]
         a, b, c = w.buffers()
         ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
         fn = dgett_device if w.dtype == "d" else sgett_device
