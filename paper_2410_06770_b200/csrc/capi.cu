@@ -31,6 +31,7 @@ enum class Mode { Auto, Ref, Tiled, Serial, Ffma };
 std::mutex g_mu;
 Mode g_mode = Mode::Auto;
 int g_split = 0;
+bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
 thread_local std::string t_last_error;
@@ -44,6 +45,8 @@ void read_env() {
   if (k) gett_set_kernel(k);
   const char* s = std::getenv("GETT_SPLIT_K");
   if (s) g_split = std::atoi(s);
+  const char* wsv = std::getenv("GETT_DGETT_WS");
+  if (wsv) g_dgett_ws = std::atoi(wsv) != 0;
   const char* pl = std::getenv("GETT_PIPELINE");
   if (pl) g_pipeline_slabs = std::atoi(pl);
 }
@@ -370,6 +373,13 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
                        stream));
     g_launches += splits > 1 ? 2 : 1;
     t_last_kernel = splits > 1 ? "sgett_tc3xtf32_splitk" : "sgett_tc3xtf32";
+    return 0;
+  }
+  if (sizeof(T) == 8 && g_dgett_ws) {
+    CK(launch_dgett_ws(*reinterpret_cast<TiledParams<double>*>(&tp), a_kf, b_kf, a_vec, b_vec,
+                       stream));
+    g_launches += splits > 1 ? 2 : 1;
+    t_last_kernel = splits > 1 ? "dgett_dmma_ws_splitk" : "dgett_dmma_ws";
     return 0;
   }
   CK(launch_tiled<T>(tp, a_kf, b_kf, a_vec, b_vec, stream));

@@ -20,6 +20,10 @@ cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 template <typename T>
 cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s);
 
+// DGETT warp-specialised (producer warp + DMMA consumer warps), dgett_ws.cu
+cudaError_t launch_dgett_ws(const TiledParams<double>& p, bool a_kf, bool b_kf, bool a_vec,
+                            bool b_vec, cudaStream_t s);
+
 // SGETT 3xTF32 on tcgen05 (sgett_tc.cu)
 cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec,
                             bool b_vec, cudaStream_t s);
