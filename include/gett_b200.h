@@ -121,6 +121,45 @@ int gett_sgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, co
                       int64_t len_c, void* stream,
                       int32_t* err_codes, int64_t* err_info, int max_errs);
 
+/* ---- complex xGETT: cgett / zgett (kernel.py:187-200) ----
+ * Buffers are interleaved (re, im) pairs (numpy complex64 / complex128 memory);
+ * offsets, lengths and increments count complex elements.  Products follow the
+ * reference's complex multiply: re = a.re*b.re - a.im*b.im, im = a.re*b.im + a.im*b.re. */
+int gett_zgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+               int64_t offset_a, int64_t len_a,
+               int rank_b, const int64_t* ext_b, const int64_t* inc_b, const double* b,
+               int64_t offset_b, int64_t len_b,
+               int conts, const int64_t* cont_a, const int64_t* cont_b,
+               int perm_len, const int64_t* perm,
+               int inc_c_len, const int64_t* inc_c, double* c, int64_t offset_c, int64_t len_c,
+               int32_t* err_codes, int64_t* err_info, int max_errs);
+int gett_cgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+               int64_t offset_a, int64_t len_a,
+               int rank_b, const int64_t* ext_b, const int64_t* inc_b, const float* b,
+               int64_t offset_b, int64_t len_b,
+               int conts, const int64_t* cont_a, const int64_t* cont_b,
+               int perm_len, const int64_t* perm,
+               int inc_c_len, const int64_t* inc_c, float* c, int64_t offset_c, int64_t len_c,
+               int32_t* err_codes, int64_t* err_info, int max_errs);
+int gett_zgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+                      int64_t offset_a, int64_t len_a,
+                      int rank_b, const int64_t* ext_b, const int64_t* inc_b, const double* b,
+                      int64_t offset_b, int64_t len_b,
+                      int conts, const int64_t* cont_a, const int64_t* cont_b,
+                      int perm_len, const int64_t* perm,
+                      int inc_c_len, const int64_t* inc_c, double* c, int64_t offset_c,
+                      int64_t len_c, void* stream,
+                      int32_t* err_codes, int64_t* err_info, int max_errs);
+int gett_cgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+                      int64_t offset_a, int64_t len_a,
+                      int rank_b, const int64_t* ext_b, const int64_t* inc_b, const float* b,
+                      int64_t offset_b, int64_t len_b,
+                      int conts, const int64_t* cont_a, const int64_t* cont_b,
+                      int perm_len, const int64_t* perm,
+                      int inc_c_len, const int64_t* inc_c, float* c, int64_t offset_c,
+                      int64_t len_c, void* stream,
+                      int32_t* err_codes, int64_t* err_info, int max_errs);
+
 /* ---- planning helpers ---- */
 /* Validation only.  c_mode selects how the output view takes part:
  *   GETT_CHECK_C_NONE     plan.validate(a, b, spec, inc_c)           (plan.py:162-234)

@@ -135,6 +135,47 @@ static inline void advance(int64_t* coords, const int64_t* exts, int n) {
 DEFINE_LOOP(loop_d, double)
 DEFINE_LOOP(loop_s, float)
 
+/* Complex (cgett/zgett, kernel.py:187-200): buffers are interleaved (re, im)
+ * pairs.  The product is numba's complex multiply, unfused:
+ *   re = a.re*b.re - a.im*b.im,  im = a.re*b.im + a.im*b.re,
+ * then c = c + prod componentwise, in the element's real type. */
+#define DEFINE_LOOP_C(NAME, T)                                                                \
+  static void NAME(const oplan_t* p, T* c, const T* a, const T* b, int64_t lo, int64_t hi) { \
+    int64_t coord_free[MAXR];                                                                 \
+    int64_t coord_cont[MAXR];                                                                 \
+    int64_t rem = lo;                                                                         \
+    for (int j = 0; j < p->num_free; ++j) {                                                   \
+      coord_free[j] = rem % p->ext_free[j];                                                   \
+      rem /= p->ext_free[j];                                                                  \
+    }                                                                                         \
+    for (int64_t f = lo; f < hi; ++f) {                                                       \
+      int64_t idx_c = p->base_c, free_a = p->base_a, free_b = p->base_b;                      \
+      for (int j = 0; j < p->num_free; ++j) {                                                 \
+        idx_c += p->out_inc[j] * coord_free[j];                                               \
+        if (p->from_a[j]) free_a += p->src_inc[j] * coord_free[j];                            \
+        else free_b += p->src_inc[j] * coord_free[j];                                         \
+      }                                                                                       \
+      for (int k = 0; k < p->num_cont; ++k) coord_cont[k] = 0;                                \
+      for (int64_t q = 0; q < p->size_cont; ++q) {                                            \
+        int64_t idx_a = free_a, idx_b = free_b;                                               \
+        for (int k = 0; k < p->num_cont; ++k) {                                               \
+          idx_a += p->inc_ca[k] * coord_cont[k];                                              \
+          idx_b += p->inc_cb[k] * coord_cont[k];                                              \
+        }                                                                                     \
+        T ar = a[2 * idx_a], ai = a[2 * idx_a + 1], br = b[2 * idx_b], bi = b[2 * idx_b + 1];  \
+        T ac = ar * br, bd = ai * bi, ad = ar * bi, bc = ai * br;                             \
+        T pr = ac - bd, pi = ad + bc;                                                         \
+        c[2 * idx_c] = c[2 * idx_c] + pr;                                                     \
+        c[2 * idx_c + 1] = c[2 * idx_c + 1] + pi;                                             \
+        advance(coord_cont, p->ext_cont, p->num_cont);                                        \
+      }                                                                                       \
+      advance(coord_free, p->ext_free, p->num_free);                                          \
+    }                                                                                         \
+  }
+
+DEFINE_LOOP_C(loop_z, double)
+DEFINE_LOOP_C(loop_c, float)
+
 typedef struct {
   const oplan_t* p;
   void *c;
@@ -143,12 +184,15 @@ typedef struct {
   int is_double;
 } job_t;
 
+/* is_double doubles as the element kind: 0 = s, 1 = d, 2 = c, 3 = z */
 static void* run_job(void* arg) {
   job_t* j = (job_t*)arg;
-  if (j->is_double)
-    loop_d(j->p, (double*)j->c, (const double*)j->a, (const double*)j->b, j->lo, j->hi);
-  else
-    loop_s(j->p, (float*)j->c, (const float*)j->a, (const float*)j->b, j->lo, j->hi);
+  switch (j->is_double) {
+    case 1: loop_d(j->p, (double*)j->c, (const double*)j->a, (const double*)j->b, j->lo, j->hi); break;
+    case 0: loop_s(j->p, (float*)j->c, (const float*)j->a, (const float*)j->b, j->lo, j->hi); break;
+    case 3: loop_z(j->p, (double*)j->c, (const double*)j->a, (const double*)j->b, j->lo, j->hi); break;
+    default: loop_c(j->p, (float*)j->c, (const float*)j->a, (const float*)j->b, j->lo, j->hi); break;
+  }
   return NULL;
 }
 
@@ -202,5 +246,24 @@ int oracle_sgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const f
                  const int64_t* cont_b, const int64_t* perm, const int64_t* inc_c, float* c,
                  int64_t off_c, int64_t free_lo, int64_t free_hi, int nthreads) {
   return run(0, rank_a, ext_a, inc_a, a, off_a, rank_b, ext_b, inc_b, b, off_b, conts, cont_a,
+             cont_b, perm, inc_c, c, off_c, free_lo, free_hi, nthreads);
+}
+
+/* interleaved (re, im) buffers; offsets, lengths and increments in complex elements */
+int oracle_zgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+                 int64_t off_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,
+                 const double* b, int64_t off_b, int conts, const int64_t* cont_a,
+                 const int64_t* cont_b, const int64_t* perm, const int64_t* inc_c, double* c,
+                 int64_t off_c, int64_t free_lo, int64_t free_hi, int nthreads) {
+  return run(3, rank_a, ext_a, inc_a, a, off_a, rank_b, ext_b, inc_b, b, off_b, conts, cont_a,
+             cont_b, perm, inc_c, c, off_c, free_lo, free_hi, nthreads);
+}
+
+int oracle_cgett(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+                 int64_t off_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,
+                 const float* b, int64_t off_b, int conts, const int64_t* cont_a,
+                 const int64_t* cont_b, const int64_t* perm, const int64_t* inc_c, float* c,
+                 int64_t off_c, int64_t free_lo, int64_t free_hi, int nthreads) {
+  return run(2, rank_a, ext_a, inc_a, a, off_a, rank_b, ext_b, inc_b, b, off_b, conts, cont_a,
              cont_b, perm, inc_c, c, off_c, free_lo, free_hi, nthreads);
 }

@@ -45,7 +45,7 @@ def lib():
             build()
         L = ctypes.CDLL(path)
         i64p = ctypes.POINTER(ctypes.c_int64)
-        for name in ("oracle_dgett", "oracle_sgett"):
+        for name in ("oracle_dgett", "oracle_sgett", "oracle_zgett", "oracle_cgett"):
             f = getattr(L, name)
             f.restype = ctypes.c_int
             f.argtypes = [ctypes.c_int, i64p, i64p, ctypes.c_void_p, ctypes.c_int64,
@@ -84,6 +84,19 @@ def oracle_dgett(*args, **kw):
 def oracle_sgett(*args, **kw):
     """Reference-order float32 contraction into c (in place)."""
     _call("oracle_sgett", np.float32, *args, **kw)
+
+
+def oracle_zgett(*args, **kw):
+    """Reference-order complex128 contraction into c (kernel.py:195-200)."""
+    _call("oracle_zgett", np.complex128, *args, **kw)
+
+
+def oracle_cgett(*args, **kw):
+    """Reference-order complex64 contraction into c (kernel.py:187-192)."""
+    _call("oracle_cgett", np.complex64, *args, **kw)
+
+
+ORACLE = {"d": oracle_dgett, "s": oracle_sgett, "z": oracle_zgett, "c": oracle_cgett}
 
 
 # ---------------------------------------------------------------------------

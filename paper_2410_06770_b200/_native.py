@@ -15,6 +15,7 @@ LIB_PATH = os.environ.get("GETT_LIB_PATH") or os.path.join(_HERE, "libgett_b200.
 # every symbol include/gett_b200.h declares (checked by tests/test_abi.py)
 EXPORTS = (
     "gett_dgett", "gett_sgett", "gett_dgett_device", "gett_sgett_device",
+    "gett_zgett", "gett_cgett", "gett_zgett_device", "gett_cgett_device",
     "gett_validate", "gett_derive_output_extents",
     "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
     "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_last_kernel", "gett_last_error",
@@ -42,11 +43,11 @@ def _load():
                  ctypes.c_int, i64p, i64p, vp, ctypes.c_int64, ctypes.c_int64,
                  ctypes.c_int, i64p, i64p, ctypes.c_int, i64p,
                  ctypes.c_int, i64p, vp, ctypes.c_int64, ctypes.c_int64]
-    for name in ("gett_dgett", "gett_sgett"):
+    for name in ("gett_dgett", "gett_sgett", "gett_zgett", "gett_cgett"):
         f = getattr(lib, name)
         f.restype = ctypes.c_int
         f.argtypes = gett_args + [i32p, i64p, ctypes.c_int]
-    for name in ("gett_dgett_device", "gett_sgett_device"):
+    for name in ("gett_dgett_device", "gett_sgett_device", "gett_zgett_device", "gett_cgett_device"):
         f = getattr(lib, name)
         f.restype = ctypes.c_int
         f.argtypes = gett_args + [vp, i32p, i64p, ctypes.c_int]

@@ -277,12 +277,14 @@ bool vec_ok(const GroupDev& fast, bool fast_tab_div, const GroupDev& slow, bool 
 }
 
 template <typename T>
-int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, DevState& ds) {
+int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, DevState& ds,
+               int neg = 0, bool force_tiled = false) {
   const Plan& p = dp.plan;
   const T* A = p.swapped ? b : a;  // kernel roles A' / B'
   const T* B = p.swapped ? a : b;
   Mode mode = g_mode;
-  if (p.c_may_alias) mode = Mode::Serial;
+  if (force_tiled && mode != Mode::Ffma) mode = Mode::Tiled;  // complex real parts
+  else if (p.c_may_alias) mode = Mode::Serial;
   const int64_t M = p.gm.G, N = p.gn.G, K = p.gk.G;
   if (mode == Mode::Auto) {
     if (K <= 8 || M * N * K <= (1LL << 18)) mode = Mode::Ref;
@@ -347,6 +349,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   tp.k_chunk = (int32_t)kchunk;
   tp.splits = (int32_t)splits;
   tp.ws = nullptr;
+  tp.neg = neg;
   if (splits > 1) {
     int rc = ensure(ds.ws, (size_t)splits * M * N * sizeof(T));
     if (rc) return rc;
@@ -568,6 +571,127 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   return 0;
 }
 
+// Complex contraction on device buffers.  a2/b2/c2 point at each view's base
+// element as a real (re, im)-interleaved array.  ref/serial: complex kernels
+// in reference order; tiled: four real GETTs on the re/im sub-views (every
+// increment doubled; im = base + 1) through the tensor-core kernels:
+//   C.re += A.re B.re,  C.re -= A.im B.im,  C.im += A.re B.im,  C.im += A.im B.re
+template <typename R>
+int run_complex(DevPlan& cp, const View& va, const View& vb, const Spec& sp, const R* a2,
+                const R* b2, R* c2, cudaStream_t stream, DevState& ds) {
+  const Plan& p = cp.plan;
+  Mode mode = g_mode;
+  if (p.c_may_alias) mode = Mode::Serial;
+  const int64_t M = p.gm.G, N = p.gn.G, K = p.gk.G;
+  if (mode == Mode::Auto) mode = (K <= 8 || M * N * K <= (1LL << 18)) ? Mode::Ref : Mode::Tiled;
+  const bool z = sizeof(R) == 8;
+  if (mode == Mode::Serial) {
+    SerialParams<R> s;
+    s.A = a2; s.B = b2; s.C = c2;
+    s.num_free = cp.serial_nf;
+    s.num_cont = cp.serial_nc;
+    s.size_free = p.size_free;
+    s.size_cont = p.size_cont;
+    s.tab = cp.serial_tab;
+    CK(launch_serial_c<R>(s, stream));
+    ++g_launches;
+    t_last_kernel = z ? "zgett_serial" : "cgett_serial";
+    return 0;
+  }
+  if (mode == Mode::Ref) {
+    RefParams<R> rp;
+    rp.A = p.swapped ? b2 : a2;
+    rp.B = p.swapped ? a2 : b2;
+    rp.C = c2;
+    rp.gm = cp.gm; rp.gn = cp.gn;
+    rp.M = (int32_t)M; rp.N = (int32_t)N;
+    rp.k_inner = (int32_t)p.gk_ref.e_in;
+    rp.k_sa = p.gk_ref.s_in[0];
+    rp.k_sb = p.gk_ref.s_in[1];
+    rp.k_outer = (int32_t)p.gk_ref.T[0].size();
+    rp.kta = cp.kref_a;
+    rp.ktb = cp.kref_b;
+    CK(launch_ref_c<R>(rp, stream));
+    ++g_launches;
+    t_last_kernel = z ? "zgett_ref_order" : "cgett_ref_order";
+    return 0;
+  }
+  // real sub-views: same extents, doubled increments
+  std::vector<int64_t> ia(va.rank), ib(vb.rank), ic(sp.inc_c_len);
+  for (int d = 0; d < va.rank; ++d) ia[d] = 2 * va.inc[d];
+  for (int d = 0; d < vb.rank; ++d) ib[d] = 2 * vb.inc[d];
+  for (int d = 0; d < sp.inc_c_len; ++d) ic[d] = 2 * sp.inc_c[d];
+  View ra{va.rank, va.ext, ia.data(), 0, 2 * va.len};
+  View rb{vb.rank, vb.ext, ib.data(), 0, 2 * vb.len};
+  Spec rs = sp;
+  rs.inc_c = ic.data();
+  std::shared_ptr<DevPlan> rp;
+  int rc = get_plan(z ? 'd' : 's', ra, rb, rs, 0, 0, &rp);
+  if (rc) return rc;
+  if ((rc = run_device<R>(*rp, a2, b2, c2, stream, ds, 0, true))) return rc;
+  if ((rc = run_device<R>(*rp, a2 + 1, b2 + 1, c2, stream, ds, 1, true))) return rc;
+  if ((rc = run_device<R>(*rp, a2, b2 + 1, c2 + 1, stream, ds, 0, true))) return rc;
+  if ((rc = run_device<R>(*rp, a2 + 1, b2, c2 + 1, stream, ds, 0, true))) return rc;
+  t_last_kernel = z ? "zgett_4x_dmma" : "cgett_4x_tc3xtf32";
+  return 0;
+}
+
+// cgett / zgett: pointers are interleaved (re, im) reals; offsets, lengths and
+// increments count complex elements (the reference's complex64/128 buffers).
+template <typename R>
+int gett_impl_complex(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
+                      const R* a, int64_t off_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+                      const int64_t* inc_b, const R* b, int64_t off_b, int64_t len_b, int conts,
+                      const int64_t* cont_a, const int64_t* cont_b, int perm_len,
+                      const int64_t* perm, int inc_c_len, const int64_t* inc_c, R* c,
+                      int64_t off_c, int64_t len_c, cudaStream_t stream, int32_t* codes,
+                      int64_t* info, int max_errs) {
+  if (rank_a < 0 || rank_b < 0 || conts < 0 || perm_len < 0 || inc_c_len < 0 || off_a < 0 ||
+      off_b < 0 || off_c < 0 || len_a < 0 || len_b < 0 || len_c < 0) {
+    t_last_error = "negative rank/count/offset/length";
+    return GETT_E_INVALID_ARG;
+  }
+  std::lock_guard<std::mutex> lock(g_mu);
+  read_env();
+  t_last_kernel = "none";
+  View va{rank_a, ext_a, inc_a, off_a, len_a};
+  View vb{rank_b, ext_b, inc_b, off_b, len_b};
+  Spec sp{conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c};
+  View vc{0, nullptr, nullptr, off_c, len_c};
+  std::vector<Error> errs = validate(va, vb, sp, CMode::Derived, vc);
+  if (!errs.empty()) return fill_errors(errs, codes, info, max_errs);
+  for (int d = 0; d < rank_a; ++d)
+    if (ext_a[d] == 0) return 0;
+  for (int d = 0; d < rank_b; ++d)
+    if (ext_b[d] == 0) return 0;
+  std::shared_ptr<DevPlan> cp;
+  int rc = get_plan(sizeof(R) == 8 ? 'z' : 'c', va, vb, sp, off_c, len_c, &cp);
+  if (rc) return rc;
+  const Plan& p = cp->plan;
+  int dev;
+  DevState& ds = dev_state(&dev);
+  if (!host) return run_complex<R>(*cp, va, vb, sp, a + 2 * off_a, b + 2 * off_b, c + 2 * off_c, stream, ds);
+  const int64_t lo_a = off_a + p.fp_lo[0], lo_b = off_b + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1) * 2;
+  const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1) * 2;
+  const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1) * 2;
+  if ((rc = ensure(ds.a, na * sizeof(R))) || (rc = ensure(ds.b, nb * sizeof(R))) ||
+      (rc = ensure(ds.c, nc * sizeof(R))))
+    return rc;
+  R* da = (R*)ds.a.p;
+  R* db = (R*)ds.b.p;
+  R* dc = (R*)ds.c.p;
+  cudaStream_t s = ds.stream;
+  CK(cudaMemcpyAsync(da, a + 2 * lo_a, na * sizeof(R), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(db, b + 2 * lo_b, nb * sizeof(R), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc, c + 2 * lo_c, nc * sizeof(R), cudaMemcpyHostToDevice, s));
+  rc = run_complex<R>(*cp, va, vb, sp, da - 2 * p.fp_lo[0], db - 2 * p.fp_lo[1], dc - 2 * p.fp_lo[2], s, ds);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c + 2 * lo_c, dc, nc * sizeof(R), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
 template <typename T>
 int zero_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64_t off,
               int64_t len, T* buf, cudaStream_t stream) {
@@ -661,6 +785,25 @@ int gett_sgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, co
                           offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c,
                           c, offset_c, len_c, (cudaStream_t)stream, err_codes, err_info, max_errs);
 }
+
+#define GETT_COMPLEX_ENTRY(NAME, R, HOST, STREAM_PARAM, STREAM_ARG)                              \
+  int NAME(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const R* a, int64_t offset_a,   \
+           int64_t len_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b, const R* b,      \
+           int64_t offset_b, int64_t len_b, int conts, const int64_t* cont_a,                      \
+           const int64_t* cont_b, int perm_len, const int64_t* perm, int inc_c_len,                \
+           const int64_t* inc_c, R* c, int64_t offset_c, int64_t len_c STREAM_PARAM,              \
+           int32_t* err_codes, int64_t* err_info, int max_errs) {                                  \
+    return gett_impl_complex<R>(HOST, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b,     \
+                                inc_b, b, offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, \
+                                inc_c_len, inc_c, c, offset_c, len_c, STREAM_ARG, err_codes,      \
+                                err_info, max_errs);                                              \
+  }
+#define GETT_NO_STREAM_PARAM
+#define GETT_STREAM_PARAM , void* stream
+GETT_COMPLEX_ENTRY(gett_zgett, double, true, GETT_NO_STREAM_PARAM, nullptr)
+GETT_COMPLEX_ENTRY(gett_cgett, float, true, GETT_NO_STREAM_PARAM, nullptr)
+GETT_COMPLEX_ENTRY(gett_zgett_device, double, false, GETT_STREAM_PARAM, (cudaStream_t)stream)
+GETT_COMPLEX_ENTRY(gett_cgett_device, float, false, GETT_STREAM_PARAM, (cudaStream_t)stream)
 
 int gett_validate(int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
                   int64_t len_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,

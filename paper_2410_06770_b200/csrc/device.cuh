@@ -69,7 +69,14 @@ struct TiledParams {
   int32_t splits;   // split-K factor (1 = fused C += acc epilogue)
   int32_t k_chunk;  // K per split, a multiple of the k-block
   T* ws;            // [splits][M][N] partial tiles when splits > 1
+  int32_t neg = 0;  // epilogue C += -acc (the a.im*b.im term of a complex contraction)
 };
+
+// the fused epilogue's update: C + acc, or C + (-acc) == C - acc for neg
+template <typename T>
+__device__ __forceinline__ T epi(T c, T acc, int32_t neg) {
+  return neg ? c - acc : c + acc;
+}
 
 // Reference-order kernel parameters: one thread per output, K in the
 // reference order (pair 0 fastest) with unfused multiply then add.

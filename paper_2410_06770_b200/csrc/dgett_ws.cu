@@ -258,7 +258,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int j = 0; j < NJ; ++j)
 #pragma unroll
         for (int e = 0; e < 2; ++e)
-          if (cok[j * 2 + e]) p.C[ro + coff[j * 2 + e]] = cv[j][e] + acc[i][j][e];
+          if (cok[j * 2 + e]) p.C[ro + coff[j * 2 + e]] = epi(cv[j][e], acc[i][j][e], p.neg);
     } else {
       double* w = p.ws + ((int64_t)split * p.M + m) * p.N;
 #pragma unroll

@@ -323,7 +323,7 @@ __global__ void __launch_bounds__(Cfg<T>::THREADS, 1) gett_tiled_kernel(const __
 #pragma unroll
             for (int e = 0; e < 2; ++e)
               if (rok[i0 + i] && cok[j * 2 + e])
-                p.C[ro[i0 + i] + coff[j * 2 + e]] = cv[i][j][e] + acc[i0 + i][j][e];
+                p.C[ro[i0 + i] + coff[j * 2 + e]] = epi(cv[i][j][e], acc[i0 + i][j][e], p.neg);
       }
     }
 #pragma unroll
@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(Cfg<T>::THREADS, 1) gett_tiled_kernel(const __
         for (int j = 0; j < 8; ++j)
           if (cok[j]) {
             float* c = p.C + ro + coff[j];
-            *c = *c + acc[i][j];
+            *c = epi(*c, acc[i][j], p.neg);
           }
       } else {
         float* w = p.ws + ((int64_t)split * p.M + m) * p.N;
@@ -482,6 +482,87 @@ __global__ void gett_serial_kernel(const __grid_constant__ SerialParams<T> p) {
   }
 }
 
+// Complex (cgett / zgett, kernel.py:187-200): R is the real type, buffers are
+// interleaved (re, im) pairs and all offsets are in complex elements.  The
+// product is numba's complex multiply, unfused: re = ar*br - ai*bi,
+// im = ar*bi + ai*br, then c = c + prod componentwise, K in reference order.
+template <typename R>
+__device__ __forceinline__ void cmac(R& cr, R& ci, const R* a, const R* b) {
+  const R ar = __ldg(a), ai = __ldg(a + 1), br = __ldg(b), bi = __ldg(b + 1);
+  const R pr = add_rn(mul_rn(ar, br), -mul_rn(ai, bi));
+  const R pi = add_rn(mul_rn(ar, bi), mul_rn(ai, br));
+  cr = add_rn(cr, pr);
+  ci = add_rn(ci, pi);
+}
+
+template <typename R>
+__global__ void __launch_bounds__(256) gett_ref_kernel_c(const __grid_constant__ RefParams<R> p) {
+  int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (int64_t)p.M * p.N) return;
+  int32_t n = (int32_t)(idx % p.N);
+  int32_t m = (int32_t)(idx / p.N);
+  int64_t fa, ca, fb, cb;
+  p.gm.off2(m, fa, ca);
+  p.gn.off2(n, fb, cb);
+  R* c = p.C + 2 * (ca + cb);
+  R cr = c[0], ci = c[1];
+  const R* A = p.A + 2 * fa;
+  const R* B = p.B + 2 * fb;
+  for (int32_t q = 0; q < p.k_outer; ++q) {
+    const R* a = A + 2 * __ldg(p.kta + q);
+    const R* b = B + 2 * __ldg(p.ktb + q);
+    for (int32_t r = 0; r < p.k_inner; ++r) cmac(cr, ci, a + 2 * r * p.k_sa, b + 2 * r * p.k_sb);
+  }
+  c[0] = cr;
+  c[1] = ci;
+}
+
+template <typename R>
+__global__ void gett_serial_kernel_c(const __grid_constant__ SerialParams<R> p) {
+  if (blockIdx.x != 0 || threadIdx.x != 0) return;
+  const int nf = p.num_free, nc = p.num_cont;
+  const int64_t* out_inc = p.tab;
+  const int64_t* src_inc = p.tab + nf;
+  const int64_t* from_a = p.tab + 2 * nf;
+  const int64_t* ext_free = p.tab + 3 * nf;
+  const int64_t* inc_ca = p.tab + 4 * nf;
+  const int64_t* inc_cb = p.tab + 4 * nf + nc;
+  const int64_t* ext_cont = p.tab + 4 * nf + 2 * nc;
+  int64_t cf[64], cc[64];
+  for (int j = 0; j < nf; ++j) cf[j] = 0;
+  for (int64_t f = 0; f < p.size_free; ++f) {
+    int64_t ic = 0, ia0 = 0, ib0 = 0;
+    for (int j = 0; j < nf; ++j) {
+      ic += out_inc[j] * cf[j];
+      if (from_a[j]) ia0 += src_inc[j] * cf[j];
+      else ib0 += src_inc[j] * cf[j];
+    }
+    for (int k = 0; k < nc; ++k) cc[k] = 0;
+    for (int64_t q = 0; q < p.size_cont; ++q) {
+      int64_t ia = ia0, ib = ib0;
+      for (int k = 0; k < nc; ++k) {
+        ia += inc_ca[k] * cc[k];
+        ib += inc_cb[k] * cc[k];
+      }
+      volatile R* c = p.C + 2 * ic;
+      R cr = c[0], ci = c[1];
+      const R ar = p.A[2 * ia], ai = p.A[2 * ia + 1], br = p.B[2 * ib], bi = p.B[2 * ib + 1];
+      cr = add_rn(cr, add_rn(mul_rn(ar, br), -mul_rn(ai, bi)));
+      ci = add_rn(ci, add_rn(mul_rn(ar, bi), mul_rn(ai, br)));
+      c[0] = cr;
+      c[1] = ci;
+      for (int k = 0; k < nc; ++k) {
+        cc[k] = (cc[k] + 1) % ext_cont[k];
+        if (cc[k] != 0) break;
+      }
+    }
+    for (int j = 0; j < nf; ++j) {
+      cf[j] = (cf[j] + 1) % ext_free[j];
+      if (cf[j] != 0) break;
+    }
+  }
+}
+
 // C[m, n] += sum_s ws[s][m][n], s ascending, sum started at -0.0
 template <typename T>
 __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_constant__ TiledParams<T> p) {
@@ -493,7 +574,7 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
   T s = T(-0.0);
   for (int sp = 0; sp < p.splits; ++sp) s = s + p.ws[sp * mn + idx];
   T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
-  *c = *c + s;
+  *c = epi(*c, s, p.neg);
 }
 
 template <typename T>
@@ -566,6 +647,23 @@ cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s) {
   gett_serial_kernel<T><<<1, 1, 0, s>>>(p);
   return cudaGetLastError();
 }
+
+template <typename R>
+cudaError_t launch_ref_c(const RefParams<R>& p, cudaStream_t s) {
+  int64_t n = (int64_t)p.M * p.N;
+  gett_ref_kernel_c<R><<<(unsigned)((n + 255) / 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename R>
+cudaError_t launch_serial_c(const SerialParams<R>& p, cudaStream_t s) {
+  gett_serial_kernel_c<R><<<1, 1, 0, s>>>(p);
+  return cudaGetLastError();
+}
+template cudaError_t launch_ref_c<double>(const RefParams<double>&, cudaStream_t);
+template cudaError_t launch_ref_c<float>(const RefParams<float>&, cudaStream_t);
+template cudaError_t launch_serial_c<double>(const SerialParams<double>&, cudaStream_t);
+template cudaError_t launch_serial_c<float>(const SerialParams<float>&, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s) {

@@ -20,6 +20,12 @@ cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 template <typename T>
 cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s);
 
+// complex (interleaved re/im, offsets in complex elements): R = float / double
+template <typename R>
+cudaError_t launch_ref_c(const RefParams<R>& p, cudaStream_t s);
+template <typename R>
+cudaError_t launch_serial_c(const SerialParams<R>& p, cudaStream_t s);
+
 // DGETT warp-specialised (producer warp + DMMA consumer warps), dgett_ws.cu
 cudaError_t launch_dgett_ws(const TiledParams<double>& p, bool a_kf, bool b_kf, bool a_vec,
                             bool b_vec, cudaStream_t s);

@@ -349,7 +349,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       const float acc = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
       if (p.splits == 1) {
         float* c = p.C + ro + p.gn.off(1, n);
-        *c = *c + acc;
+        *c = epi(*c, acc, p.neg);
       } else {
         wrow[n] = acc;
       }

@@ -16,7 +16,7 @@ from . import _native
 from .layout import TensorView
 from .plan import ContractionSpec, decode_errors, error_capacity
 
-_DT = {"s": "float32", "d": "float64"}
+_DT = {"s": "float32", "d": "float64", "c": "complex64", "z": "complex128"}
 
 
 def _buf(t, name, prefix):
@@ -52,7 +52,7 @@ def _gett_device(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts
     info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
     if stream is None:
         stream = torch.cuda.current_stream(c.device)
-    fn = _native.LIB.gett_dgett_device if prefix == "d" else _native.LIB.gett_sgett_device
+    fn = getattr(_native.LIB, f"gett_{prefix}gett_device")
     with torch.cuda.device(c.device):
         rc = fn(a_view.rank, _native.i64(a_view.extents), _native.i64(a_view.increments),
                 a.data_ptr(), a_view.base_offset, a_view.buffer_len,
@@ -92,3 +92,13 @@ def zero_view_device(view: TensorView, buf, stream=None) -> None:
         _native.check(fn(view.rank, _native.i64(view.extents), _native.i64(view.increments),
                          view.base_offset, buf.shape[0], buf.data_ptr(),
                          ctypes.c_void_p(stream.cuda_stream)), "zero_view_device")
+
+
+def cgett_device(*args, **kw):
+    """complex64 xGETT on CUDA tensors (stream-ordered); see kernel.cgett."""
+    return _gett_device("c", *args, **kw)
+
+
+def zgett_device(*args, **kw):
+    """complex128 xGETT on CUDA tensors (stream-ordered); see kernel.zgett."""
+    return _gett_device("z", *args, **kw)

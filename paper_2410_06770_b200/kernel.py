@@ -27,8 +27,10 @@ from .plan import ContractionSpec, decode_errors, error_capacity
 _PREFIX_DTYPE = {
     "s": np.dtype(np.float32),
     "d": np.dtype(np.float64),
+    "c": np.dtype(np.complex64),
+    "z": np.dtype(np.complex128),
 }
-_ENTRY = {"s": "gett_sgett", "d": "gett_dgett"}
+_ENTRY = {"s": "gett_sgett", "d": "gett_dgett", "c": "gett_cgett", "z": "gett_zgett"}
 
 
 def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm,
@@ -103,6 +105,22 @@ def dgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
                  conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
 
 
+def cgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+          conts, cont_a, cont_b, perm, inc_c, c,
+          offset_a=0, offset_b=0, offset_c=0):
+    """64-bit complex (2x32-bit) contraction; see dgett for the parameter contract."""
+    return _gett("c", rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
+
+
+def zgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+          conts, cont_a, cont_b, perm, inc_c, c,
+          offset_a=0, offset_b=0, offset_c=0):
+    """128-bit complex (2x64-bit) contraction; see dgett for the parameter contract."""
+    return _gett("z", rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
+                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
+
+
 def zero_view(view: TensorView, buf: np.ndarray) -> None:
     """Set every element addressed by the view to zero, touching nothing else
     (kernel.py:111-113), on the GPU."""
@@ -121,15 +139,24 @@ def zero_view(view: TensorView, buf: np.ndarray) -> None:
     if not buf.flags.writeable:
         raise ValueError("assignment destination is read-only")
     w = buf if buf.flags.c_contiguous else np.ascontiguousarray(buf)
-    f = _native.LIB.gett_zero_view_d if prefix == "d" else _native.LIB.gett_zero_view_s
-    _native.check(f(view.rank, _native.i64(view.extents), _native.i64(view.increments),
-                    view.base_offset, w.shape[0], w.ctypes.data), "zero_view")
+    f = _native.LIB.gett_zero_view_d if prefix in "dz" else _native.LIB.gett_zero_view_s
+    if prefix in "cz":
+        # complex: the real and imaginary parts are two real views with
+        # doubled increments over the interleaved (re, im) buffer
+        inc2 = [2 * i for i in view.increments]
+        for part in (0, 1):
+            _native.check(f(view.rank, _native.i64(view.extents), _native.i64(inc2),
+                            2 * view.base_offset + part, 2 * w.shape[0], w.ctypes.data),
+                          "zero_view")
+    else:
+        _native.check(f(view.rank, _native.i64(view.extents), _native.i64(view.increments),
+                        view.base_offset, w.shape[0], w.ctypes.data), "zero_view")
     if w is not buf:
         buf[...] = w
 
 
 def dtype_prefix(dtype) -> str:
-    """The s/d tag for a numpy element type."""
+    """The s/d/c/z tag for a numpy element type (kernel.py:203-209)."""
     dtype = np.dtype(dtype)
     for prefix, dt in _PREFIX_DTYPE.items():
         if dt == dtype:

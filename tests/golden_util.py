@@ -28,15 +28,23 @@ class SuiteCase:
 
     @property
     def np_dtype(self):
-        return np.float64 if self.dtype == "d" else np.float32
+        return {"d": np.float64, "s": np.float32, "z": np.complex128, "c": np.complex64}[self.dtype]
 
     def buffers(self):
         rng = np.random.default_rng(self.data_seed)
         dt = self.np_dtype
-        if self.data == "int":
-            draw = lambda n: rng.integers(-4, 5, n).astype(dt)
-        else:
-            draw = lambda n: rng.uniform(-1.0, 1.0, n).astype(dt)
+
+        def draw(n):
+            if self.dtype in "cz":
+                if self.data == "int":
+                    re, im = rng.integers(-4, 5, n), rng.integers(-4, 5, n)
+                else:
+                    re, im = rng.uniform(-1.0, 1.0, n), rng.uniform(-1.0, 1.0, n)
+                return (re + 1j * im).astype(dt)
+            if self.data == "int":
+                return rng.integers(-4, 5, n).astype(dt)
+            return rng.uniform(-1.0, 1.0, n).astype(dt)
+
         return draw(self.a["len"]), draw(self.b["len"]), draw(self.c["len"])
 
     def args(self, a, b, c):
@@ -61,7 +69,10 @@ def load_suite():
     out = []
     for d in cases:
         arr = z[d["store"]][d["out_start"]:d["out_start"] + d["out_len"]]
-        want = arr.astype(np.float64 if d["dtype"] == "d" else np.float32)
+        real = {"d": np.float64, "s": np.float32, "z": np.float64, "c": np.float32}[d["dtype"]]
+        want = np.ascontiguousarray(arr.astype(real))
+        if d["dtype"] in "cz":
+            want = want.view(np.complex128 if d["dtype"] == "z" else np.complex64)
         out.append(SuiteCase(d, want))
     return out
 

@@ -20,7 +20,8 @@ from tests.golden_util import (load_configs, load_suite, load_zero_view, sliced_
 pytestmark = pytest.mark.gpu
 
 SUITE = load_suite()
-TOL_K = {"d": 1e-12, "s": 1e-5}
+TOL_K = {"d": 1e-12, "s": 1e-5, "z": 1e-12, "c": 1e-5}
+ENTRY = {"d": g.dgett, "s": g.sgett, "z": g.zgett, "c": g.cgett}
 
 
 def run(entry, pos, kw):
@@ -67,6 +68,41 @@ def test_known_answers(mode, kernel_mode):
     cs = np.zeros(1, np.float32)
     assert g.sgett(1, (3,), (1,), np.array([1, 2, 3], np.float32), 1, (3,), (1,), np.array([4, 5, 6], np.float32),
                    1, (0,), (0,), (), (), cs) == [] and cs[0] == np.float32(32)
+    # complex known answers (test_kernel.py:184-198)
+    cz = np.zeros(1, np.complex128)
+    assert g.zgett(1, (1,), (1,), np.array([1 + 2j]), 1, (1,), (1,), np.array([3 + 4j]),
+                   1, (0,), (0,), (), (), cz) == [] and cz[0] == (-5 + 10j)
+    cc = np.zeros(1, np.complex64)
+    assert g.cgett(1, (2,), (1,), np.array([2 - 1j, 1 + 1j], np.complex64), 1, (2,), (1,),
+                   np.array([1 + 1j, 3 + 0j], np.complex64), 1, (0,), (0,), (), (), cc) == []
+    assert cc[0] == np.complex64(6 + 4j)
+    # zero_view on complex buffers zeroes both parts of the addressed elements only
+    zb = np.arange(8, dtype=np.complex128) * (1 + 1j)
+    g.zero_view(g.TensorView(2, (2, 2), (1, 4), 1, 8), zb)
+    assert [zb[i] == 0 for i in range(8)] == [False, True, True, False, False, True, True, False]
+
+
+@pytest.mark.parametrize("mode", ["ref", "tiled"])
+def test_complex_gemm_against_numpy(mode, kernel_mode):
+    """zgett/cgett at tiled sizes: integer data exact, uniform within tolerance."""
+    kernel_mode(mode)
+    rng = np.random.default_rng(9)
+    for dt, tol in ((np.complex128, 1e-12), (np.complex64, 1e-5)):
+        for m, k, n in [(3, 5, 2), (130, 70, 129), (256, 600, 64)]:
+            for data in ("int", "uniform"):
+                draw = (lambda s: rng.integers(-4, 5, s) + 1j * rng.integers(-4, 5, s)) if data == "int" \
+                    else (lambda s: rng.uniform(-1, 1, s) + 1j * rng.uniform(-1, 1, s))
+                A, B, C = draw((m, k)).astype(dt), draw((k, n)).astype(dt), draw((m, n)).astype(dt)
+                c = C.ravel(order="F").copy()
+                entry = g.zgett if dt == np.complex128 else g.cgett
+                assert entry(2, (m, k), (1, m), A.ravel(order="F"), 2, (k, n), (1, k), B.ravel(order="F"),
+                             1, (1,), (0,), (0, 1), (1, m), c) == []
+                want = C.astype(np.complex128) + A.astype(np.complex128) @ B.astype(np.complex128)
+                got = c.reshape((m, n), order="F")
+                if data == "int":
+                    assert np.array_equal(got, want.astype(dt)), (dt, m, k, n, mode)
+                else:
+                    assert np.max(np.abs(got - want)) <= tol * k * 2, (dt, m, k, n, mode)
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -108,7 +144,7 @@ def _check_suite_case(case, mode, kernel_mode):
     a, b, c = case.buffers()
     before = c.copy()
     pos, kw = case.args(a, b, c)
-    run(g.dgett if case.dtype == "d" else g.sgett, pos, kw)
+    run(ENTRY[case.dtype], pos, kw)
     offs = case.c_offsets()
     got = c[offs]
     mask = np.ones(len(c), bool)
@@ -167,7 +203,7 @@ def test_commutativity_bit_identical(kernel_mode):
         a, b, c = case.buffers()
         pos, kw = case.args(a, b, c.copy())
         c1 = pos[13]
-        run(g.dgett if case.dtype == "d" else g.sgett, pos, kw)
+        run(ENTRY[case.dtype], pos, kw)
         fa = case.a["rank"] - case.conts
         perm = tuple(case.perm[fa:]) + tuple(case.perm[:fa])
         c2 = c.copy()
@@ -175,7 +211,7 @@ def test_commutativity_bit_identical(kernel_mode):
                 case.a["rank"], tuple(case.a["ext"]), tuple(case.a["inc"]), a,
                 case.conts, tuple(case.cont_b), tuple(case.cont_a), perm, tuple(case.c["inc"]), c2)
         kw2 = dict(offset_a=case.b["off"], offset_b=case.a["off"], offset_c=case.c["off"])
-        run(g.dgett if case.dtype == "d" else g.sgett, pos2, kw2)
+        run(ENTRY[case.dtype], pos2, kw2)
         assert c1.tobytes() == c2.tobytes(), case.id
 
 
@@ -193,7 +229,7 @@ def test_config_slices_ref_bitwise(key, kernel_mode):
     w = sliced_workload(meta)
     a, b, c = w.buffers()
     pos, kw = w.args(a, b, c)
-    run(g.dgett if w.dtype == "d" else g.sgett, pos, kw)
+    run(ENTRY[w.dtype], pos, kw)
     assert c[view_offsets(w.ext_c, w.inc_c, w.off_c)].tobytes() == want.tobytes()
 
 
@@ -204,7 +240,7 @@ def test_config_slices_tiled(key, kernel_mode):
     w = sliced_workload(meta)
     a, b, c = w.buffers()
     pos, kw = w.args(a, b, c)
-    run(g.dgett if w.dtype == "d" else g.sgett, pos, kw)
+    run(ENTRY[w.dtype], pos, kw)
     got = c[view_offsets(w.ext_c, w.inc_c, w.off_c)]
     assert k_norm_err(got, want, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K[w.dtype]
 
@@ -220,7 +256,7 @@ def test_full_config(name, kernel_mode):
     a, b, c = w.buffers()
     c0 = c.copy()
     pos, kw = w.args(a, b, c)
-    run(g.dgett if w.dtype == "d" else g.sgett, pos, kw)
+    run(ENTRY[w.dtype], pos, kw)
     offs = view_offsets(w.ext_c, w.inc_c, w.off_c)
     mask = np.ones(len(c), bool)
     mask[offs] = False

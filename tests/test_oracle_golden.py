@@ -16,7 +16,7 @@ SUITE = load_suite()
 def test_suite_covers_every_category():
     cats = {c.category for c in SUITE}
     assert len(cats) == 23
-    assert {c.dtype for c in SUITE} == {"d", "s"}
+    assert {c.dtype for c in SUITE} == {"d", "s", "c", "z"}
 
 
 @pytest.mark.parametrize("case", SUITE, ids=lambda c: c.id)
@@ -24,7 +24,7 @@ def test_oracle_matches_reference_bitwise(case):
     a, b, c = case.buffers()
     before = c.copy()
     pos, kw = case.args(a, b, c)
-    (oracle.oracle_dgett if case.dtype == "d" else oracle.oracle_sgett)(*pos, **kw)
+    oracle.ORACLE[case.dtype](*pos, **kw)
     offs = case.c_offsets()
     assert c[offs].tobytes() == case.want.tobytes()
     mask = np.ones(len(c), bool)
