@@ -6,8 +6,8 @@ as gett.kernel.dgett / sgett / zero_view.
 REF_PKG_DIR defaults to /root/reference/pkg, else baseline/_ref/pkg (a
 git-ignored copy that travels to the GPU box with gpurun).  The reference's
 tests are copied to a temp dir with a conftest.py that installs the backend
-before any test module imports gett.kernel's names.  cgett/zgett stay the
-reference's own (complex is not on this round's path).  Verification tool only:
+before any test module imports gett.kernel's names (all of s/d/c/z gett and
+zero_view are the GPU backend's).  Verification tool only:
 not part of the product, the GPU test suite or bench.py.
 """
 import os
@@ -35,12 +35,10 @@ def _adapt(entry):
 
 _k.dgett = _adapt(_b.dgett)
 _k.sgett = _adapt(_b.sgett)
-
-_ref_zero_view = _k.zero_view
+_k.cgett = _adapt(_b.cgett)
+_k.zgett = _adapt(_b.zgett)
 
 def _zero_view(view, buf):
-    if buf.dtype.kind == "c":  # complex stays on the reference (not this round's path)
-        return _ref_zero_view(view, buf)
     _b.zero_view(_b.TensorView(view.rank, view.extents, view.increments, view.base_offset,
                                view.buffer_len), buf)
 _k.zero_view = _zero_view
