@@ -1,22 +1,26 @@
-// SGETT on the 5th-generation tensor cores: 3xTF32 with tcgen05.mma + TMEM.
+// SGETT on the 5th-generation tensor cores: 3xTF32 with tcgen05.mma + TMEM,
+// warp-specialised.
 //
 // Replaces the fp32 hot loop (kernel.py:48-78 for sgett) for contractions big
-// enough to tile.  Per 128x128 output tile and k-block of 16:
-//   * 128 threads gather the A' (M x K) and B' (N x K) tiles straight from the
-//     strided views with cp.async (row offsets from the planner's groups, k
-//     offsets from a precomputed per-k table; 16-byte copies where the
-//     planner proved 4-k contiguity) into the UMMA K-major no-swizzle layout
-//     (8-row x 16-byte core matrices, LBO 128 B between k-chunks, SBO 512 B
-//     between 8-row groups).  GETT_TC_STAGES-1 k-blocks are in flight, which
-//     is what a latency-bound strided gather needs (SGETT c5 is HBM-bound);
-//   * when a k-block lands, each thread splits its own elements in place:
-//     hi = rna_tf32(x) (overwrites x), lo = x - hi (exact in fp32) into the lo
-//     tile, then fence.proxy.async publishes both to the tensor core;
-//   * one thread issues, per UMMA_K = 8 step, tcgen05.mma.kind::tf32 for
-//     lo*hi, hi*lo, hi*hi into one fp32 accumulator in TMEM (128 lanes x 128
-//     columns); tcgen05.commit frees the smem stage through an mbarrier;
-//   * epilogue: tcgen05.ld 32x32b (thread = row), C += acc through the C
-//     offset tables, or the split-K partial into the workspace.
+// enough to tile.  Per 128x128 output tile, k-blocks of 16, STAGES-deep ring:
+//   * producer warpgroup (warps 0-3): gathers the A' (M x K) and B' (N x K)
+//     k-block straight from the strided views with cp.async (row offsets
+//     decoded once per tile, k offsets stepped through the K group's outer
+//     table staged in smem; 16-byte copies where the planner proved 4-k
+//     contiguity) into the UMMA K-major no-swizzle layout (8-row x 16-byte
+//     core matrices, LBO 128 B between k-chunks, SBO 512 B between 8-row
+//     groups); completion is tracked per stage by cp.async.mbarrier.arrive,
+//     so up to STAGES k-blocks are in flight without blocking anyone;
+//   * split warpgroup (warps 4-7): when a stage lands, splits every value in
+//     place into hi = rna_tf32(x) and lo = x - hi (exact in fp32) into the
+//     stage's lo tile, fence.proxy.async, arrive;
+//   * MMA warp (warp 8): one elected thread issues, per UMMA_K = 8 step,
+//     tcgen05.mma.cta_group::1.kind::tf32 for hi*hi, lo*hi, hi*lo into one fp32
+//     accumulator in TMEM (128 lanes x 128 columns) and tcgen05.commit frees
+//     the stage for the producers;
+//   * epilogue (split warpgroup, one TMEM lane quarter per warp):
+//     tcgen05.ld 32x32b -> C += acc through the C offset tables, or the
+//     split-K partial into the workspace.
 // Accuracy: 3xTF32 products are within ~2^-22 relative, fp32 accumulation in
 // TMEM; checked against the fp64 oracle and the reference (tests/).
 #include <cstdint>
@@ -25,10 +29,7 @@
 #include "kernels.hpp"
 
 #ifndef GETT_TC_STAGES
-#define GETT_TC_STAGES 2
-#endif
-#ifndef GETT_TC_SLACK
-#define GETT_TC_SLACK 1
+#define GETT_TC_STAGES 6
 #endif
 
 namespace gett {
@@ -39,18 +40,18 @@ constexpr int BN = 128;
 constexpr int BK = 16;
 constexpr int CH = BK / 4;                     // 16-byte k-chunks per row
 constexpr int STAGES = GETT_TC_STAGES;
-constexpr int THREADS = 128;
+constexpr int WG = 128;                        // threads per warpgroup
+constexpr int THREADS = 2 * WG + 32;           // producer WG, split/epilogue WG, MMA warp
 constexpr int GROUP_M = 8;
 constexpr int LBO = 128;                       // bytes between k-chunks
 constexpr int SBO = CH * 128;                  // bytes between 8-row groups
 constexpr int TILE_BYTES = 128 * BK * 4;       // one operand part (hi or lo): 8 KB
 constexpr int STAGE_BYTES = 4 * TILE_BYTES;    // A hi, A lo, B hi, B lo
-#ifndef GETT_TC_TCAP
-#define GETT_TC_TCAP 256
-#endif
-constexpr int TCAP = GETT_TC_TCAP;             // outer k-table entries staged in smem
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + 256 + 2 * TCAP * 8;
+constexpr int TCAP = 256;                      // outer k-table entries staged in smem
+constexpr int BAR_BYTES = 256;
+constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 2 * TCAP * 8;
 constexpr uint32_t TMEM_COLS = 128;
+static_assert(3 * STAGES + 2 <= BAR_BYTES / 8, "barrier area");
 
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -69,7 +70,13 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
 }
-
+__device__ __forceinline__ void mbar_arrive(uint32_t addr) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(addr)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cpasync(uint32_t addr) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(addr) : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
   asm volatile(
       "{\n\t.reg .pred P1;\n"
@@ -111,102 +118,94 @@ struct KDec {
   FastDiv div;
 };
 
-// One operand's 128-row x BK gather with cp.async.  GKF: gmem fast along k
-// (a thread owns one 16-byte k-chunk of 4 rows) else along rows (a thread
-// owns one row, all chunks).  Units are (row, chunk) pairs.
-template <bool GKF, bool VEC>
+// One operand's 128-row x BK gather with cp.async by the producer warpgroup.
+// Warp w owns row groups 4w..4w+3 (8 rows each).  One warp instruction covers
+// 8 consecutive rows x 4 k: lane l -> row 8g + l%8 and, for 16-byte copies
+// (VEC: 4 contiguous k per row), chunk l/8 (8 rows x 64 B of gmem, four
+// conflict-free 128 B smem wavefronts); for 4-byte copies, k = 4c + l/8 of
+// chunk c (32 distinct smem banks; 8 rows x 4 k of gmem).
+template <bool VEC>
 struct Gather {
-  static constexpr int U = GKF ? 4 : CH;  // units per thread
-  int64_t roff[GKF ? 4 : 1];
-  bool rok[GKF ? 4 : 1];
-  int chunk, row0;
+  int64_t roff[4];
+  bool rok[4];
+  int lr, le, w;
+  int64_t ko[VEC ? 1 : CH];
 
-  __device__ __forceinline__ int urow(int u) const { return GKF ? row0 + 32 * u : row0; }
-  __device__ __forceinline__ int uchunk(int u) const { return GKF ? chunk : u; }
-
-  __device__ __forceinline__ void setup(const GroupDev& g, int base_row, int nrows) {
-    const int t = threadIdx.x;
-    chunk = GKF ? (t & (CH - 1)) : 0;
-    row0 = GKF ? t / CH : t;
+  __device__ __forceinline__ void setup(int warp, int lane, const GroupDev& g, int base_row,
+                                        int nrows) {
+    w = warp;
+    lr = lane & 7;
+    le = lane >> 3;
 #pragma unroll
-    for (int i = 0; i < (GKF ? 4 : 1); ++i) {
-      int r = base_row + row0 + 32 * i;
+    for (int i = 0; i < 4; ++i) {
+      int r = base_row + 8 * (4 * w + i) + lr;
       rok[i] = r < nrows;
       roff[i] = rok[i] ? g.off(0, r) : 0;
     }
   }
 
-  // k offsets of the next k-block, loaded ahead of the copies so the table
-  // reads overlap (the cp.async issue would otherwise serialise on them)
-  static constexpr int NKO = GKF ? (VEC ? 1 : 4) : BK;
-  int64_t ko[NKO];
-  int kk0, kkend;
-
-  // k -> offset by stepping the group's (outer q, inner r) decode: one fast
-  // divmod per k-block, and an outer-table read only when r wraps (the
-  // table sits in shared memory when it fits)
-  __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
-    kk0 = k0;
-    kkend = kend;
-    const int kb = GKF ? k0 + 4 * chunk : k0;
+  __device__ __forceinline__ static int64_t koff(const KDec& kd, int k) {
     int q, r;
-    kd.div.divmod(kb, q, r);
-    int64_t t = kb < kend ? kd.T[q] : 0;
+    kd.div.divmod(k, q, r);
+    return kd.T[q] + (int64_t)r * kd.s;
+  }
+
+  __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
+    if (VEC) {
+      const int k = k0 + 4 * le;
+      ko[0] = k < kend ? koff(kd, k) : 0;
+    } else {
 #pragma unroll
-    for (int e = 0; e < NKO; ++e) {
-      ko[e] = t + (int64_t)r * kd.s;
-      if (++r == kd.div.d) {
-        r = 0;
-        ++q;
-        t = (kb + e + 1 < kend) ? kd.T[q] : 0;
+      for (int c = 0; c < CH; ++c) {
+        const int k = k0 + 4 * c + le;
+        ko[c] = k < kend ? koff(kd, k) : 0;
       }
     }
   }
 
-  // issue the prepared k-block into the hi tile at smem address s
-  __device__ __forceinline__ void issue(uint8_t* s, const float* base) {
+  __device__ __forceinline__ void issue(uint8_t* s, const float* base, int k0, int kend) {
 #pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int r = urow(u), c = uchunk(u);
-      const bool rv = rok[GKF ? u : 0];
-      const int64_t ro = roff[GKF ? u : 0];
-      uint8_t* dst = s + toff(r, c);
-      const int k = kk0 + 4 * c;
+    for (int i = 0; i < 4; ++i) {
+      const int r = 8 * (4 * w + i) + lr;
       if (VEC) {
-        if (rv && k < kkend) cp_async_16(dst, base + ro + ko[0]);
+        uint8_t* dst = s + toff(r, le);
+        if (rok[i] && k0 + 4 * le < kend) cp_async_16(dst, base + roff[i] + ko[0]);
         else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int64_t o = GKF ? ko[e] : ko[4 * c + e];
-          if (rv && k + e < kkend) cp_async_4(dst + 4 * e, base + ro + o);
-          else *reinterpret_cast<float*>(dst + 4 * e) = 0.f;
+        for (int c = 0; c < CH; ++c) {
+          uint8_t* dst = s + toff(r, c) + 4 * le;
+          if (rok[i] && k0 + 4 * c + le < kend) cp_async_4(dst, base + roff[i] + ko[c]);
+          else *reinterpret_cast<float*>(dst) = 0.f;
         }
       }
     }
   }
-
-  // split this thread's own landed elements: hi in place, lo into lo tile
-  __device__ __forceinline__ void split(uint8_t* hi_s, uint8_t* lo_s) {
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const uint32_t o = toff(urow(u), uchunk(u));
-      float4 x = *reinterpret_cast<const float4*>(hi_s + o);
-      float4 h, l;
-      split4(x, h, l);
-      *reinterpret_cast<float4*>(hi_s + o) = h;
-      *reinterpret_cast<float4*>(lo_s + o) = l;
-    }
-  }
 };
+
+// split one landed 128 x BK tile: thread t handles rows t (4 chunks)
+__device__ __forceinline__ void split_tile(uint8_t* hi_s, uint8_t* lo_s, int t) {
+#pragma unroll
+  for (int c = 0; c < CH; ++c) {
+    const uint32_t o = toff(t, c);
+    float4 x = *reinterpret_cast<const float4*>(hi_s + o);
+    float4 h, l;
+    split4(x, h, l);
+    *reinterpret_cast<float4*>(hi_s + o) = h;
+    *reinterpret_cast<float4*>(lo_s + o) = l;
+  }
+}
 
 template <bool AKF, bool BKF, bool AVEC, bool BVEC>
 __global__ void __launch_bounds__(THREADS, 1)
     sgett_tc_kernel(const __grid_constant__ TiledParams<float> p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // [STAGES] free, [1] done
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + STAGES + 1);
-  int64_t* ktabs = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + 256);  // [2][TCAP]
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // gathers landed
+  uint64_t* ready = full + STAGES;                                            // split done
+  uint64_t* empty = ready + STAGES;                                           // MMAs done
+  uint64_t* done = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  int64_t* ktabs = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + BAR_BYTES);  // [2][TCAP]
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
@@ -228,11 +227,27 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int kend = min(p.K, kbeg + p.k_chunk);
   const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
+  // the K group's outer offset tables, staged in shared memory when small
+  const int n_outer = (p.gk.G + p.gk.e_in.d - 1) / p.gk.e_in.d;
+  KDec kda{p.gk.T[0], p.gk.s_in[0], p.gk.e_in}, kdb{p.gk.T[1], p.gk.s_in[1], p.gk.e_in};
+  if (n_outer <= TCAP) {
+    for (int i = tid; i < n_outer; i += THREADS) {
+      ktabs[i] = __ldg(p.gk.T[0] + i);
+      ktabs[TCAP + i] = __ldg(p.gk.T[1] + i);
+    }
+    kda.T = ktabs;
+    kdb.T = ktabs + TCAP;
+  }
   if (tid == 0) {
-    for (int s = 0; s <= STAGES; ++s) mbar_init(smem_u32(bars + s), 1);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(smem_u32(full + s), 2 * WG);  // per producer thread: cp.async + plain arrival
+      mbar_init(smem_u32(ready + s), WG);
+      mbar_init(smem_u32(empty + s), 1);      // tcgen05.commit
+    }
+    mbar_init(smem_u32(done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 0) {
+  if (warp == 8) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
@@ -242,122 +257,107 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
-
-  // the K group's outer offset tables, staged in shared memory when small
-  const int n_outer = (p.gk.G + p.gk.e_in.d - 1) / p.gk.e_in.d;
-  KDec kda{p.gk.T[0], p.gk.s_in[0], p.gk.e_in}, kdb{p.gk.T[1], p.gk.s_in[1], p.gk.e_in};
-  if (n_outer <= TCAP) {
-    for (int i = tid; i < n_outer; i += THREADS) {
-      ktabs[i] = __ldg(p.gk.T[0] + i);
-      ktabs[TCAP + i] = __ldg(p.gk.T[1] + i);
-    }
-    __syncthreads();
-    kda.T = ktabs;
-    kdb.T = ktabs + TCAP;
-  }
-  Gather<AKF, AVEC> ga;
-  Gather<BKF, BVEC> gb;
-  ga.setup(p.gm, m0, p.M);
-  gb.setup(p.gn, n0, p.N);
   auto stage = [&](int s) { return smem + s * STAGE_BYTES; };
 
-  // prefetch distance: DIST k-blocks of copies in flight; the stage being
-  // refilled was read by the MMAs of k-block kb - (STAGES - DIST), issued
-  // STAGES - DIST iterations earlier, so MMA latency stays off the loop
-  constexpr int DIST = STAGES - GETT_TC_SLACK;
+  if (warp < 4) {
+    // ---------------- producer warpgroup ----------------
+    Gather<AVEC> ga;
+    Gather<BVEC> gb;
+    ga.setup(warp, tid & 31, p.gm, m0, p.M);
+    gb.setup(warp, tid & 31, p.gn, n0, p.N);
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES, u = kb / STAGES;
+      const int k0 = kbeg + kb * BK;
+      ga.prep(kda, k0, kend);
+      gb.prep(kdb, k0, kend);
+      if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+      ga.issue(stage(s), p.A, k0, kend);
+      gb.issue(stage(s) + 2 * TILE_BYTES, p.B, k0, kend);
+      mbar_arrive_cpasync(smem_u32(full + s));
+      mbar_arrive(smem_u32(full + s));
+    }
+    cp_async_wait<0>();
+  } else if (warp < 8) {
+    // ---------------- split warpgroup, then epilogue ----------------
+    const int t = tid - WG;
+    for (int kb = 0; kb < nkb; ++kb) {
+      const int s = kb % STAGES, u = kb / STAGES;
+      mbar_wait(smem_u32(full + s), u & 1);
+      uint8_t* st = stage(s);
+      split_tile(st, st + TILE_BYTES, t);
+      split_tile(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES, t);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(smem_u32(ready + s));
+    }
+    if (nkb > 0) mbar_wait(smem_u32(done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // thread t owns accumulator row t (TMEM lane t; warp w%4 reads lanes 32(w%4)..)
+    const int m = m0 + t;
+    const bool mok = m < p.M;
+    const int64_t ro = (mok && p.splits == 1) ? p.gm.off(1, m) : 0;
+    float* wrow = p.splits > 1 ? p.ws + ((int64_t)split * p.M + (mok ? m : 0)) * p.N : nullptr;
 #pragma unroll 1
-  for (int s = 0; s < DIST; ++s) {
-    if (s < nkb) {
-      ga.prep(kda, kbeg + s * BK, kend);
-      gb.prep(kdb, kbeg + s * BK, kend);
-      ga.issue(stage(s), p.A);
-      gb.issue(stage(s) + 2 * TILE_BYTES, p.B);
-    }
-    cp_async_commit();
-  }
-  const uint32_t smem_base = smem_u32(smem);
-#pragma unroll 1
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int s = kb % STAGES;
-    const int nk = kb + DIST;
-    if (nk < nkb) {  // table reads for the refill, hidden behind this k-block's work
-      ga.prep(kda, kbeg + nk * BK, kend);
-      gb.prep(kdb, kbeg + nk * BK, kend);
-    }
-    cp_async_wait<DIST - 1>();
-    uint8_t* st = stage(s);
-#ifndef GETT_TC_NO_SPLIT
-    ga.split(st, st + TILE_BYTES);
-    gb.split(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES);
-#endif
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-      const uint32_t sb = smem_base + s * STAGE_BYTES;
-#pragma unroll
-      for (int j = 0; j < BK / 8; ++j) {
-        const uint64_t ah = sdesc(sb + 256 * j);
-        const uint64_t al = sdesc(sb + TILE_BYTES + 256 * j);
-        const uint64_t bh = sdesc(sb + 2 * TILE_BYTES + 256 * j);
-        const uint64_t bl = sdesc(sb + 3 * TILE_BYTES + 256 * j);
-        mma_tf32(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
-#ifndef GETT_TC_NO_MMA
-        mma_tf32(tmem, al, bh, 1);
-        mma_tf32(tmem, ah, bl, 1);
-#endif
-      }
-      commit(smem_u32(bars + s));
-    }
-    // refill the stage k-block kb - SLACK used, once its MMAs are done
-    if (nk < nkb) {
-      const int ns = nk % STAGES;
-      const int prev = nk - STAGES;  // last k-block that used stage ns
-      if (prev >= 0) mbar_wait(smem_u32(bars + ns), (prev / STAGES) & 1);
-#ifndef GETT_TC_NO_LOAD
-      ga.issue(stage(ns), p.A);
-      gb.issue(stage(ns) + 2 * TILE_BYTES, p.B);
-#endif
-    }
-    cp_async_commit();
-  }
-  if (tid == 0) commit(smem_u32(bars + STAGES));
-  if (nkb > 0) mbar_wait(smem_u32(bars + STAGES), 0);
-  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-
-  // epilogue: thread tid owns accumulator row tid (TMEM lane = row)
-  const int m = m0 + tid;
-  const bool mok = m < p.M;
-  const int64_t ro = (mok && p.splits == 1) ? p.gm.off(1, m) : 0;
-  float* wrow = p.splits > 1 ? p.ws + ((int64_t)split * p.M + (mok ? m : 0)) * p.N : nullptr;
-#pragma unroll 1
-  for (int c0 = 0; c0 < BN; c0 += 16) {
-    uint32_t r[16];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0;
-    asm volatile(
-        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-        : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
-          "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
-          "=r"(r[14]), "=r"(r[15])
-        : "r"(taddr));
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-    if (!mok) continue;
-#pragma unroll
-    for (int i = 0; i < 16; ++i) {
-      const int n = n0 + c0 + i;
-      if (n >= p.N) break;
-      const float acc = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
+    for (int c0 = 0; c0 < BN; c0 += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
+            "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
+            "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (!mok) continue;
       if (p.splits == 1) {
-        float* c = p.C + ro + p.gn.off(1, n);
-        *c = epi(*c, acc, p.neg);
+        float cv[16];
+        int64_t co[16];
+        const int nvalid = p.N - (n0 + c0);  // offsets may be negative: validity by index
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          co[i] = i < nvalid ? ro + p.gn.off(1, n0 + c0 + i) : 0;
+          cv[i] = i < nvalid ? p.C[co[i]] : 0.f;
+        }
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const float acc = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
+          if (i < nvalid) p.C[co[i]] = epi(cv[i], acc, p.neg);
+        }
       } else {
-        wrow[n] = acc;
+#pragma unroll
+        for (int i = 0; i < 16; ++i) {
+          const int n = n0 + c0 + i;
+          if (n < p.N) wrow[n] = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
+        }
       }
     }
+  } else {
+    // ---------------- MMA warp ----------------
+    if ((tid & 31) == 0) {
+      const uint32_t smem_base = smem_u32(smem);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES, u = kb / STAGES;
+        mbar_wait(smem_u32(ready + s), u & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sb = smem_base + s * STAGE_BYTES;
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint64_t ah = sdesc(sb + 256 * j);
+          const uint64_t al = sdesc(sb + TILE_BYTES + 256 * j);
+          const uint64_t bh = sdesc(sb + 2 * TILE_BYTES + 256 * j);
+          const uint64_t bl = sdesc(sb + 3 * TILE_BYTES + 256 * j);
+          mma_tf32(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
+          mma_tf32(tmem, al, bh, 1);
+          mma_tf32(tmem, ah, bl, 1);
+        }
+        commit(smem_u32(empty + s));
+      }
+      commit(smem_u32(done));
+    }
+    __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 0)
+  if (warp == 8)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
