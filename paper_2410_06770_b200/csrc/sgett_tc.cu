@@ -56,15 +56,25 @@ static_assert(3 * STAGES + 2 <= BAR_BYTES / 8, "barrier area");
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
+// ... with A / B MN-major (bits 15 / 16) for operands gathered along their rows
+__host__ __device__ constexpr uint32_t idesc(bool a_mn, bool b_mn) {
+  return IDESC | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16);
+}
+// MN-major no-swizzle layout (rows contiguous): 16-byte chunk of 4 rows at k,
+// core matrix 8 k x 16 B; SBO 128 B between row chunks, LBO 4 KB between k-groups
+constexpr int MN_SBO = 128, MN_LBO = 32 * 128;
+__device__ __forceinline__ uint32_t toff_mn(int mc, int k) {
+  return (uint32_t)(mc * MN_SBO + (k & 7) * 16 + (k >> 3) * MN_LBO);
+}
 
 __device__ __forceinline__ uint32_t toff(int r, int c) {
   return (uint32_t)((r >> 3) * SBO + c * LBO + (r & 7) * 16);
 }
 
 // shared-memory matrix descriptor (sm_100: version 1 at bit 46), no swizzle
-__device__ __forceinline__ uint64_t sdesc(uint32_t saddr) {
-  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(LBO >> 4) << 16) |
-         ((uint64_t)(SBO >> 4) << 32) | (1ull << 46);
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo = LBO, uint32_t sbo = SBO) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) |
+         ((uint64_t)(sbo >> 4) << 32) | (1ull << 46);
 }
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
@@ -88,13 +98,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc) {
+__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc,
+                                         uint32_t id = IDESC) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
       "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
       "}" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(IDESC), "r"(acc)
+      "l"(a), "l"(b), "r"(id), "r"(acc)
       : "memory");
 }
 
@@ -183,11 +194,25 @@ struct Gather {
   }
 };
 
-// split one landed 128 x BK tile: thread t handles rows t (4 chunks)
+template <bool KF, bool VEC>
+struct GatherSel {
+  using type = Gather<VEC>;
+};
+// rows-contiguous operands use 4-byte copies in the K-major layout (the
+// MN-major UMMA layout for kind::tf32 did not reproduce a CPU product in
+// tools/umma_layout_test.cu, so it is not used)
+template <>
+struct GatherSel<false, true> {
+  using type = Gather<false>;
+};
+
+// split one landed tile (8 KB, either layout): 512 dense 16-byte units, thread t
+// handles units t, t+128, t+256, t+384 (consecutive threads -> consecutive
+// 16 B: conflict-free)
 __device__ __forceinline__ void split_tile(uint8_t* hi_s, uint8_t* lo_s, int t) {
 #pragma unroll
-  for (int c = 0; c < CH; ++c) {
-    const uint32_t o = toff(t, c);
+  for (int i = 0; i < 4; ++i) {
+    const uint32_t o = (uint32_t)(t + WG * i) * 16;
     float4 x = *reinterpret_cast<const float4*>(hi_s + o);
     float4 h, l;
     split4(x, h, l);
@@ -200,6 +225,7 @@ template <bool AKF, bool BKF, bool AVEC, bool BVEC>
 __global__ void __launch_bounds__(THREADS, 1)
     sgett_tc_kernel(const __grid_constant__ TiledParams<float> p) {
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr bool AMN = false, BMN = false;  // K-major smem layouts for both operands
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // gathers landed
   uint64_t* ready = full + STAGES;                                            // split done
   uint64_t* empty = ready + STAGES;                                           // MMAs done
@@ -261,8 +287,8 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   if (warp < 4) {
     // ---------------- producer warpgroup ----------------
-    Gather<AVEC> ga;
-    Gather<BVEC> gb;
+    typename GatherSel<AKF, AVEC>::type ga;
+    typename GatherSel<BKF, BVEC>::type gb;
     ga.setup(warp, tid & 31, p.gm, m0, p.M);
     gb.setup(warp, tid & 31, p.gn, n0, p.N);
     for (int kb = 0; kb < nkb; ++kb) {
@@ -341,13 +367,18 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t sb = smem_base + s * STAGE_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
-          const uint64_t ah = sdesc(sb + 256 * j);
-          const uint64_t al = sdesc(sb + TILE_BYTES + 256 * j);
-          const uint64_t bh = sdesc(sb + 2 * TILE_BYTES + 256 * j);
-          const uint64_t bl = sdesc(sb + 3 * TILE_BYTES + 256 * j);
-          mma_tf32(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
-          mma_tf32(tmem, al, bh, 1);
-          mma_tf32(tmem, ah, bl, 1);
+          // per k-step j: K-major advances 256 B (2 k-chunks), MN-major one k-group
+          const uint32_t ja = AMN ? j * MN_LBO : 256 * j, jb = BMN ? j * MN_LBO : 256 * j;
+          const uint32_t alb = AMN ? MN_LBO : LBO, asb = AMN ? MN_SBO : SBO;
+          const uint32_t blb = BMN ? MN_LBO : LBO, bsb = BMN ? MN_SBO : SBO;
+          const uint64_t ah = sdesc(sb + ja, alb, asb);
+          const uint64_t al = sdesc(sb + TILE_BYTES + ja, alb, asb);
+          const uint64_t bh = sdesc(sb + 2 * TILE_BYTES + jb, blb, bsb);
+          const uint64_t bl = sdesc(sb + 3 * TILE_BYTES + jb, blb, bsb);
+          constexpr uint32_t ID = idesc(AMN, BMN);
+          mma_tf32(tmem, ah, bh, (kb | j) != 0, ID);  // first MMA of the tile overwrites D
+          mma_tf32(tmem, al, bh, 1, ID);
+          mma_tf32(tmem, ah, bl, 1, ID);
         }
         commit(smem_u32(empty + s));
       }
@@ -386,8 +417,6 @@ cudaError_t launch2(const TiledParams<float>& p, bool av, bool bv, cudaStream_t 
 
 cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
                             cudaStream_t s) {
-  if (!a_kf) a_vec = false;  // vectors only along k
-  if (!b_kf) b_vec = false;
   cudaError_t e;
   if (a_kf && b_kf) e = tc::launch2<true, true>(p, a_vec, b_vec, s);
   else if (a_kf) e = tc::launch2<true, false>(p, a_vec, b_vec, s);
