@@ -27,6 +27,9 @@ __global__ void k(const float* A, const float* B, float* D, int mode, int layout
     uint32_t ok = (m / 8) * 256 + (kk / 4) * 128 + (m % 8) * 16 + (kk % 4) * 4;
     uint32_t om = layout == 1 ? (m / 4) * 128 + kk * 16 + (m % 4) * 4
                 : layout == 2 ? (m / 32) * 1024 + kk * 128 + (m % 32) * 4
+                : layout == 4 ? ([&] { uint32_t lg = (m / 32) * 1024 + kk * 128 + (m % 32) * 4;
+                                       return lg ^ (((lg >> 7) & 7u) << 4); })()
+                : layout == 5 ? ok
                 : kk * 512 + m * 4;
     *(float*)((uint8_t*)sa + (mode == 0 ? ok : om)) = a;
     *(float*)((uint8_t*)sb + ok) = b;
@@ -48,6 +51,7 @@ __global__ void k(const float* A, const float* B, float* D, int mode, int layout
     uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24) |
                      ((mode != 0 ? 1u : 0u) << 15);
     uint64_t da = mode == 0 ? sdesc(su32(sa), 128, 256) : sdesc(su32(sa), lbo, sbo);
+    if (layout == 4) da |= (2ull << 61);  // SWIZZLE_128B
     uint64_t db = sdesc(su32(sb), 128, 256);
     asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\ttcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}"
                  ::"r"(tmem), "l"(da), "l"(db), "r"(idesc), "r"(0));
@@ -82,7 +86,8 @@ int main() {
       {0, 0, 128, 256}, {1, 1, 4096, 128}, {1, 1, 128, 4096}, {1, 1, 128, 128}, {1, 1, 16, 128},
       {1, 1, 128, 16}, {1, 1, 512, 128}, {1, 2, 1024, 128}, {1, 2, 128, 1024}, {1, 2, 512, 1024},
       {1, 2, 1024, 512}, {1, 3, 512, 128}, {1, 3, 128, 512}, {1, 3, 4096, 512}, {1, 3, 512, 4096},
-      {1, 2, 4096, 1024}, {1, 2, 1024, 4096}};
+      {1, 2, 4096, 1024}, {1, 2, 1024, 4096}, {1, 4, 1024, 8192}, {1, 4, 8192, 1024},
+      {1, 4, 1024, 1024}, {1, 5, 128, 256}};
   for (auto c : cfg) {
     int mode = c.mode;
     cudaMemset(D, 0, sizeof hD);
