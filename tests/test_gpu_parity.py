@@ -367,3 +367,99 @@ def test_signed_zero_semantics(kernel_mode):
         assert g.dgett(1, (3,), (1,), np.array([-0.0, -0.0, -0.0]),
                        1, (3,), (1,), np.ones(3), 1, (0,), (0,), (), (), c) == []
         assert np.signbit(c[0])
+
+
+# ---------------------------------------------------------------------------
+# split-K across ranks (shard.splitk_contract): the device sub-calls
+
+
+def _emulated_splitk(w, world, ta, tb, tc):
+    """`world` ranks run one after another on this GPU; reduce() emulates
+    ncclReduce(sum) onto rank 0 (non-roots deposit, the root sums last)."""
+    import torch
+
+    from paper_2410_06770_b200.device import dgett_device, sgett_device
+    from paper_2410_06770_b200.shard import splitk_contract
+
+    entry = sgett_device if w.dtype == "s" else dgett_device
+    acc = []
+
+    def reduce_for(rank):
+        def red(p):
+            if rank != 0:
+                acc.append(p.clone())
+            else:
+                for q in acc:
+                    p.add_(q)
+        return red
+
+    for rank in reversed(range(world)):
+        ci = tc if rank == 0 else tc.clone()
+        pos, kw = w.args(ta, tb, ci)
+        errs = splitk_contract(entry, pos, kw, rank, world,
+                               zeros=lambda n: torch.zeros(n, dtype=tc.dtype, device=tc.device),
+                               ones=lambda: torch.ones(1, dtype=tc.dtype, device=tc.device),
+                               reduce=reduce_for(rank))
+        assert errs == []
+        if rank != 0:
+            torch.cuda.synchronize()
+            assert torch.equal(ci, tc)  # only the owner writes C
+
+
+@pytest.mark.parametrize("name,world", [("c1", 3), ("c5", 4), ("c5", 8)])
+def test_splitk_ranks_on_device(name, world):
+    import torch
+
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+
+    w = W[name]
+    a, b, c = w.buffers()
+    c0 = c.copy()
+    ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+    _emulated_splitk(w, world, ta, tb, tc)
+    got_flat = tc.cpu().numpy()
+    offs = view_offsets(w.ext_c, w.inc_c, w.off_c)
+    mask = np.ones(len(c), bool)
+    mask[offs] = False
+    assert got_flat[mask].tobytes() == c0[mask].tobytes()
+    ref = oracle.einsum_check(w.ext_a, w.inc_a, a, w.off_a, w.ext_b, w.inc_b, b, w.off_b,
+                              w.conts, w.cont_a, w.cont_b, w.perm)
+    ref = ref + oracle.strided(c0, w.ext_c, w.inc_c, w.off_c).astype(np.float64)
+    got = oracle.strided(got_flat, w.ext_c, w.inc_c, w.off_c)
+    assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K[w.dtype]
+
+
+def test_splitk_device_nccl_group():
+    """splitk_device through a real NCCL process group (world size 1 here:
+    one GPU per gpurun box) — wiring, validation and the owner write."""
+    import socket
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2410_06770_b200.shard import splitk_device
+    from paper_2410_06770_b200.workloads import C5
+
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    store = dist.TCPStore("127.0.0.1", port, 1, True)
+    dist.init_process_group("nccl", store=store, rank=0, world_size=1,
+                            device_id=torch.device("cuda:0"))
+    try:
+        w = C5.slice_free("A", 0, 0, 8)
+        a, b, c = w.buffers()
+        want = c.copy()
+        pos, kw = w.args(a, b, want)
+        run(g.sgett, pos, kw)
+        ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+        pos, kw = w.args(ta, tb, tc)
+        assert splitk_device("s", pos, kw) == []
+        assert tc.cpu().numpy().tobytes() == want.tobytes()
+        bad = list(pos)
+        bad[12] = (0,) + tuple(bad[12][1:])  # zero output increment
+        errs = splitk_device("s", tuple(bad), kw)
+        assert errs and errs[0].code == g.ErrorCode.OutputWriteAliasing
+    finally:
+        dist.destroy_process_group()

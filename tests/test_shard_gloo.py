@@ -13,7 +13,7 @@ import torch.multiprocessing as mp
 
 from oracle import oracle
 from paper_2410_06770_b200.shard import bounds, choose_mode, shard_call
-from paper_2410_06770_b200.workloads import C1, C3, C4
+from paper_2410_06770_b200.workloads import C1, C3, C4, C5
 
 
 SMALL = {
@@ -84,3 +84,78 @@ def test_empty_slab_writes_nothing():
     args = (2, (3, 4), (4, 1), None, 2, (4, 2), (2, 1), None, 1, (1,), (0,), (0, 1), (2, 1), None)
     sargs, skw, lo, hi = shard_call(args, {}, s, 0, 8)
     assert hi - lo == 0 and 0 in sargs[1] + sargs[5]
+
+
+# --- split-K across ranks (reduction-parallel, c5) -------------------------
+
+SPLITK = {
+    "c1": lambda: C1,
+    "c5": lambda: C5.slice_free("A", 0, 0, 4).slice_free("B", 3, 0, 8),
+}
+
+
+def _splitk_worker(rank, world, port, name, out_dir):
+    import torch
+
+    from paper_2410_06770_b200.shard import full_call_errors, splitk_contract
+
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    w = SPLITK[name]()
+    a, b, c = w.buffers()
+    args, kw = w.args(a, b, c)
+    entry = oracle.oracle_sgett if w.dtype == "s" else oracle.oracle_dgett
+    errs = splitk_contract(
+        lambda *x, **y: entry(*x, **y) or [], args, kw, rank, world,
+        zeros=lambda n: np.zeros(n, dtype=c.dtype), ones=lambda: np.ones(1, dtype=c.dtype),
+        reduce=lambda p: dist.reduce(torch.from_numpy(p), dst=0, op=dist.ReduceOp.SUM),
+        validate_full=full_call_errors)
+    assert errs == []
+    np.save(os.path.join(out_dir, f"c{rank}.npy"), c)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("name,world", [("c1", 2), ("c5", 2), ("c5", 3)])
+def test_splitk_ranks_reduce_onto_owner(name, world, tmp_path):
+    mp.spawn(_splitk_worker, args=(world, _port(), name, str(tmp_path)), nprocs=world, join=True)
+    w = SPLITK[name]()
+    a, b, c = w.buffers()
+    c0 = c.copy()
+    args, kw = w.args(a, b, c)
+    (oracle.oracle_sgett if w.dtype == "s" else oracle.oracle_dgett)(*args, **kw)
+    root = np.load(tmp_path / "c0.npy")
+    # C0 added exactly once, only on the owner; non-owners leave C untouched
+    for r in range(1, world):
+        assert np.load(tmp_path / f"c{r}.npy").tobytes() == c0.tobytes()
+    k = w.size_k
+    amax = np.abs(a).max() * np.abs(b).max()
+    tol = 1e-5 if w.dtype == "s" else 1e-12
+    assert np.abs(root.astype(np.float64) - c).max() <= tol * k * amax + 0.0
+    assert not np.array_equal(root, c0)
+
+
+def test_splitk_pair_choice_and_slices():
+    from paper_2410_06770_b200.shard import (accumulate_call, choose_k_pair, k_shard_call,
+                                            output_extents, packed_increments)
+
+    # c5 contracted pairs: A dims (1, 2, 4) = (24, 32, 40); 40 % 8 == 0 -> the 40 pair
+    assert choose_k_pair(C5.ext_a, C5.cont_a, 8) == 2
+    assert choose_k_pair((3, 4), (), 2) is None
+    ext_c = output_extents(len(C5.ext_a), C5.ext_a, C5.cont_a, len(C5.ext_b), C5.ext_b, C5.cont_b,
+                           C5.perm)
+    assert ext_c == (96, 48, 16) and packed_increments(ext_c) == (768, 16, 1)
+    a, b, c = object(), object(), object()
+    args = (5, C5.ext_a, C5.inc_a, a, 4, C5.ext_b, C5.inc_b, b, 3, C5.cont_a, C5.cont_b, C5.perm,
+            C5.inc_c, c)
+    lo_hi = []
+    for r in range(3):
+        sargs, skw, lo, hi = k_shard_call(args, {"offset_c": 7}, 2, r, 3, "P")
+        assert sargs[1][4] == sargs[5][0] == hi - lo
+        assert skw["offset_a"] == lo * C5.inc_a[4] and skw["offset_b"] == lo * C5.inc_b[0]
+        assert skw["offset_c"] == 0 and sargs[13] == "P" and sargs[12] == (768, 16, 1)
+        lo_hi.append((lo, hi))
+    assert lo_hi == [(0, 13), (13, 26), (26, 40)]
+    aargs, akw = accumulate_call(ext_c, "P", "one", C5.inc_c, c, 7)
+    assert aargs[:3] == (3, ext_c, (768, 16, 1)) and aargs[4] == 0 and aargs[8] == 0
+    assert aargs[11] == (0, 1, 2) and akw["offset_c"] == 7
