@@ -183,7 +183,8 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
              int64_t len_c, std::shared_ptr<DevPlan>* out) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  std::string key = plan_key(dtype, a, b, s, off_c) + "#" + std::to_string(dev);
+  std::string key = plan_key(dtype, a, b, s, off_c);
+  key.append(reinterpret_cast<const char*>(&dev), sizeof dev);
   auto it = g_plans.map.find(key);
   if (it != g_plans.map.end()) {
     g_plans.lru.splice(g_plans.lru.begin(), g_plans.lru, it->second.second);
@@ -238,7 +239,7 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
 int get_view_plan(int rank, const int64_t* ext, const int64_t* inc, std::shared_ptr<DevPlan>* out) {
   int dev = 0;
   CK(cudaGetDevice(&dev));
-  std::string key = "zero|";
+  std::string key = "\x01zero|";
   for (int d = 0; d < rank; ++d) key += std::to_string(ext[d]) + "," + std::to_string(inc[d]) + ";";
   key += "#" + std::to_string(dev);
   auto it = g_plans.map.find(key);

@@ -6,6 +6,20 @@
 
 namespace gett {
 
+// cudaFuncSetAttribute is per device: opt a kernel into `bytes` of dynamic
+// shared memory once per device (bit d of `mask`; callers hold the API lock).
+template <class Kern>
+inline cudaError_t ensure_dyn_smem(Kern k, int bytes, unsigned long long& mask) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  if (dev < 64 && ((mask >> dev) & 1ull)) return cudaSuccess;
+  e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess && dev < 64) mask |= 1ull << dev;
+  return e;
+}
+
+
 // Division by a runtime-invariant positive int32 with one mul.hi + shift
 // (round-up reciprocal; valid for 0 <= n < 2^31, 1 <= d < 2^31).
 struct FastDiv {

@@ -273,12 +273,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <bool AKF, bool BKF, bool AV, bool BV>
 cudaError_t launch4(const TiledParams<double>& p, cudaStream_t s) {
   auto k = dgett_ws_kernel<AKF, BKF, AV, BV>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static unsigned long long configured = 0;
+  cudaError_t e = ensure_dyn_smem(k, SMEM_BYTES, configured);
+  if (e != cudaSuccess) return e;
   k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }

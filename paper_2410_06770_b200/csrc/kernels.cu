@@ -592,12 +592,9 @@ template <typename T, bool AKF, bool BKF, bool AV, bool BV>
 cudaError_t launch_t(const TiledParams<T>& p, cudaStream_t s) {
   auto k = tiled::gett_tiled_kernel<T, AKF, BKF, AV, BV>;
   constexpr size_t smem = tiled::smem_bytes<T>();
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static unsigned long long configured = 0;
+  cudaError_t e = ensure_dyn_smem(k, (int)smem, configured);
+  if (e != cudaSuccess) return e;
   dim3 grid((unsigned)(p.tiles_m * p.tiles_n * p.splits));
   k<<<grid, tiled::Cfg<T>::THREADS, smem, s>>>(p);
   return cudaGetLastError();

@@ -297,19 +297,24 @@ Group fold_view(int rank, const int64_t* ext, const int64_t* inc) {
 }
 
 std::string plan_key(char dtype, const View& a, const View& b, const Spec& s, int64_t off_c) {
+  // Binary key (raw int64 words): the descriptor minus every offset.  One
+  // allocation, no formatting — this runs on every call.
   (void)off_c;
-  std::ostringstream o;
-  o << dtype << '|' << a.rank << ':';
-  for (int d = 0; d < a.rank; ++d) o << a.ext[d] << ',' << a.inc[d] << ';';
-  o << '|' << b.rank << ':';
-  for (int d = 0; d < b.rank; ++d) o << b.ext[d] << ',' << b.inc[d] << ';';
-  o << '|' << s.conts << ':';
-  for (int k = 0; k < s.conts; ++k) o << s.cont_a[k] << ',' << s.cont_b[k] << ';';
-  o << '|';
-  for (int k = 0; k < s.perm_len; ++k) o << s.perm[k] << ',';
-  o << '|';
-  for (int k = 0; k < s.inc_c_len; ++k) o << s.inc_c[k] << ',';
-  return o.str();
+  std::string k;
+  k.reserve(8 * (4 + 2 * a.rank + 2 * b.rank + 2 * s.conts + s.perm_len + s.inc_c_len) + 1);
+  auto put = [&](int64_t v) { k.append(reinterpret_cast<const char*>(&v), 8); };
+  k.push_back(dtype);
+  put(a.rank);
+  for (int d = 0; d < a.rank; ++d) { put(a.ext[d]); put(a.inc[d]); }
+  put(b.rank);
+  for (int d = 0; d < b.rank; ++d) { put(b.ext[d]); put(b.inc[d]); }
+  put(s.conts);
+  for (int i = 0; i < s.conts; ++i) { put(s.cont_a[i]); put(s.cont_b[i]); }
+  put(s.perm_len);
+  for (int i = 0; i < s.perm_len; ++i) put(s.perm[i]);
+  put(s.inc_c_len);
+  for (int i = 0; i < s.inc_c_len; ++i) put(s.inc_c[i]);
+  return k;
 }
 
 }  // namespace gett

@@ -194,17 +194,104 @@ struct Gather {
   }
 };
 
+// Rows-contiguous operand with 16-byte row chunks (unit-stride inner row mode,
+// extent and all offsets divisible by 4): staged MN-major, [k][128 rows] fp32
+// (512 B per k), and transposed into the K-major hi/lo tiles by the split
+// warpgroup (split_tile_rv) — the tf32 UMMA reads K-major only.  Warp w,
+// instruction i copies k = 4w + i: lane l -> rows 4l..4l+3, so one warp
+// instruction moves 512 contiguous bytes of gmem into 512 contiguous bytes of
+// smem (the 4-byte path needs 16 instructions for the same k-block).
+struct GatherRV {
+  int64_t roff;
+  bool rok;
+  int lane, w;
+  int64_t ko[4];
+
+  __device__ __forceinline__ void setup(int warp, int ln, const GroupDev& g, int base_row,
+                                        int nrows) {
+    w = warp;
+    lane = ln;
+    const int r = base_row + 4 * lane;
+    rok = r < nrows;
+    roff = rok ? g.off(0, r) : 0;
+  }
+
+  __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = k0 + 4 * w + i;
+      ko[i] = k < kend ? Gather<true>::koff(kd, k) : 0;
+    }
+  }
+
+  __device__ __forceinline__ void issue(uint8_t* s, const float* base, int k0, int kend) {
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int k = 4 * w + i;
+      uint8_t* dst = s + k * 512 + lane * 16;
+      if (rok && k0 + k < kend) cp_async_16(dst, base + roff + ko[i]);
+      else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+  }
+};
+
 template <bool KF, bool VEC>
 struct GatherSel {
   using type = Gather<VEC>;
 };
-// rows-contiguous operands use 4-byte copies in the K-major layout (the
-// MN-major UMMA layout for kind::tf32 did not reproduce a CPU product in
-// tools/umma_layout_test.cu, so it is not used)
 template <>
 struct GatherSel<false, true> {
+  using type = GatherRV;
+};
+template <>
+struct GatherSel<false, false> {
   using type = Gather<false>;
 };
+
+// split + transpose one MN-major staged tile ([k][row] fp32, GatherRV) into the
+// K-major hi tile (same 8 KB, in place) and lo tile.  Split thread t = 32ws + l
+// reads units (k = 4ws + l/8, rows 4rc..4rc+3 with rc = 8i + l%8), i = 0..3
+// (each 8-lane phase reads 128 contiguous bytes); after a warpgroup barrier
+// (the writes land on other threads' inputs) it stores the 4 values of a unit
+// rotated by s = (l/2)%4, so at each store the 32 lanes cover all 8 (row % 8)
+// x 4 (k % 4) positions = 32 distinct banks.
+__device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int t) {
+  const int ws = t >> 5, l = t & 31;
+  const int k = 4 * ws + (l >> 3);
+  float4 x[4];
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rc = 8 * i + (l & 7);
+    x[i] = *reinterpret_cast<const float4*>(hi_s + k * 512 + rc * 16);
+  }
+  asm volatile("bar.sync 1, 128;" ::: "memory");
+  const int rot = (l >> 1) & 3;
+#pragma unroll
+  for (int i = 0; i < 4; ++i) {
+    const int rc = 8 * i + (l & 7);
+    float4 h, lo;
+    split4(x[i], h, lo);
+    float hv[4] = {h.x, h.y, h.z, h.w}, lv[4] = {lo.x, lo.y, lo.z, lo.w};
+    // rotate left by rot with selects (no dynamic register indexing)
+    if (rot & 1) {
+      float th = hv[0], tl = lv[0];
+      hv[0] = hv[1]; hv[1] = hv[2]; hv[2] = hv[3]; hv[3] = th;
+      lv[0] = lv[1]; lv[1] = lv[2]; lv[2] = lv[3]; lv[3] = tl;
+    }
+    if (rot & 2) {
+      float th0 = hv[0], th1 = hv[1], tl0 = lv[0], tl1 = lv[1];
+      hv[0] = hv[2]; hv[1] = hv[3]; hv[2] = th0; hv[3] = th1;
+      lv[0] = lv[2]; lv[1] = lv[3]; lv[2] = tl0; lv[3] = tl1;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int row = 4 * rc + ((j + rot) & 3);
+      const uint32_t o = toff(row, k >> 2) + (k & 3) * 4;
+      *reinterpret_cast<float*>(hi_s + o) = hv[j];
+      *reinterpret_cast<float*>(lo_s + o) = lv[j];
+    }
+  }
+}
 
 // split one landed tile (8 KB, either layout): 512 dense 16-byte units, thread t
 // handles units t, t+128, t+256, t+384 (consecutive threads -> consecutive
@@ -310,8 +397,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = kb % STAGES, u = kb / STAGES;
       mbar_wait(smem_u32(full + s), u & 1);
       uint8_t* st = stage(s);
-      split_tile(st, st + TILE_BYTES, t);
-      split_tile(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES, t);
+      if (!AKF && AVEC) split_tile_rv(st, st + TILE_BYTES, t);
+      else split_tile(st, st + TILE_BYTES, t);
+      if (!BKF && BVEC) split_tile_rv(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES, t);
+      else split_tile(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES, t);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(smem_u32(ready + s));
     }
@@ -395,12 +484,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 template <bool AKF, bool BKF, bool AV, bool BV>
 cudaError_t launch4(const TiledParams<float>& p, cudaStream_t s) {
   auto k = sgett_tc_kernel<AKF, BKF, AV, BV>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static unsigned long long configured = 0;
+  cudaError_t e = ensure_dyn_smem(k, SMEM_BYTES, configured);
+  if (e != cudaSuccess) return e;
   k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }

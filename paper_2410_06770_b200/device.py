@@ -14,7 +14,7 @@ import ctypes
 
 from . import _native
 from .layout import TensorView
-from .plan import ContractionSpec, decode_errors, error_capacity
+from .plan import decode_errors, prepare
 
 _DT = {"s": "float32", "d": "float64", "c": "complex64", "z": "complex128"}
 
@@ -43,29 +43,28 @@ def _gett_device(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts
     c = _buf(c, "c", prefix)
     if not (a.device == b.device == c.device):
         raise ValueError("a, b and c must live on one device")
-    a_view = TensorView(rank_a, ext_a, inc_a, offset_a, a.shape[0])
-    b_view = TensorView(rank_b, ext_b, inc_b, offset_b, b.shape[0])
-    spec = ContractionSpec(conts, cont_a, cont_b, perm)
-    inc_c = tuple(int(i) for i in inc_c)
-    cap = error_capacity(a_view.rank, b_view.rank, spec.conts)
+    pr = prepare(rank_a, ext_a, inc_a, offset_a, a.shape[0], rank_b, ext_b, inc_b, offset_b,
+                 b.shape[0], conts, cont_a, cont_b, perm, inc_c)
+    cap = pr.cap
     codes = (ctypes.c_int32 * cap)()
     info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
+    dev = c.device
     if stream is None:
-        stream = torch.cuda.current_stream(c.device)
+        stream = torch.cuda.current_stream(dev)
     fn = getattr(_native.LIB, f"gett_{prefix}gett_device")
-    with torch.cuda.device(c.device):
-        rc = fn(a_view.rank, _native.i64(a_view.extents), _native.i64(a_view.increments),
-                a.data_ptr(), a_view.base_offset, a_view.buffer_len,
-                b_view.rank, _native.i64(b_view.extents), _native.i64(b_view.increments),
-                b.data_ptr(), b_view.base_offset, b_view.buffer_len,
-                spec.conts, _native.i64(spec.cont_a), _native.i64(spec.cont_b),
-                len(spec.perm), _native.i64(spec.perm), len(inc_c), _native.i64(inc_c),
-                c.data_ptr(), int(offset_c), c.shape[0], ctypes.c_void_p(stream.cuda_stream),
-                codes, info, cap)
+    args = (*pr.args_a, a.data_ptr(), pr.a_view.base_offset, pr.a_view.buffer_len,
+            *pr.args_b, b.data_ptr(), pr.b_view.base_offset, pr.b_view.buffer_len,
+            *pr.args_spec, c.data_ptr(), int(offset_c), c.shape[0],
+            ctypes.c_void_p(stream.cuda_stream), codes, info, cap)
+    if torch.cuda.current_device() == dev.index:
+        rc = fn(*args)
+    else:
+        with torch.cuda.device(dev):
+            rc = fn(*args)
     n = _native.check(rc, prefix + "gett_device")
     if n:
-        return decode_errors(min(n, cap), codes, info, a_view.rank, a_view.extents, b_view.rank,
-                             b_view.extents, spec, inc_c)
+        return decode_errors(min(n, cap), codes, info, pr.a_view.rank, pr.a_view.extents,
+                             pr.b_view.rank, pr.b_view.extents, pr.spec, pr.inc_c)
     return []
 
 

@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native
 from .layout import TensorView
-from .plan import ContractionSpec, decode_errors, error_capacity
+from .plan import decode_errors, prepare
 
 _PREFIX_DTYPE = {
     "s": np.dtype(np.float32),
@@ -45,10 +45,9 @@ def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_
             raise TypeError(f"{name} must be a flat 1-D buffer, got shape {buf.shape}")
         if buf.dtype != dtype:
             raise TypeError(f"{name} has dtype {buf.dtype}, this entry point needs {dtype}")
-    a_view = TensorView(rank_a, ext_a, inc_a, offset_a, a.shape[0])
-    b_view = TensorView(rank_b, ext_b, inc_b, offset_b, b.shape[0])
-    spec = ContractionSpec(conts, cont_a, cont_b, perm)
-    inc_c = tuple(int(i) for i in inc_c)
+    pr = prepare(rank_a, ext_a, inc_a, offset_a, a.shape[0], rank_b, ext_b, inc_b, offset_b,
+                 b.shape[0], conts, cont_a, cont_b, perm, inc_c)
+    a_view, b_view, spec, inc_c = pr.a_view, pr.b_view, pr.spec, pr.inc_c
     a = np.ascontiguousarray(a)
     b = np.ascontiguousarray(b)
     cw = c if c.flags.c_contiguous else np.ascontiguousarray(c)
@@ -60,17 +59,13 @@ def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_
         if errs:
             return errs
         raise ValueError("assignment destination is read-only")
-    cap = error_capacity(a_view.rank, b_view.rank, spec.conts)
+    cap = pr.cap
     codes = (ctypes.c_int32 * cap)()
     info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
     rc = getattr(_native.LIB, _ENTRY[prefix])(
-        a_view.rank, _native.i64(a_view.extents), _native.i64(a_view.increments), a.ctypes.data,
-        a_view.base_offset, a_view.buffer_len,
-        b_view.rank, _native.i64(b_view.extents), _native.i64(b_view.increments), b.ctypes.data,
-        b_view.base_offset, b_view.buffer_len,
-        spec.conts, _native.i64(spec.cont_a), _native.i64(spec.cont_b),
-        len(spec.perm), _native.i64(spec.perm), len(inc_c), _native.i64(inc_c),
-        cw.ctypes.data, int(offset_c), cw.shape[0], codes, info, cap)
+        *pr.args_a, a.ctypes.data, a_view.base_offset, a_view.buffer_len,
+        *pr.args_b, b.ctypes.data, b_view.base_offset, b_view.buffer_len,
+        *pr.args_spec, cw.ctypes.data, int(offset_c), cw.shape[0], codes, info, cap)
     n = _native.check(rc, prefix + "gett")
     if n:
         return decode_errors(min(n, cap), codes, info, a_view.rank, a_view.extents, b_view.rank,

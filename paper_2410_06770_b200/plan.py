@@ -161,3 +161,51 @@ def validate(a: TensorView, b: TensorView, spec: ContractionSpec, inc_c,
         mode, rcv, _native.i64(ecv), _native.i64(icv), off_c, len_c, codes, info, cap)
     _native.check(n, "validate")
     return decode_errors(min(n, cap), codes, info, a.rank, a.extents, b.rank, b.extents, spec, inc_c)
+
+
+# ---------------------------------------------------------------------------
+# Per-call descriptor cache.  Building the views/spec (structural checks) and
+# the ctypes argument arrays costs ~15 µs of Python per call — more than the
+# device time of small contractions.  The result is a pure function of the
+# descriptor values, so repeated calls with an equal descriptor reuse it.
+# Scalars are keyed with their types (ctypes rejects e.g. float offsets, and
+# a hit must not mask that); tuple elements go through int() either way.
+
+class Prepared:
+    __slots__ = ("a_view", "b_view", "spec", "inc_c", "cap", "args_a", "args_b", "args_spec")
+
+    def __init__(self, a_view, b_view, spec, inc_c):
+        self.a_view, self.b_view, self.spec, self.inc_c = a_view, b_view, spec, inc_c
+        self.cap = error_capacity(a_view.rank, b_view.rank, spec.conts)
+        self.args_a = (a_view.rank, _native.i64(a_view.extents), _native.i64(a_view.increments))
+        self.args_b = (b_view.rank, _native.i64(b_view.extents), _native.i64(b_view.increments))
+        self.args_spec = (spec.conts, _native.i64(spec.cont_a), _native.i64(spec.cont_b),
+                          len(spec.perm), _native.i64(spec.perm), len(inc_c), _native.i64(inc_c))
+
+
+_PREP: dict = {}
+_PREP_CAP = 1024
+
+
+def prepare(rank_a, ext_a, inc_a, offset_a, len_a, rank_b, ext_b, inc_b, offset_b, len_b,
+            conts, cont_a, cont_b, perm, inc_c) -> Prepared:
+    """Views, spec and native argument arrays for one call (cached).  Raises
+    exactly what TensorView / ContractionSpec construction raises."""
+    try:
+        key = (rank_a, type(rank_a), tuple(ext_a), tuple(inc_a), offset_a, type(offset_a), len_a,
+               rank_b, type(rank_b), tuple(ext_b), tuple(inc_b), offset_b, type(offset_b), len_b,
+               conts, type(conts), tuple(cont_a), tuple(cont_b), tuple(perm), tuple(inc_c))
+        hit = _PREP.get(key)
+    except TypeError:  # unhashable or non-iterable descriptor: no caching
+        key = hit = None
+    if hit is not None:
+        return hit
+    p = Prepared(TensorView(rank_a, ext_a, inc_a, offset_a, len_a),
+                 TensorView(rank_b, ext_b, inc_b, offset_b, len_b),
+                 ContractionSpec(conts, cont_a, cont_b, perm),
+                 tuple(int(i) for i in inc_c))
+    if key is not None:
+        if len(_PREP) >= _PREP_CAP:
+            _PREP.pop(next(iter(_PREP)))
+        _PREP[key] = p
+    return p
