@@ -351,6 +351,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   tp.splits = (int32_t)splits;
   tp.ws = nullptr;
   tp.neg = neg;
+  tp.ws_t = use_tc ? 1 : 0;
   if (splits > 1) {
     int rc = ensure(ds.ws, (size_t)splits * M * N * sizeof(T));
     if (rc) return rc;

@@ -82,8 +82,9 @@ struct TiledParams {
   int32_t tiles_m, tiles_n;
   int32_t splits;   // split-K factor (1 = fused C += acc epilogue)
   int32_t k_chunk;  // K per split, a multiple of the k-block
-  T* ws;            // [splits][M][N] partial tiles when splits > 1
+  T* ws;            // [splits][M][N] partial tiles when splits > 1 ([splits][N][M] if ws_t)
   int32_t neg = 0;  // epilogue C += -acc (the a.im*b.im term of a complex contraction)
+  int32_t ws_t = 0; // split-K workspace transposed (tcgen05 SGETT epilogue: m fastest)
 };
 
 // the fused epilogue's update: C + acc, or C + (-acc) == C - acc for neg

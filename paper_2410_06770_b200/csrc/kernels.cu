@@ -569,8 +569,14 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t mn = (int64_t)p.M * p.N;
   if (idx >= mn) return;
-  int32_t n = (int32_t)(idx % p.N);
-  int32_t m = (int32_t)(idx / p.N);
+  int32_t n, m;
+  if (p.ws_t) {  // [splits][N][M]: consecutive threads read consecutive m
+    m = (int32_t)(idx % p.M);
+    n = (int32_t)(idx / p.M);
+  } else {
+    n = (int32_t)(idx % p.N);
+    m = (int32_t)(idx / p.N);
+  }
   T s = T(-0.0);
   for (int sp = 0; sp < p.splits; ++sp) s = s + p.ws[sp * mn + idx];
   T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);

@@ -5,35 +5,56 @@
 // enough to tile.  Per 128x128 output tile, k-blocks of 16, STAGES-deep ring:
 //   * producer warpgroup (warps 0-3): gathers the A' (M x K) and B' (N x K)
 //     k-block straight from the strided views with cp.async (row offsets
-//     decoded once per tile, k offsets stepped through the K group's outer
-//     table staged in smem; 16-byte copies where the planner proved 4-k
-//     contiguity) into the UMMA K-major no-swizzle layout (8-row x 16-byte
-//     core matrices, LBO 128 B between k-chunks, SBO 512 B between 8-row
-//     groups); completion is tracked per stage by cp.async.mbarrier.arrive,
-//     so up to STAGES k-blocks are in flight without blocking anyone;
-//   * split warpgroup (warps 4-7): when a stage lands, splits every value in
-//     place into hi = rna_tf32(x) and lo = x - hi (exact in fp32) into the
-//     stage's lo tile, fence.proxy.async, arrive;
-//   * MMA warp (warp 8): one elected thread issues, per UMMA_K = 8 step,
+//     decoded once per tile, k offsets from this CTA's slice of the K group's
+//     outer table staged in smem) — 16-byte copies along k (K-major core
+//     layout: 8-row x 16-byte core matrices, LBO 128 B between k-chunks, SBO
+//     512 B between 8-row groups) or along rows (staged [k][row]) where the
+//     planner proved 4-element contiguity, else 4-byte copies; completion is
+//     tracked per stage by cp.async.mbarrier.arrive;
+//   * split warpgroups (warps 4-11): when a stage lands, split every value into
+//     hi = rna_tf32(x) and lo = x - hi (exact in fp32).  A' goes to TMEM
+//     (tcgen05.st, lane = row, column = k: the MMA's A operand is read from
+//     TMEM, so A' never round-trips through shared memory); B' is split in
+//     place into its K-major hi/lo tiles (transposed from [k][row] staging when
+//     gathered along rows); fence, arrive;
+//   * MMA warp (warp 12): one elected thread issues, per UMMA_K = 8 step,
 //     tcgen05.mma.cta_group::1.kind::tf32 for hi*hi, lo*hi, hi*lo into one fp32
 //     accumulator in TMEM (128 lanes x 128 columns) and tcgen05.commit frees
-//     the stage for the producers;
-//   * epilogue (split warpgroup, one TMEM lane quarter per warp):
-//     tcgen05.ld 32x32b -> C += acc through the C offset tables, or the
-//     split-K partial into the workspace.
+//     the stage (smem + its TMEM A slot) for the producers;
+//   * epilogue (split warpgroups; warp w reads TMEM lane quarter w%4, columns
+//     64h..64h+63 for warpgroup h): tcgen05.ld 32x32b -> C += acc through the C
+//     offset tables, or the split-K partial into the workspace.
+// Shared memory traffic per k-block (the bound): 16 KB gathered, 16 KB read
+// by the split, 16 KB of B' hi/lo written, 24 KB of B' read by the MMAs.
 // Accuracy: 3xTF32 products are within ~2^-22 relative, fp32 accumulation in
 // TMEM; checked against the fp64 oracle and the reference (tests/).
 #include <cstdint>
+#include <cstdio>
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.hpp"
 
 #ifndef GETT_TC_STAGES
-#define GETT_TC_STAGES 6
+#define GETT_TC_STAGES 8
 #endif
 
 namespace gett {
 namespace tc {
+
+// Optional per-role cycle accounting (tuning builds only: make variant
+// EXTRA=-DGETT_TC_TRACE); blocks 0 and gridDim.x-1 printf their totals.
+#ifdef GETT_TC_TRACE
+#define TR_DECL(...) long long __VA_ARGS__;
+#define TR_T0() long long _tr0 = clock64();
+#define TR_ADD(v) { long long _tr1 = clock64(); v += _tr1 - _tr0; _tr0 = _tr1; }
+#define TR_PRINT(...) do { if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) printf(__VA_ARGS__); } while (0)
+#else
+#define TR_DECL(...)
+#define TR_T0()
+#define TR_ADD(v)
+#define TR_PRINT(...) do { } while (0)
+#endif
 
 constexpr int BM = 128;
 constexpr int BN = 128;
@@ -41,32 +62,26 @@ constexpr int BK = 16;
 constexpr int CH = BK / 4;                     // 16-byte k-chunks per row
 constexpr int STAGES = GETT_TC_STAGES;
 constexpr int WG = 128;                        // threads per warpgroup
-constexpr int THREADS = 2 * WG + 32;           // producer WG, split/epilogue WG, MMA warp
+constexpr int SPLIT = 2 * WG;                  // split/epilogue threads (two warpgroups)
+constexpr int MMA_WARP = (WG + SPLIT) / 32;    // warp 12
+constexpr int THREADS = WG + SPLIT + 32;       // producer WG, 2 split/epilogue WGs, MMA warp
 constexpr int GROUP_M = 8;
 constexpr int LBO = 128;                       // bytes between k-chunks
 constexpr int SBO = CH * 128;                  // bytes between 8-row groups
-constexpr int TILE_BYTES = 128 * BK * 4;       // one operand part (hi or lo): 8 KB
-constexpr int STAGE_BYTES = 4 * TILE_BYTES;    // A hi, A lo, B hi, B lo
+constexpr int TILE_BYTES = 128 * BK * 4;       // one operand part: 8 KB
+constexpr int STAGE_BYTES = 3 * TILE_BYTES;    // A fp32 staging, B hi, B lo
 constexpr int TCAP = 256;                      // outer k-table entries staged in smem
 constexpr int BAR_BYTES = 256;
 constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 2 * TCAP * 8;
-constexpr uint32_t TMEM_COLS = 128;
+constexpr uint32_t ACC_COLS = BN;              // fp32 accumulator columns
+constexpr uint32_t A_COLS = 2 * BK;            // per stage: A hi (BK cols), A lo (BK cols)
+constexpr uint32_t TMEM_COLS = 512;            // power of two >= ACC_COLS + STAGES * A_COLS
+static_assert(ACC_COLS + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
 static_assert(3 * STAGES + 2 <= BAR_BYTES / 8, "barrier area");
 
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
                            ((uint32_t)(BM >> 4) << 24);
-// ... with A / B MN-major (bits 15 / 16) for operands gathered along their rows
-__host__ __device__ constexpr uint32_t idesc(bool a_mn, bool b_mn) {
-  return IDESC | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16);
-}
-// MN-major no-swizzle layout (rows contiguous): 16-byte chunk of 4 rows at k,
-// core matrix 8 k x 16 B; SBO 128 B between row chunks, LBO 4 KB between k-groups
-constexpr int MN_SBO = 128, MN_LBO = 32 * 128;
-__device__ __forceinline__ uint32_t toff_mn(int mc, int k) {
-  return (uint32_t)(mc * MN_SBO + (k & 7) * 16 + (k >> 3) * MN_LBO);
-}
-
 __device__ __forceinline__ uint32_t toff(int r, int c) {
   return (uint32_t)((r >> 3) * SBO + c * LBO + (r & 7) * 16);
 }
@@ -98,14 +113,14 @@ __device__ __forceinline__ void mbar_wait(uint32_t addr, uint32_t parity) {
       : "memory");
 }
 
-__device__ __forceinline__ void mma_tf32(uint32_t tmem, uint64_t a, uint64_t b, uint32_t acc,
-                                         uint32_t id = IDESC) {
+// A from TMEM (lane = row, 32-bit column = k), B from shared memory
+__device__ __forceinline__ void mma_tf32_ta(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t acc) {
   asm volatile(
       "{\n\t.reg .pred p;\n\t"
       "setp.ne.b32 p, %4, 0;\n\t"
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t"
-      "}" ::"r"(tmem),
-      "l"(a), "l"(b), "r"(id), "r"(acc)
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(IDESC), "r"(acc)
       : "memory");
 }
 
@@ -124,9 +139,10 @@ __device__ __forceinline__ void split4(float4 x, float4& h, float4& l) {
 
 // k-group decoder for one operand: offset(k) = T[k / e_in] + (k % e_in) * s
 struct KDec {
-  const int64_t* T;
+  const int64_t* T;  // outer table, indexed from q0 (a CTA's slice staged in smem)
   int64_t s;
   FastDiv div;
+  int q0;
 };
 
 // One operand's 128-row x BK gather with cp.async by the producer warpgroup.
@@ -140,7 +156,10 @@ struct Gather {
   int64_t roff[4];
   bool rok[4];
   int lr, le, w;
-  int64_t ko[VEC ? 1 : CH];
+  // k offsets of two k-blocks (software pipelined); VEC keeps the table part
+  // apart (kt) so its load is consumed only at issue; the 4-byte path adds it
+  // at once (register budget)
+  int64_t ko[2][VEC ? 1 : CH], kt[2][1];
 
   __device__ __forceinline__ void setup(int warp, int lane, const GroupDev& g, int base_row,
                                         int nrows) {
@@ -158,35 +177,45 @@ struct Gather {
   __device__ __forceinline__ static int64_t koff(const KDec& kd, int k) {
     int q, r;
     kd.div.divmod(k, q, r);
-    return kd.T[q] + (int64_t)r * kd.s;
+    return kd.T[q - kd.q0] + (int64_t)r * kd.s;
+  }
+  // the same offset as table entry + inner part, kept apart so the table load
+  // is consumed only when the copy is issued (a k-block later)
+  __device__ __forceinline__ static void koff2(const KDec& kd, int k, int64_t& t, int64_t& in) {
+    int q, r;
+    kd.div.divmod(k, q, r);
+    t = kd.T[q - kd.q0];
+    in = (int64_t)r * kd.s;
   }
 
+  template <int P>
   __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
     if (VEC) {
       const int k = k0 + 4 * le;
-      ko[0] = k < kend ? koff(kd, k) : 0;
+      if (k < kend) koff2(kd, k, kt[P][0], ko[P][0]);
     } else {
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
         const int k = k0 + 4 * c + le;
-        ko[c] = k < kend ? koff(kd, k) : 0;
+        ko[P][c] = k < kend ? koff(kd, k) : 0;
       }
     }
   }
 
+  template <int P>
   __device__ __forceinline__ void issue(uint8_t* s, const float* base, int k0, int kend) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int r = 8 * (4 * w + i) + lr;
       if (VEC) {
         uint8_t* dst = s + toff(r, le);
-        if (rok[i] && k0 + 4 * le < kend) cp_async_16(dst, base + roff[i] + ko[0]);
+        if (rok[i] && k0 + 4 * le < kend) cp_async_16(dst, base + roff[i] + kt[P][0] + ko[P][0]);
         else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
       } else {
 #pragma unroll
         for (int c = 0; c < CH; ++c) {
           uint8_t* dst = s + toff(r, c) + 4 * le;
-          if (rok[i] && k0 + 4 * c + le < kend) cp_async_4(dst, base + roff[i] + ko[c]);
+          if (rok[i] && k0 + 4 * c + le < kend) cp_async_4(dst, base + roff[i] + ko[P][c]);
           else *reinterpret_cast<float*>(dst) = 0.f;
         }
       }
@@ -205,7 +234,7 @@ struct GatherRV {
   int64_t roff;
   bool rok;
   int lane, w;
-  int64_t ko[4];
+  int64_t ko[2][4], kt[2][4];
 
   __device__ __forceinline__ void setup(int warp, int ln, const GroupDev& g, int base_row,
                                         int nrows) {
@@ -216,20 +245,22 @@ struct GatherRV {
     roff = rok ? g.off(0, r) : 0;
   }
 
+  template <int P>
   __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int k = k0 + 4 * w + i;
-      ko[i] = k < kend ? Gather<true>::koff(kd, k) : 0;
+      if (k < kend) Gather<true>::koff2(kd, k, kt[P][i], ko[P][i]);
     }
   }
 
+  template <int P>
   __device__ __forceinline__ void issue(uint8_t* s, const float* base, int k0, int kend) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int k = 4 * w + i;
       uint8_t* dst = s + k * 512 + lane * 16;
-      if (rok && k0 + k < kend) cp_async_16(dst, base + roff + ko[i]);
+      if (rok && k0 + k < kend) cp_async_16(dst, base + roff + kt[P][i] + ko[P][i]);
       else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
     }
   }
@@ -249,26 +280,27 @@ struct GatherSel<false, false> {
 };
 
 // split + transpose one MN-major staged tile ([k][row] fp32, GatherRV) into the
-// K-major hi tile (same 8 KB, in place) and lo tile.  Split thread t = 32ws + l
-// reads units (k = 4ws + l/8, rows 4rc..4rc+3 with rc = 8i + l%8), i = 0..3
-// (each 8-lane phase reads 128 contiguous bytes); after a warpgroup barrier
-// (the writes land on other threads' inputs) it stores the 4 values of a unit
-// rotated by s = (l/2)%4, so at each store the 32 lanes cover all 8 (row % 8)
-// x 4 (k % 4) positions = 32 distinct banks.
+// K-major hi tile (same 8 KB, in place) and lo tile.  The tile is 16 blocks of
+// 4 k x 8 row-chunks; split warp ws takes blocks 2ws, 2ws+1: lane l reads the
+// unit (k = 4kg + l/8, rows 4rc..4rc+3 with rc = 8rcg + l%8) — each 8-lane phase
+// reads 128 contiguous bytes.  After a barrier over the split threads (the
+// writes land on other threads' inputs) it stores the 4 values rotated by
+// s = (l/2)%4, so at each store the 32 lanes cover all 8 (row % 8) x 4 (k % 4)
+// positions = 32 distinct banks.
+constexpr int RV_BLOCKS = 16 / (SPLIT / 32);
 __device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int t) {
   const int ws = t >> 5, l = t & 31;
-  const int k = 4 * ws + (l >> 3);
-  float4 x[4];
+  float4 x[RV_BLOCKS];
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int rc = 8 * i + (l & 7);
+  for (int i = 0; i < RV_BLOCKS; ++i) {
+    const int b = ws * RV_BLOCKS + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
     x[i] = *reinterpret_cast<const float4*>(hi_s + k * 512 + rc * 16);
   }
-  asm volatile("bar.sync 1, 128;" ::: "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(SPLIT) : "memory");
   const int rot = (l >> 1) & 3;
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const int rc = 8 * i + (l & 7);
+  for (int i = 0; i < RV_BLOCKS; ++i) {
+    const int b = ws * RV_BLOCKS + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
     float4 h, lo;
     split4(x[i], h, lo);
     float hv[4] = {h.x, h.y, h.z, h.w}, lv[4] = {lo.x, lo.y, lo.z, lo.w};
@@ -293,13 +325,13 @@ __device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int 
   }
 }
 
-// split one landed tile (8 KB, either layout): 512 dense 16-byte units, thread t
-// handles units t, t+128, t+256, t+384 (consecutive threads -> consecutive
-// 16 B: conflict-free)
+// split one landed K-major tile (8 KB): 512 dense 16-byte units, split thread t
+// handles units t + SPLIT*i (consecutive threads -> consecutive 16 B:
+// conflict-free)
 __device__ __forceinline__ void split_tile(uint8_t* hi_s, uint8_t* lo_s, int t) {
 #pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const uint32_t o = (uint32_t)(t + WG * i) * 16;
+  for (int i = 0; i < 512 / SPLIT; ++i) {
+    const uint32_t o = (uint32_t)(t + SPLIT * i) * 16;
     float4 x = *reinterpret_cast<const float4*>(hi_s + o);
     float4 h, l;
     split4(x, h, l);
@@ -308,11 +340,46 @@ __device__ __forceinline__ void split_tile(uint8_t* hi_s, uint8_t* lo_s, int t) 
   }
 }
 
+// A' k-block -> TMEM: split thread (warp w, lane l) owns row 32(w%4) + l and
+// k 8h..8h+7 of warpgroup h; reads them from the staging tile (K-major core
+// layout: two 16-byte chunks; [k][row] staging: eight words, consecutive lanes
+// on consecutive words), splits, and writes hi / lo with tcgen05.st into the
+// stage's A columns.  Warp w may only touch TMEM lanes 32(w%4)..+31.
+template <bool RV>
+__device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, uint32_t col, int warp,
+                                             int lane) {
+  const int row = 32 * (warp & 3) + lane, h = (warp - 4) >> 2;
+  float v[8];
+  if (RV) {
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float*>(st + (8 * h + i) * 512 + row * 4);
+  } else {
+    const float4 x0 = *reinterpret_cast<const float4*>(st + toff(row, 2 * h));
+    const float4 x1 = *reinterpret_cast<const float4*>(st + toff(row, 2 * h + 1));
+    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
+    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
+  }
+  uint32_t hi[8], lo[8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi[i]) : "f"(v[i]));
+    lo[i] = __float_as_uint(v[i] - __uint_as_float(hi[i]));
+  }
+  const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col + 8 * h;
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
+               "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]),
+               "r"(hi[7])
+               : "memory");
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + BK),
+               "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]),
+               "r"(lo[7])
+               : "memory");
+}
+
 template <bool AKF, bool BKF, bool AVEC, bool BVEC>
 __global__ void __launch_bounds__(THREADS, 1)
     sgett_tc_kernel(const __grid_constant__ TiledParams<float> p) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr bool AMN = false, BMN = false;  // K-major smem layouts for both operands
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // gathers landed
   uint64_t* ready = full + STAGES;                                            // split done
   uint64_t* empty = ready + STAGES;                                           // MMAs done
@@ -340,27 +407,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   const int kend = min(p.K, kbeg + p.k_chunk);
   const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
 
-  // the K group's outer offset tables, staged in shared memory when small
-  const int n_outer = (p.gk.G + p.gk.e_in.d - 1) / p.gk.e_in.d;
-  KDec kda{p.gk.T[0], p.gk.s_in[0], p.gk.e_in}, kdb{p.gk.T[1], p.gk.s_in[1], p.gk.e_in};
-  if (n_outer <= TCAP) {
-    for (int i = tid; i < n_outer; i += THREADS) {
-      ktabs[i] = __ldg(p.gk.T[0] + i);
-      ktabs[TCAP + i] = __ldg(p.gk.T[1] + i);
+  // this CTA's slice [q0, q1] of the K group's outer offset tables, staged in
+  // shared memory when it fits (c5: 34 of 768 entries)
+  KDec kda{p.gk.T[0], p.gk.s_in[0], p.gk.e_in, 0}, kdb{p.gk.T[1], p.gk.s_in[1], p.gk.e_in, 0};
+  if (nkb > 0) {
+    const int q0 = kbeg / p.gk.e_in.d, q1 = (kend - 1) / p.gk.e_in.d;
+    if (q1 - q0 + 1 <= TCAP) {
+      for (int i = tid; i <= q1 - q0; i += THREADS) {
+        ktabs[i] = __ldg(p.gk.T[0] + q0 + i);
+        ktabs[TCAP + i] = __ldg(p.gk.T[1] + q0 + i);
+      }
+      kda.T = ktabs;
+      kdb.T = ktabs + TCAP;
+      kda.q0 = kdb.q0 = q0;
     }
-    kda.T = ktabs;
-    kdb.T = ktabs + TCAP;
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(full + s), 2 * WG);  // per producer thread: cp.async + plain arrival
-      mbar_init(smem_u32(ready + s), WG);
+      mbar_init(smem_u32(ready + s), SPLIT);
       mbar_init(smem_u32(empty + s), 1);      // tcgen05.commit
     }
     mbar_init(smem_u32(done), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 8) {
+  if (warp == MMA_WARP) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      smem_u32(tmem_slot)),
                  "r"(TMEM_COLS));
@@ -378,41 +449,70 @@ __global__ void __launch_bounds__(THREADS, 1)
     typename GatherSel<BKF, BVEC>::type gb;
     ga.setup(warp, tid & 31, p.gm, m0, p.M);
     gb.setup(warp, tid & 31, p.gn, n0, p.N);
-    for (int kb = 0; kb < nkb; ++kb) {
+    TR_DECL(tp = 0, tw = 0, ti = 0)
+    TR_T0()
+    // k offsets run one k-block ahead of the copies (two register sets, loop
+    // unrolled by 2), so the k-table lookups never sit on the issue path
+    auto step = [&](auto par, int kb) {
+      constexpr int P = decltype(par)::value;
       const int s = kb % STAGES, u = kb / STAGES;
       const int k0 = kbeg + kb * BK;
-      ga.prep(kda, k0, kend);
-      gb.prep(kdb, k0, kend);
       if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
-      ga.issue(stage(s), p.A, k0, kend);
-      gb.issue(stage(s) + 2 * TILE_BYTES, p.B, k0, kend);
+      TR_ADD(tw)
+      ga.template issue<P>(stage(s), p.A, k0, kend);
+      gb.template issue<P>(stage(s) + TILE_BYTES, p.B, k0, kend);
       mbar_arrive_cpasync(smem_u32(full + s));
       mbar_arrive(smem_u32(full + s));
+      TR_ADD(ti)
+      ga.template prep<P>(kda, k0 + 2 * BK, kend);
+      gb.template prep<P>(kdb, k0 + 2 * BK, kend);
+      TR_ADD(tp)
+    };
+    ga.template prep<0>(kda, kbeg, kend);
+    gb.template prep<0>(kdb, kbeg, kend);
+    ga.template prep<1>(kda, kbeg + BK, kend);
+    gb.template prep<1>(kdb, kbeg + BK, kend);
+    for (int kb = 0; kb < nkb; kb += 2) {
+      step(std::integral_constant<int, 0>{}, kb);
+      if (kb + 1 < nkb) step(std::integral_constant<int, 1>{}, kb + 1);
     }
     cp_async_wait<0>();
-  } else if (warp < 8) {
+    if (tid == 0) TR_PRINT("blk %d producer: prep %lld wait_empty %lld issue %lld (nkb %d)\n", blockIdx.x, tp, tw, ti, nkb);
+  } else if (warp < MMA_WARP) {
     // ---------------- split warpgroup, then epilogue ----------------
     const int t = tid - WG;
+    TR_DECL(tw = 0, tsp = 0, te = 0)
+    TR_T0()
     for (int kb = 0; kb < nkb; ++kb) {
       const int s = kb % STAGES, u = kb / STAGES;
       mbar_wait(smem_u32(full + s), u & 1);
+      TR_ADD(tw)
       uint8_t* st = stage(s);
-      if (!AKF && AVEC) split_tile_rv(st, st + TILE_BYTES, t);
-      else split_tile(st, st + TILE_BYTES, t);
-      if (!BKF && BVEC) split_tile_rv(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES, t);
-      else split_tile(st + 2 * TILE_BYTES, st + 3 * TILE_BYTES, t);
+      split_a_tmem<!AKF && AVEC>(st, tmem, ACC_COLS + s * A_COLS, warp, tid & 31);
+      if (!BKF && BVEC) split_tile_rv(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
+      else split_tile(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       mbar_arrive(smem_u32(ready + s));
+      TR_ADD(tsp)
     }
     if (nkb > 0) mbar_wait(smem_u32(done), 0);
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    // thread t owns accumulator row t (TMEM lane t; warp w%4 reads lanes 32(w%4)..)
-    const int m = m0 + t;
+    TR_DECL(twd = 0)
+    TR_ADD(twd)
+    // warp w may only read TMEM lanes 32(w%4)..32(w%4)+31: thread owns accumulator
+    // row 32(w%4) + lane, and split warpgroup h = (w-4)/4 takes columns 64h..64h+63
+    const int lane_row = 32 * (warp & 3) + (tid & 31);
+    const int cbeg = 64 * ((warp - 4) >> 2);
+    const int m = m0 + lane_row;
     const bool mok = m < p.M;
     const int64_t ro = (mok && p.splits == 1) ? p.gm.off(1, m) : 0;
-    float* wrow = p.splits > 1 ? p.ws + ((int64_t)split * p.M + (mok ? m : 0)) * p.N : nullptr;
+    // split-K partials, transposed [split][N][M]: a warp's 32 rows are 32
+    // consecutive floats per column (coalesced); the reduce reads it m-fastest
+    float* wcol = p.splits > 1 ? p.ws + (int64_t)split * p.M * p.N + (mok ? m : 0) : nullptr;
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
+    for (int c0 = cbeg; c0 < cbeg + 64; c0 += 16) {
       uint32_t r[16];
       const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
       asm volatile(
@@ -441,43 +541,45 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + c0 + i;
-          if (n < p.N) wrow[n] = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
+          if (n < p.N) wcol[(int64_t)n * p.M] = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
         }
       }
     }
+    TR_ADD(te)
+    if (t == 0) TR_PRINT("blk %d split: wait_full %lld split %lld wait_done %lld epilogue %lld\n", blockIdx.x, tw, tsp, twd, te);
   } else {
     // ---------------- MMA warp ----------------
     if ((tid & 31) == 0) {
       const uint32_t smem_base = smem_u32(smem);
+      TR_DECL(tw = 0, tm = 0)
+      TR_T0()
       for (int kb = 0; kb < nkb; ++kb) {
         const int s = kb % STAGES, u = kb / STAGES;
         mbar_wait(smem_u32(ready + s), u & 1);
+        TR_ADD(tw)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sb = smem_base + s * STAGE_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
-          // per k-step j: K-major advances 256 B (2 k-chunks), MN-major one k-group
-          const uint32_t ja = AMN ? j * MN_LBO : 256 * j, jb = BMN ? j * MN_LBO : 256 * j;
-          const uint32_t alb = AMN ? MN_LBO : LBO, asb = AMN ? MN_SBO : SBO;
-          const uint32_t blb = BMN ? MN_LBO : LBO, bsb = BMN ? MN_SBO : SBO;
-          const uint64_t ah = sdesc(sb + ja, alb, asb);
-          const uint64_t al = sdesc(sb + TILE_BYTES + ja, alb, asb);
-          const uint64_t bh = sdesc(sb + 2 * TILE_BYTES + jb, blb, bsb);
-          const uint64_t bl = sdesc(sb + 3 * TILE_BYTES + jb, blb, bsb);
-          constexpr uint32_t ID = idesc(AMN, BMN);
-          mma_tf32(tmem, ah, bh, (kb | j) != 0, ID);  // first MMA of the tile overwrites D
-          mma_tf32(tmem, al, bh, 1, ID);
-          mma_tf32(tmem, ah, bl, 1, ID);
+          // k-step j: B' K-major tiles advance 256 B (2 k-chunks), A' 8 TMEM columns
+          const uint32_t ah = tmem + ACC_COLS + s * A_COLS + 8 * j, al = ah + BK;
+          const uint64_t bh = sdesc(sb + TILE_BYTES + 256 * j);
+          const uint64_t bl = sdesc(sb + 2 * TILE_BYTES + 256 * j);
+          mma_tf32_ta(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
+          mma_tf32_ta(tmem, al, bh, 1);
+          mma_tf32_ta(tmem, ah, bl, 1);
         }
         commit(smem_u32(empty + s));
+        TR_ADD(tm)
       }
       commit(smem_u32(done));
+      TR_PRINT("blk %d mma: wait_ready %lld issue %lld\n", blockIdx.x, tw, tm);
     }
     __syncwarp();
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == 8)
+  if (warp == MMA_WARP)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
