@@ -14,15 +14,20 @@ import ctypes
 
 from . import _native
 from .layout import TensorView
-from .plan import decode_errors, prepare
+from .plan import decode_errors, err_buffers, prepare
 
 _DT = {"s": "float32", "d": "float64", "c": "complex64", "z": "complex128"}
+
+
+_WANT = {}
 
 
 def _buf(t, name, prefix):
     import torch
 
-    want = getattr(torch, _DT[prefix])
+    want = _WANT.get(prefix)
+    if want is None:
+        want = _WANT[prefix] = getattr(torch, _DT[prefix])
     if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise TypeError(f"{name} must be a CUDA tensor")
     if t.dim() != 1:
@@ -34,6 +39,17 @@ def _buf(t, name, prefix):
     return t
 
 
+def _raw_stream(dev_index):
+    """Handle of the current torch stream on a device.  The private raw-stream
+    query avoids building a torch.cuda.Stream object (several µs per call)."""
+    import torch
+
+    raw = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+    if raw is not None:
+        return raw(dev_index)
+    return torch.cuda.current_stream(dev_index).cuda_stream
+
+
 def _gett_device(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b,
                  perm, inc_c, c, offset_a=0, offset_b=0, offset_c=0, stream=None):
     import torch
@@ -41,21 +57,19 @@ def _gett_device(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts
     a = _buf(a, "a", prefix)
     b = _buf(b, "b", prefix)
     c = _buf(c, "c", prefix)
-    if not (a.device == b.device == c.device):
+    dev = c.device
+    if not (a.device == b.device == dev):
         raise ValueError("a, b and c must live on one device")
     pr = prepare(rank_a, ext_a, inc_a, offset_a, a.shape[0], rank_b, ext_b, inc_b, offset_b,
                  b.shape[0], conts, cont_a, cont_b, perm, inc_c)
     cap = pr.cap
-    codes = (ctypes.c_int32 * cap)()
-    info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
-    dev = c.device
-    if stream is None:
-        stream = torch.cuda.current_stream(dev)
-    fn = getattr(_native.LIB, f"gett_{prefix}gett_device")
+    codes, info = err_buffers(cap)
+    handle = _raw_stream(dev.index) if stream is None else stream.cuda_stream
+    fn = _FN[prefix]
     args = (*pr.args_a, a.data_ptr(), pr.a_view.base_offset, pr.a_view.buffer_len,
             *pr.args_b, b.data_ptr(), pr.b_view.base_offset, pr.b_view.buffer_len,
             *pr.args_spec, c.data_ptr(), int(offset_c), c.shape[0],
-            ctypes.c_void_p(stream.cuda_stream), codes, info, cap)
+            ctypes.c_void_p(handle), codes, info, cap)
     if torch.cuda.current_device() == dev.index:
         rc = fn(*args)
     else:
@@ -66,6 +80,9 @@ def _gett_device(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts
         return decode_errors(min(n, cap), codes, info, pr.a_view.rank, pr.a_view.extents,
                              pr.b_view.rank, pr.b_view.extents, pr.spec, pr.inc_c)
     return []
+
+
+_FN = {p: getattr(_native.LIB, f"gett_{p}gett_device") for p in "sdcz"}
 
 
 def dgett_device(*args, **kw):

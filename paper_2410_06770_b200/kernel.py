@@ -22,7 +22,7 @@ import numpy as np
 
 from . import _native
 from .layout import TensorView
-from .plan import decode_errors, prepare
+from .plan import decode_errors, err_buffers, prepare
 
 _PREFIX_DTYPE = {
     "s": np.dtype(np.float32),
@@ -60,8 +60,7 @@ def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_
             return errs
         raise ValueError("assignment destination is read-only")
     cap = pr.cap
-    codes = (ctypes.c_int32 * cap)()
-    info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
+    codes, info = err_buffers(cap)
     rc = getattr(_native.LIB, _ENTRY[prefix])(
         *pr.args_a, a.ctypes.data, a_view.base_offset, a_view.buffer_len,
         *pr.args_b, b.ctypes.data, b_view.base_offset, b_view.buffer_len,

@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import ctypes
 import enum
+import threading
 from dataclasses import dataclass
 
 from . import _native
@@ -209,3 +210,18 @@ def prepare(rank_a, ext_a, inc_a, offset_a, len_a, rank_b, ext_b, inc_b, offset_
             _PREP.pop(next(iter(_PREP)))
         _PREP[key] = p
     return p
+
+
+_TLS = threading.local()
+
+
+def err_buffers(cap):
+    """Per-thread error-report buffers (the native side writes them only on a
+    validation failure, and the caller decodes them before returning)."""
+    bufs = getattr(_TLS, "bufs", None)
+    if bufs is None:
+        bufs = _TLS.bufs = {}
+    pair = bufs.get(cap)
+    if pair is None:
+        pair = bufs[cap] = ((ctypes.c_int32 * cap)(), (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))())
+    return pair
