@@ -260,6 +260,8 @@ def run_ours(args):
                 "d2h_bytes_per_step": int(d2h),
                 "how": "dgett() on pinned numpy buffers: H2D spans + kernel + D2H C span, wall clock"},
     }
+    if world == 1 and not args.no_configs:
+        line["other_configs"] = other_configs(dev)
     if world == 1 and not args.no_cpu_baseline:
         threads = len(os.sched_getaffinity(0))
         rows = calibrate_rows(threads, 10.0)
@@ -272,6 +274,45 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def other_configs(dev):
+    """The other BASELINE configs (parity cases, not the headline): device time
+    per call, each call timed alone with CUDA events after an L2 flush (a 256 MB
+    write, > 126 MB L2), median of 7.  Reported for context only."""
+    import torch
+
+    import paper_2410_06770_b200 as g
+    from paper_2410_06770_b200.device import dgett_device, sgett_device
+    from paper_2410_06770_b200.workloads import CONFIGS
+
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device=dev)
+    out = {}
+    for name in ("c1", "c3", "c4", "c5"):
+        w = CONFIGS[name]
+        a, b, c = w.buffers()
+        ta, tb, tc = (torch.from_numpy(x).to(dev) for x in (a, b, c))
+        fn = dgett_device if w.dtype == "d" else sgett_device
+        pos, kw = w.args(ta, tb, tc)
+        for _ in range(3):
+            assert fn(*pos, **kw) == []
+        times = []
+        for _ in range(7):
+            flush.zero_()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn(*pos, **kw)
+            e1.record()
+            e1.synchronize()
+            times.append(e0.elapsed_time(e1))
+        ms = float(np.median(times))
+        out[name] = {"gflops": round(w.flops / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 4),
+                     "dtype": "f64" if w.dtype == "d" else "f32", "kernel": g.last_kernel(),
+                     "l2": "flushed before each call"}
+        del ta, tb, tc
+    del flush
+    torch.cuda.empty_cache()
+    return out
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -279,6 +320,7 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-configs", action="store_true", help="skip the other_configs timings")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -341,7 +341,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   if (g_split > 0) splits = g_split;
   else if (tiles < 148 && kblocks >= 8) {
     splits = 148 / tiles;  // one wave of CTAs (1 CTA per SM for both tiled kernels)
-    if (splits > kblocks / 4) splits = kblocks / 4;
+    if (splits > kblocks / 2) splits = kblocks / 2;  // >= 2 k-blocks per slice
     if (splits < 1) splits = 1;
   }
   if (splits > kblocks) splits = kblocks;
