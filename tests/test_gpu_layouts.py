@@ -14,7 +14,6 @@ import paper_2410_06770_b200 as g
 
 pytestmark = pytest.mark.gpu
 
-M, N = 200, 136
 TOL = {"s": 1e-5, "d": 1e-12}
 
 
@@ -33,7 +32,7 @@ def _view(order, dims, vec, rng_pad):
     return inc, step
 
 
-def _case(dtype, a_kf, a_vec, b_kf, b_vec, c_rowmajor, kmodes, seed):
+def _case(dtype, a_kf, a_vec, b_kf, b_vec, c_rowmajor, kmodes, seed, M, N):
     rng = np.random.default_rng(seed)
     k1, k2 = kmodes
     # A (m, k1, k2); B (k1, k2, n); contract A1-B0, A2-B1; C[m, n]
@@ -62,12 +61,15 @@ LAYOUTS = list(itertools.product([True, False], repeat=5))
 
 @pytest.mark.parametrize("dtype", ["s", "d"])
 @pytest.mark.parametrize("kmodes,split", [((25, 40), 0), ((500, 2), 1)])
-def test_layout_matrix(dtype, kmodes, split, kernel_mode):
+# (200, 136): square-ish tiles; (24, 300) and (300, 40): one narrow operand
+# (mostly-padded tiles, C row-major vs column-major flips the role swap)
+@pytest.mark.parametrize("M,N", [(200, 136), (24, 300), (300, 40)])
+def test_layout_matrix(dtype, kmodes, split, M, N, kernel_mode):
     kernel_mode("tiled", split=split)
     entry = g.sgett if dtype == "s" else g.dgett
     for i, (a_kf, a_vec, b_kf, b_vec, c_row) in enumerate(LAYOUTS):
         (a, a_dims, a_inc, off_a, b, b_dims, b_inc, off_b, c, c_inc,
-         off_c) = _case(dtype, a_kf, a_vec, b_kf, b_vec, c_row, kmodes, 100 + i)
+         off_c) = _case(dtype, a_kf, a_vec, b_kf, b_vec, c_row, kmodes, 100 + i, M, N)
         c0 = c.copy()
         errs = entry(3, a_dims, a_inc, a, 3, b_dims, b_inc, b, 2, (1, 2), (0, 1), (0, 1), c_inc, c,
                      offset_a=off_a, offset_b=off_b, offset_c=off_c)
