@@ -130,6 +130,24 @@ class Workload:
         return replace(self, **kw)
 
 
+def colmajor(w: "Workload") -> "Workload":
+    """The same contraction with every tensor packed first-dimension-fastest
+    (the reference's canonical layout, layout.py:10-11; SURVEY §8d asks for a
+    column-major variant of c3/c4 in parity tests)."""
+    def packed(ext):
+        inc, step = [], 1
+        for e in ext:
+            inc.append(step)
+            step *= int(e)
+        return tuple(inc), step
+
+    inc_a, len_a = packed(w.ext_a)
+    inc_b, len_b = packed(w.ext_b)
+    inc_c, len_c = packed(w.ext_c)
+    return replace(w, name=w.name + "_colmajor", inc_a=inc_a, len_a=len_a, inc_b=inc_b,
+                   len_b=len_b, inc_c=inc_c, len_c=len_c, off_a=0, off_b=0, off_c=0)
+
+
 def _rowmajor(ext):
     inc = [1] * len(ext)
     for i in range(len(ext) - 2, -1, -1):

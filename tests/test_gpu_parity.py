@@ -463,3 +463,51 @@ def test_splitk_device_nccl_group():
         assert errs and errs[0].code == g.ErrorCode.OutputWriteAliasing
     finally:
         dist.destroy_process_group()
+
+
+# ---------------------------------------------------------------------------
+# SURVEY §8d variants: column-major (the reference's canonical layout) and the
+# zeroed-C reading "C = contract(A, B)"
+
+
+@pytest.mark.parametrize("name", ["c3", "c4", "c5"])
+def test_full_config_column_major(name, kernel_mode):
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+    from paper_2410_06770_b200.workloads import colmajor
+
+    kernel_mode("auto")
+    w = colmajor(W[name])
+    a, b, c = w.buffers()
+    c0 = c.copy()
+    pos, kw = w.args(a, b, c)
+    run(ENTRY[w.dtype], pos, kw)
+    ref = oracle.einsum_check(w.ext_a, w.inc_a, a, w.off_a, w.ext_b, w.inc_b, b, w.off_b,
+                              w.conts, w.cont_a, w.cont_b, w.perm)
+    ref = ref + oracle.strided(c0, w.ext_c, w.inc_c, w.off_c).astype(np.float64)
+    got = oracle.strided(c, w.ext_c, w.inc_c, w.off_c)
+    assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K[w.dtype]
+    assert g.last_kernel().split("_")[0] in ("dgett", "sgett")
+
+
+@pytest.mark.parametrize("name", ["c1", "c4", "c5"])
+def test_zeroed_c_then_contract(name, kernel_mode):
+    """zero_view on C's view, then xGETT: C = contract(A, B); padding keeps its
+    bytes through both steps."""
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+
+    kernel_mode("auto")
+    w = W[name]
+    a, b, c = w.buffers()
+    c0 = c.copy()
+    g.zero_view(g.TensorView(len(w.ext_c), w.ext_c, w.inc_c, w.off_c, len(c)), c)
+    offs = view_offsets(w.ext_c, w.inc_c, w.off_c)
+    assert not np.any(c[offs])
+    pos, kw = w.args(a, b, c)
+    run(ENTRY[w.dtype], pos, kw)
+    mask = np.ones(len(c), bool)
+    mask[offs] = False
+    assert c[mask].tobytes() == c0[mask].tobytes()
+    ref = oracle.einsum_check(w.ext_a, w.inc_a, a, w.off_a, w.ext_b, w.inc_b, b, w.off_b,
+                              w.conts, w.cont_a, w.cont_b, w.perm)
+    got = oracle.strided(c, w.ext_c, w.inc_c, w.off_c)
+    assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K[w.dtype]
