@@ -32,6 +32,7 @@ std::mutex g_mu;
 Mode g_mode = Mode::Auto;
 int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
+bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles >= 2 waves (GETT_STREAM_K=0: off)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
 thread_local std::string t_last_error;
@@ -47,6 +48,8 @@ void read_env() {
   if (s) g_split = std::atoi(s);
   const char* wsv = std::getenv("GETT_DGETT_WS");
   if (wsv) g_dgett_ws = std::atoi(wsv) != 0;
+  const char* skv = std::getenv("GETT_STREAM_K");
+  if (skv) g_stream_k = std::atoi(skv) != 0;
   const char* pl = std::getenv("GETT_PIPELINE");
   if (pl) g_pipeline_slabs = std::atoi(pl);
 }
@@ -97,11 +100,21 @@ struct Scratch {
   void* p = nullptr;
   size_t bytes = 0;
 };
+// Workspaces written by kernels are per stream: launches on different streams
+// of one device may overlap.
+struct StreamWs {
+  Scratch ws;         // split-K partials
+  Scratch part;       // stream-K tail partials
+  Scratch flags;      // stream-K publish flags (zeroed on allocation)
+  int32_t epoch = 0;  // stream-K launches so far on this stream
+};
 struct DevState {
   cudaStream_t stream = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
   std::vector<cudaEvent_t> events;
-  Scratch a, b, c, ws;
+  Scratch a, b, c;
+  std::unordered_map<cudaStream_t, StreamWs> sws;
+  int sms = 0;
   cudaEvent_t event(size_t i) {
     while (events.size() <= i) {
       cudaEvent_t e;
@@ -352,10 +365,11 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   tp.ws = nullptr;
   tp.neg = neg;
   tp.ws_t = use_tc ? 1 : 0;
+  StreamWs& sw = ds.sws[stream];
   if (splits > 1) {
-    int rc = ensure(ds.ws, (size_t)splits * M * N * sizeof(T));
+    int rc = ensure(sw.ws, (size_t)splits * M * N * sizeof(T));
     if (rc) return rc;
-    tp.ws = (T*)ds.ws.p;
+    tp.ws = (T*)sw.ws.p;
   }
   // gather directions and vector widths
   bool a_kf = dp.gk.e_in.d > 1 && (dp.gm.e_in.d == 1 || iabs(dp.gk.s_in[0]) < iabs(dp.gm.s_in[0]));
@@ -381,10 +395,38 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     return 0;
   }
   if (sizeof(T) == 8 && g_dgett_ws) {
-    CK(launch_dgett_ws(*reinterpret_cast<TiledParams<double>*>(&tp), a_kf, b_kf, a_vec, b_vec,
-                       stream));
+    SkParams sk;
+    if (!ds.sms) {
+      int dev = 0;
+      CK(cudaGetDevice(&dev));
+      CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    const int64_t G = ds.sms;
+    if (g_stream_k && splits == 1 && tiles >= 2 * G) {
+      // persistent: the last 1-2 waves of tiles are shared out by k-block
+      // units (each CTA's share >= one tile), the rest run data-parallel
+      const int64_t waves = (tiles + G - 1) / G;
+      sk.enabled = 1;
+      sk.grid = (int32_t)G;
+      sk.nkb = dgett_ws_tiles_k((int)K);
+      sk.sk_tile0 = (int32_t)((waves - 2) * G);
+      sk.sk_units = (tiles - sk.sk_tile0) * sk.nkb;
+      int rc = ensure(sw.part, (size_t)G * 128 * 128 * sizeof(double));
+      if (rc) return rc;
+      const size_t fbytes = (size_t)G * sizeof(int32_t);
+      if (sw.flags.bytes < fbytes) {
+        if ((rc = ensure(sw.flags, fbytes))) return rc;
+        CK(cudaMemsetAsync(sw.flags.p, 0, sw.flags.bytes, stream));
+      }
+      if (++sw.epoch <= 0) sw.epoch = 1;
+      sk.part = (double*)sw.part.p;
+      sk.flags = (int32_t*)sw.flags.p;
+      sk.epoch = sw.epoch;
+    }
+    CK(launch_dgett_ws(*reinterpret_cast<TiledParams<double>*>(&tp), sk, a_kf, b_kf, a_vec,
+                       b_vec, stream));
     g_launches += splits > 1 ? 2 : 1;
-    t_last_kernel = splits > 1 ? "dgett_dmma_ws_splitk" : "dgett_dmma_ws";
+    t_last_kernel = splits > 1 ? "dgett_dmma_ws_splitk" : sk.enabled ? "dgett_dmma_ws_sk" : "dgett_dmma_ws";
     return 0;
   }
   CK(launch_tiled<T>(tp, a_kf, b_kf, a_vec, b_vec, stream));
@@ -891,6 +933,12 @@ int gett_set_pipeline(int slabs) {
   return 0;
 }
 
+int gett_set_stream_k(int on) {
+  if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
+  g_stream_k = on != 0;
+  return 0;
+}
+
 const char* gett_last_kernel(void) { return t_last_kernel; }
 const char* gett_last_error(void) { return t_last_error.c_str(); }
 int64_t gett_launch_count(void) { return g_launches; }
@@ -903,12 +951,17 @@ void gett_release_caches(void) {
     int cur;
     cudaGetDevice(&cur);
     cudaSetDevice(kv.first);
-    for (Scratch* s : {&kv.second.a, &kv.second.b, &kv.second.c, &kv.second.ws})
+    cudaDeviceSynchronize();  // kernels may still use the workspaces
+    for (Scratch* s : {&kv.second.a, &kv.second.b, &kv.second.c})
       if (s->p) {
         cudaFree(s->p);
         s->p = nullptr;
         s->bytes = 0;
       }
+    for (auto& sv : kv.second.sws)
+      for (Scratch* s : {&sv.second.ws, &sv.second.part, &sv.second.flags})
+        if (s->p) cudaFree(s->p);
+    kv.second.sws.clear();
     cudaSetDevice(cur);
   }
 }

@@ -87,6 +87,19 @@ struct TiledParams {
   int32_t ws_t = 0; // split-K workspace transposed (tcgen05 SGETT epilogue: m fastest)
 };
 
+// Persistent stream-K schedule of the DGETT kernel (dgett_ws.cu); enabled == 0
+// launches one CTA per tile (and split-K slice).
+struct SkParams {
+  int32_t enabled = 0;
+  int32_t grid = 0;       // persistent CTAs (one per SM)
+  int32_t nkb = 0;        // k-blocks per tile
+  int32_t sk_tile0 = 0;   // tiles [sk_tile0, ntiles) are shared out by k-block units
+  int64_t sk_units = 0;   // (ntiles - sk_tile0) * nkb
+  double* part = nullptr; // [grid][128*128] tail partials
+  int32_t* flags = nullptr;  // [grid] "part published" epochs
+  int32_t epoch = 0;
+};
+
 // the fused epilogue's update: C + acc, or C + (-acc) == C - acc for neg
 template <typename T>
 __device__ __forceinline__ T epi(T c, T acc, int32_t neg) {

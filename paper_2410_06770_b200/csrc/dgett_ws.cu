@@ -118,9 +118,104 @@ __device__ __forceinline__ void produce(double* s, const double* base, const int
   }
 }
 
+// One unit of work for a CTA: k-blocks [kb0, kb1) of tile `tile` (k-block kb
+// covers k in [kbase + kb*BK, +BK) clipped to kend), and what the epilogue does
+// with the accumulator.
+enum SegKind : int {
+  SEG_FULL = 0,    // whole tile: C += acc
+  SEG_SPLITK = 1,  // split-K slice: partial -> workspace (gett_splitk_reduce_kernel)
+  SEG_HEAD = 2,    // stream-K: first part of a tile; adds the tail's partial, then C += acc
+  SEG_TAIL = 3,    // stream-K: last part of a tile; partial -> part[cta], flag[cta] = epoch
+};
+struct Seg {
+  int tile, split, kbase, kend, kb0, kb1, kind;
+};
+
+// Per-CTA work list, identical in the producer and consumer roles.
+//   grid mode (sk.enabled == 0): one segment = tile blockIdx.x % ntiles, split
+//     blockIdx.x / ntiles (the classic one-tile-per-CTA launch, split-K capable);
+//   stream-K mode: the CTA first takes its equal share [c*U/G, (c+1)*U/G) of
+//     the k-block units of the stream-K tiles (the last 1-2 waves' worth), then
+//     the data-parallel tiles c, c+G, ...  Units are equal in length, so tile
+//     boundaries fall at different times in different CTAs: the C epilogues of
+//     concurrently running CTAs no longer hit HBM in one synchronized burst,
+//     and the partial last wave disappears.  A tile cut by the CTA boundary c
+//     is shared by CTA c-1 (head) and CTA c (tail); every share is >= one tile,
+//     so no tile is cut twice.
+struct SegIter {
+  int64_t u, u_end;  // stream-K units still to take
+  int dp;            // next data-parallel tile
+  bool done;
+};
+
+__device__ __forceinline__ void seg_init(const TiledParams<double>& p, const SkParams& sk,
+                                         SegIter& it) {
+  it.done = false;
+  if (!sk.enabled) {
+    it.u = it.u_end = 0;
+    it.dp = -1;
+    return;
+  }
+  const int64_t G = gridDim.x, c = blockIdx.x;
+  it.u = sk.sk_units * c / G;
+  it.u_end = sk.sk_units * (c + 1) / G;
+  it.dp = (int)c;
+}
+
+__device__ __forceinline__ bool seg_next(const TiledParams<double>& p, const SkParams& sk,
+                                         SegIter& it, Seg& sg) {
+  if (it.done) return false;
+  if (!sk.enabled) {
+    const int ntiles = p.tiles_m * p.tiles_n;
+    sg.tile = blockIdx.x % ntiles;
+    sg.split = blockIdx.x / ntiles;
+    sg.kbase = sg.split * p.k_chunk;
+    sg.kend = min(p.K, sg.kbase + p.k_chunk);
+    sg.kb0 = 0;
+    sg.kb1 = sg.kend > sg.kbase ? (sg.kend - sg.kbase + BK - 1) / BK : 0;
+    sg.kind = p.splits == 1 ? SEG_FULL : SEG_SPLITK;
+    it.done = true;
+    return true;
+  }
+  sg.split = 0;
+  sg.kbase = 0;
+  sg.kend = p.K;
+  if (it.u < it.u_end) {
+    const int nkb = sk.nkb;
+    sg.tile = sk.sk_tile0 + (int)(it.u / nkb);
+    sg.kb0 = (int)(it.u % nkb);
+    sg.kb1 = (int)min((int64_t)nkb, sg.kb0 + (it.u_end - it.u));
+    sg.kind = sg.kb0 == 0 ? (sg.kb1 == nkb ? SEG_FULL : SEG_HEAD) : SEG_TAIL;
+    it.u += sg.kb1 - sg.kb0;
+    return true;
+  }
+  if (it.dp < sk.sk_tile0) {
+    sg.tile = it.dp;
+    sg.kb0 = 0;
+    sg.kb1 = sk.nkb;
+    sg.kind = SEG_FULL;
+    it.dp += gridDim.x;
+    return true;
+  }
+  it.done = true;
+  return false;
+}
+
+__device__ __forceinline__ void tile_origin(const TiledParams<double>& p, int tile, int& m0,
+                                            int& n0) {
+  const int per_group = GROUP_M * p.tiles_n;
+  const int group = tile / per_group;
+  const int first_m = group * GROUP_M;
+  const int gsize = min(p.tiles_m - first_m, GROUP_M);
+  const int in_group = tile % per_group;
+  m0 = (first_m + in_group % gsize) * BM;
+  n0 = (in_group / gsize) * BN;
+}
+
 template <bool AKF, bool BKF, bool AVEC, bool BVEC>
 __global__ void __launch_bounds__(THREADS, 1)
-    dgett_ws_kernel(const __grid_constant__ TiledParams<double> p) {
+    dgett_ws_kernel(const __grid_constant__ TiledParams<double> p,
+                    const __grid_constant__ SkParams sk) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   double* smem = reinterpret_cast<double*>(smem_raw);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * STAGE_ELEMS * 8);
@@ -130,30 +225,6 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
-  const int ntiles = p.tiles_m * p.tiles_n;
-  const int tile = blockIdx.x % ntiles;
-  const int split = blockIdx.x / ntiles;
-  int tm, tn;
-  {
-    int per_group = GROUP_M * p.tiles_n;
-    int group = tile / per_group;
-    int first_m = group * GROUP_M;
-    int gsize = min(p.tiles_m - first_m, GROUP_M);
-    int in_group = tile % per_group;
-    tm = first_m + in_group % gsize;
-    tn = in_group / gsize;
-  }
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int kbeg = split * p.k_chunk;
-  const int kend = min(p.K, kbeg + p.k_chunk);
-  const int nkb = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-  const int mvalid = min(128, p.M - m0), nvalid = min(128, p.N - n0);
-
-  // row offsets of this tile's A' rows and B' rows (one decode per row)
-  for (int r = tid; r < 128; r += THREADS) {
-    rowoff_a[r] = r < mvalid ? p.gm.off(0, m0 + r) : 0;
-    rowoff_b[r] = r < nvalid ? p.gn.off(0, n0 + r) : 0;
-  }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(smem_u32(full + s), 2 * PW * 32);  // per producer lane: cp.async + plain arrival
@@ -163,20 +234,38 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   __syncthreads();
 
+  SegIter it;
+  seg_init(p, sk, it);
+  Seg sg;
+
   if (warp >= CW) {
     // ---------------- producer warpgroup ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
-    const int pw = warp - CW;
-    for (int kb = 0; kb < nkb; ++kb) {
-      const int s = kb % STAGES, u = kb / STAGES;
-      if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
-      double* sa = smem + s * STAGE_ELEMS;
-      double* sb = sa + OPER_ELEMS;
-      const int k0 = kbeg + kb * BK;
-      produce<AKF, AVEC, true>(sa, p.A, rowoff_a, mvalid, p.gk, 0, k0, kend, pw, lane);
-      produce<BKF, BVEC, false>(sb, p.B, rowoff_b, nvalid, p.gk, 1, k0, kend, pw, lane);
-      mbar_arrive_cpasync(smem_u32(full + s));  // fires when this lane's copies land
-      mbar_arrive(smem_u32(full + s));          // publishes this lane's padding stores
+    const int pw = warp - CW, ptid = tid - CW * 32;
+    uint32_t g = 0;  // k-blocks produced so far (the stage ring runs across segments)
+    while (seg_next(p, sk, it, sg)) {
+      int m0, n0;
+      tile_origin(p, sg.tile, m0, n0);
+      const int mvalid = min(BM, p.M - m0), nvalid = min(BN, p.N - n0);
+      // the previous segment's copies were issued with the old row offsets:
+      // all producer warps pass before they are overwritten
+      asm volatile("bar.sync 2, %0;" ::"n"(PW * 32) : "memory");
+      for (int r = ptid; r < 128; r += PW * 32) {
+        rowoff_a[r] = r < mvalid ? p.gm.off(0, m0 + r) : 0;
+        rowoff_b[r] = r < nvalid ? p.gn.off(0, n0 + r) : 0;
+      }
+      asm volatile("bar.sync 2, %0;" ::"n"(PW * 32) : "memory");
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
+        const int s = g % STAGES, u = g / STAGES;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        double* sa = smem + s * STAGE_ELEMS;
+        double* sb = sa + OPER_ELEMS;
+        const int k0 = sg.kbase + kb * BK;
+        produce<AKF, AVEC, true>(sa, p.A, rowoff_a, mvalid, p.gk, 0, k0, sg.kend, pw, lane);
+        produce<BKF, BVEC, false>(sb, p.B, rowoff_b, nvalid, p.gk, 1, k0, sg.kend, pw, lane);
+        mbar_arrive_cpasync(smem_u32(full + s));  // fires when this lane's copies land
+        mbar_arrive(smem_u32(full + s));          // publishes this lane's padding stores
+      }
     }
     cp_async_wait<0>();
     return;
@@ -185,11 +274,6 @@ __global__ void __launch_bounds__(THREADS, 1)
   // ---------------- consumer warpgroups ----------------
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
   const int wm0 = (warp / WARPS_N) * WM, wn0 = (warp % WARPS_N) * WN;
-  double acc[MI][NJ][2];
-#pragma unroll
-  for (int i = 0; i < MI; ++i)
-#pragma unroll
-    for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = -0.0;
   int aoff[MI], boff[NJ];
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
@@ -204,99 +288,155 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int AKS = AKF ? 4 : 4 * RF_PITCH;
   constexpr int BKS = BKF ? 4 : 4 * RF_PITCH;
 
-  for (int kb = 0; kb < nkb; ++kb) {
-    const int s = kb % STAGES, u = kb / STAGES;
-    mbar_wait(smem_u32(full + s), u & 1);
-    const double* As = smem + s * STAGE_ELEMS;
-    const double* Bs = As + OPER_ELEMS;
-    double a[2][MI], b[2][NJ];
+  uint32_t g = 0;
+  while (seg_next(p, sk, it, sg)) {
+    int m0, n0;
+    tile_origin(p, sg.tile, m0, n0);
+    double acc[MI][NJ][2];
 #pragma unroll
-    for (int i = 0; i < MI; ++i) a[0][i] = As[aoff[i]];
+    for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int j = 0; j < NJ; ++j) b[0][j] = Bs[boff[j]];
+      for (int j = 0; j < NJ; ++j) acc[i][j][0] = acc[i][j][1] = -0.0;
+
+#pragma unroll 1
+    for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
+      const int s = g % STAGES, u = g / STAGES;
+      mbar_wait(smem_u32(full + s), u & 1);
+      const double* As = smem + s * STAGE_ELEMS;
+      const double* Bs = As + OPER_ELEMS;
+      double a[2][MI], b[2][NJ];
 #pragma unroll
-    for (int ks = 0; ks < BK / 4; ++ks) {
-      const int cur = ks & 1;
-      if (ks + 1 < BK / 4) {
+      for (int i = 0; i < MI; ++i) a[0][i] = As[aoff[i]];
 #pragma unroll
-        for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[aoff[i] + (ks + 1) * AKS];
+      for (int j = 0; j < NJ; ++j) b[0][j] = Bs[boff[j]];
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[boff[j] + (ks + 1) * BKS];
+      for (int ks = 0; ks < BK / 4; ++ks) {
+        const int cur = ks & 1;
+        if (ks + 1 < BK / 4) {
+#pragma unroll
+          for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[aoff[i] + (ks + 1) * AKS];
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[boff[j] + (ks + 1) * BKS];
+        }
+#pragma unroll
+        for (int i = 0; i < MI; ++i)
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
       }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(empty + s));
+    }
+
+    // epilogue: acc[i][j][e] is C'(m0+wm0+i*8+lane/4, n0+wn0+j*8+2*(lane%4)+e)
+    if (sg.kind == SEG_TAIL) {
+      // publish this part for the head's CTA (boundary blockIdx.x)
+      double* w = sk.part + (int64_t)blockIdx.x * (BM * BN);
 #pragma unroll
       for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) dmma884(acc[i][j][0], acc[i][j][1], a[cur][i], b[cur][j]);
+        for (int j = 0; j < NJ; ++j)
+          __stcg(reinterpret_cast<double2*>(w + (wm0 + i * 8 + (lane >> 2)) * BN + wn0 + j * 8 +
+                                            2 * (lane & 3)),
+                 make_double2(acc[i][j][0], acc[i][j][1]));
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(CW * 32) : "memory");
+      if (tid == 0)
+        asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sk.flags + blockIdx.x),
+                     "r"(sk.epoch)
+                     : "memory");
+      continue;
     }
-    __syncwarp();
-    if (lane == 0) mbar_arrive(smem_u32(empty + s));
-  }
-
-  // epilogue: acc[i][j][e] is C'(m0+wm0+i*8+lane/4, n0+wn0+j*8+2*(lane%4)+e)
-  int64_t coff[NJ * 2];
-  bool cok[NJ * 2];
+    if (sg.kind == SEG_HEAD) {
+      // wait for the tail (CTA blockIdx.x + 1, which started on it first) and
+      // add its part: acc = head + tail, the same order for every element
+      const int* f = sk.flags + blockIdx.x + 1;
+      int v;
+      do {
+        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+      } while (v != sk.epoch);
+      const double* w = sk.part + (int64_t)(blockIdx.x + 1) * (BM * BN);
 #pragma unroll
-  for (int j = 0; j < NJ; ++j)
+      for (int i = 0; i < MI; ++i)
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
-      int n = n0 + wn0 + j * 8 + 2 * (lane & 3) + e;
-      cok[j * 2 + e] = n < p.N;
-      coff[j * 2 + e] = (n < p.N) ? (p.splits == 1 ? p.gn.off(1, n) : (int64_t)n) : 0;
+        for (int j = 0; j < NJ; ++j) {
+          const double2 t = __ldcg(reinterpret_cast<const double2*>(
+              w + (wm0 + i * 8 + (lane >> 2)) * BN + wn0 + j * 8 + 2 * (lane & 3)));
+          acc[i][j][0] = acc[i][j][0] + t.x;
+          acc[i][j][1] = acc[i][j][1] + t.y;
+        }
     }
+    const bool to_c = sg.kind != SEG_SPLITK;
+    int64_t coff[NJ * 2];
+    bool cok[NJ * 2];
 #pragma unroll
-  for (int i = 0; i < MI; ++i) {
-    const int m = m0 + wm0 + i * 8 + (lane >> 2);
-    if (m >= p.M) continue;
-    if (p.splits == 1) {
-      const int64_t ro = p.gm.off(1, m);
-      double cv[NJ][2];  // all loads of the row first, then the stores
+    for (int j = 0; j < NJ; ++j)
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+      for (int e = 0; e < 2; ++e) {
+        int n = n0 + wn0 + j * 8 + 2 * (lane & 3) + e;
+        cok[j * 2 + e] = n < p.N;
+        coff[j * 2 + e] = (n < p.N) ? (to_c ? p.gn.off(1, n) : (int64_t)n) : 0;
+      }
 #pragma unroll
-        for (int e = 0; e < 2; ++e) cv[j][e] = cok[j * 2 + e] ? p.C[ro + coff[j * 2 + e]] : 0.0;
+    for (int i = 0; i < MI; ++i) {
+      const int m = m0 + wm0 + i * 8 + (lane >> 2);
+      if (m >= p.M) continue;
+      if (to_c) {
+        const int64_t ro = p.gm.off(1, m);
+        double cv[NJ][2];  // all loads of the row first, then the stores
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (cok[j * 2 + e]) p.C[ro + coff[j * 2 + e]] = epi(cv[j][e], acc[i][j][e], p.neg);
-    } else {
-      double* w = p.ws + ((int64_t)split * p.M + m) * p.N;
+          for (int e = 0; e < 2; ++e) cv[j][e] = cok[j * 2 + e] ? p.C[ro + coff[j * 2 + e]] : 0.0;
 #pragma unroll
-      for (int j = 0; j < NJ; ++j)
+        for (int j = 0; j < NJ; ++j)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
-          if (cok[j * 2 + e]) w[coff[j * 2 + e]] = acc[i][j][e];
+          for (int e = 0; e < 2; ++e)
+            if (cok[j * 2 + e]) p.C[ro + coff[j * 2 + e]] = epi(cv[j][e], acc[i][j][e], p.neg);
+      } else {
+        double* w = p.ws + ((int64_t)sg.split * p.M + m) * p.N;
+#pragma unroll
+        for (int j = 0; j < NJ; ++j)
+#pragma unroll
+          for (int e = 0; e < 2; ++e)
+            if (cok[j * 2 + e]) w[coff[j * 2 + e]] = acc[i][j][e];
+      }
     }
   }
 }
 
 template <bool AKF, bool BKF, bool AV, bool BV>
-cudaError_t launch4(const TiledParams<double>& p, cudaStream_t s) {
+cudaError_t launch4(const TiledParams<double>& p, const SkParams& sk, unsigned grid,
+                    cudaStream_t s) {
   auto k = dgett_ws_kernel<AKF, BKF, AV, BV>;
   static unsigned long long configured = 0;
   cudaError_t e = ensure_dyn_smem(k, SMEM_BYTES, configured);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p);
+  k<<<grid, THREADS, SMEM_BYTES, s>>>(p, sk);
   return cudaGetLastError();
 }
 
 template <bool AKF, bool BKF>
-cudaError_t launch2(const TiledParams<double>& p, bool av, bool bv, cudaStream_t s) {
-  if (av && bv) return launch4<AKF, BKF, true, true>(p, s);
-  if (av) return launch4<AKF, BKF, true, false>(p, s);
-  if (bv) return launch4<AKF, BKF, false, true>(p, s);
-  return launch4<AKF, BKF, false, false>(p, s);
+cudaError_t launch2(const TiledParams<double>& p, const SkParams& sk, unsigned grid, bool av,
+                    bool bv, cudaStream_t s) {
+  if (av && bv) return launch4<AKF, BKF, true, true>(p, sk, grid, s);
+  if (av) return launch4<AKF, BKF, true, false>(p, sk, grid, s);
+  if (bv) return launch4<AKF, BKF, false, true>(p, sk, grid, s);
+  return launch4<AKF, BKF, false, false>(p, sk, grid, s);
 }
 
 }  // namespace ws
 
-cudaError_t launch_dgett_ws(const TiledParams<double>& p, bool a_kf, bool b_kf, bool a_vec,
-                            bool b_vec, cudaStream_t s) {
+int dgett_ws_tiles_k(int K) { return (K + ws::BK - 1) / ws::BK; }
+
+cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, bool a_kf,
+                            bool b_kf, bool a_vec, bool b_vec, cudaStream_t s) {
+  const unsigned grid = sk.enabled ? (unsigned)sk.grid
+                                   : (unsigned)(p.tiles_m * p.tiles_n * p.splits);
   cudaError_t e;
-  if (a_kf && b_kf) e = ws::launch2<true, true>(p, a_vec, b_vec, s);
-  else if (a_kf) e = ws::launch2<true, false>(p, a_vec, b_vec, s);
-  else if (b_kf) e = ws::launch2<false, true>(p, a_vec, b_vec, s);
-  else e = ws::launch2<false, false>(p, a_vec, b_vec, s);
+  if (a_kf && b_kf) e = ws::launch2<true, true>(p, sk, grid, a_vec, b_vec, s);
+  else if (a_kf) e = ws::launch2<true, false>(p, sk, grid, a_vec, b_vec, s);
+  else if (b_kf) e = ws::launch2<false, true>(p, sk, grid, a_vec, b_vec, s);
+  else e = ws::launch2<false, false>(p, sk, grid, a_vec, b_vec, s);
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_splitk_reduce<double>(p, s);
 }

@@ -27,8 +27,9 @@ template <typename R>
 cudaError_t launch_serial_c(const SerialParams<R>& p, cudaStream_t s);
 
 // DGETT warp-specialised (producer warp + DMMA consumer warps), dgett_ws.cu
-cudaError_t launch_dgett_ws(const TiledParams<double>& p, bool a_kf, bool b_kf, bool a_vec,
-                            bool b_vec, cudaStream_t s);
+cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, bool a_kf,
+                            bool b_kf, bool a_vec, bool b_vec, cudaStream_t s);
+int dgett_ws_tiles_k(int K);  // k-blocks per tile
 
 // SGETT 3xTF32 on tcgen05 (sgett_tc.cu)
 cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec,

@@ -511,3 +511,35 @@ def test_zeroed_c_then_contract(name, kernel_mode):
                               w.conts, w.cont_a, w.cont_b, w.perm)
     got = oracle.strided(c, w.ext_c, w.inc_c, w.off_c)
     assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K[w.dtype]
+
+
+# ---------------------------------------------------------------------------
+# DGETT persistent stream-K schedule (tiles split between two CTAs: the head
+# adds the tail's published partial) — deterministic, and equal in accuracy
+# to the one-CTA-per-tile launch
+
+
+@pytest.mark.parametrize("name", ["c3", "c4"])
+def test_stream_k_deterministic_and_accurate(name, kernel_mode):
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+
+    w = W[name]
+    a, b, c = w.buffers()
+    outs = {}
+    for sk in (True, False):
+        kernel_mode("auto", pipeline=0, stream_k=sk)
+        for rep in range(2):
+            cc = c.copy()
+            pos, kw = w.args(a, b, cc)
+            run(ENTRY[w.dtype], pos, kw)
+            kname = g.last_kernel()
+            if rep:
+                assert cc.tobytes() == outs[sk].tobytes(), "run-to-run difference"
+            outs[sk] = cc
+        assert kname == ("dgett_dmma_ws_sk" if sk else "dgett_dmma_ws")
+    ref = oracle.einsum_check(w.ext_a, w.inc_a, a, w.off_a, w.ext_b, w.inc_b, b, w.off_b,
+                              w.conts, w.cont_a, w.cont_b, w.perm)
+    ref = ref + oracle.strided(c, w.ext_c, w.inc_c, w.off_c).astype(np.float64)
+    for sk, cc in outs.items():
+        got = oracle.strided(cc, w.ext_c, w.inc_c, w.off_c)
+        assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"], sk
