@@ -200,8 +200,10 @@ int gett_zero_view_s_device(int rank, const int64_t* ext, const int64_t* inc, in
 /* ---- runtime control ---- */
 /* Kernel selection: "auto" (default), "ref" (reference-order kernel, bitwise
  * equal to the reference on all data), "tiled" (tensor-core / register-tiled
- * kernel), "serial" (one GPU thread, literal reference loop).  Also set by
- * the environment variable GETT_KERNEL.  Returns 0 or GETT_E_INVALID_ARG. */
+ * kernel), "dot" (one warp per output: few outputs, long K), "ffma" (SGETT on
+ * the FP32 FFMA core instead of tcgen05), "serial" (one GPU thread, literal
+ * reference loop).  Also set by the environment variable GETT_KERNEL.
+ * Returns 0 or GETT_E_INVALID_ARG. */
 int gett_set_kernel(const char* name);
 /* Force the split-K factor of the tiled kernel (0 = automatic). */
 int gett_set_split_k(int split);

@@ -26,7 +26,7 @@
 namespace gett {
 namespace {
 
-enum class Mode { Auto, Ref, Tiled, Serial, Ffma };
+enum class Mode { Auto, Ref, Tiled, Serial, Ffma, Dot };
 
 std::mutex g_mu;
 Mode g_mode = Mode::Auto;
@@ -302,6 +302,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   const int64_t M = p.gm.G, N = p.gn.G, K = p.gk.G;
   if (mode == Mode::Auto) {
     if (K <= 8 || M * N * K <= (1LL << 18)) mode = Mode::Ref;
+    else if (M * N <= (1LL << 14) && K >= 64 && M * N * K <= (1LL << 23)) mode = Mode::Dot;
     else mode = Mode::Tiled;
   }
   if (mode == Mode::Serial) {
@@ -321,7 +322,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     ++g_launches;
     return 0;
   }
-  if (mode == Mode::Ref) {
+  if (mode == Mode::Ref || mode == Mode::Dot) {
     RefParams<T> rp;
     rp.A = A; rp.B = B; rp.C = c;
     rp.gm = dp.gm; rp.gn = dp.gn;
@@ -332,8 +333,13 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     rp.k_outer = (int32_t)p.gk_ref.T[0].size();
     rp.kta = dp.kref_a;
     rp.ktb = dp.kref_b;
-    CK(launch_ref<T>(rp, stream));
-    t_last_kernel = sizeof(T) == 8 ? "dgett_ref_order" : "sgett_ref_order";
+    if (mode == Mode::Dot) {
+      CK(launch_dot<T>(rp, stream));
+      t_last_kernel = sizeof(T) == 8 ? "dgett_dot" : "sgett_dot";
+    } else {
+      CK(launch_ref<T>(rp, stream));
+      t_last_kernel = sizeof(T) == 8 ? "dgett_ref_order" : "sgett_ref_order";
+    }
     ++g_launches;
     return 0;
   }
@@ -917,6 +923,7 @@ int gett_set_kernel(const char* name) {
   else if (!strcmp(name, "tiled")) g_mode = Mode::Tiled;
   else if (!strcmp(name, "serial")) g_mode = Mode::Serial;
   else if (!strcmp(name, "ffma")) g_mode = Mode::Ffma;  // SGETT: register-tiled FFMA core
+  else if (!strcmp(name, "dot")) g_mode = Mode::Dot;    // warp per output (few outputs, long K)
   else return GETT_E_INVALID_ARG;
   return 0;
 }

@@ -440,6 +440,46 @@ __global__ void __launch_bounds__(256) gett_ref_kernel(const __grid_constant__ R
   *c = acc;
 }
 
+// Few outputs, long K (c1: 960 outputs x K 1280): one warp per output, lanes
+// stride the K range (reference order decode), a fixed xor-butterfly sum, then
+// C + acc.  Accumulators start at -0.0 like the tiled kernels; the order is
+// fixed, so results are deterministic (not bitwise equal to the sequential
+// loop except on exactly representable data).
+template <typename T>
+__global__ void __launch_bounds__(256) gett_dot_kernel(const __grid_constant__ RefParams<T> p) {
+  const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (w >= (int64_t)p.M * p.N) return;  // warp-uniform
+  const int32_t n = (int32_t)(w % p.N);
+  const int32_t m = (int32_t)(w / p.N);
+  int64_t fa, ca, fb, cb;
+  p.gm.off2(m, fa, ca);
+  p.gn.off2(n, fb, cb);
+  const T* A = p.A + fa;
+  const T* B = p.B + fb;
+  T acc = T(-0.0);
+  int32_t q = 0, r = lane;
+  while (r >= p.k_inner && q < p.k_outer) {
+    r -= p.k_inner;
+    ++q;
+  }
+  for (; q < p.k_outer;) {
+    acc = add_rn(acc, mul_rn(__ldg(A + __ldg(p.kta + q) + (int64_t)r * p.k_sa),
+                             __ldg(B + __ldg(p.ktb + q) + (int64_t)r * p.k_sb)));
+    r += 32;
+    while (r >= p.k_inner && q < p.k_outer) {
+      r -= p.k_inner;
+      ++q;
+    }
+  }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+  if (lane == 0) {
+    T* c = p.C + ca + cb;
+    *c = add_rn(*c, acc);
+  }
+}
+
 // kernel.py:48-78 verbatim on one thread (odometer order, c read each MAC)
 template <typename T>
 __global__ void gett_serial_kernel(const __grid_constant__ SerialParams<T> p) {
@@ -646,6 +686,13 @@ cudaError_t launch_ref(const RefParams<T>& p, cudaStream_t s) {
 }
 
 template <typename T>
+cudaError_t launch_dot(const RefParams<T>& p, cudaStream_t s) {
+  const int64_t threads = (int64_t)p.M * p.N * 32;
+  gett_dot_kernel<T><<<(unsigned)((threads + 255) / 256), 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s) {
   gett_serial_kernel<T><<<1, 1, 0, s>>>(p);
   return cudaGetLastError();
@@ -687,6 +734,8 @@ template cudaError_t launch_splitk_reduce<double>(const TiledParams<double>&, cu
 template cudaError_t launch_splitk_reduce<float>(const TiledParams<float>&, cudaStream_t);
 template cudaError_t launch_ref<double>(const RefParams<double>&, cudaStream_t);
 template cudaError_t launch_ref<float>(const RefParams<float>&, cudaStream_t);
+template cudaError_t launch_dot<double>(const RefParams<double>&, cudaStream_t);
+template cudaError_t launch_dot<float>(const RefParams<float>&, cudaStream_t);
 template cudaError_t launch_serial<double>(const SerialParams<double>&, cudaStream_t);
 template cudaError_t launch_serial<float>(const SerialParams<float>&, cudaStream_t);
 template cudaError_t launch_zero<double>(double*, const GroupDev&, cudaStream_t);

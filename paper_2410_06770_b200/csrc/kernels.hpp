@@ -15,6 +15,8 @@ cudaError_t launch_ref(const RefParams<T>& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s);
 template <typename T>
+cudaError_t launch_dot(const RefParams<T>& p, cudaStream_t s);  // warp per output
+template <typename T>
 cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 
 template <typename T>

@@ -39,7 +39,7 @@ def k_norm_err(got, want, w_or_k, amax=1.0, bmax=1.0):
 # ---------------------------------------------------------------------------
 # known answers (restating the reference's test_kernel.py cases)
 
-MODES = ["auto", "ref", "tiled"]
+MODES = ["auto", "ref", "tiled", "dot"]
 
 
 @pytest.mark.parametrize("mode", MODES)
@@ -159,7 +159,7 @@ def _check_suite_case(case, mode, kernel_mode):
         assert k_norm_err(got, case.want, k) <= TOL_K[case.dtype]
 
 
-@pytest.mark.parametrize("mode", ["ref", "tiled", "auto", "ffma"])
+@pytest.mark.parametrize("mode", ["ref", "tiled", "auto", "ffma", "dot"])
 def test_golden_suite(mode, kernel_mode):
     failures = []
     for case in SUITE:
