@@ -543,3 +543,38 @@ def test_stream_k_deterministic_and_accurate(name, kernel_mode):
     for sk, cc in outs.items():
         got = oracle.strided(cc, w.ext_c, w.inc_c, w.off_c)
         assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"], sk
+
+
+def test_concurrent_streams_keep_separate_workspaces(kernel_mode):
+    """Two device calls in flight on two streams at once — a split-K SGETT (c5)
+    and a stream-K DGETT (c3), twice each — must not share partial-sum
+    workspaces: results equal the same calls run alone."""
+    import torch
+
+    from paper_2410_06770_b200.device import dgett_device, sgett_device
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+
+    kernel_mode("auto")
+    jobs = []
+    for name, fn in (("c5", sgett_device), ("c3", dgett_device)):
+        w = W[name]
+        a, b, c = w.buffers()
+        ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+        alone = torch.from_numpy(c).cuda()
+        pos, kw = w.args(ta, tb, alone)
+        assert fn(*pos, **kw) == []
+        torch.cuda.synchronize()
+        jobs.append((w, fn, ta, tb, c, alone))
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    work = [(job, st, torch.from_numpy(job[4]).cuda()) for _ in range(2)
+            for job, st in zip(jobs, streams)]
+    torch.cuda.synchronize()  # inputs in place; the launches below overlap
+    outs = []
+    for (w, fn, ta, tb, c, alone), st, tc in work:
+        with torch.cuda.stream(st):
+            pos, kw = w.args(ta, tb, tc)
+            assert fn(*pos, **kw) == []
+        outs.append((tc, alone))
+    torch.cuda.synchronize()
+    for tc, alone in outs:
+        assert torch.equal(tc, alone)
