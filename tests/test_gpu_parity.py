@@ -578,3 +578,36 @@ def test_concurrent_streams_keep_separate_workspaces(kernel_mode):
     torch.cuda.synchronize()
     for tc, alone in outs:
         assert torch.equal(tc, alone)
+
+
+@pytest.mark.parametrize("mode", ["auto", "tiled", "ref"])
+def test_offsets_beyond_32_bits(mode, kernel_mode):
+    """Views whose offsets pass 2**31 elements (int64
+    offsets): A lives at element 2**31 + 17 of a 8.6 GB fp32 buffer, C near
+    2**31 of another; checked against the same contraction at offset 0."""
+    import torch
+
+    from paper_2410_06770_b200.device import sgett_device
+
+    kernel_mode(mode)
+    big = (1 << 31) + 70000
+    rng = np.random.default_rng(7)
+    M, K, N = 200, 300, 136
+    a_small = rng.uniform(-1, 1, M * K).astype(np.float32)
+    b = torch.from_numpy(rng.uniform(-1, 1, K * N).astype(np.float32)).cuda()
+    ta = torch.zeros(big, dtype=torch.float32, device="cuda")
+    tc = torch.zeros(big, dtype=torch.float32, device="cuda")
+    off_a, off_c = (1 << 31) + 17, (1 << 31) - 5
+    ta[off_a:off_a + M * K] = torch.from_numpy(a_small).cuda()
+    args = lambda A, C, oa, oc: ((2, (M, K), (K, 1), A, 2, (K, N), (N, 1), b, 1, (1,), (0,),  # noqa: E731
+                                  (0, 1), (N, 1), C), dict(offset_a=oa, offset_c=oc))
+    pos, kw = args(ta, tc, off_a, off_c)
+    assert sgett_device(*pos, **kw) == []
+    ref_c = torch.zeros(M * N, dtype=torch.float32, device="cuda")
+    pos, kw = args(torch.from_numpy(a_small).cuda(), ref_c, 0, 0)
+    assert sgett_device(*pos, **kw) == []
+    torch.cuda.synchronize()
+    assert torch.equal(tc[off_c:off_c + M * N], ref_c)
+    assert int(torch.count_nonzero(tc[:off_c])) == 0 and int(torch.count_nonzero(tc[off_c + M * N:])) == 0
+    del ta, tc
+    torch.cuda.empty_cache()
