@@ -333,6 +333,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     rp.k_outer = (int32_t)p.gk_ref.T[0].size();
     rp.kta = dp.kref_a;
     rp.ktb = dp.kref_b;
+    rp.kdiv = FastDiv::make(rp.k_inner);
     if (mode == Mode::Dot) {
       CK(launch_dot<T>(rp, stream));
       t_last_kernel = sizeof(T) == 8 ? "dgett_dot" : "sgett_dot";

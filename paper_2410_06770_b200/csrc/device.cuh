@@ -120,6 +120,7 @@ struct RefParams {
   int32_t k_outer;      // outer table length
   const int64_t* kta;   // outer offsets in A'
   const int64_t* ktb;   // outer offsets in B'
+  FastDiv kdiv;         // division by k_inner (dot kernel)
 };
 
 // Serial kernel: the literal reference loop (kernel.py:48-78) on one thread,

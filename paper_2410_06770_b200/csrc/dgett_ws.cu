@@ -3,7 +3,8 @@
 // handshakes, no block-wide barrier in the main loop); two consumer
 // warpgroups run only shared-memory fragment loads + FP64 DMMA
 // (mma.sync m8n8k4 -> DMMA.8x8x4) and the fused C += acc epilogue through the
-// C offset tables.  setmaxnreg moves registers from the producer warpgroup
+// C offset tables (red.global.add.f64: one IEEE add per element at L2, no
+// C loads on the SM).  setmaxnreg moves registers from the producer warpgroup
 // (56) to the consumers (208): 2 consumer + 1 producer warp per SM sub-partition.
 //
 // Same semantics and layouts as gett_tiled_kernel<double> (kernels.cu): the
@@ -12,12 +13,27 @@
 // fragment reads); K-tail padding is A' -0.0, B' +0.0 so signed zeros match the
 // sequential reference loop (kernel.py:76); split-K writes partials.
 #include <cstdint>
+#include <cstdio>
 
 #include "device.cuh"
 #include "kernels.hpp"
 
 namespace gett {
 namespace ws {
+
+// Optional per-role cycle accounting (tuning builds only: make variant
+// EXTRA=-DGETT_WS_TRACE); blocks 0 and gridDim.x-1 printf their totals.
+#ifdef GETT_WS_TRACE
+#define TR_DECL(...) long long __VA_ARGS__;
+#define TR_T0() long long _tr0 = clock64();
+#define TR_ADD(v) { long long _tr1 = clock64(); v += _tr1 - _tr0; _tr0 = _tr1; }
+#define TR_PRINT(...) do { if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) printf(__VA_ARGS__); } while (0)
+#else
+#define TR_DECL(...)
+#define TR_T0()
+#define TR_ADD(v)
+#define TR_PRINT(...) do { } while (0)
+#endif
 
 constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, PAD = 4, GROUP_M = 8;
 constexpr int CW = 8;                   // consumer warps (2 warpgroups), warp tile 64 x 32
@@ -289,7 +305,11 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int BKS = BKF ? 4 : 4 * RF_PITCH;
 
   uint32_t g = 0;
+  TR_DECL(cw = 0, cc = 0, ce = 0, cx = 0)
+  TR_T0()
+  int nseg = 0;
   while (seg_next(p, sk, it, sg)) {
+    ++nseg;
     int m0, n0;
     tile_origin(p, sg.tile, m0, n0);
     double acc[MI][NJ][2];
@@ -302,6 +322,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
       const int s = g % STAGES, u = g / STAGES;
       mbar_wait(smem_u32(full + s), u & 1);
+      TR_ADD(cw)
       const double* As = smem + s * STAGE_ELEMS;
       const double* Bs = As + OPER_ELEMS;
       double a[2][MI], b[2][NJ];
@@ -325,6 +346,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(empty + s));
+      TR_ADD(cc)
     }
 
     // epilogue: acc[i][j][e] is C'(m0+wm0+i*8+lane/4, n0+wn0+j*8+2*(lane%4)+e)
@@ -344,6 +366,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(sk.flags + blockIdx.x),
                      "r"(sk.epoch)
                      : "memory");
+      TR_ADD(cx)
       continue;
     }
     if (sg.kind == SEG_HEAD) {
@@ -382,16 +405,18 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (m >= p.M) continue;
       if (to_c) {
         const int64_t ro = p.gm.off(1, m);
-        double cv[NJ][2];  // all loads of the row first, then the stores
-#pragma unroll
-        for (int j = 0; j < NJ; ++j)
-#pragma unroll
-          for (int e = 0; e < 2; ++e) cv[j][e] = cok[j * 2 + e] ? p.C[ro + coff[j * 2 + e]] : 0.0;
+        // C += acc as fire-and-forget fp64 reductions at L2: one IEEE
+        // round-to-nearest add per element (each element is updated by exactly
+        // one thread), so the result equals C + acc and stays deterministic,
+        // and the SM never waits for the C loads
 #pragma unroll
         for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            if (cok[j * 2 + e]) p.C[ro + coff[j * 2 + e]] = epi(cv[j][e], acc[i][j][e], p.neg);
+            if (cok[j * 2 + e])
+              asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p.C + ro + coff[j * 2 + e]),
+                           "d"(p.neg ? -acc[i][j][e] : acc[i][j][e])
+                           : "memory");
       } else {
         double* w = p.ws + ((int64_t)sg.split * p.M + m) * p.N;
 #pragma unroll
@@ -401,7 +426,11 @@ __global__ void __launch_bounds__(THREADS, 1)
             if (cok[j * 2 + e]) w[coff[j * 2 + e]] = acc[i][j][e];
       }
     }
+    TR_ADD(ce)
   }
+  if (warp == 0 && lane == 0)
+    TR_PRINT("blk %d consumer0: segs %d wait_full %lld compute %lld epilogue %lld tail_publish %lld\n",
+             blockIdx.x, nseg, cw, cc, ce, cx);
 }
 
 template <bool AKF, bool BKF, bool AV, bool BV>

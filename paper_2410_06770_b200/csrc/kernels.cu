@@ -445,8 +445,22 @@ __global__ void __launch_bounds__(256) gett_ref_kernel(const __grid_constant__ R
 // C + acc.  Accumulators start at -0.0 like the tiled kernels; the order is
 // fixed, so results are deterministic (not bitwise equal to the sequential
 // loop except on exactly representable data).
+constexpr int DOT_TAB = 1024;  // outer K entries staged in smem per block
+
 template <typename T>
 __global__ void __launch_bounds__(256) gett_dot_kernel(const __grid_constant__ RefParams<T> p) {
+  __shared__ int64_t ta_s[DOT_TAB], tb_s[DOT_TAB];
+  const int64_t* kta = p.kta;
+  const int64_t* ktb = p.ktb;
+  if (p.k_outer <= DOT_TAB) {  // block-uniform: stage the outer K tables once
+    for (int i = threadIdx.x; i < p.k_outer; i += blockDim.x) {
+      ta_s[i] = __ldg(p.kta + i);
+      tb_s[i] = __ldg(p.ktb + i);
+    }
+    __syncthreads();
+    kta = ta_s;
+    ktb = tb_s;
+  }
   const int64_t w = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (int64_t)p.M * p.N) return;  // warp-uniform
@@ -458,19 +472,15 @@ __global__ void __launch_bounds__(256) gett_dot_kernel(const __grid_constant__ R
   const T* A = p.A + fa;
   const T* B = p.B + fb;
   T acc = T(-0.0);
-  int32_t q = 0, r = lane;
-  while (r >= p.k_inner && q < p.k_outer) {
-    r -= p.k_inner;
-    ++q;
-  }
-  for (; q < p.k_outer;) {
-    acc = add_rn(acc, mul_rn(__ldg(A + __ldg(p.kta + q) + (int64_t)r * p.k_sa),
-                             __ldg(B + __ldg(p.ktb + q) + (int64_t)r * p.k_sb)));
-    r += 32;
-    while (r >= p.k_inner && q < p.k_outer) {
-      r -= p.k_inner;
-      ++q;
-    }
+  const int32_t K = p.k_inner * p.k_outer;
+  // independent iterations (one fast division each), so the loads of several
+  // k steps are in flight at once
+#pragma unroll 4
+  for (int32_t k = lane; k < K; k += 32) {
+    int32_t q, r;
+    p.kdiv.divmod(k, q, r);
+    acc = add_rn(acc, mul_rn(__ldg(A + kta[q] + (int64_t)r * p.k_sa),
+                             __ldg(B + ktb[q] + (int64_t)r * p.k_sb)));
   }
 #pragma unroll
   for (int off = 16; off > 0; off >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
