@@ -35,6 +35,10 @@
 #include "device.cuh"
 #include "kernels.hpp"
 
+// tuning builds only: skip the loads (1), the split (2) or the MMAs (4)
+#ifndef GETT_TC_ABLATE
+#define GETT_TC_ABLATE 0
+#endif
 #ifndef GETT_TC_STAGES
 #define GETT_TC_STAGES 8
 #endif
@@ -129,95 +133,119 @@ __device__ __forceinline__ void commit(uint32_t bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void split4(float4 x, float4& h, float4& l) {
-  uint32_t t;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.x)); h.x = __uint_as_float(t); l.x = x.x - h.x;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.y)); h.y = __uint_as_float(t); l.y = x.y - h.y;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.z)); h.z = __uint_as_float(t); l.z = x.z - h.z;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(t) : "f"(x.w)); h.w = __uint_as_float(t); l.w = x.w - h.w;
+// 3xTF32 split with the tensor core's own rounding: kind::tf32 reads the top
+// 19 bits of a 32-bit operand (truncation, tools/tf32_trunc_test.cu), so a raw
+// fp32 value IS its hi part and only lo = x - trunc_tf32(x) (exact in fp32)
+// has to be produced.  hi*hi + lo*hi + hi*lo then misses lo*lo and lo's own
+// truncation: < 2^-19 relative per product (accuracy checked in tests/).
+__device__ __forceinline__ float tf32_lo(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
 
-// k-group decoder for one operand: offset(k) = T[k / e_in] + (k % e_in) * s
+// cp.async with zero fill: sz = 0 writes zeros and reads nothing (the source
+// address is still kept inside the view)
+__device__ __forceinline__ void cp_async_16z(uint32_t dst, const void* src, uint32_t sz) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(dst), "l"(src), "r"(sz));
+}
+__device__ __forceinline__ void cp_async_4z(uint32_t dst, const void* src, uint32_t sz) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(dst), "l"(src), "r"(sz));
+}
+
+// k-group decoder for both operands: offset_t(k) = T_t[k / e_in] + (k % e_in)
+// * s_t, in bytes.  The CTA's slice of the outer tables is staged in shared
+// memory when it fits (STAGED), else read from global memory.
 struct KDec {
-  const int64_t* T;  // outer table, indexed from q0 (a CTA's slice staged in smem)
-  int64_t s;
+  const int64_t* T[2];  // global outer tables (element offsets)
+  uint32_t Ts[2];       // shared-memory addresses of the staged slices (bytes)
+  int q0;               // first staged entry
+  int64_t s[2];         // inner strides, bytes
   FastDiv div;
-  int q0;
 };
+
+// Lane-parallel k offsets for one k-block: lane l looks up operand l/16 at
+// k = k0 + l%16 (0 past kend), so a warp decodes all 2 x BK offsets of the
+// k-block with one divmod + one table load per lane; the gathers then take the
+// ones they need with shuffles (kofs).
+template <bool STAGED>
+__device__ __forceinline__ int64_t klane(const KDec& kd, int k0, int kend, int lane) {
+  const int t = lane >> 4, k = k0 + (lane & 15);
+  if (k >= kend) return 0;
+  int q, r;
+  kd.div.divmod(k, q, r);
+  int64_t tb;
+  if (STAGED) {
+    const uint32_t a = (t ? kd.Ts[1] : kd.Ts[0]) + 8u * (uint32_t)(q - kd.q0);
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(tb) : "r"(a));
+  } else {
+    tb = __ldg((t ? kd.T[1] : kd.T[0]) + q) * 4;
+  }
+  return tb + (int64_t)r * (t ? kd.s[1] : kd.s[0]);
+}
+static_assert(BK == 16, "klane covers 16 k per operand");
+
+// offset of operand t at k-block-relative k (0..15) from the klane values
+__device__ __forceinline__ int64_t kofs(int64_t v, int t, int kk) {
+  return __shfl_sync(0xffffffffu, v, 16 * t + kk);
+}
 
 // One operand's 128-row x BK gather with cp.async by the producer warpgroup.
 // Warp w owns row groups 4w..4w+3 (8 rows each).  One warp instruction covers
 // 8 consecutive rows x 4 k: lane l -> row 8g + l%8 and, for 16-byte copies
 // (VEC: 4 contiguous k per row), chunk l/8 (8 rows x 64 B of gmem, four
 // conflict-free 128 B smem wavefronts); for 4-byte copies, k = 4c + l/8 of
-// chunk c (32 distinct smem banks; 8 rows x 4 k of gmem).
+// chunk c (32 distinct smem banks; 8 rows x 4 k of gmem).  Row base pointers
+// are decoded once per tile; a copy is one 64-bit add + cp.async (zero fill
+// for rows past the view and the K tail).
 template <bool VEC>
 struct Gather {
-  int64_t roff[4];
-  bool rok[4];
-  int lr, le, w;
-  // k offsets of two k-blocks (software pipelined); VEC keeps the table part
-  // apart (kt) so its load is consumed only at issue; the 4-byte path adds it
-  // at once (register budget)
-  int64_t ko[2][VEC ? 1 : CH], kt[2][1];
+  const char* rp[4];
+  uint32_t rsz[4];  // copy size for the row (0 past the view)
+  uint32_t dst0;    // this thread's unit in a tile (bytes)
+  int le;
+  int64_t ko[2][VEC ? 1 : CH];  // k offsets (bytes; 0 in the K tail) ...
+  uint32_t km[2][VEC ? 1 : CH];  // ... and copy-size masks (0 in the K tail)
 
-  __device__ __forceinline__ void setup(int warp, int lane, const GroupDev& g, int base_row,
-                                        int nrows) {
-    w = warp;
-    lr = lane & 7;
+  __device__ __forceinline__ void setup(int warp, int lane, const GroupDev& g, const float* base,
+                                        int base_row, int nrows) {
+    const int lr = lane & 7;
     le = lane >> 3;
+    const char* r0 = reinterpret_cast<const char*>(base + g.off(0, 0));
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      int r = base_row + 8 * (4 * w + i) + lr;
-      rok[i] = r < nrows;
-      roff[i] = rok[i] ? g.off(0, r) : 0;
+      int r = base_row + 8 * (4 * warp + i) + lr;
+      const bool ok = r < nrows;
+      rp[i] = ok ? reinterpret_cast<const char*>(base + g.off(0, r)) : r0;
+      rsz[i] = ok ? (VEC ? 16u : 4u) : 0u;
     }
+    dst0 = toff(8 * (4 * warp) + lr, VEC ? le : 0) + (VEC ? 0 : 4 * le);
   }
 
-  __device__ __forceinline__ static int64_t koff(const KDec& kd, int k) {
-    int q, r;
-    kd.div.divmod(k, q, r);
-    return kd.T[q - kd.q0] + (int64_t)r * kd.s;
-  }
-  // the same offset as table entry + inner part, kept apart so the table load
-  // is consumed only when the copy is issued (a k-block later)
-  __device__ __forceinline__ static void koff2(const KDec& kd, int k, int64_t& t, int64_t& in) {
-    int q, r;
-    kd.div.divmod(k, q, r);
-    t = kd.T[q - kd.q0];
-    in = (int64_t)r * kd.s;
-  }
-
+  // take this k-block's offsets of operand t from the warp's klane values
   template <int P>
-  __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
+  __device__ __forceinline__ void prep(int64_t kl, int t, int k0, int kend) {
     if (VEC) {
-      const int k = k0 + 4 * le;
-      if (k < kend) koff2(kd, k, kt[P][0], ko[P][0]);
+      ko[P][0] = kofs(kl, t, 4 * le);
+      km[P][0] = k0 + 4 * le < kend ? ~0u : 0u;
     } else {
 #pragma unroll
       for (int c = 0; c < CH; ++c) {
-        const int k = k0 + 4 * c + le;
-        ko[P][c] = k < kend ? koff(kd, k) : 0;
+        ko[P][c] = kofs(kl, t, 4 * c + le);
+        km[P][c] = k0 + 4 * c + le < kend ? ~0u : 0u;
       }
     }
   }
 
   template <int P>
-  __device__ __forceinline__ void issue(uint8_t* s, const float* base, int k0, int kend) {
+  __device__ __forceinline__ void issue(uint32_t s) {
+    // row group i is 8 rows = SBO bytes further on
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int r = 8 * (4 * w + i) + lr;
       if (VEC) {
-        uint8_t* dst = s + toff(r, le);
-        if (rok[i] && k0 + 4 * le < kend) cp_async_16(dst, base + roff[i] + kt[P][0] + ko[P][0]);
-        else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+        cp_async_16z(s + dst0 + i * SBO, rp[i] + ko[P][0], rsz[i] & km[P][0]);
       } else {
 #pragma unroll
-        for (int c = 0; c < CH; ++c) {
-          uint8_t* dst = s + toff(r, c) + 4 * le;
-          if (rok[i] && k0 + 4 * c + le < kend) cp_async_4(dst, base + roff[i] + ko[P][c]);
-          else *reinterpret_cast<float*>(dst) = 0.f;
-        }
+        for (int c = 0; c < CH; ++c)
+          cp_async_4z(s + dst0 + i * SBO + c * LBO, rp[i] + ko[P][c], rsz[i] & km[P][c]);
       }
     }
   }
@@ -225,43 +253,42 @@ struct Gather {
 
 // Rows-contiguous operand with 16-byte row chunks (unit-stride inner row mode,
 // extent and all offsets divisible by 4): staged MN-major, [k][128 rows] fp32
-// (512 B per k), and transposed into the K-major hi/lo tiles by the split
-// warpgroup (split_tile_rv) — the tf32 UMMA reads K-major only.  Warp w,
-// instruction i copies k = 4w + i: lane l -> rows 4l..4l+3, so one warp
-// instruction moves 512 contiguous bytes of gmem into 512 contiguous bytes of
-// smem (the 4-byte path needs 16 instructions for the same k-block).
+// (512 B per k), and transposed by the split warpgroup (split_a_tmem /
+// split_tile_rv) — the tf32 UMMA reads K-major only.  Warp w, instruction i
+// copies k = 4w + i: lane l -> rows 4l..4l+3, so one warp instruction moves
+// 512 contiguous bytes of gmem into 512 contiguous bytes of smem.
 struct GatherRV {
-  int64_t roff;
-  bool rok;
-  int lane, w;
-  int64_t ko[2][4], kt[2][4];
+  const char* rp;
+  uint32_t rsz;
+  uint32_t dst0;
+  int w;
+  int64_t ko[2][4];
+  uint32_t km[2][4];
 
-  __device__ __forceinline__ void setup(int warp, int ln, const GroupDev& g, int base_row,
-                                        int nrows) {
+  __device__ __forceinline__ void setup(int warp, int lane, const GroupDev& g, const float* base,
+                                        int base_row, int nrows) {
     w = warp;
-    lane = ln;
     const int r = base_row + 4 * lane;
-    rok = r < nrows;
-    roff = rok ? g.off(0, r) : 0;
+    const bool ok = r < nrows;
+    rp = reinterpret_cast<const char*>(base + g.off(0, ok ? r : 0));
+    rsz = ok ? 16u : 0u;
+    dst0 = (uint32_t)(4 * w * 512 + lane * 16);
   }
 
   template <int P>
-  __device__ __forceinline__ void prep(const KDec& kd, int k0, int kend) {
+  __device__ __forceinline__ void prep(int64_t kl, int t, int k0, int kend) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int k = k0 + 4 * w + i;
-      if (k < kend) Gather<true>::koff2(kd, k, kt[P][i], ko[P][i]);
+      ko[P][i] = kofs(kl, t, 4 * w + i);
+      km[P][i] = k0 + 4 * w + i < kend ? ~0u : 0u;
     }
   }
 
   template <int P>
-  __device__ __forceinline__ void issue(uint8_t* s, const float* base, int k0, int kend) {
+  __device__ __forceinline__ void issue(uint32_t s) {
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
-      const int k = 4 * w + i;
-      uint8_t* dst = s + k * 512 + lane * 16;
-      if (rok && k0 + k < kend) cp_async_16(dst, base + roff + kt[P][i] + ko[P][i]);
-      else *reinterpret_cast<float4*>(dst) = make_float4(0.f, 0.f, 0.f, 0.f);
+      cp_async_16z(s + dst0 + i * 512, rp + ko[P][i], rsz & km[P][i]);
     }
   }
 };
@@ -279,14 +306,14 @@ struct GatherSel<false, false> {
   using type = Gather<false>;
 };
 
-// split + transpose one MN-major staged tile ([k][row] fp32, GatherRV) into the
-// K-major hi tile (same 8 KB, in place) and lo tile.  The tile is 16 blocks of
-// 4 k x 8 row-chunks; split warp ws takes blocks 2ws, 2ws+1: lane l reads the
-// unit (k = 4kg + l/8, rows 4rc..4rc+3 with rc = 8rcg + l%8) — each 8-lane phase
-// reads 128 contiguous bytes.  After a barrier over the split threads (the
-// writes land on other threads' inputs) it stores the 4 values rotated by
-// s = (l/2)%4, so at each store the 32 lanes cover all 8 (row % 8) x 4 (k % 4)
-// positions = 32 distinct banks.
+// transpose one MN-major staged tile ([k][row] fp32, GatherRV) into the
+// K-major hi tile (same 8 KB, in place: the raw value is the hi part) and the
+// lo tile.  The tile is 16 blocks of 4 k x 8 row-chunks; split warp ws takes
+// blocks 2ws, 2ws+1: lane l reads the unit (k = 4kg + l/8, rows 4rc..4rc+3
+// with rc = 8rcg + l%8) — each 8-lane phase reads 128 contiguous bytes.  After
+// a barrier over the split threads (the writes land on other threads' inputs)
+// it stores the 4 values rotated by s = (l/2)%4, so at each store the 32 lanes
+// cover all 8 (row % 8) x 4 (k % 4) positions = 32 distinct banks.
 constexpr int RV_BLOCKS = 16 / (SPLIT / 32);
 __device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int t) {
   const int ws = t >> 5, l = t & 31;
@@ -301,50 +328,44 @@ __device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int 
 #pragma unroll
   for (int i = 0; i < RV_BLOCKS; ++i) {
     const int b = ws * RV_BLOCKS + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
-    float4 h, lo;
-    split4(x[i], h, lo);
-    float hv[4] = {h.x, h.y, h.z, h.w}, lv[4] = {lo.x, lo.y, lo.z, lo.w};
+    float hv[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
     // rotate left by rot with selects (no dynamic register indexing)
     if (rot & 1) {
-      float th = hv[0], tl = lv[0];
+      float th = hv[0];
       hv[0] = hv[1]; hv[1] = hv[2]; hv[2] = hv[3]; hv[3] = th;
-      lv[0] = lv[1]; lv[1] = lv[2]; lv[2] = lv[3]; lv[3] = tl;
     }
     if (rot & 2) {
-      float th0 = hv[0], th1 = hv[1], tl0 = lv[0], tl1 = lv[1];
+      float th0 = hv[0], th1 = hv[1];
       hv[0] = hv[2]; hv[1] = hv[3]; hv[2] = th0; hv[3] = th1;
-      lv[0] = lv[2]; lv[1] = lv[3]; lv[2] = tl0; lv[3] = tl1;
     }
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       const int row = 4 * rc + ((j + rot) & 3);
       const uint32_t o = toff(row, k >> 2) + (k & 3) * 4;
       *reinterpret_cast<float*>(hi_s + o) = hv[j];
-      *reinterpret_cast<float*>(lo_s + o) = lv[j];
+      *reinterpret_cast<float*>(lo_s + o) = tf32_lo(hv[j]);
     }
   }
 }
 
-// split one landed K-major tile (8 KB): 512 dense 16-byte units, split thread t
-// handles units t + SPLIT*i (consecutive threads -> consecutive 16 B:
-// conflict-free)
-__device__ __forceinline__ void split_tile(uint8_t* hi_s, uint8_t* lo_s, int t) {
+// lo part of one landed K-major tile (8 KB; the tile itself is the hi part):
+// 512 dense 16-byte units, split thread t handles units t + SPLIT*i
+// (consecutive threads -> consecutive 16 B: conflict-free)
+__device__ __forceinline__ void split_tile(const uint8_t* hi_s, uint8_t* lo_s, int t) {
 #pragma unroll
   for (int i = 0; i < 512 / SPLIT; ++i) {
     const uint32_t o = (uint32_t)(t + SPLIT * i) * 16;
-    float4 x = *reinterpret_cast<const float4*>(hi_s + o);
-    float4 h, l;
-    split4(x, h, l);
-    *reinterpret_cast<float4*>(hi_s + o) = h;
-    *reinterpret_cast<float4*>(lo_s + o) = l;
+    const float4 x = *reinterpret_cast<const float4*>(hi_s + o);
+    *reinterpret_cast<float4*>(lo_s + o) =
+        make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
   }
 }
 
 // A' k-block -> TMEM: split thread (warp w, lane l) owns row 32(w%4) + l and
 // k 8h..8h+7 of warpgroup h; reads them from the staging tile (K-major core
 // layout: two 16-byte chunks; [k][row] staging: eight words, consecutive lanes
-// on consecutive words), splits, and writes hi / lo with tcgen05.st into the
-// stage's A columns.  Warp w may only touch TMEM lanes 32(w%4)..+31.
+// on consecutive words) and writes the raw values (hi) and lo with tcgen05.st
+// into the stage's A columns.  Warp w may only touch TMEM lanes 32(w%4)..+31.
 template <bool RV>
 __device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, uint32_t col, int warp,
                                              int lane) {
@@ -362,8 +383,8 @@ __device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, u
   uint32_t hi[8], lo[8];
 #pragma unroll
   for (int i = 0; i < 8; ++i) {
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(hi[i]) : "f"(v[i]));
-    lo[i] = __float_as_uint(v[i] - __uint_as_float(hi[i]));
+    hi[i] = __float_as_uint(v[i]);
+    lo[i] = __float_as_uint(tf32_lo(v[i]));
   }
   const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col + 8 * h;
   asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
@@ -409,22 +430,23 @@ __global__ void __launch_bounds__(THREADS, 1)
 
   // this CTA's slice [q0, q1] of the K group's outer offset tables, staged in
   // shared memory when it fits (c5: 34 of 768 entries)
-  KDec kda{p.gk.T[0], p.gk.s_in[0], p.gk.e_in, 0}, kdb{p.gk.T[1], p.gk.s_in[1], p.gk.e_in, 0};
+  // (in bytes)
+  KDec kd{{p.gk.T[0], p.gk.T[1]}, {0u, 0u}, 0, {p.gk.s_in[0] * 4, p.gk.s_in[1] * 4}, p.gk.e_in};
   if (nkb > 0) {
     const int q0 = kbeg / p.gk.e_in.d, q1 = (kend - 1) / p.gk.e_in.d;
     if (q1 - q0 + 1 <= TCAP) {
       for (int i = tid; i <= q1 - q0; i += THREADS) {
-        ktabs[i] = __ldg(p.gk.T[0] + q0 + i);
-        ktabs[TCAP + i] = __ldg(p.gk.T[1] + q0 + i);
+        ktabs[i] = __ldg(p.gk.T[0] + q0 + i) * 4;
+        ktabs[TCAP + i] = __ldg(p.gk.T[1] + q0 + i) * 4;
       }
-      kda.T = ktabs;
-      kdb.T = ktabs + TCAP;
-      kda.q0 = kdb.q0 = q0;
+      kd.Ts[0] = smem_u32(ktabs);
+      kd.Ts[1] = smem_u32(ktabs + TCAP);
+      kd.q0 = q0;
     }
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(full + s), 2 * WG);  // per producer thread: cp.async + plain arrival
+      mbar_init(smem_u32(full + s), WG);  // per producer thread: its cp.async group (zero fill included)
       mbar_init(smem_u32(ready + s), SPLIT);
       mbar_init(smem_u32(empty + s), 1);      // tcgen05.commit
     }
@@ -447,35 +469,46 @@ __global__ void __launch_bounds__(THREADS, 1)
     // ---------------- producer warpgroup ----------------
     typename GatherSel<AKF, AVEC>::type ga;
     typename GatherSel<BKF, BVEC>::type gb;
-    ga.setup(warp, tid & 31, p.gm, m0, p.M);
-    gb.setup(warp, tid & 31, p.gn, n0, p.N);
+    ga.setup(warp, tid & 31, p.gm, p.A, m0, p.M);
+    gb.setup(warp, tid & 31, p.gn, p.B, n0, p.N);
+    const uint32_t sbase = smem_u32(smem);
     TR_DECL(tp = 0, tw = 0, ti = 0)
     TR_T0()
+    const int lane = tid & 31;
     // k offsets run one k-block ahead of the copies (two register sets, loop
     // unrolled by 2), so the k-table lookups never sit on the issue path
-    auto step = [&](auto par, int kb) {
-      constexpr int P = decltype(par)::value;
-      const int s = kb % STAGES, u = kb / STAGES;
-      const int k0 = kbeg + kb * BK;
-      if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
-      TR_ADD(tw)
-      ga.template issue<P>(stage(s), p.A, k0, kend);
-      gb.template issue<P>(stage(s) + TILE_BYTES, p.B, k0, kend);
-      mbar_arrive_cpasync(smem_u32(full + s));
-      mbar_arrive(smem_u32(full + s));
-      TR_ADD(ti)
-      ga.template prep<P>(kda, k0 + 2 * BK, kend);
-      gb.template prep<P>(kdb, k0 + 2 * BK, kend);
-      TR_ADD(tp)
+    auto run = [&](auto staged) {
+      constexpr bool ST = decltype(staged)::value;
+      auto prep = [&](auto par, int k0) {
+        constexpr int P = decltype(par)::value;
+        const int64_t kl = klane<ST>(kd, k0, kend, lane);
+        ga.template prep<P>(kl, 0, k0, kend);
+        gb.template prep<P>(kl, 1, k0, kend);
+      };
+      auto step = [&](auto par, int kb) {
+        constexpr int P = decltype(par)::value;
+        const int s = kb % STAGES, u = kb / STAGES;
+        const int k0 = kbeg + kb * BK;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        TR_ADD(tw)
+        if (!(GETT_TC_ABLATE & 1)) {
+          ga.template issue<P>(sbase + s * STAGE_BYTES);
+          gb.template issue<P>(sbase + s * STAGE_BYTES + TILE_BYTES);
+        }
+        mbar_arrive_cpasync(smem_u32(full + s));
+        TR_ADD(ti)
+        prep(par, k0 + 2 * BK);
+        TR_ADD(tp)
+      };
+      prep(std::integral_constant<int, 0>{}, kbeg);
+      prep(std::integral_constant<int, 1>{}, kbeg + BK);
+      for (int kb = 0; kb < nkb; kb += 2) {
+        step(std::integral_constant<int, 0>{}, kb);
+        if (kb + 1 < nkb) step(std::integral_constant<int, 1>{}, kb + 1);
+      }
     };
-    ga.template prep<0>(kda, kbeg, kend);
-    gb.template prep<0>(kdb, kbeg, kend);
-    ga.template prep<1>(kda, kbeg + BK, kend);
-    gb.template prep<1>(kdb, kbeg + BK, kend);
-    for (int kb = 0; kb < nkb; kb += 2) {
-      step(std::integral_constant<int, 0>{}, kb);
-      if (kb + 1 < nkb) step(std::integral_constant<int, 1>{}, kb + 1);
-    }
+    if (kd.Ts[0]) run(std::true_type{});
+    else run(std::false_type{});
     cp_async_wait<0>();
     if (tid == 0) TR_PRINT("blk %d producer: prep %lld wait_empty %lld issue %lld (nkb %d)\n", blockIdx.x, tp, tw, ti, nkb);
   } else if (warp < MMA_WARP) {
@@ -488,9 +521,11 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(smem_u32(full + s), u & 1);
       TR_ADD(tw)
       uint8_t* st = stage(s);
-      split_a_tmem<!AKF && AVEC>(st, tmem, ACC_COLS + s * A_COLS, warp, tid & 31);
-      if (!BKF && BVEC) split_tile_rv(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
-      else split_tile(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
+      if (!(GETT_TC_ABLATE & 2)) {
+        split_a_tmem<!AKF && AVEC>(st, tmem, ACC_COLS + s * A_COLS, warp, tid & 31);
+        if (!BKF && BVEC) split_tile_rv(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
+        else split_tile(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -565,6 +600,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           const uint32_t ah = tmem + ACC_COLS + s * A_COLS + 8 * j, al = ah + BK;
           const uint64_t bh = sdesc(sb + TILE_BYTES + 256 * j);
           const uint64_t bl = sdesc(sb + 2 * TILE_BYTES + 256 * j);
+          if (GETT_TC_ABLATE & 4) continue;
           mma_tf32_ta(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
           mma_tf32_ta(tmem, al, bh, 1);
           mma_tf32_ta(tmem, ah, bl, 1);

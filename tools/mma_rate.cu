@@ -1,0 +1,169 @@
+// tcgen05.mma issue-rate micro-benchmark: cycles per back-to-back MMA for
+// kind::tf32 / kind::f16, M = 128, N in {64, 128, 256}, A from shared memory
+// or from TMEM, B from shared memory (K-major, no swizzle).  One CTA per SM
+// (grid 148), one elected thread issues; block 0's clock64 span is reported.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/mma_rate tools/mma_rate.cu
+#include <cstdint>
+#include <cstdio>
+
+__device__ __forceinline__ uint32_t su32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ uint64_t sdesc(uint32_t a, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((a >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         (1ull << 46);
+}
+
+template <int N, bool ATM, bool F16>
+__global__ void rate(long long* out, int iters) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  uint64_t* bar = (uint64_t*)(sm + 98304);
+  uint32_t* slot = (uint32_t*)(bar + 2);
+  for (int i = threadIdx.x; i < 98304 / 4; i += blockDim.x) ((float*)sm)[i] = 0.f;
+  if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;
+  constexpr uint32_t AF = F16 ? 0u : 2u;
+  constexpr uint32_t IDESC =
+      (1u << 4) | (AF << 7) | (AF << 10) | ((uint32_t)(N >> 3) << 17) | ((128u >> 4) << 24);
+  if (threadIdx.x == 0) {
+    const uint32_t base = su32(sm);
+    // A: 128 rows x 32 B of K at base (SBO 256: two 16 B chunks per 8-row group)
+    // B: N rows x 32 B at base + 32 KB
+    const uint64_t ad = sdesc(base, 128, 256), bd = sdesc(base + 32768, 128, 256);
+    long long t0 = clock64();
+    for (int it = 0; it < iters; ++it) {
+#define MMA_TM(K) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t" \
+                     "tcgen05.mma.cta_group::1.kind::" K " [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem), \
+                     "r"(tmem + 256), "l"(bd), "r"(IDESC), "r"(it))
+#define MMA_SS(K) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t" \
+                     "tcgen05.mma.cta_group::1.kind::" K " [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem), \
+                     "l"(ad), "l"(bd), "r"(IDESC), "r"(it))
+      if (ATM) {
+        if (F16) MMA_TM("f16"); else MMA_TM("tf32");
+      } else {
+        if (F16) MMA_SS("f16"); else MMA_SS("tf32");
+      }
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar)));
+    asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W_%=;\n\t}" ::"r"(su32(bar)));
+    out[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int N, bool ATM, bool F16>
+void run(long long* d) {
+  auto k = rate<N, ATM, F16>;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 98304 + 64);
+  const int iters = 4096;
+  k<<<148, 128, 98304 + 64>>>(d, iters);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h[148];
+  cudaMemcpy(h, d, sizeof h, cudaMemcpyDeviceToHost);
+  long long mx = 0;
+  for (int i = 0; i < 148; ++i) mx = h[i] > mx ? h[i] : mx;
+  const double cyc = (double)h[0] / iters;
+  const double kk = F16 ? 16 : 8;
+  printf("{\"kind\": \"%s\", \"N\": %d, \"a_from\": \"%s\", \"cycles_per_mma\": %.2f, "
+         "\"max_block_cycles_per_mma\": %.2f, \"mac_per_clk\": %.0f, \"err\": \"%s\"}\n",
+         F16 ? "f16" : "tf32", N, ATM ? "tmem" : "smem", cyc, (double)mx / iters,
+         128.0 * N * kk / cyc, cudaGetErrorString(e));
+}
+
+
+// The SGETT kernel's MMA issue pattern without its producers: per k-block 2
+// k-steps x (hi*hi, lo*hi, hi*lo), A hi/lo in TMEM at column abase + 32 s
+// (+16 for lo) of stage s, B hi/lo K-major tiles per stage in smem (SBO 512),
+// one tcgen05.commit per k-block onto the stage's mbarrier (never waited).
+template <int ABASE, bool COMMIT>
+__global__ void pattern(long long* out, int kblocks) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  constexpr int STG = 8, TB = 8192, SB = 3 * TB;
+  uint64_t* bar = (uint64_t*)(sm + STG * SB);
+  uint32_t* slot = (uint32_t*)(bar + STG + 1);
+  for (int i = threadIdx.x; i < STG * SB / 4; i += blockDim.x) ((float*)sm)[i] = 0.f;
+  if (threadIdx.x == 0) {
+    for (int i = 0; i <= STG; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((128u >> 3) << 17) | ((128u >> 4) << 24);
+  if (threadIdx.x == 0) {
+    const uint32_t base = su32(sm);
+    long long t0 = clock64();
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STG;
+      const uint32_t sb = base + s * SB;
+      for (int j = 0; j < 2; ++j) {
+        const uint32_t ah = tmem + ABASE + s * 32 + 8 * j, al = ah + 16;
+        const uint64_t bh = sdesc(sb + TB + 256 * j, 128, 512), bl = sdesc(sb + 2 * TB + 256 * j, 128, 512);
+#define MMA_P(A, B, ACC) asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t" \
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem), \
+                     "r"(A), "l"(B), "r"(IDESC), "r"((int)(ACC)))
+        MMA_P(ah, bh, (kb | j) != 0);
+        MMA_P(al, bh, 1);
+        MMA_P(ah, bl, 1);
+      }
+      if (COMMIT)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + s)));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + STG)));
+    asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W_%=;\n\t}" ::"r"(su32(bar + STG)));
+    out[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int ABASE, bool COMMIT>
+void runp(long long* d) {
+  auto k = pattern<ABASE, COMMIT>;
+  const int smem = 8 * 3 * 8192 + 128;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int kb = 2048;
+  k<<<148, 128, smem>>>(d, kb);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("{\"pattern\": \"sgett_tc k-block\", \"a_col_base\": %d, \"commit\": %d, \"cycles_per_kblock\": %.1f, "
+         "\"ideal\": 384, \"err\": \"%s\"}\n", ABASE, (int)COMMIT, (double)h / kb, cudaGetErrorString(e));
+}
+
+int main() {
+  long long* d;
+  cudaMalloc(&d, 8 * 148);
+  run<64, false, false>(d);
+  run<128, false, false>(d);
+  run<256, false, false>(d);
+  run<64, true, false>(d);
+  run<128, true, false>(d);
+  run<256, true, false>(d);
+  run<128, false, true>(d);
+  run<256, false, true>(d);
+  run<128, true, true>(d);
+  run<256, true, true>(d);
+  runp<128, true>(d);
+  runp<128, false>(d);
+  runp<256, true>(d);
+  return 0;
+}
