@@ -8,6 +8,7 @@
 //   -> host path only: H2D of the addressed spans before, D2H of C's span after.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -33,6 +34,7 @@ Mode g_mode = Mode::Auto;
 int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
 bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles >= 2 waves (GETT_STREAM_K=0: off)
+bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=0: cp.async gathers)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
 thread_local std::string t_last_error;
@@ -50,6 +52,8 @@ void read_env() {
   if (wsv) g_dgett_ws = std::atoi(wsv) != 0;
   const char* skv = std::getenv("GETT_STREAM_K");
   if (skv) g_stream_k = std::atoi(skv) != 0;
+  const char* tv = std::getenv("GETT_TMA");
+  if (tv) g_tma = std::atoi(tv) != 0;
   const char* pl = std::getenv("GETT_PIPELINE");
   if (pl) g_pipeline_slabs = std::atoi(pl);
 }
@@ -78,6 +82,17 @@ struct DevPlan {
   // residues used by the vector-load checks: every table entry divisible by 2 / 4
   bool am_even2 = false, am_even4 = false, ak_even2 = false, ak_even4 = false;
   bool bn_even2 = false, bn_even4 = false, bk_even2 = false, bk_even4 = false;
+  // SGETT TMA operand layouts (sgett_tc.cu): decided once per plan, tensor
+  // maps re-encoded when the operand base pointers change
+  int tma_state = 0;  // 0: not decided, 1: both operands TMA-fed, -1: gathers
+  struct TmaLayout {
+    uint64_t dims[5], strides[5];  // elements
+    uint32_t box[5];
+    int64_t base_off;              // element offset of coordinate 0
+    TmaOperand op;
+  } tma_l[2];
+  TmaParams tma_p{};
+  const void* tma_base[2] = {nullptr, nullptr};
   ~DevPlan() {
     if (d_tab) {
       int cur = -1;
@@ -290,6 +305,190 @@ bool vec_ok(const GroupDev& fast, bool fast_tab_div, const GroupDev& slow, bool 
   return ((uintptr_t)base % 16) == 0;
 }
 
+// ---- TMA operand layouts for the SGETT kernel (device.cuh TmaParams) ----
+
+struct AffDim {
+  int64_t ext, stride;  // elements
+};
+
+// A group's offsets in tensor t as mixed-radix affine dims, inner first
+// (extent-1 dims dropped): the inner mode (e_in, s_in) and the outer table
+// decomposed greedily; false unless every table entry matches and every
+// stride is positive.
+bool affine_dims(const Group& g, int t, std::vector<AffDim>& d) {
+  d.clear();
+  if (g.e_in > 1) d.push_back({g.e_in, g.s_in[t]});
+  const std::vector<int64_t>& T = g.T[t];
+  const int64_t L = (int64_t)T.size();
+  std::vector<AffDim> outer;
+  int64_t pos = 1;
+  while (pos < L) {
+    const int64_t st = T[pos] - T[0];
+    int64_t e = 1;
+    while (pos * e < L && T[pos * e] - T[0] == e * st) ++e;
+    if (L % (pos * e) != 0) return false;
+    outer.push_back({e, st});
+    pos *= e;
+  }
+  for (int64_t q = 0; q < L; ++q) {
+    int64_t r = q, o = 0;
+    for (const AffDim& a : outer) {
+      o += (r % a.ext) * a.stride;
+      r /= a.ext;
+    }
+    if (T[q] - T[0] != o) return false;
+  }
+  for (const AffDim& a : outer) d.push_back(a);
+  for (const AffDim& a : d)
+    if (a.stride <= 0) return false;
+  return true;
+}
+
+// TMA layout of one operand: rows from group gr (tensor tr), k from gk
+// (tensor tk).  K-major when the inner k mode is unit-stride (8-float SW32
+// boxes), else rows-major when the inner row mode is; a 128-row tile must be
+// one box (inner row extent a multiple of 128, or 128/e_in rows of the next
+// dim, or a single tile).
+bool tma_layout(const Group& gr, int tr, const Group& gk, int tk, DevPlan::TmaLayout& L) {
+  std::vector<AffDim> R, K;
+  if (!affine_dims(gr, tr, R) || !affine_dims(gk, tk, K)) return false;
+  if (R.empty() || K.empty() || R.size() > 3 || K.size() > 3) return false;
+  if (K[0].ext % 8 != 0) return false;
+  const bool kf = K[0].stride == 1;
+  if (!kf && !(R[0].stride == 1 && R[0].ext % 4 == 0)) return false;
+  const int64_t rows = gr.G, r0 = R[0].ext;
+  int nrb;  // row dims carried by the box
+  uint32_t rb[2] = {1, 1};
+  if (r0 % 128 == 0) {
+    nrb = 1;
+    rb[0] = 128;
+  } else if (128 % r0 == 0 && R.size() >= 2 &&
+             (R[1].ext % (128 / r0) == 0 || (rows <= 128 && R.size() == 2))) {
+    nrb = 2;
+    rb[0] = (uint32_t)r0;
+    rb[1] = (uint32_t)(128 / r0);
+  } else if (R.size() == 1 && rows <= 128) {
+    nrb = 1;
+    rb[0] = 128;
+  } else {
+    return false;
+  }
+  // box-carrying dims first (their order is the smem layout), then the rest
+  // by ascending stride
+  struct D {
+    int64_t ext, stride;
+    uint32_t box;
+    int kind, idx;  // 0 row, 1 k
+  };
+  std::vector<D> dims, rest;
+  if (kf) dims.push_back({K[0].ext, K[0].stride, 8u, 1, 0});
+  for (int i = 0; i < nrb; ++i) dims.push_back({R[i].ext, R[i].stride, rb[i], 0, i});
+  if (!kf) dims.push_back({K[0].ext, K[0].stride, 8u, 1, 0});
+  for (size_t i = nrb; i < R.size(); ++i) rest.push_back({R[i].ext, R[i].stride, 1u, 0, (int)i});
+  for (size_t i = 1; i < K.size(); ++i) rest.push_back({K[i].ext, K[i].stride, 1u, 1, (int)i});
+  std::sort(rest.begin(), rest.end(), [](const D& x, const D& y) { return x.stride < y.stride; });
+  for (const D& x : rest) dims.push_back(x);
+  if (dims.size() > 5 || dims[0].stride != 1) return false;
+  for (size_t i = 1; i < dims.size(); ++i)
+    if (dims[i].stride % 4 != 0 || dims[i].stride * 4 >= (1LL << 40)) return false;
+  std::memset(&L.op, 0, sizeof L.op);
+  L.op.kf = kf ? 1 : 0;
+  L.op.nr = (int32_t)R.size();
+  L.op.nk = (int32_t)K.size();
+  for (int i = 0; i < 5; ++i) {
+    if (i < (int)dims.size()) {
+      L.dims[i] = (uint64_t)dims[i].ext;
+      L.strides[i] = (uint64_t)dims[i].stride;
+      L.box[i] = dims[i].box;
+      if (dims[i].kind == 0) {
+        L.op.r_ext[dims[i].idx] = (int32_t)dims[i].ext;
+        L.op.r_pos[dims[i].idx] = i;
+      } else {
+        L.op.k_ext[dims[i].idx] = (int32_t)dims[i].ext;
+        L.op.k_pos[dims[i].idx] = i;
+      }
+    } else {
+      L.dims[i] = 1;
+      L.strides[i] = 4;
+      L.box[i] = 1;
+    }
+  }
+  L.base_off = gr.T[tr][0] + gk.T[tk][0];
+  return true;
+}
+
+typedef CUresult (*TmaEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
+                                CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                CUtensorMapFloatOOBfill);
+
+TmaEncodeFn tma_encode_fn() {
+  static TmaEncodeFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&fn, cudaEnableDefault, &q) !=
+            cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+  }
+  return fn;
+}
+
+bool tma_encode(const DevPlan::TmaLayout& L, const float* base, CUtensorMap* map) {
+  TmaEncodeFn enc = tma_encode_fn();
+  if (!enc) return false;
+  const float* g = base + L.base_off;
+  if ((uintptr_t)g % 16 != 0) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    dims[i] = L.dims[i];
+    box[i] = L.box[i];
+    if (i) strides[i - 1] = L.strides[i] * 4;
+  }
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(g), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE,
+             L.op.kf ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
+             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Both SGETT operands TMA-fed? (K a multiple of the 16-wide k-block; both
+// layouts affine and encodable at these base pointers)
+const TmaParams* sgett_tma(DevPlan& dp, const float* A, const float* B) {
+  const Plan& p = dp.plan;
+  if (dp.tma_state == 0) {
+    dp.tma_state = -1;
+    if (p.gk.G % 16 == 0 && p.gm.G > 1 && p.gn.G > 1 && tma_layout(p.gm, 0, p.gk, 0, dp.tma_l[0]) &&
+        tma_layout(p.gn, 0, p.gk, 1, dp.tma_l[1]))
+      dp.tma_state = 1;
+    if (std::getenv("GETT_TMA_DEBUG")) {
+      std::fprintf(stderr, "gett tma: %s\n", dp.tma_state == 1 ? "on" : "off");
+      for (int t = 0; dp.tma_state == 1 && t < 2; ++t) {
+        const DevPlan::TmaLayout& L = dp.tma_l[t];
+        std::fprintf(stderr, "  op %d kf %d base_off %lld dims", t, L.op.kf, (long long)L.base_off);
+        for (int i = 0; i < 5; ++i)
+          std::fprintf(stderr, " (%llu,%llu,%u)", (unsigned long long)L.dims[i],
+                       (unsigned long long)L.strides[i], L.box[i]);
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
+  if (dp.tma_state != 1) return nullptr;
+  if (dp.tma_base[0] != A || dp.tma_base[1] != B) {
+    if (!tma_encode(dp.tma_l[0], A, &dp.tma_p.map[0]) || !tma_encode(dp.tma_l[1], B, &dp.tma_p.map[1])) {
+      dp.tma_base[0] = dp.tma_base[1] = nullptr;
+      return nullptr;
+    }
+    dp.tma_p.op[0] = dp.tma_l[0].op;
+    dp.tma_p.op[1] = dp.tma_l[1].op;
+    dp.tma_base[0] = A;
+    dp.tma_base[1] = B;
+  }
+  return &dp.tma_p;
+}
+
 template <typename T>
 int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, DevState& ds,
                int neg = 0, bool force_tiled = false) {
@@ -395,10 +594,18 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     b_vec = b_kf ? vec_ok(gkB, bkd, dp.gn, bnd, V, B) : vec_ok(dp.gn, bnd, gkB, bkd, V, B);
   }
   if (use_tc) {
-    CK(launch_sgett_tc(*reinterpret_cast<TiledParams<float>*>(&tp), a_kf, b_kf, a_vec, b_vec,
+    const TmaParams* tma =
+        g_tma ? sgett_tma(dp, reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B))
+              : nullptr;
+    if (tma) {
+      a_kf = tma->op[0].kf != 0;
+      b_kf = tma->op[1].kf != 0;
+    }
+    CK(launch_sgett_tc(*reinterpret_cast<TiledParams<float>*>(&tp), tma, a_kf, b_kf, a_vec, b_vec,
                        stream));
     g_launches += splits > 1 ? 2 : 1;
-    t_last_kernel = splits > 1 ? "sgett_tc3xtf32_splitk" : "sgett_tc3xtf32";
+    t_last_kernel = tma ? (splits > 1 ? "sgett_tc3xtf32_tma_splitk" : "sgett_tc3xtf32_tma")
+                        : (splits > 1 ? "sgett_tc3xtf32_splitk" : "sgett_tc3xtf32");
     return 0;
   }
   if (sizeof(T) == 8 && g_dgett_ws) {

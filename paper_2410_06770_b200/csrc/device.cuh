@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 namespace gett {
@@ -98,6 +99,26 @@ struct SkParams {
   double* part = nullptr; // [grid][128*128] tail partials
   int32_t* flags = nullptr;  // [grid] "part published" epochs
   int32_t epoch = 0;
+};
+
+
+// TMA-fed operands of the SGETT kernel (sgett_tc.cu), built by the host when a
+// tile's rows and a k-block's k values are boxes of an affine (<= 5-D,
+// positive-stride) view: one rank-5 tensor map per operand (unused dims have
+// extent 1).  K-major operands (kf) put the inner k mode in TMA dim 0 and load
+// 8-float boxes with SWIZZLE_32B (the UMMA K-major SW32 layout, 4 KB per 8 k);
+// rows-major operands put the rows first and load [8 k][128 rows] boxes (the
+// [k][row] staging of the cp.async path).  The row index (k index) is the
+// mixed radix of its dims' coordinates, inner first, at TMA dims r_pos (k_pos).
+struct TmaOperand {
+  int32_t kf;
+  int32_t nr, nk;
+  int32_t r_ext[3], r_pos[3];
+  int32_t k_ext[3], k_pos[3];
+};
+struct TmaParams {
+  CUtensorMap map[2];   // A', B'
+  TmaOperand op[2];
 };
 
 // the fused epilogue's update: C + acc, or C + (-acc) == C - acc for neg

@@ -33,9 +33,9 @@ cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, bo
                             bool b_kf, bool a_vec, bool b_vec, cudaStream_t s);
 int dgett_ws_tiles_k(int K);  // k-blocks per tile
 
-// SGETT 3xTF32 on tcgen05 (sgett_tc.cu)
-cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec,
-                            bool b_vec, cudaStream_t s);
+// SGETT 3xTF32 on tcgen05 (sgett_tc.cu); tp != nullptr: both operands TMA-fed
+cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bool a_kf, bool b_kf,
+                            bool a_vec, bool b_vec, cudaStream_t s);
 
 int tiled_bm();
 int tiled_bn();

@@ -306,28 +306,31 @@ struct GatherSel<false, false> {
   using type = Gather<false>;
 };
 
-// transpose one MN-major staged tile ([k][row] fp32, GatherRV) into the
-// K-major hi tile (same 8 KB, in place: the raw value is the hi part) and the
-// lo tile.  The tile is 16 blocks of 4 k x 8 row-chunks; split warp ws takes
-// blocks 2ws, 2ws+1: lane l reads the unit (k = 4kg + l/8, rows 4rc..4rc+3
-// with rc = 8rcg + l%8) — each 8-lane phase reads 128 contiguous bytes.  After
-// a barrier over the split threads (the writes land on other threads' inputs)
-// it stores the 4 values rotated by s = (l/2)%4, so at each store the 32 lanes
-// cover all 8 (row % 8) x 4 (k % 4) positions = 32 distinct banks.
-constexpr int RV_BLOCKS = 16 / (SPLIT / 32);
-__device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int t) {
-  const int ws = t >> 5, l = t & 31;
-  float4 x[RV_BLOCKS];
+// The split warpgroups take alternate k-blocks: warpgroup h (threads tw =
+// 0..127 of it, warps wq = 0..3) prepares all of k-block kb = h, h+2, ...
+
+// transpose one MN-major staged tile ([k][row] fp32) into the K-major hi tile
+// (same 8 KB, in place: the raw value is the hi part) and the lo tile.  The
+// tile is 16 blocks of 4 k x 8 row-chunks; warp wq takes blocks 4wq..4wq+3:
+// lane l reads the unit (k = 4kg + l/8, rows 4rc..4rc+3 with rc = 8rcg + l%8)
+// — each 8-lane phase reads 128 contiguous bytes.  After a barrier over the
+// warpgroup (the writes land on other threads' inputs) it stores the 4 values
+// rotated by s = (l/2)%4, so at each store the 32 lanes cover all 8 (row % 8)
+// x 4 (k % 4) positions = 32 distinct banks.
+__device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int tw, int h) {
+  constexpr int NB = 4;
+  const int wq = tw >> 5, l = tw & 31;
+  float4 x[NB];
 #pragma unroll
-  for (int i = 0; i < RV_BLOCKS; ++i) {
-    const int b = ws * RV_BLOCKS + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
+  for (int i = 0; i < NB; ++i) {
+    const int b = wq * NB + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
     x[i] = *reinterpret_cast<const float4*>(hi_s + k * 512 + rc * 16);
   }
-  asm volatile("bar.sync 1, %0;" ::"n"(SPLIT) : "memory");
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "n"(WG) : "memory");
   const int rot = (l >> 1) & 3;
 #pragma unroll
-  for (int i = 0; i < RV_BLOCKS; ++i) {
-    const int b = ws * RV_BLOCKS + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
+  for (int i = 0; i < NB; ++i) {
+    const int b = wq * NB + i, k = 4 * (b >> 2) + (l >> 3), rc = 8 * (b & 3) + (l & 7);
     float hv[4] = {x[i].x, x[i].y, x[i].z, x[i].w};
     // rotate left by rot with selects (no dynamic register indexing)
     if (rot & 1) {
@@ -349,57 +352,134 @@ __device__ __forceinline__ void split_tile_rv(uint8_t* hi_s, uint8_t* lo_s, int 
 }
 
 // lo part of one landed K-major tile (8 KB; the tile itself is the hi part):
-// 512 dense 16-byte units, split thread t handles units t + SPLIT*i
-// (consecutive threads -> consecutive 16 B: conflict-free)
-__device__ __forceinline__ void split_tile(const uint8_t* hi_s, uint8_t* lo_s, int t) {
+// 512 dense 16-byte units, thread tw handles units tw + 128 i (consecutive
+// threads -> consecutive 16 B: conflict-free); layout-agnostic
+__device__ __forceinline__ void split_tile(const uint8_t* hi_s, uint8_t* lo_s, int tw) {
 #pragma unroll
-  for (int i = 0; i < 512 / SPLIT; ++i) {
-    const uint32_t o = (uint32_t)(t + SPLIT * i) * 16;
+  for (int i = 0; i < 512 / WG; ++i) {
+    const uint32_t o = (uint32_t)(tw + WG * i) * 16;
     const float4 x = *reinterpret_cast<const float4*>(hi_s + o);
     *reinterpret_cast<float4*>(lo_s + o) =
         make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
   }
 }
 
-// A' k-block -> TMEM: split thread (warp w, lane l) owns row 32(w%4) + l and
-// k 8h..8h+7 of warpgroup h; reads them from the staging tile (K-major core
-// layout: two 16-byte chunks; [k][row] staging: eight words, consecutive lanes
-// on consecutive words) and writes the raw values (hi) and lo with tcgen05.st
-// into the stage's A columns.  Warp w may only touch TMEM lanes 32(w%4)..+31.
-template <bool RV>
-__device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, uint32_t col, int warp,
+// byte offset of (row r, k) in one SWIZZLE_32B box of 128 rows x 8 floats
+// (the TMA SW32 write pattern = the UMMA K-major SW32 layout; checked by
+// tools/umma_tma_test.cu)
+__device__ __forceinline__ uint32_t sw32_off(int r, int k) {
+  return (uint32_t)(r * 32 + ((((k >> 2) ^ (r >> 2)) & 1) << 4) + (k & 3) * 4);
+}
+
+// A' k-block -> TMEM: thread (warp wq of the warpgroup, lane l) owns row
+// 32 wq + l (TMEM lane quarter wq = warp % 4) and all BK k of the k-block,
+// read from the staging tile — LAYOUT 0: K-major no-swizzle core matrices (4
+// 16-byte chunks), 1: [k][row] (16 words, consecutive lanes on consecutive
+// words), 2: two TMA SW32 boxes — and writes the raw values (hi) and lo with
+// tcgen05.st into the stage's A columns.
+template <int LAYOUT>
+__device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, uint32_t col, int wq,
                                              int lane) {
-  const int row = 32 * (warp & 3) + lane, h = (warp - 4) >> 2;
-  float v[8];
-  if (RV) {
+  const int row = 32 * wq + lane;
+  float v[BK];
+  if (LAYOUT == 1) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = *reinterpret_cast<const float*>(st + (8 * h + i) * 512 + row * 4);
+    for (int i = 0; i < BK; ++i) v[i] = *reinterpret_cast<const float*>(st + i * 512 + row * 4);
   } else {
-    const float4 x0 = *reinterpret_cast<const float4*>(st + toff(row, 2 * h));
-    const float4 x1 = *reinterpret_cast<const float4*>(st + toff(row, 2 * h + 1));
-    v[0] = x0.x; v[1] = x0.y; v[2] = x0.z; v[3] = x0.w;
-    v[4] = x1.x; v[5] = x1.y; v[6] = x1.z; v[7] = x1.w;
-  }
-  uint32_t hi[8], lo[8];
 #pragma unroll
-  for (int i = 0; i < 8; ++i) {
+    for (int c = 0; c < BK / 4; ++c) {
+      const uint32_t o = LAYOUT == 0 ? toff(row, c) : 4096 * (c >> 1) + sw32_off(row, 4 * (c & 1));
+      const float4 x = *reinterpret_cast<const float4*>(st + o);
+      v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
+    }
+  }
+  uint32_t hi[BK], lo[BK];
+#pragma unroll
+  for (int i = 0; i < BK; ++i) {
     hi[i] = __float_as_uint(v[i]);
     lo[i] = __float_as_uint(tf32_lo(v[i]));
   }
-  const uint32_t ta = tmem + ((uint32_t)(32 * (warp & 3)) << 16) + col + 8 * h;
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta),
-               "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]),
-               "r"(hi[7])
-               : "memory");
-  asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(ta + BK),
-               "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]),
-               "r"(lo[7])
-               : "memory");
+  const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + col;
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta),
+      "r"(hi[0]), "r"(hi[1]), "r"(hi[2]), "r"(hi[3]), "r"(hi[4]), "r"(hi[5]), "r"(hi[6]), "r"(hi[7]),
+      "r"(hi[8]), "r"(hi[9]), "r"(hi[10]), "r"(hi[11]), "r"(hi[12]), "r"(hi[13]), "r"(hi[14]), "r"(hi[15])
+      : "memory");
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(ta + BK),
+      "r"(lo[0]), "r"(lo[1]), "r"(lo[2]), "r"(lo[3]), "r"(lo[4]), "r"(lo[5]), "r"(lo[6]), "r"(lo[7]),
+      "r"(lo[8]), "r"(lo[9]), "r"(lo[10]), "r"(lo[11]), "r"(lo[12]), "r"(lo[13]), "r"(lo[14]), "r"(lo[15])
+      : "memory");
 }
 
-template <bool AKF, bool BKF, bool AVEC, bool BVEC>
+// ---- TMA-fed operands (TmaParams, built by the host for affine views) ----
+
+// SWIZZLE_32B K-major descriptor: SBO 256 B (8 rows x 32 B), LBO unused
+__device__ __forceinline__ uint64_t sdesc_sw32(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
+         (1ull << 46) | (6ull << 61);
+}
+
+// TMA box coordinates of one operand for one producer lane: the tile's row
+// coordinates (fixed per CTA) plus the lane's k digits, advanced by a k-block
+// (16 k) per step with carries (k_ext[0] is a multiple of 8); no dynamic
+// register indexing.
+struct TmaCoord {
+  int32_t r[5];        // row coordinates
+  int32_t d0, d1, d2;  // k digits (inner first)
+  int32_t e0, e1, nk, kp0, kp1, kp2;
+  __device__ __forceinline__ void init(const TmaOperand& op, int row0, int k) {
+#pragma unroll
+    for (int i = 0; i < 5; ++i) r[i] = 0;
+    int q = row0;
+#pragma unroll
+    for (int i = 0; i < 3; ++i) {
+      if (i < op.nr) {
+        const int v = q % op.r_ext[i];
+        q /= op.r_ext[i];
+#pragma unroll
+        for (int j = 0; j < 5; ++j)
+          if (op.r_pos[i] == j) r[j] = v;
+      }
+    }
+    nk = op.nk;
+    e0 = op.k_ext[0];
+    e1 = nk > 1 ? op.k_ext[1] : 1;
+    kp0 = op.k_pos[0];
+    kp1 = nk > 1 ? op.k_pos[1] : -1;
+    kp2 = nk > 2 ? op.k_pos[2] : -1;
+    d0 = k % e0;
+    q = k / e0;
+    d1 = q % e1;
+    d2 = q / e1;
+  }
+  __device__ __forceinline__ void step() {
+    d0 += BK;
+    while (d0 >= e0) {
+      d0 -= e0;
+      if (++d1 >= e1) {
+        d1 = 0;
+        ++d2;
+      }
+    }
+  }
+  __device__ __forceinline__ void coords(int32_t* c) const {
+#pragma unroll
+    for (int j = 0; j < 5; ++j)
+      c[j] = r[j] + (kp0 == j ? d0 : 0) + (kp1 == j ? d1 : 0) + (kp2 == j ? d2 : 0);
+  }
+};
+
+__device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int32_t* c, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+      : "memory");
+}
+
+template <bool AKF, bool BKF, bool AVEC, bool BVEC, bool TMA>
 __global__ void __launch_bounds__(THREADS, 1)
-    sgett_tc_kernel(const __grid_constant__ TiledParams<float> p) {
+    sgett_tc_kernel(const __grid_constant__ TiledParams<float> p, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // gathers landed
   uint64_t* ready = full + STAGES;                                            // split done
@@ -446,8 +526,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(full + s), WG);  // per producer thread: its cp.async group (zero fill included)
-      mbar_init(smem_u32(ready + s), SPLIT);
+      // per producer thread: its cp.async group (zero fill included); TMA: the
+      // expect_tx arrival of the one issuing thread
+      mbar_init(smem_u32(full + s), TMA ? 1 : WG);
+      mbar_init(smem_u32(ready + s), 4);  // the 4 warps of the split warpgroup of this k-block
       mbar_init(smem_u32(empty + s), 1);      // tcgen05.commit
     }
     mbar_init(smem_u32(done), 1);
@@ -465,7 +547,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   const uint32_t tmem = *tmem_slot;
   auto stage = [&](int s) { return smem + s * STAGE_BYTES; };
 
-  if (warp < 4) {
+  if (TMA && warp < 4) {
+    // ---------------- producer: lanes 0-3 of warp 0 each issue one TMA box
+    // per k-block (A' k 0-7 / 8-15, B' k 0-7 / 8-15); lane 0 posts the bytes
+    const int lane = tid & 31;
+    if (warp == 0 && lane < 4) {
+      const int t = lane >> 1, h = lane & 1;
+      TmaCoord cc;
+      if (t) cc.init(tp.op[1], n0, kbeg + 8 * h);
+      else cc.init(tp.op[0], m0, kbeg + 8 * h);
+      const CUtensorMap* map = t ? &tp.map[1] : &tp.map[0];
+      const uint32_t dst0 = smem_u32(smem) + t * TILE_BYTES + 4096 * h;
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES, u = kb / STAGES;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        const uint32_t fb = smem_u32(full + s);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(2 * TILE_BYTES)
+                       : "memory");
+        int32_t c[5];
+        cc.coords(c);
+        tma_load5(dst0 + s * STAGE_BYTES, map, c, fb);
+        cc.step();
+      }
+    }
+  } else if (warp < 4) {
     // ---------------- producer warpgroup ----------------
     typename GatherSel<AKF, AVEC>::type ga;
     typename GatherSel<BKF, BVEC>::type gb;
@@ -513,23 +619,26 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (tid == 0) TR_PRINT("blk %d producer: prep %lld wait_empty %lld issue %lld (nkb %d)\n", blockIdx.x, tp, tw, ti, nkb);
   } else if (warp < MMA_WARP) {
     // ---------------- split warpgroup, then epilogue ----------------
-    const int t = tid - WG;
-    TR_DECL(tw = 0, tsp = 0, te = 0)
+    const int h = (warp - 4) >> 2, wq = warp & 3, tw = (tid - WG) & (WG - 1), lane = tid & 31;
+    TR_DECL(tw_ = 0, tsp = 0, te = 0)
     TR_T0()
-    for (int kb = 0; kb < nkb; ++kb) {
+    constexpr int ALAY = TMA ? (AKF ? 2 : 1) : ((!AKF && AVEC) ? 1 : 0);
+    constexpr bool BRV = TMA ? !BKF : (!BKF && BVEC);
+    for (int kb = h; kb < nkb; kb += 2) {
       const int s = kb % STAGES, u = kb / STAGES;
       mbar_wait(smem_u32(full + s), u & 1);
-      TR_ADD(tw)
+      TR_ADD(tw_)
       uint8_t* st = stage(s);
       if (!(GETT_TC_ABLATE & 2)) {
-        split_a_tmem<!AKF && AVEC>(st, tmem, ACC_COLS + s * A_COLS, warp, tid & 31);
-        if (!BKF && BVEC) split_tile_rv(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
-        else split_tile(st + TILE_BYTES, st + 2 * TILE_BYTES, t);
+        split_a_tmem<ALAY>(st, tmem, ACC_COLS + s * A_COLS, wq, lane);
+        if (BRV) split_tile_rv(st + TILE_BYTES, st + 2 * TILE_BYTES, tw, h);
+        else split_tile(st + TILE_BYTES, st + 2 * TILE_BYTES, tw);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
-      mbar_arrive(smem_u32(ready + s));
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ready + s));
       TR_ADD(tsp)
     }
     if (nkb > 0) mbar_wait(smem_u32(done), 0);
@@ -581,7 +690,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       }
     }
     TR_ADD(te)
-    if (t == 0) TR_PRINT("blk %d split: wait_full %lld split %lld wait_done %lld epilogue %lld\n", blockIdx.x, tw, tsp, twd, te);
+    if (tid == WG) TR_PRINT("blk %d split: wait_full %lld split %lld wait_done %lld epilogue %lld\n", blockIdx.x, tw_, tsp, twd, te);
   } else {
     // ---------------- MMA warp ----------------
     if ((tid & 31) == 0) {
@@ -598,8 +707,12 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < BK / 8; ++j) {
           // k-step j: B' K-major tiles advance 256 B (2 k-chunks), A' 8 TMEM columns
           const uint32_t ah = tmem + ACC_COLS + s * A_COLS + 8 * j, al = ah + BK;
-          const uint64_t bh = sdesc(sb + TILE_BYTES + 256 * j);
-          const uint64_t bl = sdesc(sb + 2 * TILE_BYTES + 256 * j);
+          // B' K-major tiles: no-swizzle core matrices (k-step = 256 B), or the
+          // TMA SW32 boxes (k-step = one 4 KB box)
+          constexpr bool SW = TMA && BKF;
+          const uint64_t bh = SW ? sdesc_sw32(sb + TILE_BYTES + 4096 * j) : sdesc(sb + TILE_BYTES + 256 * j);
+          const uint64_t bl =
+              SW ? sdesc_sw32(sb + 2 * TILE_BYTES + 4096 * j) : sdesc(sb + 2 * TILE_BYTES + 256 * j);
           if (GETT_TC_ABLATE & 4) continue;
           mma_tf32_ta(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
           mma_tf32_ta(tmem, al, bh, 1);
@@ -619,33 +732,35 @@ __global__ void __launch_bounds__(THREADS, 1)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
 
-template <bool AKF, bool BKF, bool AV, bool BV>
-cudaError_t launch4(const TiledParams<float>& p, cudaStream_t s) {
-  auto k = sgett_tc_kernel<AKF, BKF, AV, BV>;
+template <bool AKF, bool BKF, bool AV, bool BV, bool TMA>
+cudaError_t launch4(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
+  auto k = sgett_tc_kernel<AKF, BKF, AV, BV, TMA>;
   static unsigned long long configured = 0;
   cudaError_t e = ensure_dyn_smem(k, SMEM_BYTES, configured);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p);
+  k<<<(unsigned)(p.tiles_m * p.tiles_n * p.splits), THREADS, SMEM_BYTES, s>>>(p, tp);
   return cudaGetLastError();
 }
 
 template <bool AKF, bool BKF>
-cudaError_t launch2(const TiledParams<float>& p, bool av, bool bv, cudaStream_t s) {
-  if (av && bv) return launch4<AKF, BKF, true, true>(p, s);
-  if (av) return launch4<AKF, BKF, true, false>(p, s);
-  if (bv) return launch4<AKF, BKF, false, true>(p, s);
-  return launch4<AKF, BKF, false, false>(p, s);
+cudaError_t launch2(const TiledParams<float>& p, const TmaParams* tp, bool av, bool bv, cudaStream_t s) {
+  if (tp) return launch4<AKF, BKF, false, false, true>(p, *tp, s);
+  static const TmaParams none{};
+  if (av && bv) return launch4<AKF, BKF, true, true, false>(p, none, s);
+  if (av) return launch4<AKF, BKF, true, false, false>(p, none, s);
+  if (bv) return launch4<AKF, BKF, false, true, false>(p, none, s);
+  return launch4<AKF, BKF, false, false, false>(p, none, s);
 }
 
 }  // namespace tc
 
-cudaError_t launch_sgett_tc(const TiledParams<float>& p, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
-                            cudaStream_t s) {
+cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bool a_kf, bool b_kf,
+                            bool a_vec, bool b_vec, cudaStream_t s) {
   cudaError_t e;
-  if (a_kf && b_kf) e = tc::launch2<true, true>(p, a_vec, b_vec, s);
-  else if (a_kf) e = tc::launch2<true, false>(p, a_vec, b_vec, s);
-  else if (b_kf) e = tc::launch2<false, true>(p, a_vec, b_vec, s);
-  else e = tc::launch2<false, false>(p, a_vec, b_vec, s);
+  if (a_kf && b_kf) e = tc::launch2<true, true>(p, tp, a_vec, b_vec, s);
+  else if (a_kf) e = tc::launch2<true, false>(p, tp, a_vec, b_vec, s);
+  else if (b_kf) e = tc::launch2<false, true>(p, tp, a_vec, b_vec, s);
+  else e = tc::launch2<false, false>(p, tp, a_vec, b_vec, s);
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_splitk_reduce<float>(p, s);
 }
