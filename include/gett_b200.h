@@ -214,6 +214,9 @@ int gett_set_pipeline(int slabs);
 /* DGETT persistent stream-K schedule (1 = on when the tiles fill >= 2 waves,
  * the default; 0 = one CTA per tile).  Also GETT_STREAM_K. */
 int gett_set_stream_k(int on);
+/* SGETT operands fed by TMA tensor maps when both views are affine boxes
+ * (1 = on, the default; 0 = cp.async gathers only).  Also GETT_TMA. */
+int gett_set_tma(int on);
 /* Name of the kernel the last call launched ("none" if none). */
 const char* gett_last_kernel(void);
 /* Text of the last CUDA / internal failure. */

@@ -18,7 +18,7 @@ EXPORTS = (
     "gett_zgett", "gett_cgett", "gett_zgett_device", "gett_cgett_device",
     "gett_validate", "gett_derive_output_extents",
     "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
-    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_last_kernel", "gett_last_error",
+    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
 )
 
@@ -74,6 +74,8 @@ def _load():
     lib.gett_set_pipeline.argtypes = [ctypes.c_int]
     lib.gett_set_stream_k.restype = ctypes.c_int
     lib.gett_set_stream_k.argtypes = [ctypes.c_int]
+    lib.gett_set_tma.restype = ctypes.c_int
+    lib.gett_set_tma.argtypes = [ctypes.c_int]
     lib.gett_last_kernel.restype = ctypes.c_char_p
     lib.gett_last_kernel.argtypes = []
     lib.gett_last_error.restype = ctypes.c_char_p
@@ -127,6 +129,12 @@ def set_stream_k(on: bool) -> None:
     """DGETT persistent stream-K schedule on (default) / off."""
     if LIB.gett_set_stream_k(1 if on else 0) != 0:
         raise ValueError(f"bad stream-K switch {on}")
+
+
+def set_tma(on: bool) -> None:
+    """SGETT TMA-fed operands for affine views on (default) / off."""
+    if LIB.gett_set_tma(1 if on else 0) != 0:
+        raise ValueError(f"bad TMA switch {on}")
 
 
 def last_kernel() -> str:

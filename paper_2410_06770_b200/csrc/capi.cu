@@ -356,20 +356,21 @@ bool tma_layout(const Group& gr, int tr, const Group& gk, int tk, DevPlan::TmaLa
   if (K[0].ext % 8 != 0) return false;
   const bool kf = K[0].stride == 1;
   if (!kf && !(R[0].stride == 1 && R[0].ext % 4 == 0)) return false;
-  const int64_t rows = gr.G, r0 = R[0].ext;
+  const int64_t r0 = R[0].ext;
   int nrb;  // row dims carried by the box
   uint32_t rb[2] = {1, 1};
   if (r0 % 128 == 0) {
     nrb = 1;
     rb[0] = 128;
-  } else if (128 % r0 == 0 && R.size() >= 2 &&
-             (R[1].ext % (128 / r0) == 0 || (rows <= 128 && R.size() == 2))) {
+  } else if (128 % r0 == 0 && R.size() >= 2 && (R[1].ext % (128 / r0) == 0 || R.size() == 2)) {
+    // (the last tile of a two-dim row group may run past the outer extent:
+    // zero-filled, as rows past the view)
     nrb = 2;
     rb[0] = (uint32_t)r0;
     rb[1] = (uint32_t)(128 / r0);
-  } else if (R.size() == 1 && rows <= 128) {
+  } else if (R.size() == 1) {
     nrb = 1;
-    rb[0] = 128;
+    rb[0] = 128;  // the last tile's rows past the extent are zero-filled
   } else {
     return false;
   }
@@ -1151,6 +1152,12 @@ int gett_set_pipeline(int slabs) {
 int gett_set_stream_k(int on) {
   if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
   g_stream_k = on != 0;
+  return 0;
+}
+
+int gett_set_tma(int on) {
+  if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
+  g_tma = on != 0;
   return 0;
 }
 

@@ -16,16 +16,18 @@ def pytest_configure(config):
 @pytest.fixture
 def kernel_mode():
     """Set the native kernel family for one test, restoring auto after."""
-    from paper_2410_06770_b200 import set_kernel, set_pipeline, set_split_k, set_stream_k
+    from paper_2410_06770_b200 import set_kernel, set_pipeline, set_split_k, set_stream_k, set_tma
 
-    def use(name, split=0, pipeline=-1, stream_k=True):
+    def use(name, split=0, pipeline=-1, stream_k=True, tma=True):
         set_kernel(name)
         set_split_k(split)
         set_pipeline(pipeline)
         set_stream_k(stream_k)
+        set_tma(tma)
 
     yield use
     set_kernel("auto")
     set_split_k(0)
     set_pipeline(-1)
     set_stream_k(True)
+    set_tma(True)
