@@ -642,6 +642,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       TR_ADD(tsp)
     }
     if (nkb > 0) mbar_wait(smem_u32(done), 0);
+    // the split-K reduce (a programmatic dependent launch) may be scheduled now
+    asm volatile("griddepcontrol.launch_dependents;");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
     TR_DECL(twd = 0)
     TR_ADD(twd)
