@@ -35,7 +35,10 @@ namespace ws {
 #define TR_PRINT(...) do { } while (0)
 #endif
 
-constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, PAD = 4, GROUP_M = 8;
+#ifndef GETT_WS_GROUP_M
+#define GETT_WS_GROUP_M 16  // c2: DRAM read 1.54 -> 1.28 GB per launch vs 8, same time
+#endif
+constexpr int BM = 128, BN = 128, BK = 32, STAGES = 3, PAD = 4, GROUP_M = GETT_WS_GROUP_M;
 constexpr int CW = 8;                   // consumer warps (2 warpgroups), warp tile 64 x 32
 constexpr int PW = 4;                   // producer warps (1 warpgroup)
 constexpr int THREADS = (CW + PW) * 32;
