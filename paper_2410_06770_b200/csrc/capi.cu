@@ -418,6 +418,10 @@ bool tma_layout(const Group& gr, int tr, const Group& gk, int tk, DevPlan::TmaLa
   return true;
 }
 
+#ifndef GETT_TMA_PROMO
+#define GETT_TMA_PROMO CU_TENSOR_MAP_L2_PROMOTION_L2_256B
+#endif
+
 typedef CUresult (*TmaEncodeFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*,
                                 CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
@@ -452,7 +456,7 @@ bool tma_encode(const DevPlan::TmaLayout& L, const float* base, CUtensorMap* map
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(g), dims, strides, box, es,
              CU_TENSOR_MAP_INTERLEAVE_NONE,
              L.op.kf ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
-             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             GETT_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Both SGETT operands TMA-fed? (K a multiple of the 16-wide k-block; both
@@ -519,6 +523,19 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     sp.tab = dp.serial_tab;
     CK(launch_serial<T>(sp, stream));
     t_last_kernel = sizeof(T) == 8 ? "dgett_serial" : "sgett_serial";
+    ++g_launches;
+    return 0;
+  }
+  if (mode == Mode::Dot && K <= kDotStagedMaxK) {
+    // staged-row dot kernel: stream the operand whose inner k mode is
+    // unit-stride (or the smaller stride), stage the other
+    DotParams<T> q;
+    q.A = A; q.B = B; q.C = c;
+    q.gm = dp.gm; q.gn = dp.gn; q.gk = dp.gk;
+    q.M = (int32_t)M; q.N = (int32_t)N; q.K = (int32_t)K;
+    q.stream_a = iabs(dp.gk.s_in[0]) <= iabs(dp.gk.s_in[1]) ? 1 : 0;
+    CK(launch_dot_staged<T>(q, stream));
+    t_last_kernel = sizeof(T) == 8 ? "dgett_dot" : "sgett_dot";
     ++g_launches;
     return 0;
   }

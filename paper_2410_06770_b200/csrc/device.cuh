@@ -144,6 +144,20 @@ struct RefParams {
   FastDiv kdiv;         // division by k_inner (dot kernel)
 };
 
+// Staged dot kernel (few outputs, long K): one operand's row is staged in
+// shared memory in the K order of gk, the other ("streamed") is read along its
+// unit-stride inner k mode, one warp per output.  stream_a: A' rows are
+// streamed (k tensor 0) and B' rows staged, else the reverse.
+template <typename T>
+struct DotParams {
+  const T* A;
+  const T* B;
+  T* C;
+  GroupDev gm, gn, gk;
+  int32_t M, N, K;
+  int32_t stream_a;
+};
+
 // Serial kernel: the literal reference loop (kernel.py:48-78) on one thread,
 // used when distinct output coordinates may address the same C element.
 template <typename T>

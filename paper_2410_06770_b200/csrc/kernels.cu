@@ -493,6 +493,59 @@ __global__ void __launch_bounds__(256) gett_dot_kernel(const __grid_constant__ R
   }
 }
 
+// Few outputs, long K: block = one staged row (of A' or B') x 8 streamed rows,
+// one warp per output.  The staged row's K values are gathered once into
+// shared memory in gk's order, with the streamed operand's k offsets beside
+// them; lanes then walk k = lane, lane+32, ... so the streamed operand is read
+// along its unit-stride inner k mode (coalesced) and the staged values without
+// bank conflicts.  Per output: lane-sequential unfused sums from -0.0, a fixed
+// xor butterfly, C + acc: deterministic.
+template <typename T>
+__global__ void __launch_bounds__(256) gett_dot_staged_kernel(const __grid_constant__ DotParams<T> p) {
+  extern __shared__ __align__(16) unsigned char dsm[];
+  T* sv = reinterpret_cast<T*>(dsm);                                   // [K] staged values
+  int64_t* ko = reinterpret_cast<int64_t*>(dsm + ((size_t)p.K * sizeof(T) + 15) / 16 * 16);  // [K]
+  const bool sa = p.stream_a != 0;
+  const GroupDev& gs = sa ? p.gn : p.gm;  // staged rows
+  const GroupDev& gr = sa ? p.gm : p.gn;  // streamed rows
+  const T* S = sa ? p.B : p.A;
+  const T* R = sa ? p.A : p.B;
+  const int ts = sa ? 1 : 0, tr = sa ? 0 : 1;
+  const int NR = sa ? p.M : p.N;
+  const int nrb = (NR + 7) / 8;
+  const int rs = blockIdx.x / nrb;
+  const T* srow = S + gs.off(0, rs);
+  for (int k = threadIdx.x; k < p.K; k += blockDim.x) {
+    int64_t os, orr;
+    p.gk.off2(k, os, orr);
+    sv[k] = __ldg(srow + (ts ? orr : os));
+    ko[k] = tr ? orr : os;
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rr = (blockIdx.x % nrb) * 8 + warp;
+  if (rr >= NR) return;  // warp-uniform
+  const T* rrow = R + gr.off(0, rr);
+  T acc = T(-0.0);
+  int k = lane;
+  // loads of 8 k steps issued before their (sequential) accumulation
+  for (; k + 32 * 7 < p.K; k += 32 * 8) {
+    T v[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[j] = __ldg(rrow + ko[k + 32 * j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = add_rn(acc, mul_rn(v[j], sv[k + 32 * j]));
+  }
+  for (; k < p.K; k += 32) acc = add_rn(acc, mul_rn(__ldg(rrow + ko[k]), sv[k]));
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) acc = add_rn(acc, __shfl_xor_sync(0xffffffffu, acc, off));
+  if (lane == 0) {
+    const int m = sa ? rr : rs, n = sa ? rs : rr;
+    T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
+    *c = add_rn(*c, acc);
+  }
+}
+
 // kernel.py:48-78 verbatim on one thread (odometer order, c read each MAC)
 template <typename T>
 __global__ void gett_serial_kernel(const __grid_constant__ SerialParams<T> p) {
@@ -729,6 +782,20 @@ cudaError_t launch_dot(const RefParams<T>& p, cudaStream_t s) {
 }
 
 template <typename T>
+cudaError_t launch_dot_staged(const DotParams<T>& p, cudaStream_t s) {
+  const int NR = p.stream_a ? p.M : p.N, NS = p.stream_a ? p.N : p.M;
+  const size_t smem = ((size_t)p.K * sizeof(T) + 15) / 16 * 16 + (size_t)p.K * sizeof(int64_t);
+  auto k = gett_dot_staged_kernel<T>;
+  if (smem > 48 * 1024) {
+    static unsigned long long configured = 0;
+    cudaError_t e = ensure_dyn_smem(k, (int)smem, configured);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<(unsigned)(NS * ((NR + 7) / 8)), 256, smem, s>>>(p);
+  return cudaGetLastError();
+}
+
+template <typename T>
 cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s) {
   gett_serial_kernel<T><<<1, 1, 0, s>>>(p);
   return cudaGetLastError();
@@ -772,6 +839,8 @@ template cudaError_t launch_ref<double>(const RefParams<double>&, cudaStream_t);
 template cudaError_t launch_ref<float>(const RefParams<float>&, cudaStream_t);
 template cudaError_t launch_dot<double>(const RefParams<double>&, cudaStream_t);
 template cudaError_t launch_dot<float>(const RefParams<float>&, cudaStream_t);
+template cudaError_t launch_dot_staged<double>(const DotParams<double>&, cudaStream_t);
+template cudaError_t launch_dot_staged<float>(const DotParams<float>&, cudaStream_t);
 template cudaError_t launch_serial<double>(const SerialParams<double>&, cudaStream_t);
 template cudaError_t launch_serial<float>(const SerialParams<float>&, cudaStream_t);
 template cudaError_t launch_zero<double>(double*, const GroupDev&, cudaStream_t);

@@ -17,6 +17,9 @@ cudaError_t launch_serial(const SerialParams<T>& p, cudaStream_t s);
 template <typename T>
 cudaError_t launch_dot(const RefParams<T>& p, cudaStream_t s);  // warp per output
 template <typename T>
+cudaError_t launch_dot_staged(const DotParams<T>& p, cudaStream_t s);  // staged row, warp per output
+constexpr int kDotStagedMaxK = 4096;
+template <typename T>
 cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 
 template <typename T>
