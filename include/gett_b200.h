@@ -211,7 +211,7 @@ int gett_set_split_k(int split);
  * free mode into `slabs` sub-contractions (-1 = automatic for calls moving
  * >= 64 MB, 0 = off, n >= 2 = always n slabs).  Also GETT_PIPELINE. */
 int gett_set_pipeline(int slabs);
-/* DGETT persistent stream-K schedule (1 = on when the tiles fill >= 2 waves,
+/* DGETT persistent stream-K schedule (1 = on when the tiles exceed one wave,
  * the default; 0 = one CTA per tile).  Also GETT_STREAM_K. */
 int gett_set_stream_k(int on);
 /* SGETT operands fed by TMA tensor maps when both views are affine boxes

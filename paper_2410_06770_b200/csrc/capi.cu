@@ -33,7 +33,7 @@ std::mutex g_mu;
 Mode g_mode = Mode::Auto;
 int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
-bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles >= 2 waves (GETT_STREAM_K=0: off)
+bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles > 1 wave and not whole waves (GETT_STREAM_K=0: off)
 bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=0: cp.async gathers)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
@@ -634,14 +634,15 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
       CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t G = ds.sms;
-    if (g_stream_k && splits == 1 && tiles >= 2 * G) {
-      // persistent: the last 1-2 waves of tiles are shared out by k-block
-      // units (each CTA's share >= one tile), the rest run data-parallel
+    if (g_stream_k && splits == 1 && tiles > G && tiles % G != 0) {
+      // persistent: the last 1-2 waves of tiles (all of them below 2 waves)
+      // are shared out by k-block units (each CTA's share >= one tile, since
+      // tiles > G), the rest run data-parallel
       const int64_t waves = (tiles + G - 1) / G;
       sk.enabled = 1;
       sk.grid = (int32_t)G;
       sk.nkb = dgett_ws_tiles_k((int)K);
-      sk.sk_tile0 = (int32_t)((waves - 2) * G);
+      sk.sk_tile0 = (int32_t)((waves < 2 ? 0 : waves - 2) * G);
       sk.sk_units = (tiles - sk.sk_tile0) * sk.nkb;
       int rc = ensure(sw.part, (size_t)G * 128 * 128 * sizeof(double));
       if (rc) return rc;
@@ -729,10 +730,27 @@ int host_pipelined(DevPlan& full, const View& a, const View& b, const Spec& s, c
   // the non-owning operand, whole
   if (owner == 0) CK(cudaMemcpyAsync(base_b + lo_b, hb + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
   else CK(cudaMemcpyAsync(base_a + lo_a, ha + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
+  // slab boundaries: the last two slabs are short (1 and 2 granules of 128
+  // rows, or rows when the mode is small) so that little compute and D2H is
+  // left after the last H2D (small slabs run split-K across the SMs); the rest
+  // are uniform, on granule boundaries
+  std::vector<int64_t> bnd(S + 1);
+  {
+    const int64_t g = E >= 16 * 128 ? 128 : 1;
+    const int64_t R = E - 3 * g;
+    if (S >= 4 && R >= (S - 2) * g) {
+      for (int64_t i = 0; i <= S - 2; ++i) bnd[i] = (R * i / (S - 2)) / g * g;
+      bnd[S - 2] = R;
+      bnd[S - 1] = R + 2 * g;
+      bnd[S] = E;
+    } else {
+      for (int64_t i = 0; i <= S; ++i) bnd[i] = E * i / S;
+    }
+  }
   std::vector<int64_t> ext_o(ov.ext, ov.ext + ov.rank);
   std::vector<int64_t> ext_c(p.ext_c);
   for (int64_t sl = 0; sl < S; ++sl) {
-    const int64_t lo = E * sl / S, hi = E * (sl + 1) / S;
+    const int64_t lo = bnd[sl], hi = bnd[sl + 1];
     ext_o[dim] = hi - lo;
     ext_c[q] = hi - lo;
     View sa = a, sb = b;

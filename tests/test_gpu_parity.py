@@ -545,6 +545,37 @@ def test_stream_k_deterministic_and_accurate(name, kernel_mode):
         assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"], sk
 
 
+@pytest.mark.parametrize("rows", [640, 1152])
+def test_stream_k_below_two_waves(rows, kernel_mode):
+    """Tiles between one and two waves (640 x 4096 -> 160 tiles, 1152 x 4096 ->
+    288 tiles on 148 SMs) run stream-K over all tiles: deterministic, within
+    the fp64 K-normalised bar of an fp64 contraction, and C's padding intact."""
+    rng = np.random.default_rng(rows)
+    M, N, K = rows, 4096, 256
+    a = rng.uniform(-1, 1, M * (K + 8)).astype(np.float64)
+    b = rng.uniform(-1, 1, K * (N + 4)).astype(np.float64)
+    c0 = rng.uniform(-1, 1, M * (N + 2)).astype(np.float64)
+    args = lambda cc: (2, (M, K), (K + 8, 1), a, 2, (K, N), (N + 4, 1), b, 1, (1,), (0,),  # noqa: E731
+                       (0, 1), (N + 2, 1), cc)
+    outs = []
+    for sk in (True, True, False):
+        kernel_mode("tiled", pipeline=0, stream_k=sk)
+        cc = c0.copy()
+        assert g.dgett(*args(cc)) == []
+        assert g.last_kernel() == ("dgett_dmma_ws_sk" if sk else "dgett_dmma_ws")
+        outs.append(cc)
+    assert outs[0].tobytes() == outs[1].tobytes(), "run-to-run difference"
+    A = oracle.strided(a, (M, K), (K + 8, 1), 0).astype(np.float64)
+    B = oracle.strided(b, (K, N), (N + 4, 1), 0).astype(np.float64)
+    ref = oracle.strided(c0, (M, N), (N + 2, 1), 0) + A @ B
+    mask = np.ones(len(c0), bool)
+    mask[np.add.outer(np.arange(M) * (N + 2), np.arange(N)).ravel()] = False
+    for cc in (outs[0], outs[2]):
+        got = oracle.strided(cc, (M, N), (N + 2, 1), 0)
+        assert k_norm_err(got, ref, K, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"]
+        assert cc[mask].tobytes() == c0[mask].tobytes()
+
+
 def test_concurrent_streams_keep_separate_workspaces(kernel_mode):
     """Two device calls in flight on two streams at once — a split-K SGETT (c5)
     and a stream-K DGETT (c3), twice each — must not share partial-sum
