@@ -512,7 +512,13 @@ __global__ void __launch_bounds__(THREADS, 1)
   // shared memory when it fits (c5: 34 of 768 entries)
   // (in bytes)
   KDec kd{{p.gk.T[0], p.gk.T[1]}, {0u, 0u}, 0, {p.gk.s_in[0] * 4, p.gk.s_in[1] * 4}, p.gk.e_in};
-  if (nkb > 0) {
+  if (TMA) {
+    // the boxes' descriptors, fetched while the barriers are set up
+    if (tid == 0) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[0]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[1]) : "memory");
+    }
+  } else if (nkb > 0) {  // (the gathers' k tables; not used by the TMA path)
     const int q0 = kbeg / p.gk.e_in.d, q1 = (kend - 1) / p.gk.e_in.d;
     if (q1 - q0 + 1 <= TCAP) {
       for (int i = tid; i <= q1 - q0; i += THREADS) {
