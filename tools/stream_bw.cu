@@ -184,11 +184,105 @@ void run_tma(char* buf, size_t bytes, int stages, int grid) {
          cudaGetErrorString(e ? e : cudaGetLastError()));
 }
 
+
+// mode 5: c5's orig-A operand exactly as the SGETT kernel loads it — rank-4
+// tensor (k4 40 x 1, m3 16 x 40, m0 48 x 983040, k12 768 x 1280 floats),
+// SWIZZLE_32B boxes (8, 16, 8, 1); 144 CTAs = 6 row tiles x 24 K slices, each
+// walks its 1280 k in 80 k-blocks of two boxes (8 KB) per stage; optional
+// second operand (c5's orig B: rows 96 x 1, k4 40 x 73728, k2 32 x 2304, k1
+// 24 x 96) as [8 k][128 rows] boxes (OOB rows zero), 8 KB per stage
+template <bool WITH_B>
+__global__ void stream_c5(const __grid_constant__ CUtensorMap ta, const __grid_constant__ CUtensorMap tb, int stages) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  constexpr int STB = WITH_B ? 16384 : 8192;
+  uint64_t* full = (uint64_t*)(sm + stages * STB);
+  uint64_t* empty = full + stages;
+  const int tid = threadIdx.x;
+  if (tid == 0) {
+    for (int s = 0; s < stages; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(full + s)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(empty + s)));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  __syncthreads();
+  const int tile = blockIdx.x % 6, split = blockIdx.x / 6;
+  const int kbeg = split * 1280;
+  if (tid == 0) {
+    for (int kb = 0; kb < 80; ++kb) {
+      const int s = kb % stages, u = kb / stages;
+      if (u > 0) wait(su32(empty + s), (u - 1) & 1);
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(full + s)), "r"(STB) : "memory");
+      for (int h = 0; h < 2; ++h) {
+        const int k = kbeg + kb * 16 + 8 * h;
+        const int k4 = k % 40, k12 = k / 40;
+        asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                     ::"r"(su32(sm + s * STB + 4096 * h)), "l"(&ta), "r"(k4), "r"(0), "r"(8 * tile), "r"(k12), "r"(su32(full + s)) : "memory");
+        if (WITH_B) {
+          const int k2 = k12 % 32, k1 = k12 / 32;
+          asm volatile("cp.async.bulk.tensor.4d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5}], [%6];"
+                       ::"r"(su32(sm + s * STB + 8192 + 4096 * h)), "l"(&tb), "r"(0), "r"(k4), "r"(k2), "r"(k1), "r"(su32(full + s)) : "memory");
+        }
+      }
+    }
+  } else if (tid == 32) {
+    for (int kb = 0; kb < 80; ++kb) {
+      const int s = kb % stages, u = kb / stages;
+      wait(su32(full + s), u & 1);
+      arrive(su32(empty + s));
+    }
+  }
+}
+
+template <bool WITH_B>
+void run_c5(int stages) {
+  static EncodeFn enc = nullptr;
+  if (!enc) {
+    cudaDriverEntryPointQueryResult q;
+    cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&enc, cudaEnableDefault, &q);
+  }
+  float *A, *B;
+  cudaMalloc(&A, 47185920ull * 4);
+  cudaMalloc(&B, 2949120ull * 4);
+  cudaMemset(A, 0, 47185920ull * 4);
+  cudaMemset(B, 0, 2949120ull * 4);
+  CUtensorMap ta, tb;
+  cuuint64_t da[4] = {40, 16, 48, 768}, sa[3] = {160, 3932160, 5120};
+  cuuint32_t ba[4] = {8, 16, 8, 1}, es[4] = {1, 1, 1, 1};
+  enc(&ta, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, A, da, sa, ba, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  cuuint64_t db[4] = {96, 40, 32, 24}, sb[3] = {294912, 9216, 384};
+  cuuint32_t bb[4] = {128, 8, 1, 1};
+  enc(&tb, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, B, db, sb, bb, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+      CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  auto k = stream_c5<WITH_B>;
+  const int smem = stages * (WITH_B ? 16384 : 8192) + 2 * stages * 8;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  k<<<144, 64, smem>>>(ta, tb, stages);
+  cudaEventRecord(e0);
+  for (int i = 0; i < 10; ++i) k<<<144, 64, smem>>>(ta, tb, stages);
+  cudaEventRecord(e1);
+  cudaError_t e = cudaEventSynchronize(e1);
+  float ms;
+  cudaEventElapsedTime(&ms, e0, e1);
+  printf("{\"mode\": \"c5_%s\", \"stages\": %d, \"us_per_pass\": %.1f, \"err\": \"%s\"}\n", WITH_B ? "A+B" : "A", stages,
+         ms * 100.0, cudaGetErrorString(e ? e : cudaGetLastError()));
+  cudaFree(A);
+  cudaFree(B);
+}
+
 int main() {
   const size_t bytes = 1ull << 30;
   char* buf;
   cudaMalloc(&buf, bytes);
   cudaMemset(buf, 1, bytes);
+  for (int st : {8, 16}) {
+    run_c5<false>(st);
+    run_c5<true>(st);
+  }
   for (int g : {148, 48, 16}) {
     run_tma<8>(buf, bytes, 8, g);
     run_tma<32>(buf, bytes, 8, g);
