@@ -634,10 +634,11 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
       CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t G = ds.sms;
-    if (g_stream_k && splits == 1 && tiles > G && tiles % G != 0) {
+    if (g_stream_k && splits == 1 && tiles % G != 0 && 2 * tiles > G) {
       // persistent: the last 1-2 waves of tiles (all of them below 2 waves)
-      // are shared out by k-block units (each CTA's share >= one tile, since
-      // tiles > G), the rest run data-parallel
+      // are shared out by k-block units, the rest run data-parallel; below one
+      // wave (G/2 < tiles < G, where split-K cannot help) the shares are
+      // shorter than a tile and the heads add several parts
       const int64_t waves = (tiles + G - 1) / G;
       sk.enabled = 1;
       sk.grid = (int32_t)G;

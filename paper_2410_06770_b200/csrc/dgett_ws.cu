@@ -159,8 +159,10 @@ struct Seg {
 //     boundaries fall at different times in different CTAs: the C epilogues of
 //     concurrently running CTAs no longer hit HBM in one synchronized burst,
 //     and the partial last wave disappears.  A tile cut by the CTA boundary c
-//     is shared by CTA c-1 (head) and CTA c (tail); every share is >= one tile,
-//     so no tile is cut twice.
+//     is shared by CTA c-1 (head) and CTA c (tail); with fewer tiles than CTAs
+//     the shares are shorter than a tile and a tile may also have middle
+//     pieces (CTAs whose whole share lies inside it): they publish like tails
+//     and the head adds all of them in CTA order.
 struct SegIter {
   int64_t u, u_end;  // stream-K units still to take
   int dp;            // next data-parallel tile
@@ -373,23 +375,29 @@ __global__ void __launch_bounds__(THREADS, 1)
       continue;
     }
     if (sg.kind == SEG_HEAD) {
-      // wait for the tail (CTA blockIdx.x + 1, which started on it first) and
-      // add its part: acc = head + tail, the same order for every element
-      const int* f = sk.flags + blockIdx.x + 1;
-      int v;
-      do {
-        asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
-      } while (v != sk.epoch);
-      const double* w = sk.part + (int64_t)(blockIdx.x + 1) * (BM * BN);
+      // the rest of the tile belongs to CTAs blockIdx.x + 1, ... (one, or more
+      // when the shares are shorter than a tile); wait for each one's published
+      // part and add them in CTA order: acc = head + p1 + p2 ..., the same
+      // order for every element
+      const int64_t G = gridDim.x;
+      const int64_t tile_end = (int64_t)(sg.tile - sk.sk_tile0 + 1) * sk.nkb;
+      for (int64_t c2 = blockIdx.x + 1; c2 < G && sk.sk_units * c2 / G < tile_end; ++c2) {
+        const int* f = sk.flags + c2;
+        int v;
+        do {
+          asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        } while (v != sk.epoch);
+        const double* w = sk.part + c2 * (BM * BN);
 #pragma unroll
-      for (int i = 0; i < MI; ++i)
+        for (int i = 0; i < MI; ++i)
 #pragma unroll
-        for (int j = 0; j < NJ; ++j) {
-          const double2 t = __ldcg(reinterpret_cast<const double2*>(
-              w + (wm0 + i * 8 + (lane >> 2)) * BN + wn0 + j * 8 + 2 * (lane & 3)));
-          acc[i][j][0] = acc[i][j][0] + t.x;
-          acc[i][j][1] = acc[i][j][1] + t.y;
-        }
+          for (int j = 0; j < NJ; ++j) {
+            const double2 t = __ldcg(reinterpret_cast<const double2*>(
+                w + (wm0 + i * 8 + (lane >> 2)) * BN + wn0 + j * 8 + 2 * (lane & 3)));
+            acc[i][j][0] = acc[i][j][0] + t.x;
+            acc[i][j][1] = acc[i][j][1] + t.y;
+          }
+      }
     }
     const bool to_c = sg.kind != SEG_SPLITK;
     int64_t coff[NJ * 2];

@@ -545,11 +545,13 @@ def test_stream_k_deterministic_and_accurate(name, kernel_mode):
         assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"], sk
 
 
-@pytest.mark.parametrize("rows", [640, 1152])
+@pytest.mark.parametrize("rows", [384, 512, 640, 1152])
 def test_stream_k_below_two_waves(rows, kernel_mode):
-    """Tiles between one and two waves (640 x 4096 -> 160 tiles, 1152 x 4096 ->
-    288 tiles on 148 SMs) run stream-K over all tiles: deterministic, within
-    the fp64 K-normalised bar of an fp64 contraction, and C's padding intact."""
+    """Tiles below two waves run stream-K over all tiles — between one and two
+    waves (640 x 4096 -> 160 tiles, 1152 x 4096 -> 288 tiles on 148 SMs) and
+    below one wave (384 -> 96, 512 -> 128 tiles: shares shorter than a tile,
+    heads adding several parts): deterministic, within the fp64 K-normalised
+    bar of an fp64 contraction, and C's padding intact."""
     rng = np.random.default_rng(rows)
     M, N, K = rows, 4096, 256
     a = rng.uniform(-1, 1, M * (K + 8)).astype(np.float64)
