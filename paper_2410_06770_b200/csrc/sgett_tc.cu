@@ -42,6 +42,9 @@
 #ifndef GETT_TC_STAGES
 #define GETT_TC_STAGES 8
 #endif
+#ifndef GETT_TC_LO
+#define GETT_TC_LO 3
+#endif
 
 namespace gett {
 namespace tc {
@@ -73,15 +76,22 @@ constexpr int GROUP_M = 8;
 constexpr int LBO = 128;                       // bytes between k-chunks
 constexpr int SBO = CH * 128;                  // bytes between 8-row groups
 constexpr int TILE_BYTES = 128 * BK * 4;       // one operand part: 8 KB
-constexpr int STAGE_BYTES = 3 * TILE_BYTES;    // A fp32 staging, B hi, B lo
+constexpr int STAGE_BYTES = 2 * TILE_BYTES;    // A fp32 staging, B raw (= B hi)
+// B' lo tiles live in a short ring of their own: a stage's raw data must stay
+// until its MMAs finish, but lo only from the split to the MMAs, so the loads
+// can run STAGES k-blocks ahead with LO_BUFS lo tiles
+constexpr int LO_BUFS = GETT_TC_LO;
 constexpr int TCAP = 256;                      // outer k-table entries staged in smem
-constexpr int BAR_BYTES = 256;
-constexpr int SMEM_BYTES = STAGES * STAGE_BYTES + BAR_BYTES + 2 * TCAP * 8;
+constexpr int BAR_BYTES = 512;
+constexpr int LO_OFF = STAGES * STAGE_BYTES;   // lo ring
+constexpr int BAR_OFF = LO_OFF + LO_BUFS * TILE_BYTES;
+constexpr int SMEM_BYTES = BAR_OFF + BAR_BYTES + 2 * TCAP * 8;
 constexpr uint32_t ACC_COLS = BN;              // fp32 accumulator columns
 constexpr uint32_t A_COLS = 2 * BK;            // per stage: A hi (BK cols), A lo (BK cols)
 constexpr uint32_t TMEM_COLS = 512;            // power of two >= ACC_COLS + STAGES * A_COLS
 static_assert(ACC_COLS + STAGES * A_COLS <= TMEM_COLS, "TMEM budget");
-static_assert(3 * STAGES + 2 <= BAR_BYTES / 8, "barrier area");
+static_assert(3 * STAGES + 2 + LO_BUFS <= BAR_BYTES / 8, "barrier area");
+static_assert(SMEM_BYTES <= 227 * 1024, "shared memory budget");
 
 // instruction descriptor: D f32, A/B tf32, both K-major, N = 128, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(BN >> 3) << 17) |
@@ -481,12 +491,13 @@ template <bool AKF, bool BKF, bool AVEC, bool BVEC, bool TMA>
 __global__ void __launch_bounds__(THREADS, 1)
     sgett_tc_kernel(const __grid_constant__ TiledParams<float> p, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(1024) uint8_t smem[];
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);  // gathers landed
-  uint64_t* ready = full + STAGES;                                            // split done
-  uint64_t* empty = ready + STAGES;                                           // MMAs done
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);  // gathers landed
+  uint64_t* ready = full + STAGES;                               // split done
+  uint64_t* empty = ready + STAGES;                              // MMAs done (stage reusable)
   uint64_t* done = empty + STAGES;
+  uint64_t* lofree = done + 1;                                   // MMAs done (lo tile reusable)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
-  int64_t* ktabs = reinterpret_cast<int64_t*>(smem + STAGES * STAGE_BYTES + BAR_BYTES);  // [2][TCAP]
+  int64_t* ktabs = reinterpret_cast<int64_t*>(smem + BAR_OFF + BAR_BYTES);  // [2][TCAP]
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
@@ -539,6 +550,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_init(smem_u32(empty + s), 1);      // tcgen05.commit
     }
     mbar_init(smem_u32(done), 1);
+    for (int l = 0; l < LO_BUFS; ++l) mbar_init(smem_u32(lofree + l), 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
@@ -635,10 +647,14 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(smem_u32(full + s), u & 1);
       TR_ADD(tw_)
       uint8_t* st = stage(s);
+      // the lo tile of k-block kb: free once the MMAs of kb - LO_BUFS are done
+      const int lb = kb % LO_BUFS, lu = kb / LO_BUFS;
+      if (lu > 0) mbar_wait(smem_u32(lofree + lb), (lu - 1) & 1);
+      uint8_t* lo = smem + LO_OFF + lb * TILE_BYTES;
       if (!(GETT_TC_ABLATE & 2)) {
         split_a_tmem<ALAY>(st, tmem, ACC_COLS + s * A_COLS, wq, lane);
-        if (BRV) split_tile_rv(st + TILE_BYTES, st + 2 * TILE_BYTES, tw, h);
-        else split_tile(st + TILE_BYTES, st + 2 * TILE_BYTES, tw);
+        if (BRV) split_tile_rv(st + TILE_BYTES, lo, tw, h);
+        else split_tile(st + TILE_BYTES, lo, tw);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -711,6 +727,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         TR_ADD(tw)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t sb = smem_base + s * STAGE_BYTES;
+        const uint32_t lob = smem_base + LO_OFF + (kb % LO_BUFS) * TILE_BYTES;
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           // k-step j: B' K-major tiles advance 256 B (2 k-chunks), A' 8 TMEM columns
@@ -719,14 +736,14 @@ __global__ void __launch_bounds__(THREADS, 1)
           // TMA SW32 boxes (k-step = one 4 KB box)
           constexpr bool SW = TMA && BKF;
           const uint64_t bh = SW ? sdesc_sw32(sb + TILE_BYTES + 4096 * j) : sdesc(sb + TILE_BYTES + 256 * j);
-          const uint64_t bl =
-              SW ? sdesc_sw32(sb + 2 * TILE_BYTES + 4096 * j) : sdesc(sb + 2 * TILE_BYTES + 256 * j);
+          const uint64_t bl = SW ? sdesc_sw32(lob + 4096 * j) : sdesc(lob + 256 * j);
           if (GETT_TC_ABLATE & 4) continue;
           mma_tf32_ta(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
           mma_tf32_ta(tmem, al, bh, 1);
           mma_tf32_ta(tmem, ah, bl, 1);
         }
         commit(smem_u32(empty + s));
+        commit(smem_u32(lofree + kb % LO_BUFS));
         TR_ADD(tm)
       }
       commit(smem_u32(done));
