@@ -35,6 +35,10 @@ namespace ws {
 #define TR_PRINT(...) do { } while (0)
 #endif
 
+// tuning builds only: skip the C += acc reductions (measures the epilogue's cost)
+#ifndef GETT_WS_NO_EPI
+#define GETT_WS_NO_EPI 0
+#endif
 #ifndef GETT_WS_GROUP_M
 #define GETT_WS_GROUP_M 16  // c2: DRAM read 1.54 -> 1.28 GB per launch vs 8, same time
 #endif
@@ -424,7 +428,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < NJ; ++j)
 #pragma unroll
           for (int e = 0; e < 2; ++e)
-            if (cok[j * 2 + e])
+            if (cok[j * 2 + e] && !GETT_WS_NO_EPI)
               asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p.C + ro + coff[j * 2 + e]),
                            "d"(p.neg ? -acc[i][j][e] : acc[i][j][e])
                            : "memory");
