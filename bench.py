@@ -274,6 +274,21 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# fp32 via 3xTF32: a third of the tf32 MMA rate measured by tools/mma_rate.cu
+# (2046 MAC/clk/SM x 148 SMs x 1.965 GHz)
+TF32X3_PEAK_TFLOPS = 2 * 2046 * 148 * 1.965e9 / 3 / 1e12
+
+
+def hbm_gbs():
+    """HBM GB/s: MEASURED_PEAKS.json (driver-written) when present, else the
+    value it held on this pool's B200s."""
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"])
+    except (OSError, KeyError, ValueError):
+        return 6538.6
+
+
 def other_configs(dev):
     """The other BASELINE configs (parity cases, not the headline): device time
     per call, each call timed alone with CUDA events after an L2 flush (a 256 MB
@@ -304,9 +319,17 @@ def other_configs(dev):
             e1.synchronize()
             times.append(e0.elapsed_time(e1))
         ms = float(np.median(times))
+        # roofline of the config: the larger of the HBM time for its algorithmic
+        # bytes and the tensor time for its FLOPs (FP64 DMMA peak; fp32 at a
+        # third of the measured tf32 MMA issue rate, 3xTF32)
+        t_hbm = w.alg_bytes / (hbm_gbs() * 1e9)
+        t_tc = w.flops / ((FP64_PEAK_TFLOPS if w.dtype == "d" else TF32X3_PEAK_TFLOPS) * 1e12)
+        bound = "hbm" if t_hbm > t_tc else "tensor"
         out[name] = {"gflops": round(w.flops / (ms * 1e-3) / 1e9, 2), "ms": round(ms, 4),
                      "dtype": "f64" if w.dtype == "d" else "f32", "kernel": g.last_kernel(),
-                     "l2": "flushed before each call"}
+                     "l2": "flushed before each call",
+                     "roofline": {"bound": bound, "floor_ms": round(max(t_hbm, t_tc) * 1e3, 4),
+                                  "frac": round(max(t_hbm, t_tc) / (ms * 1e-3), 4)}}
         del ta, tb, tc
     del flush
     torch.cuda.empty_cache()
