@@ -35,7 +35,8 @@
 #include "device.cuh"
 #include "kernels.hpp"
 
-// tuning builds only: skip the loads (1), the split (2) or the MMAs (4)
+// tuning builds only: skip the loads (1), the split (2), the MMAs (4), or B''s
+// lo tile and its MMA (8)
 #ifndef GETT_TC_ABLATE
 #define GETT_TC_ABLATE 0
 #endif
@@ -654,7 +655,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (!(GETT_TC_ABLATE & 2)) {
         split_a_tmem<ALAY>(st, tmem, ACC_COLS + s * A_COLS, wq, lane);
         if (BRV) split_tile_rv(st + TILE_BYTES, lo, tw, h);
-        else split_tile(st + TILE_BYTES, lo, tw);
+        else if (!(GETT_TC_ABLATE & 8)) split_tile(st + TILE_BYTES, lo, tw);
       }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -740,7 +741,7 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (GETT_TC_ABLATE & 4) continue;
           mma_tf32_ta(tmem, ah, bh, (kb | j) != 0);  // first MMA of the tile overwrites D
           mma_tf32_ta(tmem, al, bh, 1);
-          mma_tf32_ta(tmem, ah, bl, 1);
+          if (!(GETT_TC_ABLATE & 8)) mma_tf32_ta(tmem, ah, bl, 1);
         }
         commit(smem_u32(empty + s));
         commit(smem_u32(lofree + kb % LO_BUFS));
