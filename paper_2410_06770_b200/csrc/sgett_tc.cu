@@ -680,17 +680,25 @@ __global__ void __launch_bounds__(THREADS, 1)
     // split-K partials, transposed [split][N][M]: a warp's 32 rows are 32
     // consecutive floats per column (coalesced); the reduce reads it m-fastest
     float* wcol = p.splits > 1 ? p.ws + (int64_t)split * p.M * p.N + (mok ? m : 0) : nullptr;
-#pragma unroll 1
-    for (int c0 = cbeg; c0 < cbeg + 64; c0 += 16) {
-      uint32_t r[16];
-      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)c0;
+    // all 64 of this thread's columns leave TMEM before one wait (the loads
+    // pipeline instead of paying the TMEM latency per 16 columns)
+    uint32_t rr[64];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t taddr = tmem + ((uint32_t)((warp & 3) * 32) << 16) + (uint32_t)(cbeg + 16 * q);
+      uint32_t* r = rr + 16 * q;
       asm volatile(
           "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
           : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]),
             "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]),
             "=r"(r[14]), "=r"(r[15])
           : "r"(taddr));
-      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c0 = cbeg + 16 * q;
+      const uint32_t* r = rr + 16 * q;
       if (!mok) continue;
       if (p.splits == 1) {
         float cv[16];
