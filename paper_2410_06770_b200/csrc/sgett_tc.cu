@@ -2,32 +2,35 @@
 // warp-specialised.
 //
 // Replaces the fp32 hot loop (kernel.py:48-78 for sgett) for contractions big
-// enough to tile.  Per 128x128 output tile, k-blocks of 16, STAGES-deep ring:
-//   * producer warpgroup (warps 0-3): gathers the A' (M x K) and B' (N x K)
-//     k-block straight from the strided views with cp.async (row offsets
-//     decoded once per tile, k offsets from this CTA's slice of the K group's
-//     outer table staged in smem) — 16-byte copies along k (K-major core
-//     layout: 8-row x 16-byte core matrices, LBO 128 B between k-chunks, SBO
-//     512 B between 8-row groups) or along rows (staged [k][row]) where the
-//     planner proved 4-element contiguity, else 4-byte copies; completion is
-//     tracked per stage by cp.async.mbarrier.arrive;
-//   * split warpgroups (warps 4-11): when a stage lands, split every value into
-//     hi = rna_tf32(x) and lo = x - hi (exact in fp32).  A' goes to TMEM
-//     (tcgen05.st, lane = row, column = k: the MMA's A operand is read from
-//     TMEM, so A' never round-trips through shared memory); B' is split in
-//     place into its K-major hi/lo tiles (transposed from [k][row] staging when
-//     gathered along rows); fence, arrive;
-//   * MMA warp (warp 12): one elected thread issues, per UMMA_K = 8 step,
+// enough to tile.  Per 128x128 output tile, k-blocks of 16, STAGES-deep ring
+// of (A' staging, B' raw) plus a LO_BUFS-deep ring of B' lo tiles:
+//   * loads — TMA (TMA=true, both operands affine boxes, capi.cu tma_layout):
+//     four lanes of the producer warp issue one cp.async.bulk.tensor box each
+//     per k-block (K-major operands as SWIZZLE_32B [128 rows][8 k] boxes =
+//     the UMMA K-major SW32 layout; rows-major operands as [8 k][128 rows]);
+//     gathers (otherwise): the producer warpgroup cp.asyncs the tiles straight
+//     from the strided views (16 B along k into the no-swizzle K-major core
+//     layout, or along rows into [k][row] staging, else 4 B; zero fill past
+//     the view; k offsets decoded lane-parallel from the staged K table);
+//   * split warpgroups (warps 4-11, alternate k-blocks): the tensor core reads
+//     a raw fp32 operand as tf32 by truncation, so the raw value is the hi
+//     part and only lo = x - trunc(x) (exact) is produced: A' hi/lo go to TMEM
+//     (tcgen05.st, lane = row, column = k: A' never returns to shared memory);
+//     a K-major B' tile is used in place as B' hi and its lo written to the lo
+//     ring; a rows-major B' is transposed into K-major hi (in place) and lo;
+//   * MMA warp (warp 12): one thread issues, per UMMA_K = 8 step,
 //     tcgen05.mma.cta_group::1.kind::tf32 for hi*hi, lo*hi, hi*lo into one fp32
-//     accumulator in TMEM (128 lanes x 128 columns) and tcgen05.commit frees
-//     the stage (smem + its TMEM A slot) for the producers;
+//     accumulator in TMEM (128 lanes x 128 columns); tcgen05.commit frees the
+//     stage (smem + its TMEM A slot) and, separately, the lo tile;
 //   * epilogue (split warpgroups; warp w reads TMEM lane quarter w%4, columns
 //     64h..64h+63 for warpgroup h): tcgen05.ld 32x32b -> C += acc through the C
-//     offset tables, or the split-K partial into the workspace.
-// Shared memory traffic per k-block (the bound): 16 KB gathered, 16 KB read
-// by the split, 16 KB of B' hi/lo written, 24 KB of B' read by the MMAs.
-// Accuracy: 3xTF32 products are within ~2^-22 relative, fp32 accumulation in
-// TMEM; checked against the fp64 oracle and the reference (tests/).
+//     offset tables, or the split-K partial (transposed, coalesced) into the
+//     workspace.
+// Shared memory traffic per k-block: 16 KB loaded, 16 KB read by the split,
+// 8 KB of B' lo written, 24 KB of B' read by the MMAs.
+// Accuracy: each product misses lo*lo and lo's own truncation (< 2^-19
+// relative), fp32 accumulation in TMEM; checked against the fp64 oracle and
+// the reference (tests/).
 #include <cstdint>
 #include <cstdio>
 #include <type_traits>
