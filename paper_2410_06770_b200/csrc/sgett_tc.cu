@@ -495,6 +495,11 @@ template <bool AKF, bool BKF, bool AVEC, bool BVEC, bool TMA>
 __global__ void __launch_bounds__(THREADS, 1)
     sgett_tc_kernel(const __grid_constant__ TiledParams<float> p, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(1024) uint8_t smem[];
+#ifdef GETT_TC_TRACE
+  unsigned long long g_entry;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_entry));
+  const long long c_entry = clock64();
+#endif
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFF);  // gathers landed
   uint64_t* ready = full + STAGES;                               // split done
   uint64_t* empty = ready + STAGES;                              // MMAs done (stage reusable)
@@ -567,6 +572,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+#ifdef GETT_TC_TRACE
+  const long long c_setup = clock64() - c_entry;
+#endif
   auto stage = [&](int s) { return smem + s * STAGE_BYTES; };
 
   if (TMA && warp < 4) {
@@ -767,6 +775,14 @@ __global__ void __launch_bounds__(THREADS, 1)
   __syncthreads();
   if (warp == MMA_WARP)
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+#ifdef GETT_TC_TRACE
+  if (threadIdx.x == 0 && (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1)) {
+    unsigned long long g_exit;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(g_exit));
+    printf("blk %d entry_ns %llu setup %lld life %lld clk %llu ns\n", blockIdx.x, g_entry, c_setup,
+           clock64() - c_entry, g_exit - g_entry);
+  }
+#endif
 }
 
 template <bool AKF, bool BKF, bool AV, bool BV, bool TMA>
