@@ -644,3 +644,45 @@ def test_offsets_beyond_32_bits(mode, kernel_mode):
     assert int(torch.count_nonzero(tc[:off_c])) == 0 and int(torch.count_nonzero(tc[off_c + M * N:])) == 0
     del ta, tc
     torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------------------
+# dot mode (few outputs, long K): the staged-row kernel up to K = 4096, the
+# warp-per-output kernel above; both operand orders of the streamed / staged
+# roles, negative increments and non-affine K tables
+
+
+@pytest.mark.parametrize("K1,K2", [(32, 40), (64, 64), (17, 241)])
+@pytest.mark.parametrize("neg", [False, True])
+@pytest.mark.parametrize("a_kfast", [True, False])
+def test_dot_kernels_match_fp64(K1, K2, neg, a_kfast, kernel_mode):
+    kernel_mode("dot")
+    rng = np.random.default_rng(K1 * 1000 + K2 + 7 * neg + a_kfast)
+    M, N = 24, 20
+    # A (m, k1, k2), B (k1, k2, n): the K-fast operand streams, the other is staged
+    a_dims, b_dims = (M, K1, K2), (K1, K2, N)
+    if a_kfast:
+        a_inc = (K1 * K2 + 3, K2, 1)
+        b_inc = (1, K1 + 2, (K1 + 2) * K2)
+    else:
+        a_inc = (1, M + 1, (M + 1) * K1)
+        b_inc = (K2 * N + 5, N, 1)
+    sign = -1 if neg else 1
+    a_inc = tuple(sign * i for i in a_inc)
+    span = lambda ext, inc: sum((e - 1) * abs(i) for e, i in zip(ext, inc)) + 1  # noqa: E731
+    a = rng.uniform(-1, 1, span(a_dims, a_inc) + 4)
+    b = rng.uniform(-1, 1, span(b_dims, b_inc) + 4)
+    off_a = span(a_dims, a_inc) - 1 if neg else 0
+    c0 = rng.uniform(-1, 1, M * N + 8)
+    c = c0.copy()
+    assert g.dgett(3, a_dims, a_inc, a, 3, b_dims, b_inc, b, 2, (1, 2), (0, 1), (0, 1), (N, 1), c,
+                   offset_a=off_a, offset_c=3) == []
+    assert g.last_kernel() == "dgett_dot"
+    A = oracle.strided(a, a_dims, a_inc, off_a).astype(np.float64)
+    B = oracle.strided(b, b_dims, b_inc, 0).astype(np.float64)
+    want = oracle.strided(c0, (M, N), (N, 1), 3) + np.einsum("mij,ijn->mn", A, B)
+    got = oracle.strided(c, (M, N), (N, 1), 3)
+    assert k_norm_err(got, want, K1 * K2, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"]
+    mask = np.ones(len(c0), bool)
+    mask[3:3 + M * N] = False
+    assert c[mask].tobytes() == c0[mask].tobytes()
