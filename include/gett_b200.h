@@ -217,6 +217,10 @@ int gett_set_stream_k(int on);
 /* SGETT operands fed by TMA tensor maps when both views are affine boxes
  * (1 = on, the default; 0 = cp.async gathers only).  Also GETT_TMA. */
 int gett_set_tma(int on);
+/* SGETT CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256 per pair) for
+ * split-K shapes with a K-major operand of >= 256 rows and a rows-major one of
+ * <= 128 (e.g. c5); 0 = off (the default), 1 = on.  Also GETT_PAIR. */
+int gett_set_pair(int on);
 /* Name of the kernel the last call launched ("none" if none). */
 const char* gett_last_kernel(void);
 /* Text of the last CUDA / internal failure. */

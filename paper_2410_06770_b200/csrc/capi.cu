@@ -35,6 +35,7 @@ int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
 bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles > 1 wave and not whole waves (GETT_STREAM_K=0: off)
 bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=0: cp.async gathers)
+bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
 thread_local std::string t_last_error;
@@ -52,6 +53,8 @@ void read_env() {
   if (wsv) g_dgett_ws = std::atoi(wsv) != 0;
   const char* skv = std::getenv("GETT_STREAM_K");
   if (skv) g_stream_k = std::atoi(skv) != 0;
+  const char* pv = std::getenv("GETT_PAIR");
+  if (pv) g_pair = std::atoi(pv) != 0;
   const char* tv = std::getenv("GETT_TMA");
   if (tv) g_tma = std::atoi(tv) != 0;
   const char* pl = std::getenv("GETT_PIPELINE");
@@ -93,6 +96,12 @@ struct DevPlan {
   } tma_l[2];
   TmaParams tma_p{};
   const void* tma_base[2] = {nullptr, nullptr};
+  // CTA-pair SGETT on swapped roles (A2 = B' K-major, B2 = A' rows-major)
+  int pair_state = 0;  // 0 undecided, 1 usable, -1 not
+  TmaLayout pair_l[2];
+  TmaParams pair_p{};
+  const void* pair_base[2] = {nullptr, nullptr};
+  GroupDev pgk{};      // dp.gk with its two tensors exchanged
   ~DevPlan() {
     if (d_tab) {
       int cur = -1;
@@ -349,7 +358,7 @@ bool affine_dims(const Group& g, int t, std::vector<AffDim>& d) {
 // boxes), else rows-major when the inner row mode is; a 128-row tile must be
 // one box (inner row extent a multiple of 128, or 128/e_in rows of the next
 // dim, or a single tile).
-bool tma_layout(const Group& gr, int tr, const Group& gk, int tk, DevPlan::TmaLayout& L) {
+bool tma_layout(const Group& gr, int tr, const Group& gk, int tk, DevPlan::TmaLayout& L, int tile = 128) {
   std::vector<AffDim> R, K;
   if (!affine_dims(gr, tr, R) || !affine_dims(gk, tk, K)) return false;
   if (R.empty() || K.empty() || R.size() > 3 || K.size() > 3) return false;
@@ -359,18 +368,18 @@ bool tma_layout(const Group& gr, int tr, const Group& gk, int tk, DevPlan::TmaLa
   const int64_t r0 = R[0].ext;
   int nrb;  // row dims carried by the box
   uint32_t rb[2] = {1, 1};
-  if (r0 % 128 == 0) {
+  if (r0 % tile == 0) {
     nrb = 1;
-    rb[0] = 128;
-  } else if (128 % r0 == 0 && R.size() >= 2 && (R[1].ext % (128 / r0) == 0 || R.size() == 2)) {
+    rb[0] = (uint32_t)tile;
+  } else if (tile % r0 == 0 && R.size() >= 2 && (R[1].ext % (tile / r0) == 0 || R.size() == 2)) {
     // (the last tile of a two-dim row group may run past the outer extent:
     // zero-filled, as rows past the view)
     nrb = 2;
     rb[0] = (uint32_t)r0;
-    rb[1] = (uint32_t)(128 / r0);
+    rb[1] = (uint32_t)(tile / r0);
   } else if (R.size() == 1) {
     nrb = 1;
-    rb[0] = 128;  // the last tile's rows past the extent are zero-filled
+    rb[0] = (uint32_t)tile;  // the last tile's rows past the extent are zero-filled
   } else {
     return false;
   }
@@ -494,6 +503,82 @@ const TmaParams* sgett_tma(DevPlan& dp, const float* A, const float* B) {
   return &dp.tma_p;
 }
 
+// CTA-pair SGETT (sgett_tc.cu pair kernel) on the swapped roles: M2 = the
+// plan's N (a K-major B', its rows 256 per pair in TMEM), N2 = the plan's M
+// (a rows-major A' of <= 128 rows, split across the pair).  Returns 1 when
+// launched, 0 when the call does not fit, < 0 on error.
+int try_sgett_pair(DevPlan& dp, const float* A, const float* B, float* C, int neg, cudaStream_t stream,
+                   DevState& ds, StreamWs& sw) {
+  const Plan& p = dp.plan;
+  if (!g_pair || !g_tma) return 0;
+  const int64_t K = p.gk.G;
+  if (dp.pair_state == 0) {
+    // orientation 1 (swap): the K-major operand is the plan's B' (c5);
+    // orientation 2: it is the plan's A'
+    dp.pair_state = -1;
+    for (int o = 1; o <= 2 && dp.pair_state < 0; ++o) {
+      const Group& big = o == 1 ? p.gn : p.gm;    // rows of the K-major operand
+      const Group& narrow = o == 1 ? p.gm : p.gn;
+      const int tb = o == 1 ? 1 : 0, tn = o == 1 ? 0 : 1;  // their k tensors in gk
+      if (K % 16 == 0 && big.G >= 256 && narrow.G <= 128 && narrow.G % 16 == 0 &&
+          tma_layout(big, 0, p.gk, tb, dp.pair_l[0]) && dp.pair_l[0].op.kf == 1 &&
+          tma_layout(narrow, 0, p.gk, tn, dp.pair_l[1], (int)(narrow.G / 2)) && dp.pair_l[1].op.kf == 0) {
+        dp.pair_state = o;
+        dp.pgk = dp.gk;
+        if (o == 1) {
+          std::swap(dp.pgk.T[0], dp.pgk.T[1]);
+          std::swap(dp.pgk.s_in[0], dp.pgk.s_in[1]);
+        }
+      }
+    }
+  }
+  if (dp.pair_state < 1) return 0;
+  const bool sw1 = dp.pair_state == 1;
+  const float* A2 = sw1 ? B : A;  // K-major operand (rows in TMEM)
+  const float* B2 = sw1 ? A : B;  // narrow rows-major operand
+  if (dp.pair_base[0] != A2 || dp.pair_base[1] != B2) {
+    if (!tma_encode(dp.pair_l[0], A2, &dp.pair_p.map[0]) || !tma_encode(dp.pair_l[1], B2, &dp.pair_p.map[1])) {
+      dp.pair_base[0] = dp.pair_base[1] = nullptr;
+      return 0;
+    }
+    dp.pair_p.op[0] = dp.pair_l[0].op;
+    dp.pair_p.op[1] = dp.pair_l[1].op;
+    dp.pair_base[0] = A2;
+    dp.pair_base[1] = B2;
+  }
+  if (!ds.sms) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const int64_t M2 = sw1 ? p.gn.G : p.gm.G, N2 = sw1 ? p.gm.G : p.gn.G;
+  const int64_t pairs = (M2 + 255) / 256, kblocks = K / 16;
+  int64_t splits = g_split > 0 ? g_split : ds.sms / (2 * pairs);
+  if (splits > kblocks / 2) splits = kblocks / 2;
+  if (splits < 1) splits = 1;
+  const int64_t kchunk = ((kblocks + splits - 1) / splits) * 16;
+  splits = (K + kchunk - 1) / kchunk;
+  TiledParams<float> tp;
+  tp.A = A2; tp.B = B2; tp.C = C;
+  tp.gm = sw1 ? dp.gn : dp.gm;
+  tp.gn = sw1 ? dp.gm : dp.gn;
+  tp.gk = dp.pgk;
+  tp.M = (int32_t)M2; tp.N = (int32_t)N2; tp.K = (int32_t)K;
+  tp.tiles_m = (int32_t)pairs;  // (for the reduce: one column of tiles)
+  tp.tiles_n = 1;
+  tp.splits = (int32_t)splits;
+  tp.k_chunk = (int32_t)kchunk;
+  tp.neg = neg;
+  tp.ws_t = 1;
+  int rc = ensure(sw.ws, (size_t)splits * M2 * N2 * sizeof(float));
+  if (rc) return rc;
+  tp.ws = (float*)sw.ws.p;
+  CK(launch_sgett_tc_pair(tp, dp.pair_p, stream));
+  g_launches += 2;
+  t_last_kernel = "sgett_tc3xtf32_pair_splitk";
+  return 1;
+}
+
 template <typename T>
 int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, DevState& ds,
                int neg = 0, bool force_tiled = false) {
@@ -610,6 +695,12 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     bool bnd = V == 2 ? dp.bn_even2 : dp.bn_even4;
     a_vec = a_kf ? vec_ok(gkA, akd, dp.gm, amd, V, A) : vec_ok(dp.gm, amd, gkA, akd, V, A);
     b_vec = b_kf ? vec_ok(gkB, bkd, dp.gn, bnd, V, B) : vec_ok(dp.gn, bnd, gkB, bkd, V, B);
+  }
+  if (use_tc && sizeof(T) == 4) {
+    const int pr = try_sgett_pair(dp, reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B),
+                                  reinterpret_cast<float*>(c), neg, stream, ds, sw);
+    if (pr < 0) return pr;
+    if (pr > 0) return 0;
   }
   if (use_tc) {
     const TmaParams* tma =
@@ -1188,6 +1279,12 @@ int gett_set_pipeline(int slabs) {
 int gett_set_stream_k(int on) {
   if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
   g_stream_k = on != 0;
+  return 0;
+}
+
+int gett_set_pair(int on) {
+  if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
+  g_pair = on != 0;
   return 0;
 }
 

@@ -40,6 +40,10 @@ int dgett_ws_tiles_k(int K);  // k-blocks per tile
 cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bool a_kf, bool b_kf,
                             bool a_vec, bool b_vec, cudaStream_t s);
 
+// CTA-pair SGETT (M = 256 per pair, N <= 128 split across the pair; both
+// operands TMA-fed: A' K-major, B' rows-major with NBH-row boxes); split-K
+cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s);
+
 int tiled_bm();
 int tiled_bn();
 int tiled_bk(int elt_bytes);

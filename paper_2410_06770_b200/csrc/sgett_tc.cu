@@ -785,6 +785,248 @@ __global__ void __launch_bounds__(THREADS, 1)
 #endif
 }
 
+
+// ---------------------------------------------------------------------------
+// CTA-pair variant (tcgen05.mma.cta_group::2, M = 256 per pair): for a
+// K-major A' (TMA SW32 boxes, split into each CTA's TMEM: rows 128r..128r+127
+// of the pair's 256) and a rows-major B' of at most 128 rows (one n-tile),
+// split across the pair N-wise — CTA r holds rows NBH*r..NBH*r+NBH-1 of B' in
+// its own shared memory (tools/umma_2cta_test.cu: B is split N-wise, A comes
+// from each CTA's TMEM).  Halves B' traffic per SM and removes the M padding
+// of a narrow N (c5: M' = 768 orig-A rows, N' = 96 orig-B rows).  Both CTAs
+// load and split their own parts; their split warps arrive on the leader's
+// ready barrier (cluster scope); the leader's MMA thread issues the pair MMAs
+// and multicasts each commit to both CTAs' barriers.
+namespace pair {
+#ifndef GETT_PAIR_STAGES
+#define GETT_PAIR_STAGES 12
+#endif
+constexpr int STAGES2 = GETT_PAIR_STAGES;
+constexpr int NBH_MAX = 64;                        // B' rows per CTA
+constexpr int A_BYTES = 128 * BK * 4;              // 8 KB: two SW32 boxes
+constexpr int BRAW_BYTES = NBH_MAX * BK * 4;       // 4 KB: [16 k][NBH rows]
+constexpr int STAGE2_BYTES = A_BYTES + BRAW_BYTES;
+constexpr int BT_BYTES = NBH_MAX * BK * 4;         // one K-major B' hi or lo tile
+constexpr int BHI_OFF = STAGES2 * STAGE2_BYTES;
+constexpr int BLO_OFF = BHI_OFF + LO_BUFS * BT_BYTES;
+constexpr int BAR2_OFF = BLO_OFF + LO_BUFS * BT_BYTES;
+constexpr int SMEM2_BYTES = BAR2_OFF + 512;
+static_assert(ACC_COLS + STAGES2 * A_COLS <= TMEM_COLS, "TMEM budget");
+static_assert(3 * STAGES2 + 1 + LO_BUFS <= 512 / 8, "barrier area");
+constexpr int SBO64 = CH * 128;                    // 8-row groups, K-major no-swizzle
+
+__device__ __forceinline__ void arrive_leader(uint32_t local_bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(local_bar));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(addr),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                         uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync2() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// raw [16 k][nbh rows] (TMA) -> K-major hi (raw) and lo tiles, 64-row capacity
+__device__ __forceinline__ void split_b_pair(const uint8_t* raw, uint8_t* hi, uint8_t* lo, int nbh, int tw) {
+  for (int u = tw; u < nbh * CH; u += WG) {
+    const int c = u / nbh, row = u - c * nbh;
+    float4 x;
+    x.x = *reinterpret_cast<const float*>(raw + (4 * c + 0) * nbh * 4 + row * 4);
+    x.y = *reinterpret_cast<const float*>(raw + (4 * c + 1) * nbh * 4 + row * 4);
+    x.z = *reinterpret_cast<const float*>(raw + (4 * c + 2) * nbh * 4 + row * 4);
+    x.w = *reinterpret_cast<const float*>(raw + (4 * c + 3) * nbh * 4 + row * 4);
+    const uint32_t o = (uint32_t)((row >> 3) * SBO64 + c * LBO + (row & 7) * 16);
+    *reinterpret_cast<float4*>(hi + o) = x;
+    *reinterpret_cast<float4*>(lo + o) = make_float4(tf32_lo(x.x), tf32_lo(x.y), tf32_lo(x.z), tf32_lo(x.w));
+  }
+}
+
+// grid: 2 x pairs x splits (clusters of 2); p.M = A' rows, p.N = 2 * nbh
+__global__ void __launch_bounds__(THREADS, 1)
+    sgett_tc_pair_kernel(const __grid_constant__ TiledParams<float> p, const __grid_constant__ TmaParams tp) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR2_OFF);
+  uint64_t* ready = full + STAGES2;   // leader: 8 warp arrivals (4 per CTA)
+  uint64_t* empty = ready + STAGES2;  // pair commit
+  uint64_t* done = empty + STAGES2;
+  uint64_t* lofree = done + 1;
+  __shared__ uint32_t tmem_slot;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int npairs = (p.M + 255) / 256;
+  const int cl = blockIdx.x >> 1;
+  const int pr = cl % npairs, split = cl / npairs;
+  const int m0 = pr * 256 + 128 * (int)rank;  // this CTA's A' rows
+  const int nbh = p.N / 2;
+  const int kbeg = split * p.k_chunk;
+  const int kend = min(p.K, kbeg + p.k_chunk);
+  const int nkb = kend > kbeg ? (kend - kbeg) / BK : 0;
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[0]) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[1]) : "memory");
+    for (int s = 0; s < STAGES2; ++s) {
+      mbar_init(smem_u32(full + s), 1);
+      mbar_init(smem_u32(ready + s), 8);
+      mbar_init(smem_u32(empty + s), 1);
+    }
+    mbar_init(smem_u32(done), 1);
+    for (int l = 0; l < LO_BUFS; ++l) mbar_init(smem_u32(lofree + l), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(&tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync2();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 0) {
+    // producer lanes 0-1: A' boxes (k 0-7, 8-15); lanes 2-3: B' boxes
+    if (lane < 4) {
+      const int t = lane >> 1, h = lane & 1;
+      TmaCoord cc;
+      if (t) cc.init(tp.op[1], nbh * (int)rank, kbeg + 8 * h);
+      else cc.init(tp.op[0], m0, kbeg + 8 * h);
+      const CUtensorMap* map = t ? &tp.map[1] : &tp.map[0];
+      const uint32_t dst0 = smem_u32(smem) + (t ? A_BYTES + h * 8 * nbh * 4 : 4096 * h);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES2, u = kb / STAGES2;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        const uint32_t fb = smem_u32(full + s);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(A_BYTES + 16 * nbh * 4)
+                       : "memory");
+        int32_t c[5];
+        cc.coords(c);
+        tma_load5(dst0 + s * STAGE2_BYTES, map, c, fb);
+        cc.step();
+      }
+    }
+  } else if (warp >= 4 && warp < MMA_WARP) {
+    // ---------------- split warpgroups (alternate k-blocks), then epilogue ----------------
+    const int h = (warp - 4) >> 2, wq = warp & 3, tw = (tid - WG) & (WG - 1);
+    for (int kb = h; kb < nkb; kb += 2) {
+      const int s = kb % STAGES2, u = kb / STAGES2;
+      mbar_wait(smem_u32(full + s), u & 1);
+      const int lb = kb % LO_BUFS, lu = kb / LO_BUFS;
+      if (lu > 0) mbar_wait(smem_u32(lofree + lb), (lu - 1) & 1);
+      const uint8_t* st = smem + s * STAGE2_BYTES;
+      split_a_tmem<2>(st, tmem, ACC_COLS + s * A_COLS, wq, lane);
+      split_b_pair(st + A_BYTES, smem + BHI_OFF + lb * BT_BYTES, smem + BLO_OFF + lb * BT_BYTES, nbh, tw);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) arrive_leader(smem_u32(ready + s));
+    }
+    if (nkb > 0) mbar_wait(smem_u32(done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // accumulator rows = this CTA's 128 A' rows (lane quarter wq), columns
+    // 64h..64h+63 of the 2*nbh
+    const int lane_row = 32 * wq + lane;
+    const int m = m0 + lane_row;
+    const bool mok = m < p.M;
+    const int cbeg = 64 * h, cend = min(cbeg + 64, p.N);
+    float* wcol = p.ws + (int64_t)split * p.M * p.N + (mok ? m : 0);
+    for (int c0 = cbeg; c0 < cend; c0 += 16) {
+      uint32_t r[16];
+      const uint32_t taddr = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+          : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+            "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (!mok) continue;
+#pragma unroll
+      for (int i = 0; i < 16; ++i) {
+        const int n = c0 + i;
+        if (n < p.N) wcol[(int64_t)n * p.M] = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
+      }
+    }
+  } else if (warp == MMA_WARP && rank == 0) {
+    // ---------------- MMA issue (leader CTA) ----------------
+    if (lane == 0) {
+      const uint32_t base = smem_u32(smem);
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.N >> 3) << 17) | ((256u >> 4) << 24);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGES2, u = kb / STAGES2;
+        mbar_wait_cluster(smem_u32(ready + s), u & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const int lb = kb % LO_BUFS;
+        const uint32_t bh0 = base + BHI_OFF + lb * BT_BYTES, bl0 = base + BLO_OFF + lb * BT_BYTES;
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint32_t ah = tmem + ACC_COLS + s * A_COLS + 8 * j, al = ah + BK;
+          const uint64_t bh = sdesc(bh0 + 256 * j, LBO, SBO64), bl = sdesc(bl0 + 256 * j, LBO, SBO64);
+          mma_pair(tmem, ah, bh, idesc, (kb | j) != 0);
+          mma_pair(tmem, al, bh, idesc, 1);
+          mma_pair(tmem, ah, bl, idesc, 1);
+        }
+        commit_pair(smem_u32(empty + s));
+        commit_pair(smem_u32(lofree + lb));
+      }
+      commit_pair(smem_u32(done));
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  cluster_sync2();
+  if (warp == MMA_WARP)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+}  // namespace pair
+
+cudaError_t launch_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
+  auto k = pair::sgett_tc_pair_kernel;
+  static unsigned long long configured = 0;
+  cudaError_t e = ensure_dyn_smem(k, pair::SMEM2_BYTES, configured);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * ((p.M + 255) / 256) * p.splits));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = pair::SMEM2_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, p, tp);
+}
+
 template <bool AKF, bool BKF, bool AV, bool BV, bool TMA>
 cudaError_t launch4(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
   auto k = sgett_tc_kernel<AKF, BKF, AV, BV, TMA>;
@@ -815,6 +1057,12 @@ cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bo
   else if (b_kf) e = tc::launch2<false, true>(p, tp, a_vec, b_vec, s);
   else e = tc::launch2<false, false>(p, tp, a_vec, b_vec, s);
   if (e != cudaSuccess || p.splits == 1) return e;
+  return launch_splitk_reduce<float>(p, s);
+}
+
+cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
+  cudaError_t e = tc::launch_pair(p, tp, s);
+  if (e != cudaSuccess) return e;
   return launch_splitk_reduce<float>(p, s);
 }
 

@@ -156,3 +156,34 @@ def test_tma_falls_back_on_negative_strides(kernel_mode):
     want = _strided(c0, (200, 136), c_inc, off_c) + np.einsum("mij,ijn->mn", A, B)
     got = _strided(c, (200, 136), c_inc, off_c).astype(np.float64)
     assert np.max(np.abs(got - want)) / (640 * np.abs(a).max() * np.abs(b).max()) <= 1e-5
+
+
+@pytest.mark.parametrize("M,N,K1,K2", [(96, 768, 24, 40), (64, 300, 16, 32), (128, 512, 8, 40)])
+def test_pair_kernel_matches_single_cta(M, N, K1, K2, kernel_mode):
+    """The CTA-pair kernel (tcgen05.mma.cta_group::2: B' rows 256 per pair in
+    the two CTAs' TMEM, the narrow operand split N-wise across the pair's
+    shared memory) computes the same products in the same k order as the
+    single-CTA TMA kernel: C bitwise equal, and within the fp64 bar."""
+    rng = np.random.default_rng(M + N + K1)
+    # A (m, k1, k2) rows-major (m fastest); B (n, k1, k2) K-major; C[m, n] m fastest
+    a_dims, b_dims = (M, K1, K2), (N, K1, K2)
+    a_inc = (1, M + 4, (M + 4) * K1)
+    b_inc = (K1 * K2 + 4, K2, 1)
+    a = rng.uniform(-1, 1, (M + 4) * K1 * K2 + 8).astype(np.float32)
+    b = rng.uniform(-1, 1, N * (K1 * K2 + 4) + 8).astype(np.float32)
+    c0 = rng.uniform(-1, 1, (M + 4) * N + 8).astype(np.float32)
+    outs, kernels = [], []
+    for pair in (True, False):
+        kernel_mode("tiled", pair=pair)
+        c = c0.copy()
+        assert g.sgett(3, a_dims, a_inc, a, 3, b_dims, b_inc, b, 2, (1, 2), (1, 2), (0, 1), (1, M + 4), c,
+                       offset_c=2) == []
+        kernels.append(g.last_kernel())
+        outs.append(c)
+    assert kernels[0] == "sgett_tc3xtf32_pair_splitk" and "pair" not in kernels[1], kernels
+    assert outs[0].tobytes() == outs[1].tobytes(), kernels
+    A = _strided(a, a_dims, a_inc, 0).astype(np.float64)
+    B = _strided(b, b_dims, b_inc, 0).astype(np.float64)
+    want = _strided(c0, (M, N), (1, M + 4), 2).astype(np.float64) + np.einsum("mij,nij->mn", A, B)
+    got = _strided(outs[0], (M, N), (1, M + 4), 2).astype(np.float64)
+    assert np.max(np.abs(got - want)) / (K1 * K2 * np.abs(a).max() * np.abs(b).max()) <= 1e-5
