@@ -940,8 +940,10 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int lb = kb % LO_BUFS, lu = kb / LO_BUFS;
       if (lu > 0) mbar_wait(smem_u32(lofree + lb), (lu - 1) & 1);
       const uint8_t* st = smem + s * STAGE2_BYTES;
-      split_a_tmem<2>(st, tmem, ACC_COLS + s * A_COLS, wq, lane);
-      split_b_pair(st + A_BYTES, smem + BHI_OFF + lb * BT_BYTES, smem + BLO_OFF + lb * BT_BYTES, nbh, tw);
+      if (!(GETT_TC_ABLATE & 2)) {
+        split_a_tmem<2>(st, tmem, ACC_COLS + s * A_COLS, wq, lane);
+        split_b_pair(st + A_BYTES, smem + BHI_OFF + lb * BT_BYTES, smem + BLO_OFF + lb * BT_BYTES, nbh, tw);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -988,6 +990,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         for (int j = 0; j < BK / 8; ++j) {
           const uint32_t ah = tmem + ACC_COLS + s * A_COLS + 8 * j, al = ah + BK;
           const uint64_t bh = sdesc(bh0 + 256 * j, LBO, SBO64), bl = sdesc(bl0 + 256 * j, LBO, SBO64);
+          if (GETT_TC_ABLATE & 4) continue;
           mma_pair(tmem, ah, bh, idesc, (kb | j) != 0);
           mma_pair(tmem, al, bh, idesc, 1);
           mma_pair(tmem, ah, bl, idesc, 1);
