@@ -685,6 +685,10 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
   }
   // launched as a programmatic dependent of the split-K kernel: wait for its
   // partials (no-op for an ordinary launch)
+  // C's element (offset tables, then its value) does not depend on the
+  // partials: fetched first, so its two round trips overlap the partials'
+  T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
+  const T c0 = *c;
   asm volatile("griddepcontrol.wait;" ::: "memory");
   // the slices' partials in a fixed order; loads batched 8 at a time so their
   // latencies overlap
@@ -698,8 +702,7 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
     for (int j = 0; j < 8; ++j) s = s + v[j];
   }
   for (; sp < p.splits; ++sp) s = s + __ldcg(p.ws + sp * mn + idx);
-  T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
-  *c = epi(*c, s, p.neg);
+  *c = epi(c0, s, p.neg);
 }
 
 template <typename T>
