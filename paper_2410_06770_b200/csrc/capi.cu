@@ -725,7 +725,11 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
       CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
     }
     const int64_t G = ds.sms;
-    if (g_stream_k && splits == 1 && tiles % G != 0 && 2 * tiles > G) {
+    // (not inside a CUDA-graph capture: replays would reuse the publish epoch)
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(stream, &cap));
+    if (g_stream_k && cap == cudaStreamCaptureStatusNone && splits == 1 && tiles % G != 0 &&
+        2 * tiles > G) {
       // persistent: the last 1-2 waves of tiles (all of them below 2 waves)
       // are shared out by k-block units, the rest run data-parallel; below one
       // wave (G/2 < tiles < G, where split-K cannot help) the shares are

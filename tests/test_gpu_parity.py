@@ -686,3 +686,39 @@ def test_dot_kernels_match_fp64(K1, K2, neg, a_kfast, kernel_mode):
     mask = np.ones(len(c0), bool)
     mask[3:3 + M * N] = False
     assert c[mask].tobytes() == c0[mask].tobytes()
+
+
+# ---------------------------------------------------------------------------
+# CUDA-graph replay of a device call (graph.py)
+
+
+@pytest.mark.parametrize("name", ["c1", "c3", "c4", "c5"])
+def test_graph_replay_equals_direct_calls(name, kernel_mode):
+    """Replaying a captured call twice gives C bitwise equal to three direct
+    calls (the construction runs the call once), for the dot, DGETT and
+    split-K SGETT paths (DGETT direct calls with stream-K off: a captured DGETT
+    runs one CTA per tile)."""
+    import torch
+
+    from paper_2410_06770_b200.device import dgett_device, sgett_device
+    from paper_2410_06770_b200.graph import GettGraph
+    from paper_2410_06770_b200.workloads import CONFIGS as W
+
+    kernel_mode("auto", stream_k=False)
+    w = W[name]
+    a, b, c = w.buffers()
+    fn = dgett_device if w.dtype == "d" else sgett_device
+    outs = []
+    for use_graph in (True, False):
+        ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+        pos, kw = w.args(ta, tb, tc)
+        if use_graph:
+            gg = GettGraph(fn, *pos, **kw)
+            gg.replay()
+            gg.replay()
+        else:
+            for _ in range(3):
+                assert fn(*pos, **kw) == []
+        torch.cuda.synchronize()
+        outs.append(tc.cpu().numpy())
+    assert outs[0].tobytes() == outs[1].tobytes()
