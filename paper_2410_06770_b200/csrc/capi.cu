@@ -1355,6 +1355,6 @@ void gett_release_caches(void) {
   }
 }
 
-int gett_abi_version(void) { return 100; }
+int gett_abi_version(void) { return 102; }  // 1.02: gett_set_tma, gett_set_pair
 
 }  // extern "C"
