@@ -133,3 +133,44 @@ def test_zero_view_golden_cpu_checks():
     empty = [c for c in cases if 0 in c["ext"] or any(e < 0 for e in c["ext"])]
     for c in empty:
         assert c["result"] == list(np.arange(1, c["n"] + 1, dtype=float))
+
+
+# ---------------------------------------------------------------------------
+# a plain C caller (tools/abi_c_example.c) links libgett_b200.so through
+# include/gett_b200.h alone
+
+
+def _build_c_example(tmp_path):
+    import shutil
+    import subprocess
+
+    if shutil.which("gcc") is None:
+        pytest.skip("gcc not available")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    pkg = os.path.join(root, "paper_2410_06770_b200")
+    exe = str(tmp_path / "abi_c_example")
+    subprocess.run(["gcc", "-std=c99", "-Wall", "-Werror", "-I", os.path.join(root, "include"),
+                    os.path.join(root, "tools", "abi_c_example.c"), "-L", pkg, "-lgett_b200",
+                    f"-Wl,-rpath,{pkg}", "-o", exe], check=True)
+    return exe
+
+
+def test_c_caller_gets_coded_validation_errors(tmp_path):
+    """Validation needs no GPU: a C program gets the reference-ordered error
+    codes back with C untouched."""
+    import subprocess
+
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe, "validate"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"c_untouched": 1' in r.stdout
+
+
+@pytest.mark.gpu
+def test_c_caller_contracts_on_the_gpu(tmp_path):
+    import subprocess
+
+    exe = _build_c_example(tmp_path)
+    r = subprocess.run([exe, "run"], capture_output=True, text=True)
+    assert r.returncode == 0, r.stdout + r.stderr
+    assert '"bitwise_equal": 1' in r.stdout
