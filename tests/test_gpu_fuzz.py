@@ -1,0 +1,121 @@
+"""Randomised descriptors through the tiled kernels: ranks 2-4, one to three
+contracted pairs, random mode orders and paddings (strides multiples of 4, so
+the TMA SGETT path is eligible whenever K is a multiple of 16), random C
+layouts and offsets.  Each case is checked against an fp64 contraction with
+the K-normalised bar of test_gpu_parity.py, bytes outside C's view must not
+change, and for fp32 the TMA and gather paths must agree bitwise."""
+import numpy as np
+import pytest
+
+import paper_2410_06770_b200 as g
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"s": 1e-5, "d": 1e-12}
+
+
+def _case(rng):
+    while True:
+        c = _draw(rng)
+        size_c = int(np.prod(c[10]))
+        k = int(np.prod([c[0][d] for d in c[7]]))
+        if size_c <= 400_000 and k <= 2048:
+            return c
+
+
+def _draw(rng):
+    conts = int(rng.integers(1, 4))
+    fa, fb = int(rng.integers(1, 3)), int(rng.integers(1, 3))
+    kext = [int(rng.choice([2, 4, 8, 16, 24, 40])) for _ in range(conts)]
+    fea = [int(rng.integers(8, 200)) for _ in range(fa)]
+    feb = [int(rng.integers(8, 200)) for _ in range(fb)]
+    # positions of contracted modes inside A and B
+    ra, rb = fa + conts, fb + conts
+    pos_a = list(rng.permutation(ra))
+    pos_b = list(rng.permutation(rb))
+    cont_a = tuple(int(x) for x in pos_a[:conts])
+    cont_b = tuple(int(x) for x in pos_b[:conts])
+    ext_a, ext_b = [0] * ra, [0] * rb
+    for k, (ia, ib) in enumerate(zip(cont_a, cont_b)):
+        ext_a[ia] = ext_b[ib] = kext[k]
+    for d, e in zip(pos_a[conts:], fea):
+        ext_a[d] = e
+    for d, e in zip(pos_b[conts:], feb):
+        ext_b[d] = e
+
+    def incs(ext):
+        order = rng.permutation(len(ext))
+        inc, step = [0] * len(ext), 1
+        for d in order:
+            inc[d] = step
+            pad = int(rng.choice([0, 4, 8]))
+            step *= ext[d] + pad + (4 - ext[d] % 4) % 4
+        return tuple(inc), step
+
+    inc_a, span_a = incs(ext_a)
+    inc_b, span_b = incs(ext_b)
+    rc = fa + fb
+    perm = tuple(int(x) for x in rng.permutation(rc))
+    ext_c = [0] * rc
+    free = [ext_a[d] for d in range(ra) if d not in cont_a] + [ext_b[d] for d in range(rb) if d not in cont_b]
+    for i, e in enumerate(free):
+        ext_c[perm[i]] = e
+    inc_c, span_c = incs(ext_c)
+    return (ext_a, inc_a, span_a, ext_b, inc_b, span_b, conts, cont_a, cont_b, perm, ext_c, inc_c, span_c)
+
+
+def _strided(buf, ext, inc, off):
+    return np.lib.stride_tricks.as_strided(buf[off:], shape=ext, strides=[i * buf.itemsize for i in inc])
+
+
+@pytest.mark.parametrize("dtype", ["s", "d"])
+def test_random_descriptors(dtype, kernel_mode):
+    rng = np.random.default_rng(2024 if dtype == "s" else 2025)
+    np_t = np.float32 if dtype == "s" else np.float64
+    entry = g.sgett if dtype == "s" else g.dgett
+    letters = "abcdefghijklmnop"
+    n_tma = 0
+    for case_i in range(150):
+        (ext_a, inc_a, span_a, ext_b, inc_b, span_b, conts, cont_a, cont_b, perm, ext_c, inc_c,
+         span_c) = _case(rng)
+        off_a, off_b, off_c = (int(rng.integers(0, 3)) * 4 for _ in range(3))
+        a = rng.uniform(-1, 1, off_a + span_a + 4).astype(np_t)
+        b = rng.uniform(-1, 1, off_b + span_b + 4).astype(np_t)
+        c0 = rng.uniform(-1, 1, off_c + span_c + 4).astype(np_t)
+        outs = []
+        for tma in ((True, False) if dtype == "s" else (True,)):
+            kernel_mode("tiled", tma=tma)
+            c = c0.copy()
+            assert entry(len(ext_a), tuple(ext_a), inc_a, a, len(ext_b), tuple(ext_b), inc_b, b, conts, cont_a,
+                         cont_b, perm, inc_c, c, offset_a=off_a, offset_b=off_b, offset_c=off_c) == []
+            if tma and "tma" in g.last_kernel():
+                n_tma += 1
+            outs.append(c)
+        if dtype == "s":
+            assert outs[0].tobytes() == outs[1].tobytes(), case_i
+        # fp64 reference
+        la = [letters[i] for i in range(len(ext_a))]
+        lb = [None] * len(ext_b)
+        for ia, ib in zip(cont_a, cont_b):
+            lb[ib] = la[ia]
+        nxt = iter(letters[len(ext_a):])
+        lb = [x if x is not None else next(nxt) for x in lb]
+        free_l = [la[d] for d in range(len(ext_a)) if d not in cont_a] + \
+                 [lb[d] for d in range(len(ext_b)) if d not in cont_b]
+        out_l = [None] * len(free_l)
+        for i, l in enumerate(free_l):
+            out_l[perm[i]] = l
+        A = _strided(a, ext_a, inc_a, off_a).astype(np.float64)
+        B = _strided(b, ext_b, inc_b, off_b).astype(np.float64)
+        prod = np.einsum("".join(la) + "," + "".join(lb) + "->" + "".join(out_l), A, B, optimize=True)
+        want = _strided(c0, ext_c, inc_c, off_c).astype(np.float64) + prod
+        got = _strided(outs[0], ext_c, inc_c, off_c).astype(np.float64)
+        K = int(np.prod([ext_a[d] for d in cont_a]))
+        err = np.max(np.abs(got - want)) / (K * np.abs(a).max() * np.abs(b).max())
+        assert err <= TOL[dtype], (case_i, g.last_kernel(), err)
+        mask = np.ones(len(c0), bool)
+        idx = off_c + sum(np.ix_(*[np.arange(e) * i for e, i in zip(ext_c, inc_c)]))
+        mask[np.asarray(idx).ravel()] = False
+        assert outs[0][mask].tobytes() == c0[mask].tobytes(), case_i
+    if dtype == "s":
+        assert n_tma > 0  # the TMA path was exercised
