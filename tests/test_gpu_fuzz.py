@@ -119,3 +119,62 @@ def test_random_descriptors(dtype, kernel_mode):
         assert outs[0][mask].tobytes() == c0[mask].tobytes(), case_i
     if dtype == "s":
         assert n_tma > 0  # the TMA path was exercised
+
+
+@pytest.mark.parametrize("dtype", ["s", "d"])
+def test_random_descriptors_auto_mode_negative_strides(dtype, kernel_mode):
+    """The same generator in auto mode (ref / dot / tiled / split-K chosen by
+    size) with some increments negated (base offsets moved to the high end)."""
+    rng = np.random.default_rng(7 if dtype == "s" else 8)
+    np_t = np.float32 if dtype == "s" else np.float64
+    entry = g.sgett if dtype == "s" else g.dgett
+    letters = "abcdefghijklmnop"
+    kernel_mode("auto")
+    kernels = set()
+    for case_i in range(120):
+        (ext_a, inc_a, span_a, ext_b, inc_b, span_b, conts, cont_a, cont_b, perm, ext_c, inc_c,
+         span_c) = _case(rng)
+        # shrink some cases so the ref / dot kernels are chosen too
+        if case_i % 3 == 0:
+            ext_a = [min(e, 6) if d not in cont_a else e for d, e in enumerate(ext_a)]
+            ext_b = [min(e, 6) if d not in cont_b else e for d, e in enumerate(ext_b)]
+            free = [ext_a[d] for d in range(len(ext_a)) if d not in cont_a] + \
+                   [ext_b[d] for d in range(len(ext_b)) if d not in cont_b]
+            ext_c = [0] * len(free)
+            for i, e in enumerate(free):
+                ext_c[perm[i]] = e
+        sign = lambda inc: tuple(i if rng.random() < 0.7 else -i for i in inc)  # noqa: E731
+        inc_a, inc_b = sign(inc_a), sign(inc_b)
+        low = lambda ext, inc: -sum((e - 1) * i for e, i in zip(ext, inc) if i < 0)  # noqa: E731
+        off_a, off_b, off_c = low(ext_a, inc_a), low(ext_b, inc_b), 3
+        a = rng.uniform(-1, 1, span_a + 8).astype(np_t)
+        b = rng.uniform(-1, 1, span_b + 8).astype(np_t)
+        c0 = rng.uniform(-1, 1, off_c + span_c + 4).astype(np_t)
+        c = c0.copy()
+        assert entry(len(ext_a), tuple(ext_a), inc_a, a, len(ext_b), tuple(ext_b), inc_b, b, conts, cont_a,
+                     cont_b, perm, inc_c, c, offset_a=off_a, offset_b=off_b, offset_c=off_c) == []
+        kernels.add(g.last_kernel())
+        la = [letters[i] for i in range(len(ext_a))]
+        lb = [None] * len(ext_b)
+        for ia, ib in zip(cont_a, cont_b):
+            lb[ib] = la[ia]
+        nxt = iter(letters[len(ext_a):])
+        lb = [x if x is not None else next(nxt) for x in lb]
+        free_l = [la[d] for d in range(len(ext_a)) if d not in cont_a] + \
+                 [lb[d] for d in range(len(ext_b)) if d not in cont_b]
+        out_l = [None] * len(free_l)
+        for i, l in enumerate(free_l):
+            out_l[perm[i]] = l
+        A = _strided(a, ext_a, inc_a, off_a).astype(np.float64)
+        B = _strided(b, ext_b, inc_b, off_b).astype(np.float64)
+        prod = np.einsum("".join(la) + "," + "".join(lb) + "->" + "".join(out_l), A, B, optimize=True)
+        want = _strided(c0, ext_c, inc_c, off_c).astype(np.float64) + prod
+        got = _strided(c, ext_c, inc_c, off_c).astype(np.float64)
+        K = int(np.prod([ext_a[d] for d in cont_a]))
+        err = np.max(np.abs(got - want)) / (K * np.abs(a).max() * np.abs(b).max())
+        assert err <= TOL[dtype], (case_i, g.last_kernel(), err)
+        mask = np.ones(len(c0), bool)
+        idx = off_c + sum(np.ix_(*[np.arange(e) * i for e, i in zip(ext_c, inc_c)]))
+        mask[np.asarray(idx).ravel()] = False
+        assert c[mask].tobytes() == c0[mask].tobytes(), case_i
+    assert len(kernels) >= 2, kernels
