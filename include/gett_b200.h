@@ -221,6 +221,10 @@ int gett_set_tma(int on);
  * split-K shapes with a K-major operand of >= 256 rows and a rows-major one of
  * <= 128 (e.g. c5); 0 = off (the default), 1 = on.  Also GETT_PAIR. */
 int gett_set_pair(int on);
+/* cgett / zgett on the tensor-core kernels: 1 = one real GETT on a real
+ * embedding of the smaller operand (the default), 0 = four real GETTs on the
+ * re/im sub-views.  Also GETT_COMPLEX_EMBED. */
+int gett_set_complex_embed(int on);
 /* Name of the kernel the last call launched ("none" if none). */
 const char* gett_last_kernel(void);
 /* Text of the last CUDA / internal failure. */

@@ -18,7 +18,7 @@ EXPORTS = (
     "gett_zgett", "gett_cgett", "gett_zgett_device", "gett_cgett_device",
     "gett_validate", "gett_derive_output_extents",
     "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
-    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_pair", "gett_last_kernel", "gett_last_error",
+    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
 )
 
@@ -78,6 +78,8 @@ def _load():
     lib.gett_set_tma.argtypes = [ctypes.c_int]
     lib.gett_set_pair.restype = ctypes.c_int
     lib.gett_set_pair.argtypes = [ctypes.c_int]
+    lib.gett_set_complex_embed.restype = ctypes.c_int
+    lib.gett_set_complex_embed.argtypes = [ctypes.c_int]
     lib.gett_last_kernel.restype = ctypes.c_char_p
     lib.gett_last_kernel.argtypes = []
     lib.gett_last_error.restype = ctypes.c_char_p
@@ -143,6 +145,12 @@ def set_pair(on: bool) -> None:
     """SGETT CTA-pair (cta_group::2) kernel on / off (default off)."""
     if LIB.gett_set_pair(1 if on else 0) != 0:
         raise ValueError(f"bad pair switch {on}")
+
+
+def set_complex_embed(on: bool) -> None:
+    """cgett/zgett tiled path: one embedded real GETT (default) or four real GETTs."""
+    if LIB.gett_set_complex_embed(1 if on else 0) != 0:
+        raise ValueError(f"bad complex-embed switch {on}")
 
 
 def last_kernel() -> str:

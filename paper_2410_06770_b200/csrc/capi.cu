@@ -35,6 +35,7 @@ int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
 bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles > 1 wave and not whole waves (GETT_STREAM_K=0: off)
 bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=0: cp.async gathers)
+bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one embedded GETT (GETT_COMPLEX_EMBED=0)
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 bool g_env_read = false;
@@ -53,6 +54,8 @@ void read_env() {
   if (wsv) g_dgett_ws = std::atoi(wsv) != 0;
   const char* skv = std::getenv("GETT_STREAM_K");
   if (skv) g_stream_k = std::atoi(skv) != 0;
+  const char* ce = std::getenv("GETT_COMPLEX_EMBED");
+  if (ce) g_complex_4x = std::atoi(ce) == 0;
   const char* pv = std::getenv("GETT_PAIR");
   if (pv) g_pair = std::atoi(pv) != 0;
   const char* tv = std::getenv("GETT_TMA");
@@ -136,6 +139,7 @@ struct StreamWs {
   Scratch ws;         // split-K partials
   Scratch part;       // stream-K tail partials
   Scratch flags;      // stream-K publish flags (zeroed on allocation)
+  Scratch cx;         // real embedding of a complex operand
   int32_t epoch = 0;  // stream-K launches so far on this stream
 };
 struct DevState {
@@ -989,6 +993,114 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   return 0;
 }
 
+// Complex contraction as ONE real GETT on a real embedding.  The operand with
+// fewer elements (X; the other is Y) is expanded into a dense workspace X'
+// with two extra modes: q (contracted against a new stride-1 re/im mode of Y)
+// and s (a new stride-1 re/im mode of C):
+//   X'[.., q=0, .., s] = (re x, im x),   X'[.., q=1, .., s] = (-im x, re x)
+// so  C[.., s] += sum_{k,q} Y[k, q] X'[k, q, .., s]  is the complex product
+// (re c += re y re x - im y im x,  im c += re y im x + im y re x).  X' puts s
+// first, then X's free modes in C's stride order, then q, then the contracted
+// modes in Y's stride order, so the new modes fold into the neighbouring
+// groups (an M x 2N x 2K real GETT with the same inner strides as a real call).
+template <typename R>
+int run_complex_embedded(const View& va, const View& vb, const Spec& sp, const R* a2, const R* b2,
+                         R* c2, cudaStream_t stream, DevState& ds) {
+  auto count = [](const View& v) {
+    int64_t n = 1;
+    for (int d = 0; d < v.rank; ++d) n *= v.ext[d];
+    return n;
+  };
+  const bool swap = count(va) < count(vb);  // expand A (operand order Y = B, X = A)
+  const View& vy = swap ? vb : va;
+  const View& vx = swap ? va : vb;
+  const int64_t* cy = swap ? sp.cont_b : sp.cont_a;
+  const int64_t* cx = swap ? sp.cont_a : sp.cont_b;
+  const R* py = swap ? b2 : a2;
+  const R* px = swap ? a2 : b2;
+  // old free-list index of every free mode (A's free modes, then B's)
+  auto free_index = [&](const View& v, const int64_t* cont, int base, std::vector<int>& out) {
+    out.assign(v.rank, -1);
+    for (int d = 0; d < v.rank; ++d) {
+      bool c = false;
+      for (int j = 0; j < sp.conts; ++j) c |= cont[j] == d;
+      if (!c) out[d] = base++;
+    }
+    return base;
+  };
+  std::vector<int> fa, fb;
+  const int nfa = free_index(va, sp.cont_a, 0, fa);
+  free_index(vb, sp.cont_b, nfa, fb);
+  const std::vector<int>& fy = swap ? fb : fa;
+  const std::vector<int>& fx = swap ? fa : fb;
+  // X' strides (real elements): s = 1, free modes by |C stride|, q, contracted by |Y stride|
+  std::vector<int> xfree, xcont(sp.conts);
+  for (int d = 0; d < vx.rank; ++d)
+    if (fx[d] >= 0) xfree.push_back(d);
+  std::stable_sort(xfree.begin(), xfree.end(), [&](int x, int y) {
+    return std::llabs(sp.inc_c[sp.perm[fx[x]]]) < std::llabs(sp.inc_c[sp.perm[fx[y]]]);
+  });
+  for (int j = 0; j < sp.conts; ++j) xcont[j] = j;
+  std::stable_sort(xcont.begin(), xcont.end(), [&](int x, int y) {
+    return std::llabs(vy.inc[cy[x]]) < std::llabs(vy.inc[cy[y]]);
+  });
+  ExpandParams<R> ep{};
+  std::vector<int64_t> xinc(vx.rank + 2);
+  int64_t st = 2;
+  ep.n = 0;
+  for (int d : xfree) {
+    xinc[d] = st;
+    ep.ext[ep.n] = vx.ext[d]; ep.inc[ep.n] = vx.inc[d]; ep.dst_st[ep.n] = st; ++ep.n;
+    st *= vx.ext[d];
+  }
+  const int64_t q = st;
+  st *= 2;
+  for (int j : xcont) {
+    const int d = (int)cx[j];
+    xinc[d] = st;
+    ep.ext[ep.n] = vx.ext[d]; ep.inc[ep.n] = vx.inc[d]; ep.dst_st[ep.n] = st; ++ep.n;
+    st *= vx.ext[d];
+  }
+  xinc[vx.rank] = q;
+  xinc[vx.rank + 1] = 1;
+  ep.total = 1;
+  for (int i = 0; i < ep.n; ++i) ep.total *= ep.ext[i];
+  ep.q = q;
+  ep.src = px;
+  StreamWs& sw = ds.sws[stream];
+  int rc = ensure(sw.cx, (size_t)st * sizeof(R));
+  if (rc) return rc;
+  ep.dst = (R*)sw.cx.p;
+  CK(launch_expand_complex<R>(ep, stream));
+  ++g_launches;
+  // the real spec: Y' = Y + (re/im, stride 1), X' as laid out above, C + (s, stride 1)
+  std::vector<int64_t> yext(vy.ext, vy.ext + vy.rank), yinc(vy.rank + 1), xext(vx.ext, vx.ext + vx.rank);
+  for (int d = 0; d < vy.rank; ++d) yinc[d] = 2 * vy.inc[d];
+  yext.push_back(2);
+  yinc[vy.rank] = 1;
+  xext.push_back(2);
+  xext.push_back(2);
+  std::vector<int64_t> cy2(cy, cy + sp.conts), cx2(cx, cx + sp.conts);
+  cy2.push_back(vy.rank);
+  cx2.push_back(vx.rank);
+  std::vector<int64_t> perm2, inc_c2(sp.inc_c_len + 1);
+  for (int d = 0; d < vy.rank; ++d)
+    if (fy[d] >= 0) perm2.push_back(sp.perm[fy[d]]);
+  for (int d = 0; d < vx.rank; ++d)
+    if (fx[d] >= 0) perm2.push_back(sp.perm[fx[d]]);
+  perm2.push_back(sp.inc_c_len);
+  for (int d = 0; d < sp.inc_c_len; ++d) inc_c2[d] = 2 * sp.inc_c[d];
+  inc_c2[sp.inc_c_len] = 1;
+  View ry{vy.rank + 1, yext.data(), yinc.data(), 0, 2 * vy.len};
+  View rx{vx.rank + 2, xext.data(), xinc.data(), 0, st};
+  Spec rs{sp.conts + 1, cy2.data(), cx2.data(), (int)perm2.size(), perm2.data(), sp.inc_c_len + 1, inc_c2.data()};
+  std::shared_ptr<DevPlan> rp;
+  if ((rc = get_plan(sizeof(R) == 8 ? 'd' : 's', ry, rx, rs, 0, 0, &rp))) return rc;
+  if ((rc = run_device<R>(*rp, py, ep.dst, c2, stream, ds, 0, true))) return rc;
+  t_last_kernel = sizeof(R) == 8 ? "zgett_embedded_dmma" : "cgett_embedded_tc3xtf32";
+  return 0;
+}
+
 // Complex contraction on device buffers.  a2/b2/c2 point at each view's base
 // element as a real (re, im)-interleaved array.  ref/serial: complex kernels
 // in reference order; tiled: four real GETTs on the re/im sub-views (every
@@ -1034,6 +1146,8 @@ int run_complex(DevPlan& cp, const View& va, const View& vb, const Spec& sp, con
     t_last_kernel = z ? "zgett_ref_order" : "cgett_ref_order";
     return 0;
   }
+  if (std::max(va.rank, vb.rank) + 2 <= kExpandMaxModes && !g_complex_4x)
+    return run_complex_embedded<R>(va, vb, sp, a2, b2, c2, stream, ds);
   // real sub-views: same extents, doubled increments
   std::vector<int64_t> ia(va.rank), ib(vb.rank), ic(sp.inc_c_len);
   for (int d = 0; d < va.rank; ++d) ia[d] = 2 * va.inc[d];
@@ -1320,6 +1434,12 @@ int gett_set_pair(int on) {
   return 0;
 }
 
+int gett_set_complex_embed(int on) {
+  if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
+  g_complex_4x = on == 0;
+  return 0;
+}
+
 int gett_set_tma(int on) {
   if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
   g_tma = on != 0;
@@ -1355,6 +1475,6 @@ void gett_release_caches(void) {
   }
 }
 
-int gett_abi_version(void) { return 102; }  // 1.02: gett_set_tma, gett_set_pair
+int gett_abi_version(void) { return 103; }  // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed
 
 }  // extern "C"

@@ -19,6 +19,7 @@
 // (-0.0)*(+0.0) = -0.0, the additive identity, so C + acc reproduces the
 // reference's sequential signed-zero outcomes.
 #include <cstdio>
+#include <type_traits>
 
 #include "device.cuh"
 #include "kernels.hpp"
@@ -820,6 +821,40 @@ template cudaError_t launch_ref_c<double>(const RefParams<double>&, cudaStream_t
 template cudaError_t launch_ref_c<float>(const RefParams<float>&, cudaStream_t);
 template cudaError_t launch_serial_c<double>(const SerialParams<double>&, cudaStream_t);
 template cudaError_t launch_serial_c<float>(const SerialParams<float>&, cudaStream_t);
+
+// Real embedding of a complex operand: one thread per element, the modes
+// walked fastest first so the two pair stores of neighbouring threads are
+// contiguous.
+template <typename R>
+__global__ void __launch_bounds__(256) gett_expand_complex_kernel(const __grid_constant__ ExpandParams<R> p) {
+  using V2 = typename std::conditional<sizeof(R) == 8, double2, float2>::type;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < p.total; i += (int64_t)gridDim.x * blockDim.x) {
+    int64_t rem = i, src = 0, dst = 0;
+    for (int d = 0; d < p.n; ++d) {
+      const int64_t e = p.ext[d], x = rem % e;
+      rem /= e;
+      src += x * p.inc[d];
+      dst += x * p.dst_st[d];
+    }
+    const R re = p.src[2 * src], im = p.src[2 * src + 1];
+    V2 v0, v1;
+    v0.x = re; v0.y = im;
+    v1.x = -im; v1.y = re;
+    *reinterpret_cast<V2*>(p.dst + dst) = v0;
+    *reinterpret_cast<V2*>(p.dst + dst + p.q) = v1;
+  }
+}
+
+template <typename R>
+cudaError_t launch_expand_complex(const ExpandParams<R>& p, cudaStream_t s) {
+  int64_t blocks = (p.total + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  if (blocks < 1) blocks = 1;
+  gett_expand_complex_kernel<R><<<(unsigned)blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+template cudaError_t launch_expand_complex<float>(const ExpandParams<float>&, cudaStream_t);
+template cudaError_t launch_expand_complex<double>(const ExpandParams<double>&, cudaStream_t);
 
 template <typename T>
 cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s) {

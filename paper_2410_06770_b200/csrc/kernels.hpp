@@ -31,6 +31,22 @@ cudaError_t launch_ref_c(const RefParams<R>& p, cudaStream_t s);
 template <typename R>
 cudaError_t launch_serial_c(const SerialParams<R>& p, cudaStream_t s);
 
+// Real embedding of one complex operand (run_complex in capi.cu): for each
+// element b of the strided view, dst[o] = (re b, im b) and dst[o + q] =
+// (-im b, re b), o = sum idx_d * dst_st[d] (modes fastest first).
+constexpr int kExpandMaxModes = 24;
+template <typename R>
+struct ExpandParams {
+  const R* src;  // interleaved (re, im) at the view's base element
+  R* dst;
+  int n;          // modes
+  int64_t total;  // elements of the view
+  int64_t q;      // real offset of the (-im, re) pair
+  int64_t ext[kExpandMaxModes], inc[kExpandMaxModes], dst_st[kExpandMaxModes];  // inc in complex elements
+};
+template <typename R>
+cudaError_t launch_expand_complex(const ExpandParams<R>& p, cudaStream_t s);
+
 // DGETT warp-specialised (producer warp + DMMA consumer warps), dgett_ws.cu
 cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, bool a_kf,
                             bool b_kf, bool a_vec, bool b_vec, cudaStream_t s);

@@ -16,16 +16,17 @@ def pytest_configure(config):
 @pytest.fixture
 def kernel_mode():
     """Set the native kernel family for one test, restoring auto after."""
-    from paper_2410_06770_b200 import (set_kernel, set_pair, set_pipeline, set_split_k, set_stream_k,
-                                       set_tma)
+    from paper_2410_06770_b200 import (set_complex_embed, set_kernel, set_pair, set_pipeline, set_split_k,
+                                       set_stream_k, set_tma)
 
-    def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False):
+    def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True):
         set_kernel(name)
         set_split_k(split)
         set_pipeline(pipeline)
         set_stream_k(stream_k)
         set_tma(tma)
         set_pair(pair)
+        set_complex_embed(complex_embed)
 
     yield use
     set_kernel("auto")
@@ -34,3 +35,4 @@ def kernel_mode():
     set_stream_k(True)
     set_tma(True)
     set_pair(False)
+    set_complex_embed(True)

@@ -178,3 +178,53 @@ def test_random_descriptors_auto_mode_negative_strides(dtype, kernel_mode):
         mask[np.asarray(idx).ravel()] = False
         assert c[mask].tobytes() == c0[mask].tobytes(), case_i
     assert len(kernels) >= 2, kernels
+
+
+@pytest.mark.parametrize("dtype", ["c", "z"])
+def test_random_complex_descriptors_embedded_and_4x(dtype, kernel_mode):
+    """cgett/zgett on the tiled kernels through both complex schemes: the one
+    real GETT on an embedding of the smaller operand (default) and the four
+    real GETTs on re/im sub-views.  Both against a complex128 contraction,
+    bytes outside C's view unchanged."""
+    rng = np.random.default_rng(31 if dtype == "c" else 32)
+    np_t = np.complex64 if dtype == "c" else np.complex128
+    entry = g.cgett if dtype == "c" else g.zgett
+    tol = TOL["s" if dtype == "c" else "d"] * 2
+    letters = "abcdefghijklmnop"
+    names = set()
+    for case_i in range(40):
+        (ext_a, inc_a, span_a, ext_b, inc_b, span_b, conts, cont_a, cont_b, perm, ext_c, inc_c,
+         span_c) = _case(rng)
+        off_a, off_b, off_c = (int(rng.integers(0, 3)) for _ in range(3))
+        draw = lambda n: (rng.uniform(-1, 1, n) + 1j * rng.uniform(-1, 1, n)).astype(np_t)  # noqa: E731
+        a, b, c0 = draw(off_a + span_a + 2), draw(off_b + span_b + 2), draw(off_c + span_c + 2)
+        la = [letters[i] for i in range(len(ext_a))]
+        lb = [None] * len(ext_b)
+        for ia, ib in zip(cont_a, cont_b):
+            lb[ib] = la[ia]
+        nxt = iter(letters[len(ext_a):])
+        lb = [x if x is not None else next(nxt) for x in lb]
+        free_l = [la[d] for d in range(len(ext_a)) if d not in cont_a] + \
+                 [lb[d] for d in range(len(ext_b)) if d not in cont_b]
+        out_l = [None] * len(free_l)
+        for i, l in enumerate(free_l):
+            out_l[perm[i]] = l
+        A = _strided(a, ext_a, inc_a, off_a).astype(np.complex128)
+        B = _strided(b, ext_b, inc_b, off_b).astype(np.complex128)
+        prod = np.einsum("".join(la) + "," + "".join(lb) + "->" + "".join(out_l), A, B, optimize=True)
+        want = _strided(c0, ext_c, inc_c, off_c).astype(np.complex128) + prod
+        K = int(np.prod([ext_a[d] for d in cont_a]))
+        mask = np.ones(len(c0), bool)
+        idx = off_c + sum(np.ix_(*[np.arange(e) * i for e, i in zip(ext_c, inc_c)]))
+        mask[np.asarray(idx).ravel()] = False
+        for embed in (True, False):
+            kernel_mode("tiled", complex_embed=embed)
+            c = c0.copy()
+            assert entry(len(ext_a), tuple(ext_a), inc_a, a, len(ext_b), tuple(ext_b), inc_b, b, conts, cont_a,
+                         cont_b, perm, inc_c, c, offset_a=off_a, offset_b=off_b, offset_c=off_c) == []
+            names.add(g.last_kernel())
+            got = _strided(c, ext_c, inc_c, off_c).astype(np.complex128)
+            err = np.max(np.abs(got - want)) / (K * np.abs(a).max() * np.abs(b).max())
+            assert err <= tol, (case_i, embed, g.last_kernel(), err)
+            assert c[mask].tobytes() == c0[mask].tobytes(), (case_i, embed)
+    assert any("embedded" in n for n in names) and any("4x" in n for n in names), names
