@@ -53,6 +53,9 @@
 namespace gett {
 namespace tc {
 
+// accumulator bits, or -0.0 (the additive identity) when the CTA had no k-blocks
+__device__ __forceinline__ uint32_t r_or_zero(uint32_t r, int nkb) { return nkb > 0 ? r : 0x80000000u; }
+
 // Optional per-role cycle accounting (tuning builds only: make variant
 // EXTRA=-DGETT_TC_TRACE); blocks 0 and gridDim.x-1 printf their totals.
 #ifdef GETT_TC_TRACE
@@ -88,6 +91,9 @@ constexpr int LO_BUFS = GETT_TC_LO;
 constexpr int TCAP = 256;                      // outer k-table entries staged in smem
 constexpr int BAR_BYTES = 512;
 constexpr int LO_OFF = STAGES * STAGE_BYTES;   // lo ring
+constexpr int EPI_PITCH = 65;                  // epilogue staging (floats per row)
+constexpr int EPI_ROWS = 8;                    // rows in flight per warp in the epilogue
+static_assert(2 * BM * EPI_PITCH * 4 <= STAGES * STAGE_BYTES, "epilogue staging fits the stage ring");
 constexpr int BAR_OFF = LO_OFF + LO_BUFS * TILE_BYTES;
 constexpr int SMEM_BYTES = BAR_OFF + BAR_BYTES + 2 * TCAP * 8;
 constexpr uint32_t ACC_COLS = BN;              // fp32 accumulator columns
@@ -687,7 +693,6 @@ __global__ void __launch_bounds__(THREADS, 1)
     const int cbeg = 64 * ((warp - 4) >> 2);
     const int m = m0 + lane_row;
     const bool mok = m < p.M;
-    const int64_t ro = (mok && p.splits == 1) ? p.gm.off(1, m) : 0;
     // split-K partials, transposed [split][N][M]: a warp's 32 rows are 32
     // consecutive floats per column (coalesced); the reduce reads it m-fastest
     float* wcol = p.splits > 1 ? p.ws + (int64_t)split * p.M * p.N + (mok ? m : 0) : nullptr;
@@ -706,26 +711,55 @@ __global__ void __launch_bounds__(THREADS, 1)
           : "r"(taddr));
     }
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if (p.splits == 1) {
+      // C += acc through shared memory: the planner puts C's smallest stride in
+      // N, so a thread-per-row store would touch 32 lines per warp instruction.
+      // Each warpgroup stages its 128 x 64 block (pitch 65: conflict-free both
+      // ways) in the idle stage ring; then lane l of a warp owns columns l and
+      // 32 + l of every 4th row, so each warp load / store covers 32
+      // consecutive n.
+      float* tb = reinterpret_cast<float*>(smem) + h * (BM * EPI_PITCH);
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const int c0 = cbeg + 16 * q;
-      const uint32_t* r = rr + 16 * q;
-      if (!mok) continue;
-      if (p.splits == 1) {
-        float cv[16];
-        int64_t co[16];
-        const int nvalid = p.N - (n0 + c0);  // offsets may be negative: validity by index
+      for (int i = 0; i < 64; ++i) tb[lane_row * EPI_PITCH + i] = __uint_as_float(r_or_zero(rr[i], nkb));
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(WG) : "memory");
+      int64_t con[2];
+      bool nok[2];
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          co[i] = i < nvalid ? ro + p.gn.off(1, n0 + c0 + i) : 0;
-          cv[i] = i < nvalid ? p.C[co[i]] : 0.f;
+      for (int j = 0; j < 2; ++j) {
+        const int n = n0 + cbeg + 32 * j + lane;
+        nok[j] = n < p.N;
+        con[j] = nok[j] ? p.gn.off(1, n) : 0;
+      }
+      for (int r0 = wq; r0 < BM; r0 += 4 * EPI_ROWS) {
+        float cv[EPI_ROWS][2];
+        int64_t co[EPI_ROWS][2];
+#pragma unroll
+        for (int t = 0; t < EPI_ROWS; ++t) {
+          const int r = r0 + 4 * t, mm = m0 + r;
+          const bool rok = mm < p.M;
+          const int64_t rof = rok ? p.gm.off(1, mm) : 0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            co[t][j] = rof + con[j];
+            cv[t][j] = (rok && nok[j]) ? p.C[co[t][j]] : 0.f;
+          }
         }
 #pragma unroll
-        for (int i = 0; i < 16; ++i) {
-          const float acc = nkb > 0 ? __uint_as_float(r[i]) : -0.0f;
-          if (i < nvalid) p.C[co[i]] = epi(cv[i], acc, p.neg);
+        for (int t = 0; t < EPI_ROWS; ++t) {
+          const int r = r0 + 4 * t;
+          if (m0 + r >= p.M) continue;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (nok[j]) p.C[co[t][j]] = epi(cv[t][j], tb[r * EPI_PITCH + 32 * j + lane], p.neg);
         }
-      } else {
+      }
+    } else {
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int c0 = cbeg + 16 * q;
+        const uint32_t* r = rr + 16 * q;
+        if (!mok) continue;
+        // split-K partials, m-fastest: a warp's 32 rows are 32 consecutive floats
 #pragma unroll
         for (int i = 0; i < 16; ++i) {
           const int n = n0 + c0 + i;
