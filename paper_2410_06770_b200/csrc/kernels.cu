@@ -33,6 +33,9 @@ constexpr int PAD = 4;
 #ifndef GETT_PDL
 #define GETT_PDL 0  // programmatic dependent launch of the reduce: measured slower on c5 (0.0545 vs 0.0498 ms)
 #endif
+#ifndef GETT_REDUCE_T
+#define GETT_REDUCE_T 1  // transposed-partials reduce through a shared-memory tile (0: element per thread)
+#endif
 #ifndef GETT_GROUP_M
 #define GETT_GROUP_M 8
 #endif
@@ -706,6 +709,41 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
   *c = epi(c0, s, p.neg);
 }
 
+// The same sum for transposed partials [splits][N][M] (the SGETT tcgen05
+// kernel's layout) when C's smallest stride is in N (the planner's choice):
+// a 32 m x 8 n tile per block, partials read m-fastest, staged through shared
+// memory, C read and written n-fastest (8 consecutive n: one 32 B sector per
+// row for fp32 instead of one per element).  Same order, same bits.
+template <typename T>
+__global__ void __launch_bounds__(256) gett_splitk_reduce_t_kernel(const __grid_constant__ TiledParams<T> p) {
+  __shared__ T tile[8][33];
+  const int t = threadIdx.x;
+  const int n0 = blockIdx.x * 8, m0 = blockIdx.y * 32;
+  const int64_t mn = (int64_t)p.M * p.N;
+  const int mw = m0 + t / 8, nw = n0 + t % 8;
+  const bool okw = mw < p.M && nw < p.N;
+  T* c = okw ? p.C + p.gm.off(1, mw) + p.gn.off(1, nw) : nullptr;
+  const T c0 = okw ? *c : T(0);
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int mr = m0 + t % 32, nr = n0 + t / 32;
+  if (mr < p.M && nr < p.N) {
+    const int64_t idx = (int64_t)nr * p.M + mr;
+    T s = T(-0.0);
+    int sp = 0;
+    for (; sp + 8 <= p.splits; sp += 8) {
+      T v[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) v[j] = __ldcg(p.ws + (sp + j) * mn + idx);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) s = s + v[j];
+    }
+    for (; sp < p.splits; ++sp) s = s + __ldcg(p.ws + sp * mn + idx);
+    tile[t / 32][t % 32] = s;
+  }
+  __syncthreads();
+  if (okw) *c = epi(c0, tile[t % 8][t / 8], p.neg);
+}
+
 template <typename T>
 __global__ void __launch_bounds__(256) gett_zero_kernel(T* base, const __grid_constant__ GroupDev g) {
   int64_t stride = (int64_t)gridDim.x * blockDim.x;
@@ -768,6 +806,11 @@ cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s) {
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = GETT_PDL ? 1 : 0;
+  const int64_t mt = (p.M + 31) / 32;
+  if (GETT_REDUCE_T && p.ws_t && mt <= 65535) {
+    cfg.gridDim = dim3((unsigned)((p.N + 7) / 8), (unsigned)mt);
+    return cudaLaunchKernelEx(&cfg, gett_splitk_reduce_t_kernel<T>, p);
+  }
   return cudaLaunchKernelEx(&cfg, gett_splitk_reduce_kernel<T>, p);
 }
 
