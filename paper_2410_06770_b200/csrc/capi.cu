@@ -35,6 +35,7 @@ int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
 bool g_stream_k = true;  // DGETT: persistent stream-K schedule when tiles > 1 wave and not whole waves (GETT_STREAM_K=0: off)
 bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=0: cp.async gathers)
+bool g_sk_small = true;    // DGETT: stream-K instead of split-K at 56-73 tiles (GETT_SK_SMALL=0: off)
 bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one embedded GETT (GETT_COMPLEX_EMBED=0)
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
@@ -54,6 +55,8 @@ void read_env() {
   if (wsv) g_dgett_ws = std::atoi(wsv) != 0;
   const char* skv = std::getenv("GETT_STREAM_K");
   if (skv) g_stream_k = std::atoi(skv) != 0;
+  const char* sks = std::getenv("GETT_SK_SMALL");
+  if (sks) g_sk_small = std::atoi(sks) != 0;
   const char* ce = std::getenv("GETT_COMPLEX_EMBED");
   if (ce) g_complex_4x = std::atoi(ce) == 0;
   const char* pv = std::getenv("GETT_PAIR");
@@ -670,8 +673,20 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   int64_t tiles = (int64_t)tp.tiles_m * tp.tiles_n;
   int64_t kblocks = (K + BK - 1) / BK;
   int64_t splits = 1;
+  // DGETT at 56-73 tiles: split-K would fill only 112-146 of the SMs with two
+  // slices; stream-K shares (at most ~2.6 per tile) use all of them and skip
+  // the reduce: 256 x 4096 x 4096 and 512 x 2048 x 4096 10 % faster.  Fewer
+  // tiles cut each tile into more shares and lost (768 x 768 x 2048: -11 %).
+  // (not under graph capture, where stream-K is off)
+  bool sk_small = false;
+  if (sizeof(T) == 8 && g_dgett_ws && g_stream_k && g_sk_small && g_split <= 0 && tiles >= 56 &&
+      tiles < 74 && kblocks >= 16) {
+    cudaStreamCaptureStatus cap0 = cudaStreamCaptureStatusNone;
+    CK(cudaStreamIsCapturing(stream, &cap0));
+    sk_small = cap0 == cudaStreamCaptureStatusNone;
+  }
   if (g_split > 0) splits = g_split;
-  else if (tiles < 148 && kblocks >= 8) {
+  else if (tiles < 148 && kblocks >= 8 && !sk_small) {
     splits = 148 / tiles;  // one wave of CTAs (1 CTA per SM for both tiled kernels)
     if (splits > kblocks / 2) splits = kblocks / 2;  // >= 2 k-blocks per slice
     if (splits < 1) splits = 1;
@@ -739,7 +754,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(stream, &cap));
     if (g_stream_k && cap == cudaStreamCaptureStatusNone && splits == 1 && tiles % G != 0 &&
-        2 * tiles > G) {
+        (2 * tiles > G || sk_small)) {
       // persistent: the last 1-2 waves of tiles (all of them below 2 waves)
       // are shared out by k-block units, the rest run data-parallel; below one
       // wave (G/2 < tiles < G, where split-K cannot help) the shares are

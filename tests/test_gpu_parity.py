@@ -545,15 +545,16 @@ def test_stream_k_deterministic_and_accurate(name, kernel_mode):
         assert k_norm_err(got, ref, w.size_k, np.abs(a).max(), np.abs(b).max()) <= TOL_K["d"], sk
 
 
-@pytest.mark.parametrize("rows", [384, 512, 640, 1152])
+@pytest.mark.parametrize("rows", [256, 384, 512, 640, 1152])
 def test_stream_k_below_two_waves(rows, kernel_mode):
     """Tiles below two waves run stream-K over all tiles — between one and two
     waves (640 x 4096 -> 160 tiles, 1152 x 4096 -> 288 tiles on 148 SMs) and
     below one wave (384 -> 96, 512 -> 128 tiles: shares shorter than a tile,
-    heads adding several parts): deterministic, within the fp64 K-normalised
-    bar of an fp64 contraction, and C's padding intact."""
+    heads adding several parts; 256 -> 64 tiles with K 512, where stream-K
+    replaces split-K): deterministic, within the fp64 K-normalised bar of an
+    fp64 contraction, and C's padding intact."""
     rng = np.random.default_rng(rows)
-    M, N, K = rows, 4096, 256
+    M, N, K = rows, 4096, (512 if rows == 256 else 256)
     a = rng.uniform(-1, 1, M * (K + 8)).astype(np.float64)
     b = rng.uniform(-1, 1, K * (N + 4)).astype(np.float64)
     c0 = rng.uniform(-1, 1, M * (N + 2)).astype(np.float64)
@@ -564,7 +565,8 @@ def test_stream_k_below_two_waves(rows, kernel_mode):
         kernel_mode("tiled", pipeline=0, stream_k=sk)
         cc = c0.copy()
         assert g.dgett(*args(cc)) == []
-        assert g.last_kernel() == ("dgett_dmma_ws_sk" if sk else "dgett_dmma_ws")
+        assert g.last_kernel() == ("dgett_dmma_ws_sk" if sk else
+                                   "dgett_dmma_ws_splitk" if rows == 256 else "dgett_dmma_ws")
         outs.append(cc)
     assert outs[0].tobytes() == outs[1].tobytes(), "run-to-run difference"
     A = oracle.strided(a, (M, K), (K + 8, 1), 0).astype(np.float64)
