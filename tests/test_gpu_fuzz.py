@@ -228,3 +228,52 @@ def test_random_complex_descriptors_embedded_and_4x(dtype, kernel_mode):
             assert err <= tol, (case_i, embed, g.last_kernel(), err)
             assert c[mask].tobytes() == c0[mask].tobytes(), (case_i, embed)
     assert any("embedded" in n for n in names) and any("4x" in n for n in names), names
+
+
+@pytest.mark.parametrize("embed", [True, False])
+def test_complex_edge_shapes(embed, kernel_mode):
+    """The complex schemes on edge shapes: a stride-0 (broadcast) mode in the
+    expanded operand, the smaller operand on either side, a matrix-vector
+    contraction (C rank 1), a scalar output (C rank 0) and a K of one."""
+    kernel_mode("tiled", complex_embed=embed)
+    rng = np.random.default_rng(77)
+    draw = lambda n, dt: (rng.integers(-3, 4, n) + 1j * rng.integers(-3, 4, n)).astype(dt)  # noqa: E731
+    for dt, entry in ((np.complex64, g.cgett), (np.complex128, g.zgett)):
+        # A (40 x 300) smaller than B (300 x 500), whose column mode has stride 0
+        a = draw(40 * 300, dt)
+        b = draw(300, dt)
+        c = draw(40 * 500, dt)
+        want = c.astype(np.complex128).reshape(40, 500) + \
+            (a.astype(np.complex128).reshape(40, 300) @ np.repeat(b.astype(np.complex128)[:, None], 500, 1))
+        assert entry(2, (40, 300), (300, 1), a, 2, (300, 500), (1, 0), b, 1, (1,), (0,), (0, 1), (500, 1), c) == []
+        assert np.array_equal(c.reshape(40, 500), want.astype(dt)), (dt, g.last_kernel())
+        # B smaller than A: (600 x 64) x (64 x 8)
+        a = draw(600 * 64, dt)
+        b = draw(64 * 8, dt)
+        c = draw(600 * 8, dt)
+        want = c.astype(np.complex128).reshape(600, 8) + a.astype(np.complex128).reshape(600, 64) @ \
+            b.astype(np.complex128).reshape(64, 8)
+        assert entry(2, (600, 64), (64, 1), a, 2, (64, 8), (8, 1), b, 1, (1,), (0,), (0, 1), (8, 1), c) == []
+        assert np.array_equal(c.reshape(600, 8), want.astype(dt)), (dt, g.last_kernel())
+        # matrix-vector: C rank 1
+        a = draw(700 * 90, dt)
+        b = draw(90, dt)
+        c = draw(700, dt)
+        want = c.astype(np.complex128) + a.astype(np.complex128).reshape(700, 90) @ b.astype(np.complex128)
+        assert entry(2, (700, 90), (90, 1), a, 1, (90,), (1,), b, 1, (1,), (0,), (0,), (1,), c) == []
+        assert np.array_equal(c, want.astype(dt)), (dt, g.last_kernel())
+        # scalar output: full contraction of two 30 x 40 tensors
+        a = draw(1200, dt)
+        b = draw(1200, dt)
+        c = draw(1, dt)
+        want = c.astype(np.complex128) + np.sum(a.astype(np.complex128).reshape(30, 40) *
+                                                b.astype(np.complex128).reshape(40, 30).T)
+        assert entry(2, (30, 40), (40, 1), a, 2, (40, 30), (30, 1), b, 2, (0, 1), (1, 0), (), (), c) == []
+        assert np.array_equal(c, want.astype(dt)), (dt, g.last_kernel())
+        # K of one (outer product)
+        a = draw(200, dt)
+        b = draw(300, dt)
+        c = draw(200 * 300, dt)
+        want = c.astype(np.complex128).reshape(200, 300) + np.outer(a, b).astype(np.complex128)
+        assert entry(2, (200, 1), (1, 1), a, 2, (1, 300), (300, 1), b, 1, (1,), (0,), (0, 1), (300, 1), c) == []
+        assert np.array_equal(c.reshape(200, 300), want.astype(dt)), (dt, g.last_kernel())
