@@ -42,6 +42,7 @@ int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELIN
 bool g_env_read = false;
 thread_local std::string t_last_error;
 thread_local const char* t_last_kernel = "none";
+thread_local bool t_capturing = false;  // the current device call is being captured
 int64_t g_launches = 0;
 
 void read_env() {
@@ -108,6 +109,9 @@ struct DevPlan {
   TmaParams pair_p{};
   const void* pair_base[2] = {nullptr, nullptr};
   GroupDev pgk{};      // dp.gk with its two tensors exchanged
+  // used by a call captured into a CUDA graph: the graph holds raw pointers
+  // into d_tab, so the LRU never evicts it (gett_release_caches still does)
+  bool pinned = false;
   ~DevPlan() {
     if (d_tab) {
       int cur = -1;
@@ -125,6 +129,19 @@ struct PlanCache {
   static constexpr size_t kCap = 512;
 };
 PlanCache g_plans;
+
+// drop least-recently-used plans beyond the cap, skipping plans pinned by a
+// captured CUDA graph
+void evict_plans() {
+  auto it = g_plans.lru.end();
+  while (g_plans.map.size() > PlanCache::kCap && it != g_plans.lru.begin()) {
+    --it;
+    auto m = g_plans.map.find(*it);
+    if (m->second.first->pinned) continue;
+    g_plans.map.erase(m);
+    it = g_plans.lru.erase(it);
+  }
+}
 
 // the last validated descriptor and its plan (gett_impl; under g_mu)
 struct LastCall {
@@ -239,9 +256,11 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
   if (it != g_plans.map.end()) {
     g_plans.lru.splice(g_plans.lru.begin(), g_plans.lru, it->second.second);
     *out = it->second.first;
+    if (t_capturing) (*out)->pinned = true;
     return 0;
   }
   auto dp = std::make_shared<DevPlan>();
+  dp->pinned = t_capturing;
   dp->plan = build_plan(a, b, s, off_c, len_c);
   dp->device = dev;
   const Plan& p = dp->plan;
@@ -276,11 +295,7 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
   dp->bk_even2 = all_div(p.gk.T[1], 2); dp->bk_even4 = all_div(p.gk.T[1], 4);
   g_plans.lru.push_front(key);
   g_plans.map[key] = {dp, g_plans.lru.begin()};
-  if (g_plans.map.size() > PlanCache::kCap) {
-    std::string last = g_plans.lru.back();
-    g_plans.lru.pop_back();
-    g_plans.map.erase(last);
-  }
+  evict_plans();
   *out = dp;
   return 0;
 }
@@ -311,6 +326,7 @@ int get_view_plan(int rank, const int64_t* ext, const int64_t* inc, std::shared_
   dp->gm = to_dev(dp->plan.gm, dp->d_tab, dp->d_tab);
   g_plans.lru.push_front(key);
   g_plans.map[key] = {dp, g_plans.lru.begin()};
+  evict_plans();
   *out = dp;
   return 0;
 }
@@ -592,6 +608,19 @@ int try_sgett_pair(DevPlan& dp, const float* A, const float* B, float* C, int ne
   return 1;
 }
 
+// Self-overlapping C views run the literal reference loop on ONE GPU thread
+// (their result depends on the reference's store order).  Legal but slow:
+// warn once when a call is large enough to take seconds (> 2^26 MACs).
+void warn_serial(int64_t size_free, int64_t size_cont) {
+  static bool warned = false;
+  if (warned || (double)size_free * (double)size_cont <= (double)(1LL << 26)) return;
+  warned = true;
+  std::fprintf(stderr,
+               "gett: the C view overlaps itself (distinct coordinates share elements); its %lld x %lld "
+               "MACs run in the reference's order on one GPU thread\n",
+               (long long)size_free, (long long)size_cont);
+}
+
 template <typename T>
 int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, DevState& ds,
                int neg = 0, bool force_tiled = false) {
@@ -619,6 +648,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     sp.size_free = p.size_free;
     sp.size_cont = p.size_cont;
     sp.tab = dp.serial_tab;
+    warn_serial(p.size_free, p.size_cont);
     CK(launch_serial<T>(sp, stream));
     t_last_kernel = sizeof(T) == 8 ? "dgett_serial" : "sgett_serial";
     ++g_launches;
@@ -678,15 +708,18 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   // the reduce: 256 x 4096 x 4096 and 512 x 2048 x 4096 10 % faster.  Fewer
   // tiles cut each tile into more shares and lost (768 x 768 x 2048: -11 %).
   // (not under graph capture, where stream-K is off)
+  // Under capture the shape takes one CTA per tile (no split-K either), so a
+  // captured call needs no workspace its eager twin did not allocate.
+  const bool sk_small_shape = sizeof(T) == 8 && g_dgett_ws && g_stream_k && g_sk_small &&
+                              g_split <= 0 && tiles >= 56 && tiles < 74 && kblocks >= 16;
   bool sk_small = false;
-  if (sizeof(T) == 8 && g_dgett_ws && g_stream_k && g_sk_small && g_split <= 0 && tiles >= 56 &&
-      tiles < 74 && kblocks >= 16) {
+  if (sk_small_shape) {
     cudaStreamCaptureStatus cap0 = cudaStreamCaptureStatusNone;
     CK(cudaStreamIsCapturing(stream, &cap0));
     sk_small = cap0 == cudaStreamCaptureStatusNone;
   }
   if (g_split > 0) splits = g_split;
-  else if (tiles < 148 && kblocks >= 8 && !sk_small) {
+  else if (tiles < 148 && kblocks >= 8 && !sk_small_shape) {
     splits = 148 / tiles;  // one wave of CTAs (1 CTA per SM for both tiled kernels)
     if (splits > kblocks / 2) splits = kblocks / 2;  // >= 2 k-blocks per slice
     if (splits < 1) splits = 1;
@@ -917,14 +950,25 @@ int fill_errors(const std::vector<Error>& errs, int32_t* codes, int64_t* info, i
   return n;
 }
 
-DevState& dev_state(int* dev_out) {
+int dev_state(int* dev_out, DevState** out) {
   int dev = 0;
-  cudaGetDevice(&dev);
+  CK(cudaGetDevice(&dev));
   *dev_out = dev;
   DevState& ds = g_dev[dev];
-  if (!ds.stream) cudaStreamCreateWithFlags(&ds.stream, cudaStreamNonBlocking);
-  return ds;
+  if (!ds.stream) CK(cudaStreamCreateWithFlags(&ds.stream, cudaStreamNonBlocking));
+  *out = &ds;
+  return 0;
 }
+
+// marks the calling thread's device call as captured (plans it touches are
+// pinned) for the duration of one entry point
+struct CaptureScope {
+  explicit CaptureScope(cudaStream_t s) {
+    cudaStreamCaptureStatus st = cudaStreamCaptureStatusNone;
+    t_capturing = cudaStreamIsCapturing(s, &st) == cudaSuccess && st != cudaStreamCaptureStatusNone;
+  }
+  ~CaptureScope() { t_capturing = false; }
+};
 
 template <typename T>
 int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a, const T* a,
@@ -979,8 +1023,12 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   int rc = 0;
   const Plan& p = dp->plan;
   int dev;
-  DevState& ds = dev_state(&dev);
+  DevState* dsp = nullptr;
+  if ((rc = dev_state(&dev, &dsp))) return rc;
+  DevState& ds = *dsp;
   if (!host) {
+    CaptureScope cs(stream);
+    if (t_capturing) dp->pinned = true;
     return run_device<T>(*dp, a + off_a, b + off_b, c + off_c, stream, ds);
   }
   rc = host_pipelined<T>(*dp, va, vb, sp, a, b, c, off_c, len_c, ds);
@@ -1138,6 +1186,7 @@ int run_complex(DevPlan& cp, const View& va, const View& vb, const Spec& sp, con
     s.size_free = p.size_free;
     s.size_cont = p.size_cont;
     s.tab = cp.serial_tab;
+    warn_serial(p.size_free, p.size_cont);
     CK(launch_serial_c<R>(s, stream));
     ++g_launches;
     t_last_kernel = z ? "zgett_serial" : "cgett_serial";
@@ -1216,8 +1265,14 @@ int gett_impl_complex(bool host, int rank_a, const int64_t* ext_a, const int64_t
   if (rc) return rc;
   const Plan& p = cp->plan;
   int dev;
-  DevState& ds = dev_state(&dev);
-  if (!host) return run_complex<R>(*cp, va, vb, sp, a + 2 * off_a, b + 2 * off_b, c + 2 * off_c, stream, ds);
+  DevState* dsp = nullptr;
+  if ((rc = dev_state(&dev, &dsp))) return rc;
+  DevState& ds = *dsp;
+  if (!host) {
+    CaptureScope cs(stream);
+    if (t_capturing) cp->pinned = true;
+    return run_complex<R>(*cp, va, vb, sp, a + 2 * off_a, b + 2 * off_b, c + 2 * off_c, stream, ds);
+  }
   const int64_t lo_a = off_a + p.fp_lo[0], lo_b = off_b + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
   const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1) * 2;
   const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1) * 2;
@@ -1261,7 +1316,9 @@ int zero_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64
   int rc = get_view_plan(rank, ext, inc, &dp);
   if (rc) return rc;
   int dev;
-  DevState& ds = dev_state(&dev);
+  DevState* dsp = nullptr;
+  if ((rc = dev_state(&dev, &dsp))) return rc;
+  DevState& ds = *dsp;
   if (!host) {
     CK(launch_zero<T>(buf + off, dp->gm, stream));
     ++g_launches;

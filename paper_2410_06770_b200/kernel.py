@@ -53,9 +53,14 @@ def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_
     cw = c if c.flags.c_contiguous else np.ascontiguousarray(c)
     empty = a_view.is_empty or b_view.is_empty
     if not c.flags.writeable and not empty:
-        # the reference fails at its first store into c; fail before any work
-        from .plan import validate
+        # the reference fails at its first store into c, after both validation
+        # phases (kernel.py:146-153): return their errors, else fail before any work
+        from .plan import derive_output_extents, validate
         errs = validate(a_view, b_view, spec, inc_c)
+        if not errs:
+            ext_c = derive_output_extents(a_view, b_view, spec)
+            c_view = TensorView(len(ext_c), ext_c, tuple(inc_c), int(offset_c), c.shape[0])
+            errs = validate(a_view, b_view, spec, inc_c, c_view=c_view)
         if errs:
             return errs
         raise ValueError("assignment destination is read-only")

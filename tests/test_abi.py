@@ -174,3 +174,20 @@ def test_c_caller_contracts_on_the_gpu(tmp_path):
     r = subprocess.run([exe, "run"], capture_output=True, text=True)
     assert r.returncode == 0, r.stdout + r.stderr
     assert '"bitwise_equal": 1' in r.stdout
+
+
+def test_readonly_c_returns_phase_two_errors():
+    """A read-only C whose only problem is its footprint: the reference runs
+    output_view_errors before its first store (kernel.py:149-153) and returns
+    [FootprintOutOfBounds C]; a clean read-only call raises ValueError."""
+    a = np.ones(6)
+    b = np.ones(12)
+    c = np.zeros(7)  # C [2,4] contiguous needs 8 elements
+    c.flags.writeable = False
+    errs = g.dgett(2, (2, 3), (3, 1), a, 2, (3, 4), (4, 1), b, 1, (1,), (0,), (0, 1), (4, 1), c)
+    assert [e.code for e in errs] == [g.ErrorCode.FootprintOutOfBounds]
+    assert "C" in errs[0].message
+    c = np.zeros(8)
+    c.flags.writeable = False
+    with pytest.raises(ValueError):
+        g.dgett(2, (2, 3), (3, 1), a, 2, (3, 4), (4, 1), b, 1, (1,), (0,), (0, 1), (4, 1), c)

@@ -239,14 +239,16 @@ def test_complex_edge_shapes(embed, kernel_mode):
     rng = np.random.default_rng(77)
     draw = lambda n, dt: (rng.integers(-3, 4, n) + 1j * rng.integers(-3, 4, n)).astype(dt)  # noqa: E731
     for dt, entry in ((np.complex64, g.cgett), (np.complex128, g.zgett)):
-        # A (40 x 300) smaller than B (300 x 500), whose column mode has stride 0
-        a = draw(40 * 300, dt)
+        # B (300 x 20, its column mode of stride 0) smaller than A (600 x 300):
+        # the broadcast operand is the one the embedded scheme expands
+        a = draw(600 * 300, dt)
         b = draw(300, dt)
-        c = draw(40 * 500, dt)
-        want = c.astype(np.complex128).reshape(40, 500) + \
-            (a.astype(np.complex128).reshape(40, 300) @ np.repeat(b.astype(np.complex128)[:, None], 500, 1))
-        assert entry(2, (40, 300), (300, 1), a, 2, (300, 500), (1, 0), b, 1, (1,), (0,), (0, 1), (500, 1), c) == []
-        assert np.array_equal(c.reshape(40, 500), want.astype(dt)), (dt, g.last_kernel())
+        c = draw(600 * 20, dt)
+        want = c.astype(np.complex128).reshape(600, 20) + \
+            (a.astype(np.complex128).reshape(600, 300) @ np.repeat(b.astype(np.complex128)[:, None], 20, 1))
+        assert entry(2, (600, 300), (300, 1), a, 2, (300, 20), (1, 0), b, 1, (1,), (0,), (0, 1), (20, 1), c) == []
+        assert np.array_equal(c.reshape(600, 20), want.astype(dt)), (dt, g.last_kernel())
+        assert ("embedded" in g.last_kernel()) == embed, g.last_kernel()
         # B smaller than A: (600 x 64) x (64 x 8)
         a = draw(600 * 64, dt)
         b = draw(64 * 8, dt)

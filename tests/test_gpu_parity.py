@@ -724,3 +724,43 @@ def test_graph_replay_equals_direct_calls(name, kernel_mode):
         torch.cuda.synchronize()
         outs.append(tc.cpu().numpy())
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+@pytest.mark.gpu
+def test_graph_capture_sub_wave_stream_k_shape(kernel_mode):
+    """A DGETT of 64 output tiles (1024 x 1024, K 4096): the eager call runs the
+    sub-wave stream-K schedule; the captured one must still need no new
+    workspace and give exactly the direct calls' result on integer
+    data.  Then >512 other descriptors churn the plan LRU: the captured plan is
+    pinned, so the replay still reads valid offset tables."""
+    import torch
+
+    from paper_2410_06770_b200.device import dgett_device
+    from paper_2410_06770_b200.graph import GettGraph
+
+    kernel_mode("auto", stream_k=True)
+    rng = np.random.default_rng(5)
+    M = N = 1024
+    K = 4096
+    a = rng.integers(-3, 4, M * K).astype(np.float64)
+    b = rng.integers(-3, 4, K * N).astype(np.float64)
+    c = rng.integers(-3, 4, M * N).astype(np.float64)
+    args = (2, (M, K), (K, 1), None, 2, (K, N), (N, 1), None, 1, (1,), (0,), (0, 1), (N, 1), None)
+
+    def call_args(ta, tb, tc):
+        x = list(args)
+        x[3], x[7], x[13] = ta, tb, tc
+        return x
+
+    ta, tb, tc = (torch.from_numpy(x).cuda() for x in (a, b, c))
+    gg = GettGraph(dgett_device, *call_args(ta, tb, tc))
+    # churn: 600 distinct small descriptors
+    sa = torch.ones(600, dtype=torch.float64, device="cuda")
+    sc = torch.zeros(1, dtype=torch.float64, device="cuda")
+    for e in range(1, 601):
+        assert dgett_device(1, (e,), (1,), sa, 1, (e,), (1,), sa, 1, (0,), (0,), (), (), sc) == []
+    gg.replay()
+    gg.replay()
+    torch.cuda.synchronize()
+    want = c + 3 * (a.reshape(M, K) @ b.reshape(K, N)).ravel()
+    assert tc.cpu().numpy().tobytes() == want.tobytes()
