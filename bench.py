@@ -37,7 +37,12 @@ import time
 import numpy as np
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
-REF_SRC = os.path.join(ROOT, "baseline", "_ref", "pkg", "src")
+# the pip --target install puts the package at baseline/_ref/gett; a copied
+# source tree has it at baseline/_ref/pkg/src/gett
+REF_SRC = next((d for d in (os.path.join(ROOT, "baseline", "_ref"),
+                            os.path.join(ROOT, "baseline", "_ref", "pkg", "src"))
+                if os.path.isdir(os.path.join(d, "gett"))),
+               os.path.join(ROOT, "baseline", "_ref"))
 LIB_PATH = os.path.join(ROOT, "paper_2410_06770_b200", "libgett_b200.so")
 
 
