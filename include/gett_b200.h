@@ -121,6 +121,60 @@ int gett_sgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, co
                       int64_t len_c, void* stream,
                       int32_t* err_codes, int64_t* err_info, int max_errs);
 
+/* ---- xGETT over several devices, host buffers (synchronous) ----
+ * One call drives the listed CUDA devices (the reference's
+ * concurrency rule: calls writing disjoint C
+ * footprints may run concurrently):
+ *   - slabs:   C's outermost free mode (largest |INCC|, disjoint spans) is
+ *              split into one row range per device; each device copies its
+ *              slabs of the owner operand and of C over its own PCIe link and
+ *              computes them; the other operand crosses PCIe once in total
+ *              (device j uploads chunk j, the devices exchange chunks over
+ *              NVLink).  No collective.  Each slab is the same xGETT a
+ *              one-device call on that sub-view computes (a free-mode slice).
+ *   - split-K: when the free extents cannot fill the devices (e.g. c5), the
+ *              contracted pair with the largest extent is split; device 0
+ *              computes C += A_0·B_0, device j > 0 computes P_j = A_j·B_j,
+ *              and device 0 adds C += (P_1 + ... + P_{n-1}) in that order,
+ *              loading the partials from the peers over NVLink.
+ *   - small calls (< 2^27 MACs per device) and self-overlapping C views run
+ *     on devices[0] alone.
+ * A device may be listed more than once (each occurrence is a separate lane
+ * with its own streams and staging), so devices = {0, 0} runs the whole
+ * multi-device path on one GPU.  Validation, errors and return values are
+ * those of gett_dgett / gett_sgett.  Replaces: kernel.py:158-184 (the same
+ * call; the reference is single-threaded on one CPU core). */
+int gett_dgett_multi(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+                     int64_t offset_a, int64_t len_a,
+                     int rank_b, const int64_t* ext_b, const int64_t* inc_b, const double* b,
+                     int64_t offset_b, int64_t len_b,
+                     int conts, const int64_t* cont_a, const int64_t* cont_b,
+                     int perm_len, const int64_t* perm,
+                     int inc_c_len, const int64_t* inc_c, double* c, int64_t offset_c,
+                     int64_t len_c, int n_dev, const int32_t* devices,
+                     int32_t* err_codes, int64_t* err_info, int max_errs);
+int gett_sgett_multi(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+                     int64_t offset_a, int64_t len_a,
+                     int rank_b, const int64_t* ext_b, const int64_t* inc_b, const float* b,
+                     int64_t offset_b, int64_t len_b,
+                     int conts, const int64_t* cont_a, const int64_t* cont_b,
+                     int perm_len, const int64_t* perm,
+                     int inc_c_len, const int64_t* inc_c, float* c, int64_t offset_c,
+                     int64_t len_c, int n_dev, const int32_t* devices,
+                     int32_t* err_codes, int64_t* err_info, int max_errs);
+/* Default device list of gett_dgett / gett_sgett (the unchanged drop-in
+ * signature then runs multi-device); n_dev = 0 restores the current device.
+ * Returns 0 or GETT_E_INVALID_ARG (ordinal out of range). */
+int gett_set_devices(int n_dev, const int32_t* devices);
+/* Multi-device strategy: 0 = automatic (default), 1 = always slabs,
+ * 2 = always split-K (when the call allows it; for tests); + 4 = the split-K
+ * reduce stages the partials with cudaMemcpyPeerAsync instead of loading them
+ * over NVLink (also GETT_MULTI_STAGE=1). */
+int gett_set_multi(int strategy);
+/* Description of the last host call's multi-device schedule ("none" when it
+ * ran on one device), e.g. "slabs x2 (...)", "split-K x2 (pair 2, peer-load reduce)". */
+const char* gett_last_multi(void);
+
 /* ---- complex xGETT: cgett / zgett (kernel.py:187-200) ----
  * Buffers are interleaved (re, im) pairs (numpy complex64 / complex128 memory);
  * offsets, lengths and increments count complex elements.  Products follow the

@@ -7,8 +7,9 @@ semantics.  Python calls the native library (libgett_b200.so, C ABI in
 include/gett_b200.h); the planner and the kernels are C++/CUDA.
 """
 from . import _native
-from ._native import (GettRuntimeError, last_kernel, launch_count, set_complex_embed, set_kernel,
-                      set_pipeline, set_pair, set_split_k, set_stream_k, set_tma)
+from ._native import (GettRuntimeError, last_kernel, last_multi, launch_count, set_complex_embed,
+                      set_devices, set_kernel, set_multi, set_pipeline, set_pair, set_split_k,
+                      set_stream_k, set_tma)
 from .kernel import cgett, dgett, dtype_prefix, gett_for_dtype, sgett, zero_view, zgett
 from .layout import TensorView, contiguous_increments, footprint, num_elements
 from .plan import (
@@ -27,6 +28,6 @@ __version__ = "0.1.0"
 __all__ = [
     "ContractionError", "ContractionSpec", "ErrorCode", "GettRuntimeError", "TensorView", "cgett", "zgett",
     "ValidationError", "contiguous_increments", "derive_output_extents", "dgett", "dtype_prefix",
-    "footprint", "free_dims", "gett_for_dtype", "last_kernel", "launch_count", "num_elements",
-    "output_rank", "set_complex_embed", "set_kernel", "set_pair", "set_split_k", "set_stream_k", "set_tma", "sgett", "validate", "zero_view",
+    "footprint", "free_dims", "gett_for_dtype", "last_kernel", "last_multi", "launch_count", "num_elements",
+    "output_rank", "set_complex_embed", "set_devices", "set_kernel", "set_multi", "set_pair", "set_split_k", "set_stream_k", "set_tma", "sgett", "validate", "zero_view",
 ]

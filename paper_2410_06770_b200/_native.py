@@ -20,6 +20,7 @@ EXPORTS = (
     "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
     "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
+    "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
 )
 
 ERR_INFO_WORDS = 6
@@ -51,6 +52,16 @@ def _load():
         f = getattr(lib, name)
         f.restype = ctypes.c_int
         f.argtypes = gett_args + [vp, i32p, i64p, ctypes.c_int]
+    for name in ("gett_dgett_multi", "gett_sgett_multi"):
+        f = getattr(lib, name)
+        f.restype = ctypes.c_int
+        f.argtypes = gett_args + [ctypes.c_int, i32p, i32p, i64p, ctypes.c_int]
+    lib.gett_set_devices.restype = ctypes.c_int
+    lib.gett_set_devices.argtypes = [ctypes.c_int, i32p]
+    lib.gett_set_multi.restype = ctypes.c_int
+    lib.gett_set_multi.argtypes = [ctypes.c_int]
+    lib.gett_last_multi.restype = ctypes.c_char_p
+    lib.gett_last_multi.argtypes = []
     lib.gett_validate.restype = ctypes.c_int
     lib.gett_validate.argtypes = [
         ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
@@ -151,6 +162,33 @@ def set_complex_embed(on: bool) -> None:
     """cgett/zgett tiled path: one embedded real GETT (default) or four real GETTs."""
     if LIB.gett_set_complex_embed(1 if on else 0) != 0:
         raise ValueError(f"bad complex-embed switch {on}")
+
+
+def i32(seq):
+    """A ctypes int32 array holding seq (length >= 1 so the pointer is valid)."""
+    vals = [int(x) for x in seq] or [0]
+    return (ctypes.c_int32 * len(vals))(*vals)
+
+
+def set_devices(devices) -> None:
+    """Default device list of the host entry points (dgett/sgett run across
+    these devices with the unchanged reference signature); None or () = the
+    current device.  A device may repeat (devices=(0, 0): two lanes on one GPU)."""
+    devs = [] if devices is None else [int(d) for d in devices]
+    check(LIB.gett_set_devices(len(devs), i32(devs)), "set_devices")
+
+
+def set_multi(strategy: str, staged: bool = False) -> None:
+    """Multi-device schedule: "auto" (default), "slabs" or "splitk" (tests);
+    staged=True: the split-K reduce copies the partials with cudaMemcpyPeer
+    instead of loading them from the peers."""
+    code = {"auto": 0, "slabs": 1, "splitk": 2}[strategy] | (4 if staged else 0)
+    check(LIB.gett_set_multi(code), "set_multi")
+
+
+def last_multi() -> str:
+    """The last host call's multi-device schedule ("none": one device)."""
+    return LIB.gett_last_multi().decode()
 
 
 def last_kernel() -> str:

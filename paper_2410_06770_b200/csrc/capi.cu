@@ -9,6 +9,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -29,7 +30,12 @@ namespace {
 
 enum class Mode { Auto, Ref, Tiled, Serial, Ffma, Dot };
 
-std::mutex g_mu;
+// Locks: g_plan_mu guards the plan cache and the last-call memo (short
+// sections); each device has its own DevState::mu, held while a call issues
+// work on that device, so calls on different devices run concurrently.  A
+// multi-device call takes its devices' locks in ascending order.
+std::mutex g_plan_mu;
+std::once_flag g_env_once;
 Mode g_mode = Mode::Auto;
 int g_split = 0;
 bool g_dgett_ws = true;  // DGETT: warp-specialised kernel (GETT_DGETT_WS=0: synchronous kernel)
@@ -39,15 +45,14 @@ bool g_sk_small = true;    // DGETT: stream-K instead of split-K at 56-73 tiles 
 bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one embedded GETT (GETT_COMPLEX_EMBED=0)
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
-bool g_env_read = false;
+int g_multi_stage = 0;      // multi-device split-K: 1 = stage partials by cudaMemcpyPeer instead of peer loads (GETT_MULTI_STAGE)
+std::vector<int> g_devices;  // default device list of the host entry points (gett_set_devices; empty = current device)
 thread_local std::string t_last_error;
 thread_local const char* t_last_kernel = "none";
 thread_local bool t_capturing = false;  // the current device call is being captured
-int64_t g_launches = 0;
+std::atomic<int64_t> g_launches{0};
 
-void read_env() {
-  if (g_env_read) return;
-  g_env_read = true;
+void read_env_once() {
   const char* k = std::getenv("GETT_KERNEL");
   if (k) gett_set_kernel(k);
   const char* s = std::getenv("GETT_SPLIT_K");
@@ -66,9 +71,13 @@ void read_env() {
   if (tv) g_tma = std::atoi(tv) != 0;
   const char* pl = std::getenv("GETT_PIPELINE");
   if (pl) g_pipeline_slabs = std::atoi(pl);
+  const char* ms = std::getenv("GETT_MULTI_STAGE");
+  if (ms) g_multi_stage = std::atoi(ms) != 0;
 }
+void read_env() { std::call_once(g_env_once, read_env_once); }
 
 int cuda_fail(cudaError_t e, const char* what) {
+  cudaGetLastError();  // clear a non-sticky error so the next call starts clean
   t_last_error = std::string(what) + ": " + cudaGetErrorString(e);
   return GETT_E_CUDA;
 }
@@ -111,7 +120,7 @@ struct DevPlan {
   GroupDev pgk{};      // dp.gk with its two tensors exchanged
   // used by a call captured into a CUDA graph: the graph holds raw pointers
   // into d_tab, so the LRU never evicts it (gett_release_caches still does)
-  bool pinned = false;
+  std::atomic<bool> pinned{false};
   ~DevPlan() {
     if (d_tab) {
       int cur = -1;
@@ -143,11 +152,12 @@ void evict_plans() {
   }
 }
 
-// the last validated descriptor and its plan (gett_impl; under g_mu)
+// the last validated descriptor and its plan (gett_impl; under g_plan_mu)
 struct LastCall {
-  std::vector<int64_t> key, scratch;
+  std::vector<int64_t> key;
   std::shared_ptr<DevPlan> dp;
 } g_last;
+thread_local std::vector<int64_t> t_key;  // the calling thread's descriptor key
 
 struct Scratch {
   void* p = nullptr;
@@ -162,23 +172,33 @@ struct StreamWs {
   Scratch cx;         // real embedding of a complex operand
   int32_t epoch = 0;  // stream-K launches so far on this stream
 };
-struct DevState {
+// A lane: one compute stream + two copy streams + the host path's device
+// staging of one device.  Lane 0 serves single-device calls; a multi-device
+// call that lists a device k times uses its lanes 0..k-1 (one GPU can stand in
+// for several: the multi-device path is exercised with devices = (0, 0)).
+struct Lane {
   cudaStream_t stream = nullptr;
   cudaStream_t h2d = nullptr, d2h = nullptr;  // copy streams of the pipelined host path
   std::vector<cudaEvent_t> events;
   Scratch a, b, c;
-  std::unordered_map<cudaStream_t, StreamWs> sws;
-  int sms = 0;
+  Scratch red;  // multi-device split-K: staged partials of the other lanes
   cudaEvent_t event(size_t i) {
     while (events.size() <= i) {
-      cudaEvent_t e;
-      cudaEventCreateWithFlags(&e, cudaEventDisableTiming);
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess) return nullptr;
       events.push_back(e);
     }
     return events[i];
   }
 };
-std::unordered_map<int, DevState> g_dev;
+struct DevState {
+  std::mutex mu;
+  std::unordered_map<cudaStream_t, StreamWs> sws;
+  std::vector<std::unique_ptr<Lane>> lanes;
+  int sms = 0;
+};
+constexpr int kMaxDevices = 64;
+DevState g_dev[kMaxDevices];
 
 int ensure(Scratch& s, size_t bytes) {
   if (bytes <= s.bytes) return 0;
@@ -252,6 +272,7 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
   CK(cudaGetDevice(&dev));
   std::string key = plan_key(dtype, a, b, s, off_c);
   key.append(reinterpret_cast<const char*>(&dev), sizeof dev);
+  std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.map.find(key);
   if (it != g_plans.map.end()) {
     g_plans.lru.splice(g_plans.lru.begin(), g_plans.lru, it->second.second);
@@ -307,6 +328,7 @@ int get_view_plan(int rank, const int64_t* ext, const int64_t* inc, std::shared_
   std::string key = "\x01zero|";
   for (int d = 0; d < rank; ++d) key += std::to_string(ext[d]) + "," + std::to_string(inc[d]) + ";";
   key += "#" + std::to_string(dev);
+  std::lock_guard<std::mutex> lock(g_plan_mu);
   auto it = g_plans.map.find(key);
   if (it != g_plans.map.end()) {
     g_plans.lru.splice(g_plans.lru.begin(), g_plans.lru, it->second.second);
@@ -825,27 +847,72 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
 
 constexpr int kNotPipelined = 1 << 30;
 
-// Host-buffer path with transfers overlapped: the free mode with the largest
-// C stride (outermost in C) is cut into slabs — each slab is itself an xGETT
-// on sub-views (shard.py's argument), so slab s computes while slab s+1's
-// operand/C spans are copied in and slab s-1's C span is copied out.  The
-// operand that does not own the slab mode is copied once, up front.  Slab C
-// spans must be disjoint (stride of the slab mode > span of the other C modes).
-template <typename T>
-int host_pipelined(DevPlan& full, const View& a, const View& b, const Spec& s, const T* ha,
-                   const T* hb, T* hc, int64_t off_c, int64_t len_c, DevState& ds) {
-  const Plan& p = full.plan;
-  if (g_pipeline_slabs == 0 || g_pipeline_slabs == 1 || p.c_may_alias) return kNotPipelined;
-  const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
-  const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
-  const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
-  if (g_pipeline_slabs < 0 && (na + nb + 2 * nc) * sizeof(T) < (64u << 20)) return kNotPipelined;
+// RAII: restore the caller's current device.
+struct DeviceGuard {
+  int dev = -1;
+  DeviceGuard() { cudaGetDevice(&dev); }
+  ~DeviceGuard() {
+    if (dev >= 0) cudaSetDevice(dev);
+  }
+};
+
+// Lane `i` of the current device's state (created on first use).  The caller
+// holds ds.mu.
+int get_lane(int dev, size_t i, Lane** out) {
+  DevState& ds = g_dev[dev];
+  while (ds.lanes.size() <= i) ds.lanes.emplace_back(new Lane());
+  Lane& L = *ds.lanes[i];
+  if (!L.stream) CK(cudaStreamCreateWithFlags(&L.stream, cudaStreamNonBlocking));
+  if (!L.h2d) CK(cudaStreamCreateWithFlags(&L.h2d, cudaStreamNonBlocking));
+  if (!L.d2h) CK(cudaStreamCreateWithFlags(&L.d2h, cudaStreamNonBlocking));
+  *out = &L;
+  return 0;
+}
+
+int current_device(int* dev) {
+  CK(cudaGetDevice(dev));
+  if (*dev < 0 || *dev >= kMaxDevices) {
+    t_last_error = "device ordinal >= 64";
+    return GETT_E_UNSUPPORTED;
+  }
+  return 0;
+}
+
+int event_at(Lane& L, size_t i, cudaEvent_t* e) {
+  *e = L.event(i);
+  if (!*e) {
+    t_last_error = "cudaEventCreate failed";
+    return GETT_E_CUDA;
+  }
+  return 0;
+}
+
+// The free mode that cuts an xGETT into slabs with disjoint C spans: among
+// free modes of extent > 1, the one with the largest |C increment| (outermost
+// in C), provided that increment exceeds the span of all other C modes.  A
+// slab (rows [lo, hi) of that mode) is itself an xGETT on sub-views — a
+// free-mode slice, bitwise equal to the same elements of the whole call — and
+// xGETT calls whose C footprints are disjoint may run concurrently
+// (SPEC.md:249).  This is the device-sharding rule of SURVEY §8e and the host
+// pipeline's cut.
+struct SlabCut {
+  int owner = -1, dim = -1, q = -1;  // operand (0 = A, 1 = B), its dim, C position
+  int64_t E = 0;                     // extent of the mode
+  // the owner operand's slab spans are disjoint too (its stride of the mode
+  // exceeds the span of its other modes): a slab uploads only its share of
+  // the owner.  Otherwise (c5: the cut mode is B's innermost) every slab's
+  // owner span is nearly the whole operand.
+  bool owner_disjoint = false;
+};
+
+bool slab_cut(const Plan& p, const View& a, const View& b, const Spec& s, SlabCut* out) {
   auto contracted = [](const int64_t* idx, int n, int d) {
     for (int k = 0; k < n; ++k)
       if (idx[k] == d) return true;
     return false;
   };
-  int owner = -1, dim = -1, q = -1, i = 0;
+  SlabCut c;
+  int i = 0;
   int64_t best = -1;
   for (int t = 0; t < 2; ++t) {
     const View& v = t == 0 ? a : b;
@@ -855,89 +922,415 @@ int host_pipelined(DevPlan& full, const View& a, const View& b, const Spec& s, c
       int qq = (int)s.perm[i++];
       if (v.ext[d] > 1 && iabs(s.inc_c[qq]) > best) {
         best = iabs(s.inc_c[qq]);
-        owner = t; dim = d; q = qq;
+        c.owner = t; c.dim = d; c.q = qq; c.E = v.ext[d];
       }
     }
   }
-  if (owner < 0) return kNotPipelined;
+  if (c.owner < 0) return false;
   int64_t other = 0;
   for (int qq = 0; qq < p.rank_c; ++qq)
-    if (qq != q && p.ext_c[qq] > 0) other += iabs(s.inc_c[qq]) * (p.ext_c[qq] - 1);
-  if (iabs(s.inc_c[q]) <= other) return kNotPipelined;
-  const View& ov = owner == 0 ? a : b;
-  const int64_t E = ov.ext[dim];
-  int64_t S = g_pipeline_slabs > 1 ? g_pipeline_slabs : 10;  // c2: 8 -> 8.66, 10 -> 8.43 ms
-  if (S > E) S = E;
-  if (S < 2) return kNotPipelined;
+    if (qq != c.q && p.ext_c[qq] > 0) other += iabs(s.inc_c[qq]) * (p.ext_c[qq] - 1);
+  if (iabs(s.inc_c[c.q]) <= other) return false;
+  const View& ov = c.owner == 0 ? a : b;
+  int64_t ospan = 0;
+  for (int d = 0; d < ov.rank; ++d)
+    if (d != c.dim && ov.ext[d] > 0) ospan += iabs(ov.inc[d]) * (ov.ext[d] - 1);
+  c.owner_disjoint = iabs(ov.inc[c.dim]) > ospan;
+  *out = c;
+  return true;
+}
 
-  int rc;
-  if ((rc = ensure(ds.a, na * sizeof(T))) || (rc = ensure(ds.b, nb * sizeof(T))) ||
-      (rc = ensure(ds.c, nc * sizeof(T))))
-    return rc;
-  if (!ds.h2d) CK(cudaStreamCreateWithFlags(&ds.h2d, cudaStreamNonBlocking));
-  if (!ds.d2h) CK(cudaStreamCreateWithFlags(&ds.d2h, cudaStreamNonBlocking));
-  // device bases: base[idx] mirrors host element idx over each full span
-  const int64_t lo_a = a.off + p.fp_lo[0], lo_b = b.off + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
-  T* base_a = (T*)ds.a.p - lo_a;
-  T* base_b = (T*)ds.b.p - lo_b;
-  T* base_c = (T*)ds.c.p - lo_c;
-  // the non-owning operand, whole
-  if (owner == 0) CK(cudaMemcpyAsync(base_b + lo_b, hb + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
-  else CK(cudaMemcpyAsync(base_a + lo_a, ha + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
-  // slab boundaries: the last two slabs are short (1 and 2 granules of 128
-  // rows, or rows when the mode is small) so that little compute and D2H is
-  // left after the last H2D (small slabs run split-K across the SMs); the rest
-  // are uniform, on granule boundaries
-  std::vector<int64_t> bnd(S + 1);
-  {
-    const int64_t g = E >= 16 * 128 ? 128 : 1;
-    const int64_t R = E - 3 * g;
-    if (S >= 4 && R >= (S - 2) * g) {
-      for (int64_t i = 0; i <= S - 2; ++i) bnd[i] = (R * i / (S - 2)) / g * g;
-      bnd[S - 2] = R;
-      bnd[S - 1] = R + 2 * g;
-      bnd[S] = E;
-    } else {
-      for (int64_t i = 0; i <= S; ++i) bnd[i] = E * i / S;
-    }
+// Sub-views of rows [lo, hi) of the cut mode (the ext vectors own the arrays
+// the views point at).
+struct SlabViews {
+  std::vector<int64_t> ext_o, ext_c;
+  View a, b;
+  int64_t off_c = 0;
+  SlabViews(const SlabCut& cut, const View& va, const View& vb, const Spec& s, const Plan& p,
+            int64_t off_c0, int64_t lo, int64_t hi)
+      : ext_o(cut.owner == 0 ? va.ext : vb.ext, (cut.owner == 0 ? va.ext : vb.ext) + (cut.owner == 0 ? va.rank : vb.rank)),
+        ext_c(p.ext_c), a(va), b(vb) {
+    ext_o[cut.dim] = hi - lo;
+    ext_c[cut.q] = hi - lo;
+    if (cut.owner == 0) { a.ext = ext_o.data(); a.off = va.off + lo * va.inc[cut.dim]; }
+    else { b.ext = ext_o.data(); b.off = vb.off + lo * vb.inc[cut.dim]; }
+    off_c = off_c0 + lo * s.inc_c[cut.q];
   }
-  std::vector<int64_t> ext_o(ov.ext, ov.ext + ov.rank);
-  std::vector<int64_t> ext_c(p.ext_c);
+};
+
+// Slab boundaries of rows [r0, r1) in S slabs: the last two are short (1 and
+// 2 granules of 128 rows, or rows when the range is small) so that little
+// compute and D2H is left after the last H2D (small slabs run split-K across
+// the SMs); the rest are uniform, on granule boundaries.
+std::vector<int64_t> slab_bounds(int64_t r0, int64_t r1, int64_t S) {
+  const int64_t E = r1 - r0;
+  std::vector<int64_t> bnd(S + 1);
+  const int64_t g = E >= 16 * 128 ? 128 : 1;
+  const int64_t R = E - 3 * g;
+  if (S >= 4 && R >= (S - 2) * g) {
+    for (int64_t i = 0; i <= S - 2; ++i) bnd[i] = (R * i / (S - 2)) / g * g;
+    bnd[S - 2] = R;
+    bnd[S - 1] = R + 2 * g;
+    bnd[S] = E;
+  } else {
+    for (int64_t i = 0; i <= S; ++i) bnd[i] = E * i / S;
+  }
+  for (auto& x : bnd) x += r0;
+  return bnd;
+}
+
+// Issue (no synchronisation) rows [r0, r1) of the cut mode as S slabs on one
+// lane: per slab, H2D of the owner operand's and C's slab spans on L.h2d, the
+// kernel on L.stream, D2H of C's slab span on L.d2h — slab s computes while
+// slab s+1 is copied in and slab s-1 is copied out.  base_x mirror host
+// element indices over the whole call's spans; the non-owning operand must
+// already be queued on L.h2d (or be in place).  Events from index ev0 on.
+template <typename T>
+int issue_slabs(Lane& L, DevState& ds, const SlabCut& cut, const View& a, const View& b,
+                const Spec& s, const Plan& p, const T* ha, const T* hb, T* hc, int64_t off_c,
+                int64_t len_c, int64_t r0, int64_t r1, int64_t S, T* base_a, T* base_b,
+                T* base_c, size_t ev0) {
+  const std::vector<int64_t> bnd = slab_bounds(r0, r1, S);
   for (int64_t sl = 0; sl < S; ++sl) {
-    const int64_t lo = bnd[sl], hi = bnd[sl + 1];
-    ext_o[dim] = hi - lo;
-    ext_c[q] = hi - lo;
-    View sa = a, sb = b;
-    if (owner == 0) { sa.ext = ext_o.data(); sa.off = a.off + lo * a.inc[dim]; }
-    else { sb.ext = ext_o.data(); sb.off = b.off + lo * b.inc[dim]; }
-    const int64_t soff_c = off_c + lo * s.inc_c[q];
+    if (bnd[sl + 1] == bnd[sl]) continue;
+    SlabViews v(cut, a, b, s, p, off_c, bnd[sl], bnd[sl + 1]);
     std::shared_ptr<DevPlan> dp;
-    rc = get_plan(sizeof(T) == 8 ? 'd' : 's', sa, sb, s, soff_c, len_c, &dp);
+    int rc = get_plan(sizeof(T) == 8 ? 'd' : 's', v.a, v.b, s, v.off_c, len_c, &dp);
     if (rc) return rc;
     int64_t flo, fhi;
-    const View& so = owner == 0 ? sa : sb;
+    const View& so = cut.owner == 0 ? v.a : v.b;
     footprint(so.rank, so.ext, so.inc, &flo, &fhi);
     const int64_t olo = so.off + flo;
     const size_t on = (size_t)(fhi - flo + 1);
-    T* obase = owner == 0 ? base_a : base_b;
-    const T* ohost = owner == 0 ? ha : hb;
-    CK(cudaMemcpyAsync(obase + olo, ohost + olo, on * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
-    footprint(p.rank_c, ext_c.data(), s.inc_c, &flo, &fhi);
-    const int64_t clo = soff_c + flo;
+    T* obase = cut.owner == 0 ? base_a : base_b;
+    const T* ohost = cut.owner == 0 ? ha : hb;
+    CK(cudaMemcpyAsync(obase + olo, ohost + olo, on * sizeof(T), cudaMemcpyHostToDevice, L.h2d));
+    footprint(p.rank_c, v.ext_c.data(), s.inc_c, &flo, &fhi);
+    const int64_t clo = v.off_c + flo;
     const size_t cn = (size_t)(fhi - flo + 1);
-    CK(cudaMemcpyAsync(base_c + clo, hc + clo, cn * sizeof(T), cudaMemcpyHostToDevice, ds.h2d));
-    cudaEvent_t ein = ds.event(2 * sl), eout = ds.event(2 * sl + 1);
-    CK(cudaEventRecord(ein, ds.h2d));
-    CK(cudaStreamWaitEvent(ds.stream, ein, 0));
-    rc = run_device<T>(*dp, base_a + sa.off, base_b + sb.off, base_c + soff_c, ds.stream, ds);
+    CK(cudaMemcpyAsync(base_c + clo, hc + clo, cn * sizeof(T), cudaMemcpyHostToDevice, L.h2d));
+    cudaEvent_t ein, eout;
+    if ((rc = event_at(L, ev0 + 2 * sl, &ein)) || (rc = event_at(L, ev0 + 2 * sl + 1, &eout))) return rc;
+    CK(cudaEventRecord(ein, L.h2d));
+    CK(cudaStreamWaitEvent(L.stream, ein, 0));
+    rc = run_device<T>(*dp, base_a + v.a.off, base_b + v.b.off, base_c + v.off_c, L.stream, ds);
     if (rc) return rc;
-    CK(cudaEventRecord(eout, ds.stream));
-    CK(cudaStreamWaitEvent(ds.d2h, eout, 0));
-    CK(cudaMemcpyAsync(hc + clo, base_c + clo, cn * sizeof(T), cudaMemcpyDeviceToHost, ds.d2h));
+    CK(cudaEventRecord(eout, L.stream));
+    CK(cudaStreamWaitEvent(L.d2h, eout, 0));
+    CK(cudaMemcpyAsync(hc + clo, base_c + clo, cn * sizeof(T), cudaMemcpyDeviceToHost, L.d2h));
   }
-  CK(cudaStreamSynchronize(ds.d2h));
-  CK(cudaStreamSynchronize(ds.stream));
   return 0;
+}
+
+// Host-buffer path with transfers overlapped (one device): C's outermost
+// free mode is cut into slabs (issue_slabs); the operand that does not own the
+// slab mode is copied once, up front.
+template <typename T>
+int host_pipelined(DevPlan& full, const View& a, const View& b, const Spec& s, const T* ha,
+                   const T* hb, T* hc, int64_t off_c, int64_t len_c, DevState& ds, Lane& L) {
+  const Plan& p = full.plan;
+  if (g_pipeline_slabs == 0 || g_pipeline_slabs == 1 || p.c_may_alias) return kNotPipelined;
+  const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
+  const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
+  const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
+  if (g_pipeline_slabs < 0 && (na + nb + 2 * nc) * sizeof(T) < (64u << 20)) return kNotPipelined;
+  SlabCut cut;
+  if (!slab_cut(p, a, b, s, &cut) || (!cut.owner_disjoint && g_pipeline_slabs < 0)) return kNotPipelined;
+  int64_t S = g_pipeline_slabs > 1 ? g_pipeline_slabs : 10;  // c2: 8 -> 8.66, 10 -> 8.43 ms
+  if (S > cut.E) S = cut.E;
+  if (S < 2) return kNotPipelined;
+  int rc;
+  if ((rc = ensure(L.a, na * sizeof(T))) || (rc = ensure(L.b, nb * sizeof(T))) ||
+      (rc = ensure(L.c, nc * sizeof(T))))
+    return rc;
+  // device bases: base[idx] mirrors host element idx over each full span
+  const int64_t lo_a = a.off + p.fp_lo[0], lo_b = b.off + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  T* base_a = (T*)L.a.p - lo_a;
+  T* base_b = (T*)L.b.p - lo_b;
+  T* base_c = (T*)L.c.p - lo_c;
+  if (cut.owner == 0) CK(cudaMemcpyAsync(base_b + lo_b, hb + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, L.h2d));
+  else CK(cudaMemcpyAsync(base_a + lo_a, ha + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, L.h2d));
+  rc = issue_slabs<T>(L, ds, cut, a, b, s, p, ha, hb, hc, off_c, len_c, 0, cut.E, S, base_a, base_b,
+                      base_c, 0);
+  if (rc) return rc;
+  CK(cudaStreamSynchronize(L.d2h));
+  CK(cudaStreamSynchronize(L.stream));
+  return 0;
+}
+
+// ---------------------------------------------------------------------------
+// Multi-device xGETT: one host call drives a list of devices.
+//   slabs   — the slab mode (slab_cut) is split into one row range per device;
+//             each device copies its slabs of the owner operand and of C over
+//             its own PCIe link (pipelined, issue_slabs) and computes them; the
+//             replicated operand crosses PCIe once in total: device j copies
+//             chunk j of its span from the host and the devices exchange the
+//             chunks over NVLink (cudaMemcpyPeerAsync).  No collective.
+//   split-K — when the free extents are too small to fill the devices (c5):
+//             the contracted pair with the largest extent is split, device 0
+//             computes C += A_0·B_0, device j > 0 computes P_j = A_j·B_j into
+//             a zeroed copy of C's span, and device 0 adds
+//             C += (P_1 + ... + P_{n-1}) in that fixed order (deterministic),
+//             reading the partials straight from the peers' memory over
+//             NVLink (or staging them with cudaMemcpyPeerAsync when peer
+//             access is unavailable) — the one reduce of the call.
+// A device listed k times contributes k lanes (its lanes 0..k-1), so the
+// whole path runs on a single GPU with devices = (0, 0).
+
+std::mutex g_peer_mu;
+signed char g_peer[kMaxDevices][kMaxDevices];  // 0 unknown, 1 enabled, -1 unavailable
+
+// can device `dev` load from `peer`'s memory?  (enables access once)
+bool peer_access(int dev, int peer) {
+  if (dev == peer) return true;
+  std::lock_guard<std::mutex> lk(g_peer_mu);
+  signed char& st = g_peer[dev][peer];
+  if (st == 0) {
+    int can = 0;
+    st = -1;
+    if (cudaDeviceCanAccessPeer(&can, dev, peer) == cudaSuccess && can) {
+      int cur = -1;
+      cudaGetDevice(&cur);
+      cudaSetDevice(dev);
+      cudaError_t e = cudaDeviceEnablePeerAccess(peer, 0);
+      if (e == cudaSuccess || e == cudaErrorPeerAccessAlreadyEnabled) st = 1;
+      cudaGetLastError();
+      cudaSetDevice(cur);
+    }
+  }
+  return st == 1;
+}
+
+struct LaneRef {
+  int dev;
+  Lane* L;
+};
+
+int g_multi_force = 0;  // 0 auto, 1 slabs, 2 split-K (gett_set_multi; tests)
+thread_local char t_last_multi[96] = "none";
+
+// Put the span [lo, lo + n) of host buffer h at base[i] + lo on every lane:
+// lane j uploads chunk j over its own PCIe link, then every lane pulls the
+// other chunks from their lanes (cudaMemcpyPeerAsync over NVLink; a plain
+// device copy between two lanes of one GPU), all on the lanes' h2d streams.
+// Uses event index `ev` of every lane.
+template <typename T>
+int replicate_span(std::vector<LaneRef>& lanes, const std::vector<T*>& base, const T* h, int64_t lo,
+                   size_t n_el, size_t ev) {
+  const int n = (int)lanes.size();
+  std::vector<size_t> cb(n + 1);
+  for (int j = 0; j <= n; ++j) cb[j] = n_el * j / n;
+  int rc;
+  for (int j = 0; j < n; ++j) {
+    CK(cudaSetDevice(lanes[j].dev));
+    Lane& L = *lanes[j].L;
+    CK(cudaMemcpyAsync(base[j] + lo + cb[j], h + lo + cb[j], (cb[j + 1] - cb[j]) * sizeof(T),
+                       cudaMemcpyHostToDevice, L.h2d));
+    cudaEvent_t e;
+    if ((rc = event_at(L, ev, &e))) return rc;
+    CK(cudaEventRecord(e, L.h2d));
+  }
+  for (int i = 0; i < n; ++i) {
+    CK(cudaSetDevice(lanes[i].dev));
+    Lane& L = *lanes[i].L;
+    for (int j = 0; j < n; ++j) {
+      if (j == i || cb[j + 1] == cb[j]) continue;
+      CK(cudaStreamWaitEvent(L.h2d, lanes[j].L->events[ev], 0));
+      const size_t bytes = (cb[j + 1] - cb[j]) * sizeof(T);
+      T* dst = base[i] + lo + cb[j];
+      const T* src = base[j] + lo + cb[j];
+      if (lanes[j].dev == lanes[i].dev) CK(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, L.h2d));
+      else CK(cudaMemcpyPeerAsync(dst, lanes[i].dev, src, lanes[j].dev, bytes, L.h2d));
+    }
+  }
+  return 0;
+}
+
+template <typename T>
+int multi_slabs(std::vector<LaneRef>& lanes, const SlabCut& cut, const View& a, const View& b,
+                const Spec& s, const Plan& p, const T* ha, const T* hb, T* hc, int64_t off_c,
+                int64_t len_c) {
+  const int n = (int)lanes.size();
+  const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
+  const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
+  const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
+  const int64_t lo_a = a.off + p.fp_lo[0], lo_b = b.off + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  // row ranges: granules of 128 rows when every device gets at least one
+  const int64_t g = cut.E >= 128 * n ? 128 : 1;
+  const int64_t units = (cut.E + g - 1) / g;
+  std::vector<int64_t> rb(n + 1);
+  for (int i = 0; i <= n; ++i) rb[i] = std::min(cut.E, units * i / n * g);
+  rb[n] = cut.E;
+  std::vector<T*> ba(n), bb(n), bc(n);
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    CK(cudaSetDevice(lanes[i].dev));
+    Lane& L = *lanes[i].L;
+    if ((rc = ensure(L.a, na * sizeof(T))) || (rc = ensure(L.b, nb * sizeof(T))) ||
+        (rc = ensure(L.c, nc * sizeof(T))))
+      return rc;
+    ba[i] = (T*)L.a.p - lo_a;
+    bb[i] = (T*)L.b.p - lo_b;
+    bc[i] = (T*)L.c.p - lo_c;
+  }
+  // the replicated operand: chunk j over lane j's PCIe link, then NVLink
+  if (cut.owner == 0) rc = replicate_span<T>(lanes, bb, hb, lo_b, nb, 0);
+  else rc = replicate_span<T>(lanes, ba, ha, lo_a, na, 0);
+  if (rc) return rc;
+  // each lane's rows, pipelined over its own copy streams
+  for (int i = 0; i < n; ++i) {
+    if (rb[i + 1] == rb[i]) continue;
+    CK(cudaSetDevice(lanes[i].dev));
+    const size_t lane_bytes = (size_t)((double)(na + 2 * nc) * (rb[i + 1] - rb[i]) / cut.E) * sizeof(T);
+    int64_t S = g_pipeline_slabs > 1 ? g_pipeline_slabs : (int64_t)std::min<size_t>(10, 1 + lane_bytes / (8u << 20));
+    if (g_pipeline_slabs == 0 || g_pipeline_slabs == 1) S = 1;
+    if (S > rb[i + 1] - rb[i]) S = rb[i + 1] - rb[i];
+    rc = issue_slabs<T>(*lanes[i].L, g_dev[lanes[i].dev], cut, a, b, s, p, ha, hb, hc, off_c, len_c,
+                        rb[i], rb[i + 1], S, ba[i], bb[i], bc[i], 1);
+    if (rc) return rc;
+  }
+  for (int i = 0; i < n; ++i) {
+    CK(cudaSetDevice(lanes[i].dev));
+    CK(cudaStreamSynchronize(lanes[i].L->d2h));
+    CK(cudaStreamSynchronize(lanes[i].L->stream));
+    CK(cudaStreamSynchronize(lanes[i].L->h2d));
+  }
+  std::snprintf(t_last_multi, sizeof t_last_multi, "slabs x%d (mode %d of %c, replicated %c over peers)", n,
+                cut.dim, cut.owner == 0 ? 'A' : 'B', cut.owner == 0 ? 'B' : 'A');
+  return 0;
+}
+
+template <typename T>
+int multi_splitk(std::vector<LaneRef>& lanes, int pair, const View& a, const View& b, const Spec& s,
+                 const Plan& p, const T* ha, const T* hb, T* hc, int64_t off_c, int64_t len_c) {
+  const int n = (int)lanes.size();
+  const int da = (int)s.cont_a[pair], db = (int)s.cont_b[pair];
+  const int64_t Ek = a.ext[da];
+  const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
+  const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
+  const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
+  const int64_t lo_a = a.off + p.fp_lo[0], lo_b = b.off + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  std::vector<T*> ba(n), bb(n), bc(n);
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    CK(cudaSetDevice(lanes[i].dev));
+    Lane& L = *lanes[i].L;
+    if ((rc = ensure(L.a, na * sizeof(T))) || (rc = ensure(L.b, nb * sizeof(T))) ||
+        (rc = ensure(L.c, nc * sizeof(T))))
+      return rc;
+    ba[i] = (T*)L.a.p - lo_a;
+    bb[i] = (T*)L.b.p - lo_b;
+    bc[i] = (T*)L.c.p - lo_c;
+  }
+  // A and B cross PCIe once in total (a K slice of a strided view spans
+  // nearly the whole buffer: c5's A, split along any pair, still does), C
+  // once to lane 0; lanes j > 0 accumulate into zeroed copies of C's span
+  if ((rc = replicate_span<T>(lanes, ba, ha, lo_a, na, 0))) return rc;
+  if ((rc = replicate_span<T>(lanes, bb, hb, lo_b, nb, 1))) return rc;
+  for (int i = 0; i < n; ++i) {
+    CK(cudaSetDevice(lanes[i].dev));
+    Lane& L = *lanes[i].L;
+    const int64_t k0 = Ek * i / n, k1 = Ek * (i + 1) / n;
+    std::vector<int64_t> ea(a.ext, a.ext + a.rank), eb(b.ext, b.ext + b.rank);
+    ea[da] = k1 - k0;
+    eb[db] = k1 - k0;
+    View sa = a, sb = b;
+    sa.ext = ea.data(); sa.off = a.off + k0 * a.inc[da];
+    sb.ext = eb.data(); sb.off = b.off + k0 * b.inc[db];
+    std::shared_ptr<DevPlan> dp;
+    if ((rc = get_plan(sizeof(T) == 8 ? 'd' : 's', sa, sb, s, off_c, len_c, &dp))) return rc;
+    if (i == 0) CK(cudaMemcpyAsync(L.c.p, hc + lo_c, nc * sizeof(T), cudaMemcpyHostToDevice, L.h2d));
+    else CK(cudaMemsetAsync(L.c.p, 0, nc * sizeof(T), L.h2d));
+    cudaEvent_t ein, e;
+    if ((rc = event_at(L, 2, &ein)) || (rc = event_at(L, 3, &e))) return rc;
+    CK(cudaEventRecord(ein, L.h2d));
+    CK(cudaStreamWaitEvent(L.stream, ein, 0));
+    if ((rc = run_device<T>(*dp, ba[i] + sa.off, bb[i] + sb.off, bc[i] + off_c, L.stream, g_dev[lanes[i].dev])))
+      return rc;
+    CK(cudaEventRecord(e, L.stream));
+  }
+  // device 0: C += (P_1 + ... + P_{n-1}), then C's span back to the host
+  const int d0 = lanes[0].dev;
+  Lane& L0 = *lanes[0].L;
+  CK(cudaSetDevice(d0));
+  bool direct = !g_multi_stage;
+  for (int j = 1; j < n && direct; ++j) direct = peer_access(d0, lanes[j].dev);
+  AccumParams<T> ap;
+  ap.C = bc[0] + off_c;
+  ap.n = n - 1;
+  if (!direct && (rc = ensure(L0.red, (size_t)(n - 1) * nc * sizeof(T)))) return rc;
+  for (int j = 1; j < n; ++j) {
+    CK(cudaStreamWaitEvent(L0.stream, lanes[j].L->events[3], 0));
+    if (direct) {
+      ap.P[j - 1] = bc[j] + off_c;
+    } else {
+      T* dst = (T*)L0.red.p + (size_t)(j - 1) * nc;
+      if (lanes[j].dev == d0)
+        CK(cudaMemcpyAsync(dst, lanes[j].L->c.p, nc * sizeof(T), cudaMemcpyDeviceToDevice, L0.stream));
+      else
+        CK(cudaMemcpyPeerAsync(dst, d0, lanes[j].L->c.p, lanes[j].dev, nc * sizeof(T), L0.stream));
+      ap.P[j - 1] = dst - lo_c + off_c;
+    }
+  }
+  std::shared_ptr<DevPlan> vp;
+  if ((rc = get_view_plan(p.rank_c, p.ext_c.data(), s.inc_c, &vp))) return rc;
+  ap.g = vp->gm;
+  CK(launch_accum<T>(ap, L0.stream));
+  ++g_launches;
+  CK(cudaMemcpyAsync(hc + lo_c, L0.c.p, nc * sizeof(T), cudaMemcpyDeviceToHost, L0.stream));
+  CK(cudaStreamSynchronize(L0.stream));
+  for (int j = 1; j < n; ++j) {
+    CK(cudaSetDevice(lanes[j].dev));
+    CK(cudaStreamSynchronize(lanes[j].L->stream));
+    CK(cudaStreamSynchronize(lanes[j].L->h2d));
+  }
+  std::snprintf(t_last_multi, sizeof t_last_multi, "split-K x%d (pair %d, %s reduce)", n, pair,
+                direct ? "peer-load" : "staged");
+  return 0;
+}
+
+// Choose the multi-device strategy of a validated, non-empty host call.
+// Returns kNotPipelined when the call should run on devices[0] alone.
+template <typename T>
+int host_multi(const Plan& p, const View& a, const View& b, const Spec& s, const T* ha,
+               const T* hb, T* hc, int64_t off_c, int64_t len_c, const std::vector<int>& devs) {
+  int n = std::min((int)devs.size(), kMaxParts + 1);
+  if (n < 2 || p.c_may_alias) return kNotPipelined;
+  const double macs = (double)p.size_free * (double)p.size_cont;
+  const int64_t tiles = ((p.gm.G + 127) / 128) * ((p.gn.G + 127) / 128);
+  SlabCut cut;
+  const bool can_slab = slab_cut(p, a, b, s, &cut) && cut.E >= 2 &&
+                        (cut.owner_disjoint || g_multi_force == 1);
+  int pair = -1;
+  for (int k = 0; k < s.conts; ++k)
+    if (a.ext[s.cont_a[k]] >= 2 && (pair < 0 || a.ext[s.cont_a[k]] > a.ext[s.cont_a[pair]])) pair = k;
+  int strategy = 0;  // 1 slabs, 2 split-K
+  if (g_multi_force == 1) strategy = can_slab ? 1 : 0;
+  else if (g_multi_force == 2) strategy = pair >= 0 ? 2 : 0;
+  else if (macs >= (double)n * (1 << 27)) {
+    if (can_slab && tiles >= 74 * n) strategy = 1;  // every device gets >= half a wave of tiles
+    else if (pair >= 0 && p.size_cont >= 256 * n) strategy = 2;
+    else if (can_slab) strategy = 1;
+  }
+  if (strategy == 0) return kNotPipelined;
+  if (strategy == 1 && n > cut.E) n = (int)cut.E;
+  if (strategy == 2 && n > a.ext[s.cont_a[pair]]) n = (int)a.ext[s.cont_a[pair]];
+  // lock the distinct devices in ascending order, then take lanes
+  std::vector<int> order(devs.begin(), devs.begin() + n);
+  std::sort(order.begin(), order.end());
+  order.erase(std::unique(order.begin(), order.end()), order.end());
+  std::vector<std::unique_lock<std::mutex>> locks;
+  for (int d : order) locks.emplace_back(g_dev[d].mu);
+  std::vector<LaneRef> lanes(n);
+  std::vector<int> used(kMaxDevices, 0);
+  int rc;
+  for (int i = 0; i < n; ++i) {
+    CK(cudaSetDevice(devs[i]));
+    lanes[i].dev = devs[i];
+    if ((rc = get_lane(devs[i], (size_t)used[devs[i]]++, &lanes[i].L))) return rc;
+  }
+  return strategy == 1 ? multi_slabs<T>(lanes, cut, a, b, s, p, ha, hb, hc, off_c, len_c)
+                       : multi_splitk<T>(lanes, pair, a, b, s, p, ha, hb, hc, off_c, len_c);
 }
 
 int fill_errors(const std::vector<Error>& errs, int32_t* codes, int64_t* info, int max_errs) {
@@ -950,16 +1343,6 @@ int fill_errors(const std::vector<Error>& errs, int32_t* codes, int64_t* info, i
   return n;
 }
 
-int dev_state(int* dev_out, DevState** out) {
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  *dev_out = dev;
-  DevState& ds = g_dev[dev];
-  if (!ds.stream) CK(cudaStreamCreateWithFlags(&ds.stream, cudaStreamNonBlocking));
-  *out = &ds;
-  return 0;
-}
-
 // marks the calling thread's device call as captured (plans it touches are
 // pinned) for the duration of one entry point
 struct CaptureScope {
@@ -970,21 +1353,52 @@ struct CaptureScope {
   ~CaptureScope() { t_capturing = false; }
 };
 
+// devices of a host call: explicit list, else the gett_set_devices default,
+// else none (the current device)
+int check_devices(int n_dev, const int32_t* devices, std::vector<int>* out) {
+  out->clear();
+  if (n_dev > 0) {
+    if (!devices) {
+      t_last_error = "devices is NULL";
+      return GETT_E_INVALID_ARG;
+    }
+    for (int i = 0; i < n_dev; ++i) {
+      if (devices[i] < 0 || devices[i] >= kMaxDevices) {
+        t_last_error = "device ordinal out of range";
+        return GETT_E_INVALID_ARG;
+      }
+      out->push_back(devices[i]);
+    }
+  } else {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    *out = g_devices;
+  }
+  return 0;
+}
+
 template <typename T>
 int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a, const T* a,
               int64_t off_a, int64_t len_a, int rank_b, const int64_t* ext_b,
               const int64_t* inc_b, const T* b, int64_t off_b, int64_t len_b, int conts,
               const int64_t* cont_a, const int64_t* cont_b, int perm_len, const int64_t* perm,
               int inc_c_len, const int64_t* inc_c, T* c, int64_t off_c, int64_t len_c,
-              cudaStream_t stream, int32_t* codes, int64_t* info, int max_errs) {
+              cudaStream_t stream, int32_t* codes, int64_t* info, int max_errs, int n_dev = 0,
+              const int32_t* devices = nullptr) {
   if (rank_a < 0 || rank_b < 0 || conts < 0 || perm_len < 0 || inc_c_len < 0 || off_a < 0 ||
-      off_b < 0 || off_c < 0 || len_a < 0 || len_b < 0 || len_c < 0) {
+      off_b < 0 || off_c < 0 || len_a < 0 || len_b < 0 || len_c < 0 || n_dev < 0) {
     t_last_error = "negative rank/count/offset/length";
     return GETT_E_INVALID_ARG;
   }
-  std::lock_guard<std::mutex> lock(g_mu);
   read_env();
   t_last_kernel = "none";
+  std::snprintf(t_last_multi, sizeof t_last_multi, "none");
+  std::vector<int> devs;
+  int rc = 0;
+  if (host && (rc = check_devices(n_dev, devices, &devs))) return rc;
+  DeviceGuard guard;  // a call on devices[0] / several devices restores the caller's device
+  // (validation needs no device: a bad ordinal is reported after it)
+  cudaError_t set_err = devs.empty() ? cudaSuccess : cudaSetDevice(devs[0]);
+  if (set_err != cudaSuccess) cudaGetLastError();
   View va{rank_a, ext_a, inc_a, off_a, len_a};
   View vb{rank_b, ext_b, inc_b, off_b, len_b};
   Spec sp{conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c};
@@ -992,7 +1406,7 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   // a call whose descriptor (every argument but the pointers) equals the last
   // validated one reuses its result and plan: no validation or plan-key work
   // (validation runs without CUDA: the device is only queried on a key match)
-  std::vector<int64_t>& key = g_last.scratch;
+  std::vector<int64_t>& key = t_key;
   key.clear();
   key.push_back((int64_t)sizeof(T));
   auto put = [&](int n, const int64_t* v) {
@@ -1004,10 +1418,14 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   put(conts, cont_a); put(conts, cont_b); put(perm_len, perm); put(inc_c_len, inc_c);
   key.push_back(off_c); key.push_back(len_c);
   std::shared_ptr<DevPlan> dp;
-  int cur_dev = -1;
-  if (g_last.dp && key == g_last.key && cudaGetDevice(&cur_dev) == cudaSuccess && cur_dev == g_last.dp->device) {
-    dp = g_last.dp;
-  } else {
+  {
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    int cur_dev = -1;
+    if (g_last.dp && key == g_last.key && cudaGetDevice(&cur_dev) == cudaSuccess &&
+        cur_dev == g_last.dp->device)
+      dp = g_last.dp;
+  }
+  if (!dp) {
     std::vector<Error> errs = validate(va, vb, sp, CMode::Derived, vc);
     if (!errs.empty()) return fill_errors(errs, codes, info, max_errs);
     // empty iteration space: nothing is written (kernel.py:93-94)
@@ -1015,23 +1433,35 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
       if (ext_a[d] == 0) return 0;
     for (int d = 0; d < rank_b; ++d)
       if (ext_b[d] == 0) return 0;
-    int rc = get_plan(sizeof(T) == 8 ? 'd' : 's', va, vb, sp, off_c, len_c, &dp);
-    if (rc) return rc;
-    g_last.key.swap(key);
+    if ((rc = get_plan(sizeof(T) == 8 ? 'd' : 's', va, vb, sp, off_c, len_c, &dp))) return rc;
+    std::lock_guard<std::mutex> lk(g_plan_mu);
+    g_last.key = key;
     g_last.dp = dp;
   }
-  int rc = 0;
+  if (set_err != cudaSuccess) return cuda_fail(set_err, "cudaSetDevice(devices[0])");
   const Plan& p = dp->plan;
+  if (host && devs.size() > 1) {
+    for (int d : devs) {
+      cudaError_t e = cudaSetDevice(d);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice(devices[i])");
+    }
+    rc = host_multi<T>(p, va, vb, sp, a, b, c, off_c, len_c, devs);
+    if (rc != kNotPipelined) return rc;
+    CK(cudaSetDevice(devs[0]));
+  }
   int dev;
-  DevState* dsp = nullptr;
-  if ((rc = dev_state(&dev, &dsp))) return rc;
-  DevState& ds = *dsp;
+  if ((rc = current_device(&dev))) return rc;
+  DevState& ds = g_dev[dev];
+  std::lock_guard<std::mutex> lk(ds.mu);
+  Lane* Lp = nullptr;
+  if ((rc = get_lane(dev, 0, &Lp))) return rc;
+  Lane& L = *Lp;
   if (!host) {
     CaptureScope cs(stream);
     if (t_capturing) dp->pinned = true;
     return run_device<T>(*dp, a + off_a, b + off_b, c + off_c, stream, ds);
   }
-  rc = host_pipelined<T>(*dp, va, vb, sp, a, b, c, off_c, len_c, ds);
+  rc = host_pipelined<T>(*dp, va, vb, sp, a, b, c, off_c, len_c, ds, L);
   if (rc != kNotPipelined) return rc;
   // host buffers: copy the addressed spans in, run, copy C's span back
   // (the plan is cached by descriptor only: spans use this call's offsets)
@@ -1039,13 +1469,13 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
   size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
   size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
   size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
-  if ((rc = ensure(ds.a, na * sizeof(T))) || (rc = ensure(ds.b, nb * sizeof(T))) ||
-      (rc = ensure(ds.c, nc * sizeof(T))))
+  if ((rc = ensure(L.a, na * sizeof(T))) || (rc = ensure(L.b, nb * sizeof(T))) ||
+      (rc = ensure(L.c, nc * sizeof(T))))
     return rc;
-  T* da = (T*)ds.a.p;
-  T* db = (T*)ds.b.p;
-  T* dc = (T*)ds.c.p;
-  cudaStream_t s = ds.stream;
+  T* da = (T*)L.a.p;
+  T* db = (T*)L.b.p;
+  T* dc = (T*)L.c.p;
+  cudaStream_t s = L.stream;
   CK(cudaMemcpyAsync(da, a + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(db, b + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dc, c + lo_c, nc * sizeof(T), cudaMemcpyHostToDevice, s));
@@ -1247,7 +1677,6 @@ int gett_impl_complex(bool host, int rank_a, const int64_t* ext_a, const int64_t
     t_last_error = "negative rank/count/offset/length";
     return GETT_E_INVALID_ARG;
   }
-  std::lock_guard<std::mutex> lock(g_mu);
   read_env();
   t_last_kernel = "none";
   View va{rank_a, ext_a, inc_a, off_a, len_a};
@@ -1265,9 +1694,12 @@ int gett_impl_complex(bool host, int rank_a, const int64_t* ext_a, const int64_t
   if (rc) return rc;
   const Plan& p = cp->plan;
   int dev;
-  DevState* dsp = nullptr;
-  if ((rc = dev_state(&dev, &dsp))) return rc;
-  DevState& ds = *dsp;
+  if ((rc = current_device(&dev))) return rc;
+  DevState& ds = g_dev[dev];
+  std::lock_guard<std::mutex> lk(ds.mu);
+  Lane* Lp = nullptr;
+  if ((rc = get_lane(dev, 0, &Lp))) return rc;
+  Lane& L = *Lp;
   if (!host) {
     CaptureScope cs(stream);
     if (t_capturing) cp->pinned = true;
@@ -1277,13 +1709,13 @@ int gett_impl_complex(bool host, int rank_a, const int64_t* ext_a, const int64_t
   const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1) * 2;
   const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1) * 2;
   const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1) * 2;
-  if ((rc = ensure(ds.a, na * sizeof(R))) || (rc = ensure(ds.b, nb * sizeof(R))) ||
-      (rc = ensure(ds.c, nc * sizeof(R))))
+  if ((rc = ensure(L.a, na * sizeof(R))) || (rc = ensure(L.b, nb * sizeof(R))) ||
+      (rc = ensure(L.c, nc * sizeof(R))))
     return rc;
-  R* da = (R*)ds.a.p;
-  R* db = (R*)ds.b.p;
-  R* dc = (R*)ds.c.p;
-  cudaStream_t s = ds.stream;
+  R* da = (R*)L.a.p;
+  R* db = (R*)L.b.p;
+  R* dc = (R*)L.c.p;
+  cudaStream_t s = L.stream;
   CK(cudaMemcpyAsync(da, a + 2 * lo_a, na * sizeof(R), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(db, b + 2 * lo_b, nb * sizeof(R), cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(dc, c + 2 * lo_c, nc * sizeof(R), cudaMemcpyHostToDevice, s));
@@ -1311,23 +1743,25 @@ int zero_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64
     t_last_error = "view footprint outside the buffer";
     return GETT_E_INVALID_ARG;
   }
-  std::lock_guard<std::mutex> lock(g_mu);
   std::shared_ptr<DevPlan> dp;
   int rc = get_view_plan(rank, ext, inc, &dp);
   if (rc) return rc;
   int dev;
-  DevState* dsp = nullptr;
-  if ((rc = dev_state(&dev, &dsp))) return rc;
-  DevState& ds = *dsp;
+  if ((rc = current_device(&dev))) return rc;
+  DevState& ds = g_dev[dev];
+  std::lock_guard<std::mutex> lk(ds.mu);
+  Lane* Lp = nullptr;
+  if ((rc = get_lane(dev, 0, &Lp))) return rc;
+  Lane& L = *Lp;
   if (!host) {
     CK(launch_zero<T>(buf + off, dp->gm, stream));
     ++g_launches;
     return 0;
   }
   size_t n = (size_t)(hi - lo + 1);
-  if ((rc = ensure(ds.c, n * sizeof(T)))) return rc;
-  T* d = (T*)ds.c.p;
-  cudaStream_t s = ds.stream;
+  if ((rc = ensure(L.c, n * sizeof(T)))) return rc;
+  T* d = (T*)L.c.p;
+  cudaStream_t s = L.stream;
   CK(cudaMemcpyAsync(d, buf + off + lo, n * sizeof(T), cudaMemcpyHostToDevice, s));
   CK(launch_zero<T>(d - lo, dp->gm, s));
   ++g_launches;
@@ -1389,6 +1823,62 @@ int gett_sgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, co
                           offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c,
                           c, offset_c, len_c, (cudaStream_t)stream, err_codes, err_info, max_errs);
 }
+
+int gett_dgett_multi(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const double* a,
+                     int64_t offset_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+                     const int64_t* inc_b, const double* b, int64_t offset_b, int64_t len_b,
+                     int conts, const int64_t* cont_a, const int64_t* cont_b, int perm_len,
+                     const int64_t* perm, int inc_c_len, const int64_t* inc_c, double* c,
+                     int64_t offset_c, int64_t len_c, int n_dev, const int32_t* devices,
+                     int32_t* err_codes, int64_t* err_info, int max_errs) {
+  if (n_dev < 1) {
+    t_last_error = "n_dev < 1";
+    return GETT_E_INVALID_ARG;
+  }
+  return gett_impl<double>(true, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b, inc_b, b,
+                           offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len,
+                           inc_c, c, offset_c, len_c, nullptr, err_codes, err_info, max_errs, n_dev,
+                           devices);
+}
+
+int gett_sgett_multi(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const float* a,
+                     int64_t offset_a, int64_t len_a, int rank_b, const int64_t* ext_b,
+                     const int64_t* inc_b, const float* b, int64_t offset_b, int64_t len_b,
+                     int conts, const int64_t* cont_a, const int64_t* cont_b, int perm_len,
+                     const int64_t* perm, int inc_c_len, const int64_t* inc_c, float* c,
+                     int64_t offset_c, int64_t len_c, int n_dev, const int32_t* devices,
+                     int32_t* err_codes, int64_t* err_info, int max_errs) {
+  if (n_dev < 1) {
+    t_last_error = "n_dev < 1";
+    return GETT_E_INVALID_ARG;
+  }
+  return gett_impl<float>(true, rank_a, ext_a, inc_a, a, offset_a, len_a, rank_b, ext_b, inc_b, b,
+                          offset_b, len_b, conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c,
+                          c, offset_c, len_c, nullptr, err_codes, err_info, max_errs, n_dev, devices);
+}
+
+int gett_set_devices(int n_dev, const int32_t* devices) {
+  std::vector<int> v;
+  if (n_dev < 0 || (n_dev > 0 && !devices)) return GETT_E_INVALID_ARG;
+  if (n_dev > 0) {
+    for (int i = 0; i < n_dev; ++i) {
+      if (devices[i] < 0 || devices[i] >= kMaxDevices) return GETT_E_INVALID_ARG;
+      v.push_back(devices[i]);
+    }
+  }
+  std::lock_guard<std::mutex> lk(g_plan_mu);
+  g_devices.swap(v);
+  return 0;
+}
+
+int gett_set_multi(int strategy) {
+  if (strategy < 0 || (strategy & 3) == 3 || strategy > 7) return GETT_E_INVALID_ARG;
+  g_multi_force = strategy & 3;
+  g_multi_stage = (strategy & 4) != 0;
+  return 0;
+}
+
+const char* gett_last_multi(void) { return t_last_multi; }
 
 #define GETT_COMPLEX_ENTRY(NAME, R, HOST, STREAM_PARAM, STREAM_ARG)                              \
   int NAME(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const R* a, int64_t offset_a,   \
@@ -1523,30 +2013,38 @@ const char* gett_last_error(void) { return t_last_error.c_str(); }
 int64_t gett_launch_count(void) { return g_launches; }
 
 void gett_release_caches(void) {
-  std::lock_guard<std::mutex> lock(g_mu);
-  g_plans.map.clear();
-  g_plans.lru.clear();
-  g_last.dp.reset();
-  g_last.key.clear();
-  for (auto& kv : g_dev) {
-    int cur;
-    cudaGetDevice(&cur);
-    cudaSetDevice(kv.first);
-    cudaDeviceSynchronize();  // kernels may still use the workspaces
-    for (Scratch* s : {&kv.second.a, &kv.second.b, &kv.second.c})
-      if (s->p) {
-        cudaFree(s->p);
-        s->p = nullptr;
-        s->bytes = 0;
-      }
-    for (auto& sv : kv.second.sws)
-      for (Scratch* s : {&sv.second.ws, &sv.second.part, &sv.second.flags})
-        if (s->p) cudaFree(s->p);
-    kv.second.sws.clear();
-    cudaSetDevice(cur);
+  {
+    std::lock_guard<std::mutex> lock(g_plan_mu);
+    g_plans.map.clear();
+    g_plans.lru.clear();
+    g_last.dp.reset();
+    g_last.key.clear();
   }
+  int cur = -1;
+  cudaGetDevice(&cur);
+  for (int d = 0; d < kMaxDevices; ++d) {
+    DevState& ds = g_dev[d];
+    std::lock_guard<std::mutex> lk(ds.mu);
+    if (ds.lanes.empty() && ds.sws.empty()) continue;
+    cudaSetDevice(d);
+    cudaDeviceSynchronize();  // kernels may still use the workspaces
+    for (auto& L : ds.lanes)
+      for (Scratch* s : {&L->a, &L->b, &L->c, &L->red})
+        if (s->p) {
+          cudaFree(s->p);
+          s->p = nullptr;
+          s->bytes = 0;
+        }
+    for (auto& sv : ds.sws)
+      for (Scratch* s : {&sv.second.ws, &sv.second.part, &sv.second.flags, &sv.second.cx})
+        if (s->p) cudaFree(s->p);
+    ds.sws.clear();
+  }
+  if (cur >= 0) cudaSetDevice(cur);
 }
 
-int gett_abi_version(void) { return 103; }  // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed
+// 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed;
+// 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi
+int gett_abi_version(void) { return 104; }
 
 }  // extern "C"

@@ -8,15 +8,17 @@
 namespace gett {
 
 // cudaFuncSetAttribute is per device: opt a kernel into `bytes` of dynamic
-// shared memory once per device (bit d of `mask`; callers hold the API lock).
+// shared memory once per device (bit d of `mask`).  Calls on different devices
+// may run concurrently (per-device API locks), so the mask is read and set
+// atomically; a race only repeats the (idempotent) attribute call.
 template <class Kern>
 inline cudaError_t ensure_dyn_smem(Kern k, int bytes, unsigned long long& mask) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
-  if (dev < 64 && ((mask >> dev) & 1ull)) return cudaSuccess;
+  if (dev < 64 && ((__atomic_load_n(&mask, __ATOMIC_ACQUIRE) >> dev) & 1ull)) return cudaSuccess;
   e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess && dev < 64) mask |= 1ull << dev;
+  if (e == cudaSuccess && dev < 64) __atomic_fetch_or(&mask, 1ull << dev, __ATOMIC_RELEASE);
   return e;
 }
 

@@ -751,6 +751,17 @@ __global__ void __launch_bounds__(256) gett_zero_kernel(T* base, const __grid_co
     base[g.off(0, (int32_t)i)] = T(0);
 }
 
+template <typename T>
+__global__ void __launch_bounds__(256) gett_accum_view_kernel(const __grid_constant__ AccumParams<T> p) {
+  int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.g.G; i += stride) {
+    const int64_t o = p.g.off(0, (int32_t)i);
+    T s = __ldcv(p.P[0] + o);  // volatile: peer memory written by another device's kernel
+    for (int j = 1; j < p.n; ++j) s = s + __ldcv(p.P[j] + o);
+    p.C[o] = p.C[o] + s;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 
@@ -907,6 +918,18 @@ cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s) {
   gett_zero_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(base, g);
   return cudaGetLastError();
 }
+
+template <typename T>
+cudaError_t launch_accum(const AccumParams<T>& p, cudaStream_t s) {
+  if (p.n < 1) return cudaSuccess;
+  int64_t blocks = (p.g.G + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (blocks < 1) blocks = 1;
+  gett_accum_view_kernel<T><<<(unsigned)blocks, 256, 0, s>>>(p);
+  return cudaGetLastError();
+}
+template cudaError_t launch_accum<double>(const AccumParams<double>&, cudaStream_t);
+template cudaError_t launch_accum<float>(const AccumParams<float>&, cudaStream_t);
 
 int tiled_bm() { return tiled::BM; }
 int tiled_bn() { return tiled::BN; }

@@ -22,6 +22,20 @@ constexpr int kDotStagedMaxK = 4096;
 template <typename T>
 cudaError_t launch_zero(T* base, const GroupDev& g, cudaStream_t s);
 
+// Multi-device split-K reduce: for every element of the C view (folded as
+// one group, g.T[0] / g.s_in[0]), C[o] = C[o] + (P[0][o] + ... + P[n-1][o]) in
+// that order.  The partial pointers may be peer-device memory (NVLink loads).
+constexpr int kMaxParts = 63;
+template <typename T>
+struct AccumParams {
+  T* C;
+  const T* P[kMaxParts];
+  int n;
+  GroupDev g;
+};
+template <typename T>
+cudaError_t launch_accum(const AccumParams<T>& p, cudaStream_t s);
+
 template <typename T>
 cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s);
 

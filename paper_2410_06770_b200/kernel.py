@@ -33,8 +33,11 @@ _PREFIX_DTYPE = {
 _ENTRY = {"s": "gett_sgett", "d": "gett_dgett", "c": "gett_cgett", "z": "gett_zgett"}
 
 
+_MULTI = {"s": "gett_sgett_multi", "d": "gett_dgett_multi"}
+
+
 def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm,
-          inc_c, c, offset_a, offset_b, offset_c):
+          inc_c, c, offset_a, offset_b, offset_c, devices=None):
     dtype = _PREFIX_DTYPE[prefix]
     if not isinstance(c, np.ndarray):
         raise TypeError("c must be a numpy array (results are written in place)")
@@ -66,10 +69,18 @@ def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_
         raise ValueError("assignment destination is read-only")
     cap = pr.cap
     codes, info = err_buffers(cap)
-    rc = getattr(_native.LIB, _ENTRY[prefix])(
-        *pr.args_a, a.ctypes.data, a_view.base_offset, a_view.buffer_len,
-        *pr.args_b, b.ctypes.data, b_view.base_offset, b_view.buffer_len,
-        *pr.args_spec, cw.ctypes.data, int(offset_c), cw.shape[0], codes, info, cap)
+    args = (*pr.args_a, a.ctypes.data, a_view.base_offset, a_view.buffer_len,
+            *pr.args_b, b.ctypes.data, b_view.base_offset, b_view.buffer_len,
+            *pr.args_spec, cw.ctypes.data, int(offset_c), cw.shape[0])
+    if devices is not None:
+        if prefix not in _MULTI:
+            raise TypeError(f"{prefix}gett has no multi-device form")
+        devs = [int(d) for d in devices]
+        if not devs:
+            raise ValueError("devices must list at least one CUDA device")
+        rc = getattr(_native.LIB, _MULTI[prefix])(*args, len(devs), _native.i32(devs), codes, info, cap)
+    else:
+        rc = getattr(_native.LIB, _ENTRY[prefix])(*args, codes, info, cap)
     n = _native.check(rc, prefix + "gett")
     if n:
         return decode_errors(min(n, cap), codes, info, a_view.rank, a_view.extents, b_view.rank,
@@ -81,15 +92,15 @@ def _gett(prefix, rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_
 
 def sgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
           conts, cont_a, cont_b, perm, inc_c, c,
-          offset_a=0, offset_b=0, offset_c=0):
+          offset_a=0, offset_b=0, offset_c=0, *, devices=None):
     """32-bit real contraction; see dgett for the parameter contract."""
     return _gett("s", rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
-                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
+                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c, devices)
 
 
 def dgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
           conts, cont_a, cont_b, perm, inc_c, c,
-          offset_a=0, offset_b=0, offset_c=0):
+          offset_a=0, offset_b=0, offset_c=0, *, devices=None):
     """64-bit real binary tensor contraction, accumulating into c.
 
     Arguments follow the xGETT interface order: A's rank,
@@ -99,9 +110,15 @@ def dgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
     element.  Returns [] when the contraction ran, else the validation error
     list (c untouched).  C is accumulated: clear the view first (zero_view)
     for a plain contraction.
+
+    devices (keyword, beyond the reference signature): run the call across
+    these CUDA devices — C's outermost free mode split into one slab per
+    device, or the largest contracted pair split with one reduce on
+    devices[0] when the free extents are too small (include/gett_b200.h,
+    gett_dgett_multi).  set_devices() makes a list the default.
     """
     return _gett("d", rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,
-                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c)
+                 conts, cont_a, cont_b, perm, inc_c, c, offset_a, offset_b, offset_c, devices)
 
 
 def cgett(rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b,

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert _native.LIB.gett_abi_version() == 103
+    assert _native.LIB.gett_abi_version() == 104
 
 
 @pytest.mark.parametrize("case", load_validation(), ids=lambda c: c["label"])
@@ -97,6 +97,39 @@ def test_empty_iteration_writes_nothing_without_device():
     errs = g.dgett(1, (0,), (1,), np.array([1.0]), 1, (1,), (1,), np.array([2.0]),
                    0, (), (), (0, 1), (1, 1), c)
     assert errs == [] and np.all(c == 3.0)
+
+
+def test_multi_device_call_validates_without_device():
+    """gett_dgett_multi validates (and returns the empty-space early exit)
+    before touching any device, exactly like the one-device entry."""
+    a, b, c = np.ones(6), np.ones(6), np.zeros(4)
+    args = (2, (2, 3), (3, 1), a, 2, (2, 3), (3, 1), b, 1, (1,), (0,), (0, 1), (2, 1), c)
+    want = g.dgett(*args)
+    got = g.dgett(*args, devices=(0, 1, 0))
+    assert want and [(e.code, e.message) for e in got] == [(e.code, e.message) for e in want]
+    c = np.full(4, 3.0)
+    assert g.dgett(1, (0,), (1,), np.array([1.0]), 1, (1,), (1,), np.array([2.0]),
+                   0, (), (), (0, 1), (1, 1), c, devices=(0, 1)) == [] and np.all(c == 3.0)
+    with pytest.raises(ValueError):
+        g.dgett(*args, devices=())
+    with pytest.raises(TypeError):
+        g.zgett(1, (1,), (1,), np.ones(1, np.complex128), 1, (1,), (1,), np.ones(1, np.complex128),
+                1, (0,), (0,), (), (), np.zeros(1, np.complex128), devices=(0,))
+
+
+def test_multi_device_setters():
+    from paper_2410_06770_b200 import _native
+
+    assert _native.LIB.gett_set_multi(3) == _native.E_INVALID_ARG
+    assert _native.LIB.gett_set_multi(-1) == _native.E_INVALID_ARG
+    assert _native.LIB.gett_set_devices(1, _native.i32([-1])) == _native.E_INVALID_ARG
+    for s in ("auto", "slabs", "splitk"):
+        g.set_multi(s)
+    g.set_multi("splitk", staged=True)
+    g.set_multi("auto")
+    g.set_devices((0, 0))
+    g.set_devices(None)
+    assert g.last_multi() == "none"
 
 
 def test_derive_output_extents():
