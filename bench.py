@@ -86,9 +86,24 @@ def config_obj(n):
 
 
 def shard(world, rank):
-    rows = C2.ext_a[0]
-    lo, hi = rows * rank // world, rows * (rank + 1) // world
-    return C2.slice_free("A", 0, lo, hi), hi - lo
+    """This rank's slab of c2 on the native multi-device schedule
+    (gett_multi_schedule: the partition one gett_dgett_multi call runs)."""
+    if world == 1:
+        return C2, C2.ext_a[0]
+    from paper_2410_06770_b200.shard import schedule
+
+    class _Len:
+        def __init__(self, n):
+            self.n = n
+
+        def __len__(self):
+            return self.n
+
+    pos, kw = C2.args(_Len(C2.len_a), _Len(C2.len_b), _Len(C2.len_c))
+    s = schedule(pos, kw, world)
+    assert s.strategy == "slabs", s
+    lo, hi = s.range(rank)
+    return C2.slice_free(s.owner, s.dim, lo, hi), hi - lo
 
 
 class ClockSampler:

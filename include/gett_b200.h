@@ -175,6 +175,28 @@ int gett_set_multi(int strategy);
  * ran on one device), e.g. "slabs x2 (...)", "split-K x2 (pair 2, peer-load reduce)". */
 const char* gett_last_multi(void);
 
+/* The multi-device schedule gett_{d,s}gett_multi would run for this call on
+ * n_dev devices, computed on the host (no CUDA) — also the partition a
+ * one-process-per-GPU launcher (torchrun) gives its ranks.  strategy: 0 =
+ * automatic, 1 = slabs, 2 = split-K when the call allows it (as
+ * gett_set_multi, for this query only).  sched receives
+ * 4 + 2*n_dev int64:
+ *   [0] strategy: 0 = one device, 1 = slabs, 2 = split-K
+ *   [1] lanes used (n <= n_dev; lane i is devices[i])
+ *   [2] slabs: the operand owning the cut mode (0 = A, 1 = B); else -1
+ *   [3] slabs: that operand's dimension; split-K: the contracted pair; else -1
+ *   [4 + 2i], [5 + 2i]: lane i's range [lo, hi) of that dimension / pair.
+ * Returns the validation error count (> 0: sched untouched) or a negative
+ * status.  Replaces: shard.py's Python mode choice (round 1). */
+int gett_multi_schedule(int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
+                        int64_t len_a,
+                        int rank_b, const int64_t* ext_b, const int64_t* inc_b, int64_t offset_b,
+                        int64_t len_b,
+                        int conts, const int64_t* cont_a, const int64_t* cont_b,
+                        int perm_len, const int64_t* perm, int inc_c_len, const int64_t* inc_c,
+                        int64_t offset_c, int64_t len_c, int n_dev, int strategy,
+                        int64_t* sched, int32_t* err_codes, int64_t* err_info, int max_errs);
+
 /* ---- complex xGETT: cgett / zgett (kernel.py:187-200) ----
  * Buffers are interleaved (re, im) pairs (numpy complex64 / complex128 memory);
  * offsets, lengths and increments count complex elements.  Products follow the

@@ -21,6 +21,7 @@ EXPORTS = (
     "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
     "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
+    "gett_multi_schedule",
 )
 
 ERR_INFO_WORDS = 6
@@ -56,6 +57,12 @@ def _load():
         f = getattr(lib, name)
         f.restype = ctypes.c_int
         f.argtypes = gett_args + [ctypes.c_int, i32p, i32p, i64p, ctypes.c_int]
+    lib.gett_multi_schedule.restype = ctypes.c_int
+    lib.gett_multi_schedule.argtypes = [
+        ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        ctypes.c_int, i64p, i64p, ctypes.c_int, i64p, ctypes.c_int, i64p,
+        ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i32p, i64p, ctypes.c_int]
     lib.gett_set_devices.restype = ctypes.c_int
     lib.gett_set_devices.argtypes = [ctypes.c_int, i32p]
     lib.gett_set_multi.restype = ctypes.c_int

@@ -1109,6 +1109,63 @@ struct LaneRef {
 int g_multi_force = 0;  // 0 auto, 1 slabs, 2 split-K (gett_set_multi; tests)
 thread_local char t_last_multi[96] = "none";
 
+// The multi-device schedule of a validated, non-empty call on n lanes —
+// host-only (no CUDA), shared by the in-call multi-device path and by
+// gett_multi_schedule (the torchrun per-rank partition, shard.py).
+struct MultiSched {
+  int strategy = 0;  // 0 one device, 1 slabs, 2 split-K
+  int n = 1;         // lanes used
+  SlabCut cut;       // slabs
+  int pair = -1;     // split-K: contracted pair split
+  std::vector<int64_t> lo, hi;  // per lane: rows of the cut mode / range of the pair
+};
+
+MultiSched multi_schedule(const Plan& p, const View& a, const View& b, const Spec& s, int n_in,
+                          int force) {
+  MultiSched m;
+  int n = std::min(n_in, kMaxParts + 1);
+  if (n < 2 || p.c_may_alias || p.size_free == 0 || p.size_cont == 0) return m;
+  const double macs = (double)p.size_free * (double)p.size_cont;
+  const int64_t tiles = ((p.gm.G + 127) / 128) * ((p.gn.G + 127) / 128);
+  SlabCut cut;
+  const bool can_slab = slab_cut(p, a, b, s, &cut) && cut.E >= 2 &&
+                        (cut.owner_disjoint || force == 1);
+  int pair = -1;
+  for (int k = 0; k < s.conts; ++k)
+    if (a.ext[s.cont_a[k]] >= 2 && (pair < 0 || a.ext[s.cont_a[k]] > a.ext[s.cont_a[pair]])) pair = k;
+  int strategy = 0;
+  if (force == 1) strategy = can_slab ? 1 : 0;
+  else if (force == 2) strategy = pair >= 0 ? 2 : 0;
+  else if (macs >= (double)n * (1 << 27)) {
+    if (can_slab && tiles >= 74 * n) strategy = 1;  // every device gets >= half a wave of tiles
+    else if (pair >= 0 && p.size_cont >= 256 * n) strategy = 2;
+    else if (can_slab) strategy = 1;
+  }
+  if (strategy == 0) return m;
+  m.strategy = strategy;
+  if (strategy == 1) {
+    if (n > cut.E) n = (int)cut.E;
+    m.cut = cut;
+    // row ranges: granules of 128 rows when every device gets at least one
+    const int64_t g = cut.E >= 128 * n ? 128 : 1;
+    const int64_t units = (cut.E + g - 1) / g;
+    for (int i = 0; i < n; ++i) {
+      m.lo.push_back(std::min(cut.E, units * i / n * g));
+      m.hi.push_back(i + 1 == n ? cut.E : std::min(cut.E, units * (i + 1) / n * g));
+    }
+  } else {
+    const int64_t Ek = a.ext[s.cont_a[pair]];
+    if (n > Ek) n = (int)Ek;
+    m.pair = pair;
+    for (int i = 0; i < n; ++i) {
+      m.lo.push_back(Ek * i / n);
+      m.hi.push_back(Ek * (i + 1) / n);
+    }
+  }
+  m.n = n;
+  return m;
+}
+
 // Put the span [lo, lo + n) of host buffer h at base[i] + lo on every lane:
 // lane j uploads chunk j over its own PCIe link, then every lane pulls the
 // other chunks from their lanes (cudaMemcpyPeerAsync over NVLink; a plain
@@ -1147,20 +1204,15 @@ int replicate_span(std::vector<LaneRef>& lanes, const std::vector<T*>& base, con
 }
 
 template <typename T>
-int multi_slabs(std::vector<LaneRef>& lanes, const SlabCut& cut, const View& a, const View& b,
+int multi_slabs(std::vector<LaneRef>& lanes, const MultiSched& m, const View& a, const View& b,
                 const Spec& s, const Plan& p, const T* ha, const T* hb, T* hc, int64_t off_c,
                 int64_t len_c) {
   const int n = (int)lanes.size();
+  const SlabCut& cut = m.cut;
   const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
   const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
   const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
   const int64_t lo_a = a.off + p.fp_lo[0], lo_b = b.off + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
-  // row ranges: granules of 128 rows when every device gets at least one
-  const int64_t g = cut.E >= 128 * n ? 128 : 1;
-  const int64_t units = (cut.E + g - 1) / g;
-  std::vector<int64_t> rb(n + 1);
-  for (int i = 0; i <= n; ++i) rb[i] = std::min(cut.E, units * i / n * g);
-  rb[n] = cut.E;
   std::vector<T*> ba(n), bb(n), bc(n);
   int rc;
   for (int i = 0; i < n; ++i) {
@@ -1179,14 +1231,15 @@ int multi_slabs(std::vector<LaneRef>& lanes, const SlabCut& cut, const View& a, 
   if (rc) return rc;
   // each lane's rows, pipelined over its own copy streams
   for (int i = 0; i < n; ++i) {
-    if (rb[i + 1] == rb[i]) continue;
+    const int64_t r0 = m.lo[i], r1 = m.hi[i];
+    if (r1 == r0) continue;
     CK(cudaSetDevice(lanes[i].dev));
-    const size_t lane_bytes = (size_t)((double)(na + 2 * nc) * (rb[i + 1] - rb[i]) / cut.E) * sizeof(T);
+    const size_t lane_bytes = (size_t)((double)(na + 2 * nc) * (r1 - r0) / cut.E) * sizeof(T);
     int64_t S = g_pipeline_slabs > 1 ? g_pipeline_slabs : (int64_t)std::min<size_t>(10, 1 + lane_bytes / (8u << 20));
     if (g_pipeline_slabs == 0 || g_pipeline_slabs == 1) S = 1;
-    if (S > rb[i + 1] - rb[i]) S = rb[i + 1] - rb[i];
+    if (S > r1 - r0) S = r1 - r0;
     rc = issue_slabs<T>(*lanes[i].L, g_dev[lanes[i].dev], cut, a, b, s, p, ha, hb, hc, off_c, len_c,
-                        rb[i], rb[i + 1], S, ba[i], bb[i], bc[i], 1);
+                        r0, r1, S, ba[i], bb[i], bc[i], 1);
     if (rc) return rc;
   }
   for (int i = 0; i < n; ++i) {
@@ -1201,11 +1254,12 @@ int multi_slabs(std::vector<LaneRef>& lanes, const SlabCut& cut, const View& a, 
 }
 
 template <typename T>
-int multi_splitk(std::vector<LaneRef>& lanes, int pair, const View& a, const View& b, const Spec& s,
-                 const Plan& p, const T* ha, const T* hb, T* hc, int64_t off_c, int64_t len_c) {
+int multi_splitk(std::vector<LaneRef>& lanes, const MultiSched& m, const View& a, const View& b,
+                 const Spec& s, const Plan& p, const T* ha, const T* hb, T* hc, int64_t off_c,
+                 int64_t len_c) {
   const int n = (int)lanes.size();
+  const int pair = m.pair;
   const int da = (int)s.cont_a[pair], db = (int)s.cont_b[pair];
-  const int64_t Ek = a.ext[da];
   const size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
   const size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
   const size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
@@ -1230,7 +1284,7 @@ int multi_splitk(std::vector<LaneRef>& lanes, int pair, const View& a, const Vie
   for (int i = 0; i < n; ++i) {
     CK(cudaSetDevice(lanes[i].dev));
     Lane& L = *lanes[i].L;
-    const int64_t k0 = Ek * i / n, k1 = Ek * (i + 1) / n;
+    const int64_t k0 = m.lo[i], k1 = m.hi[i];
     std::vector<int64_t> ea(a.ext, a.ext + a.rank), eb(b.ext, b.ext + b.rank);
     ea[da] = k1 - k0;
     eb[db] = k1 - k0;
@@ -1294,27 +1348,9 @@ int multi_splitk(std::vector<LaneRef>& lanes, int pair, const View& a, const Vie
 template <typename T>
 int host_multi(const Plan& p, const View& a, const View& b, const Spec& s, const T* ha,
                const T* hb, T* hc, int64_t off_c, int64_t len_c, const std::vector<int>& devs) {
-  int n = std::min((int)devs.size(), kMaxParts + 1);
-  if (n < 2 || p.c_may_alias) return kNotPipelined;
-  const double macs = (double)p.size_free * (double)p.size_cont;
-  const int64_t tiles = ((p.gm.G + 127) / 128) * ((p.gn.G + 127) / 128);
-  SlabCut cut;
-  const bool can_slab = slab_cut(p, a, b, s, &cut) && cut.E >= 2 &&
-                        (cut.owner_disjoint || g_multi_force == 1);
-  int pair = -1;
-  for (int k = 0; k < s.conts; ++k)
-    if (a.ext[s.cont_a[k]] >= 2 && (pair < 0 || a.ext[s.cont_a[k]] > a.ext[s.cont_a[pair]])) pair = k;
-  int strategy = 0;  // 1 slabs, 2 split-K
-  if (g_multi_force == 1) strategy = can_slab ? 1 : 0;
-  else if (g_multi_force == 2) strategy = pair >= 0 ? 2 : 0;
-  else if (macs >= (double)n * (1 << 27)) {
-    if (can_slab && tiles >= 74 * n) strategy = 1;  // every device gets >= half a wave of tiles
-    else if (pair >= 0 && p.size_cont >= 256 * n) strategy = 2;
-    else if (can_slab) strategy = 1;
-  }
-  if (strategy == 0) return kNotPipelined;
-  if (strategy == 1 && n > cut.E) n = (int)cut.E;
-  if (strategy == 2 && n > a.ext[s.cont_a[pair]]) n = (int)a.ext[s.cont_a[pair]];
+  const MultiSched m = multi_schedule(p, a, b, s, (int)devs.size(), g_multi_force);
+  if (m.strategy == 0) return kNotPipelined;
+  const int n = m.n;
   // lock the distinct devices in ascending order, then take lanes
   std::vector<int> order(devs.begin(), devs.begin() + n);
   std::sort(order.begin(), order.end());
@@ -1329,8 +1365,8 @@ int host_multi(const Plan& p, const View& a, const View& b, const Spec& s, const
     lanes[i].dev = devs[i];
     if ((rc = get_lane(devs[i], (size_t)used[devs[i]]++, &lanes[i].L))) return rc;
   }
-  return strategy == 1 ? multi_slabs<T>(lanes, cut, a, b, s, p, ha, hb, hc, off_c, len_c)
-                       : multi_splitk<T>(lanes, pair, a, b, s, p, ha, hb, hc, off_c, len_c);
+  return m.strategy == 1 ? multi_slabs<T>(lanes, m, a, b, s, p, ha, hb, hc, off_c, len_c)
+                         : multi_splitk<T>(lanes, m, a, b, s, p, ha, hb, hc, off_c, len_c);
 }
 
 int fill_errors(const std::vector<Error>& errs, int32_t* codes, int64_t* info, int max_errs) {
@@ -1879,6 +1915,49 @@ int gett_set_multi(int strategy) {
 }
 
 const char* gett_last_multi(void) { return t_last_multi; }
+
+int gett_multi_schedule(int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
+                        int64_t len_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,
+                        int64_t offset_b, int64_t len_b, int conts, const int64_t* cont_a,
+                        const int64_t* cont_b, int perm_len, const int64_t* perm, int inc_c_len,
+                        const int64_t* inc_c, int64_t offset_c, int64_t len_c, int n_dev,
+                        int strategy, int64_t* sched, int32_t* err_codes, int64_t* err_info,
+                        int max_errs) {
+  if (rank_a < 0 || rank_b < 0 || conts < 0 || perm_len < 0 || inc_c_len < 0 || n_dev < 1 || !sched ||
+      strategy < 0 || strategy > 2) {
+    t_last_error = "bad gett_multi_schedule arguments";
+    return GETT_E_INVALID_ARG;
+  }
+  read_env();
+  View va{rank_a, ext_a, inc_a, offset_a, len_a};
+  View vb{rank_b, ext_b, inc_b, offset_b, len_b};
+  Spec sp{conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c};
+  View vc{0, nullptr, nullptr, offset_c, len_c};
+  std::vector<Error> errs = validate(va, vb, sp, CMode::Derived, vc);
+  if (!errs.empty()) return fill_errors(errs, err_codes, err_info, max_errs);
+  for (int i = 0; i < 4 + 2 * n_dev; ++i) sched[i] = 0;
+  sched[1] = 1;
+  sched[2] = sched[3] = -1;
+  for (int d = 0; d < rank_a; ++d)
+    if (ext_a[d] == 0) return 0;
+  for (int d = 0; d < rank_b; ++d)
+    if (ext_b[d] == 0) return 0;
+  const Plan p = build_plan(va, vb, sp, offset_c, len_c);
+  const MultiSched m = multi_schedule(p, va, vb, sp, n_dev, strategy);
+  sched[0] = m.strategy;
+  sched[1] = m.n;
+  if (m.strategy == 1) {
+    sched[2] = m.cut.owner;
+    sched[3] = m.cut.dim;
+  } else if (m.strategy == 2) {
+    sched[3] = m.pair;
+  }
+  for (size_t i = 0; i < m.lo.size(); ++i) {
+    sched[4 + 2 * i] = m.lo[i];
+    sched[5 + 2 * i] = m.hi[i];
+  }
+  return 0;
+}
 
 #define GETT_COMPLEX_ENTRY(NAME, R, HOST, STREAM_PARAM, STREAM_ARG)                              \
   int NAME(int rank_a, const int64_t* ext_a, const int64_t* inc_a, const R* a, int64_t offset_a,   \

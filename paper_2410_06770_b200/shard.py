@@ -1,77 +1,109 @@
-"""Multi-GPU partitioning of one xGETT by a free mode.
+"""Multi-rank partitioning of one xGETT for one-process-per-GPU launchers
+(torchrun), on the NATIVE multi-device schedule.
 
-xGETT is closed under slicing a free mode: restricting free dimension `dim` of
-the owning operand to [lo, hi) shifts that operand's offset by lo·inc and C's
-offset by lo·inc_c[perm[i]] and shrinks one extent — the slice is itself a valid
-xGETT whose result is bitwise equal to the same elements of the full call (each
-output element's K loop is untouched).  Ranks therefore run independent slabs
-with no data-path collective.
+The partition is the one the in-call multi-device path runs
+(gett_dgett_multi, include/gett_b200.h): ``schedule()`` asks the native
+planner (gett_multi_schedule — validation, mode choice and ranges, no CUDA)
+and the helpers here only rewrite arguments:
 
-Mode choice: a free mode of the larger operand (the one not replicated), the
-largest extent first, preferring extents divisible by the world size — e.g. c3
-shards A's mode 0 (256) rather than the largest mode of C (384, owned by the small
-B), which would replicate the 268 MB A (SURVEY §8e note).
+* slabs — xGETT is closed under slicing a free mode: restricting dimension
+  `dim` of the owning operand to [lo, hi) shifts that operand's offset by
+  lo·inc and C's by lo·inc_c[perm[i]]; each rank runs its slab, no collective.
+  Calls writing disjoint C footprints may run concurrently.
+* split-K — the contraction is linear in each contracted pair: restricting
+  pair p to [lo, hi) in BOTH A and B yields the partial sum over that K
+  slice.  Every rank writes its partial into a zeroed, packed buffer; one
+  sum-reduce (NCCL for device buffers) lands ΣP on the owner, which alone adds
+  it into C (C₀ is added exactly once).  The add is itself an xGETT with no
+  contracted mode (C ← P·1 + C, K = 1).  Results equal the one-call result
+  within the K-normalised tolerance (the K sum is reassociated).
 """
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
+
+from . import _native
+
+_STRATEGY = {"auto": 0, "slabs": 1, "splitk": 2}
 
 
 @dataclass(frozen=True)
-class ShardSpec:
-    owner: str  # "A" or "B"
-    dim: int    # dimension of the owner being split
-    extent: int
+class Schedule:
+    strategy: str          # "one" (one device / rank 0 alone), "slabs", "splitk"
+    n: int                 # ranks used (ranks >= n get empty work)
+    owner: str | None      # slabs: "A" or "B", the operand whose mode is cut
+    dim: int               # slabs: that operand's dimension; split-K: the pair index
+    ranges: tuple          # per used rank: (lo, hi) of that dimension / pair
+
+    def range(self, rank: int):
+        return self.ranges[rank] if rank < self.n else (0, 0)
+
+
+def _len(buf):
+    return int(buf.shape[0]) if hasattr(buf, "shape") else len(buf)
+
+
+def schedule(args, kw, world: int, strategy: str = "auto"):
+    """The native multi-device schedule of xGETT arguments (reference order,
+    kernel.py:158-184) over `world` ranks, or the full call's ValidationError
+    list when it is invalid (every rank computes the same answer, so all ranks
+    return the errors with C untouched).  Needs no GPU."""
+    from .plan import decode_errors, error_capacity
+    from .layout import TensorView
+    from .plan import ContractionSpec
+
+    (rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm, inc_c, c) = args
+    av = TensorView(rank_a, ext_a, inc_a, kw.get("offset_a", 0), _len(a))
+    bv = TensorView(rank_b, ext_b, inc_b, kw.get("offset_b", 0), _len(b))
+    spec = ContractionSpec(conts, cont_a, cont_b, perm)
+    inc_c = tuple(int(i) for i in inc_c)
+    i64 = _native.i64
+    cap = error_capacity(av.rank, bv.rank, spec.conts) + 8
+    codes = (ctypes.c_int32 * cap)()
+    info = (ctypes.c_int64 * (cap * _native.ERR_INFO_WORDS))()
+    out = (ctypes.c_int64 * (4 + 2 * world))()
+    n = _native.LIB.gett_multi_schedule(
+        av.rank, i64(av.extents), i64(av.increments), av.base_offset, av.buffer_len,
+        bv.rank, i64(bv.extents), i64(bv.increments), bv.base_offset, bv.buffer_len,
+        spec.conts, i64(spec.cont_a), i64(spec.cont_b), len(spec.perm), i64(spec.perm),
+        len(inc_c), i64(inc_c), int(kw.get("offset_c", 0)), _len(c), int(world),
+        _STRATEGY[strategy], out, codes, info, cap)
+    _native.check(n, "multi_schedule")
+    if n:
+        return decode_errors(min(n, cap), codes, info, av.rank, av.extents, bv.rank, bv.extents,
+                             spec, inc_c)
+    kind = {0: "one", 1: "slabs", 2: "splitk"}[int(out[0])]
+    used = int(out[1])
+    ranges = tuple((int(out[4 + 2 * i]), int(out[5 + 2 * i])) for i in range(used)) if kind != "one" else ()
+    owner = {0: "A", 1: "B"}.get(int(out[2])) if kind == "slabs" else None
+    return Schedule(kind, used, owner, int(out[3]), ranges)
 
 
 def _free(rank, cont):
     return [d for d in range(rank) if d not in set(cont)]
 
 
-def choose_mode(ext_a, ext_b, cont_a, cont_b, world: int) -> ShardSpec | None:
-    """Pick the free mode to split across `world` ranks (None: nothing to split)."""
-    size_a = 1
-    for e in ext_a:
-        size_a *= int(e)
-    size_b = 1
-    for e in ext_b:
-        size_b *= int(e)
-    order = [("A", ext_a, cont_a), ("B", ext_b, cont_b)]
-    if size_b > size_a:
-        order.reverse()
-    for owner, ext, cont in order:
-        free = _free(len(ext), cont)
-        if not free:
-            continue
-        best = max(free, key=lambda d: (int(ext[d]) >= world, int(ext[d]) % world == 0, int(ext[d])))
-        if int(ext[best]) >= 1:
-            return ShardSpec(owner, best, int(ext[best]))
-    return None
-
-
-def bounds(extent: int, rank: int, world: int):
-    """Contiguous, balanced [lo, hi) slab of `extent` for `rank`."""
-    return extent * rank // world, extent * (rank + 1) // world
-
-
-def shard_call(args, kw, spec: ShardSpec, rank: int, world: int):
-    """Positional/keyword xGETT arguments (reference order, kernel.py:158-184)
-    restricted to this rank's slab.  Returns (args, kw, lo, hi); an empty slab
-    has a zero extent (the call then writes nothing, kernel.py:93-94)."""
+def shard_call(args, kw, sched: Schedule, rank: int):
+    """xGETT arguments restricted to `rank`'s slab of a "slabs" schedule.
+    Returns (args, kw, lo, hi); an empty slab has a zero extent (the call
+    then writes nothing, kernel.py:93-94)."""
+    assert sched.strategy == "slabs"
     (rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm, inc_c, c) = args
     kw = dict(kw)
-    lo, hi = bounds(spec.extent, rank, world)
-    if spec.owner == "A":
-        fi = _free(rank_a, cont_a).index(spec.dim)
+    lo, hi = sched.range(rank)
+    dim = sched.dim
+    if sched.owner == "A":
+        fi = _free(rank_a, cont_a).index(dim)
         ext = list(ext_a)
-        ext[spec.dim] = hi - lo
-        kw["offset_a"] = kw.get("offset_a", 0) + (lo * inc_a[spec.dim] if hi > lo else 0)
+        ext[dim] = hi - lo
+        kw["offset_a"] = kw.get("offset_a", 0) + (lo * inc_a[dim] if hi > lo else 0)
         ext_a = tuple(ext)
     else:
-        fi = len(_free(rank_a, cont_a)) + _free(rank_b, cont_b).index(spec.dim)
+        fi = len(_free(rank_a, cont_a)) + _free(rank_b, cont_b).index(dim)
         ext = list(ext_b)
-        ext[spec.dim] = hi - lo
-        kw["offset_b"] = kw.get("offset_b", 0) + (lo * inc_b[spec.dim] if hi > lo else 0)
+        ext[dim] = hi - lo
+        kw["offset_b"] = kw.get("offset_b", 0) + (lo * inc_b[dim] if hi > lo else 0)
         ext_b = tuple(ext)
     q = perm[fi]
     kw["offset_c"] = kw.get("offset_c", 0) + (lo * inc_c[q] if hi > lo else 0)
@@ -79,36 +111,9 @@ def shard_call(args, kw, spec: ShardSpec, rank: int, world: int):
             kw, lo, hi)
 
 
-# ---------------------------------------------------------------------------
-# Reduction-parallel split-K across ranks (c5).
-#
-# A contraction is linear in each contracted pair: restricting pair p to
-# [lo, hi) in BOTH A (dim cont_a[p]) and B (dim cont_b[p]) shifts offset_a by
-# lo·inc_a[cont_a[p]] and offset_b by lo·inc_b[cont_b[p]] and yields the
-# partial sum over that K slice.  Every rank writes its partial into a zeroed,
-# packed (row-major over C's extents) buffer P_r; one sum-reduce to the owner
-# rank forms ΣP_r, and only the owner adds it into C (C₀ is added exactly
-# once, SURVEY §7 "accumulate semantics across split-K").  The add is itself
-# an xGETT with no contracted mode: A = P (rank_c, packed increments),
-# B = the rank-0 scalar 1, perm = identity — K = 1 plans onto the reference-
-# order kernel, so C ← fma(P, 1, C) rounds once.  Results are not bitwise equal
-# to the single call (the K sum is reassociated); the tolerance is the
-# K-normalised one of the parity tests.
-# ---------------------------------------------------------------------------
-
-def choose_k_pair(ext_a, cont_a, world: int):
-    """Index p into the contracted pairs to split (None when conts == 0):
-    the largest extent, preferring one ≥ world and divisible by it."""
-    if not len(cont_a):
-        return None
-    return max(range(len(cont_a)),
-               key=lambda p: (int(ext_a[cont_a[p]]) >= world, int(ext_a[cont_a[p]]) % world == 0,
-                              int(ext_a[cont_a[p]])))
-
-
 def output_extents(rank_a, ext_a, cont_a, rank_b, ext_b, cont_b, perm):
     """C's extents: free index i (A's free dims ascending, then B's) lands at
-    output position perm[i] (plan.py:96-104 restated)."""
+    output position perm[i] (plan.py:119-127 restated)."""
     free = [int(ext_a[d]) for d in _free(rank_a, cont_a)] + [int(ext_b[d]) for d in _free(rank_b, cont_b)]
     out = [0] * len(free)
     for i, e in enumerate(free):
@@ -124,12 +129,11 @@ def packed_increments(ext):
     return tuple(inc)
 
 
-def k_shard_call(args, kw, pair: int, rank: int, world: int, partial):
-    """xGETT arguments computing this rank's K-slice partial into `partial`
-    (zeroed, packed over C's extents, offset 0).  Returns (args, kw, lo, hi)."""
+def k_shard_call(args, kw, pair: int, lo: int, hi: int, partial):
+    """xGETT arguments computing the K slice [lo, hi) of contracted pair
+    `pair` into `partial` (zeroed, packed over C's extents, offset 0)."""
     (rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm, inc_c, c) = args
     da, db = int(cont_a[pair]), int(cont_b[pair])
-    lo, hi = bounds(int(ext_a[da]), rank, world)
     ea, eb = list(ext_a), list(ext_b)
     ea[da] = eb[db] = hi - lo
     kw = dict(kw)
@@ -138,7 +142,7 @@ def k_shard_call(args, kw, pair: int, rank: int, world: int, partial):
     ext_c = output_extents(rank_a, ext_a, cont_a, rank_b, ext_b, cont_b, perm)
     kw["offset_c"] = 0
     return ((rank_a, tuple(ea), inc_a, a, rank_b, tuple(eb), inc_b, b, conts, cont_a, cont_b, perm,
-             packed_increments(ext_c), partial), kw, lo, hi)
+             packed_increments(ext_c), partial), kw)
 
 
 def accumulate_call(ext_c, partial, one, inc_c, c, offset_c=0):
@@ -149,37 +153,40 @@ def accumulate_call(ext_c, partial, one, inc_c, c, offset_c=0):
 
 
 def splitk_contract(entry, args, kw, rank: int, world: int, *, zeros, ones, reduce, root: int = 0,
-                    validate_full=None):
-    """Run one xGETT as `world` K-slices, one per rank, reduced onto `root`.
+                    strategy: str = "splitk"):
+    """Run one xGETT as K slices, one per rank, reduced onto `root`, on the
+    native schedule (strategy "splitk" forces the K split when the call has a
+    contracted pair of extent >= 2; "auto" lets the planner choose, and a
+    non-split-K answer runs the whole call on root).
 
     entry        — the xGETT callable for the buffers' kind (kernel.dgett for
-                   numpy, device.sgett_device for CUDA tensors, ...).
+                   numpy, device.sgett_device for CUDA tensors, the oracle in
+                   the CPU tests).
     zeros(n)     — a zeroed flat buffer of n elements like C.
     ones()       — a 1-element buffer holding 1.
     reduce(buf)  — in-place sum of buf over ranks onto root (e.g.
-                   torch.distributed.reduce; NCCL for CUDA tensors).
-    validate_full(args, kw) — the full call's ValidationError list (every rank
-                   computes it and returns it without touching C, so all
-                   ranks agree); None skips (the caller validated).
+                   torch.distributed.reduce; NCCL for CUDA tensors); called by
+                   every rank, also those with an empty slice.
 
-    Returns the validation errors ([] on success).  Only `root` writes C."""
-    if validate_full is not None:
-        errs = validate_full(args, kw)
-        if errs:
-            return errs
+    Returns the full call's validation errors ([] on success; every rank
+    returns the same list).  Only `root` writes C."""
+    sched = schedule(args, kw, world, strategy)
+    if isinstance(sched, list):
+        return sched
     (rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm, inc_c, c) = args
-    pair = choose_k_pair(ext_a, cont_a[:conts], world)
-    if pair is None or world == 1:
+    if sched.strategy != "splitk":
         return entry(*args, **kw) if rank == root else []
     ext_c = output_extents(rank_a, ext_a, cont_a, rank_b, ext_b, cont_b, perm)
     n = 1
     for e in ext_c:
         n *= e
     part = zeros(n)
-    sargs, skw, _, _ = k_shard_call(args, kw, pair, rank, world, part)
-    errs = entry(*sargs, **skw)
-    if errs:
-        raise RuntimeError(f"K-slice of a valid call failed validation: {errs}")
+    lo, hi = sched.range(rank)
+    if hi > lo:
+        sargs, skw = k_shard_call(args, kw, sched.dim, lo, hi, part)
+        errs = entry(*sargs, **skw)
+        if errs:
+            raise RuntimeError(f"K-slice of a valid call failed validation: {errs}")
     reduce(part)
     if rank == root:
         aargs, akw = accumulate_call(ext_c, part, ones(), inc_c, c, kw.get("offset_c", 0))
@@ -189,25 +196,7 @@ def splitk_contract(entry, args, kw, rank: int, world: int, *, zeros, ones, redu
     return []
 
 
-def full_call_errors(args, kw):
-    """The full call's validation errors in the entry points' two phases
-    (arguments, then C's footprint when the arguments are clean)."""
-    from .layout import TensorView
-    from .plan import ContractionSpec, derive_output_extents, validate
-
-    (rank_a, ext_a, inc_a, a, rank_b, ext_b, inc_b, b, conts, cont_a, cont_b, perm, inc_c, c) = args
-    av = TensorView(rank_a, ext_a, inc_a, kw.get("offset_a", 0), len(a))
-    bv = TensorView(rank_b, ext_b, inc_b, kw.get("offset_b", 0), len(b))
-    spec = ContractionSpec(conts, cont_a, cont_b, perm)
-    errs = validate(av, bv, spec, inc_c)
-    if errs:
-        return errs
-    ext_c = derive_output_extents(av, bv, spec)
-    cv = TensorView(len(ext_c), ext_c, tuple(inc_c), kw.get("offset_c", 0), len(c))
-    return validate(av, bv, spec, inc_c, c_view=cv)
-
-
-def splitk_device(prefix: str, args, kw, group=None, root: int = 0):
+def splitk_device(prefix: str, args, kw, group=None, root: int = 0, strategy: str = "splitk"):
     """split-K of one xGETT over the ranks of a torch.distributed group whose
     buffers are CUDA tensors: each rank contracts its K slice on its own GPU
     (device.<prefix>gett_device, stream-ordered) and ncclReduce(sum) lands
@@ -227,22 +216,4 @@ def splitk_device(prefix: str, args, kw, group=None, root: int = 0):
         zeros=lambda n: torch.zeros(n, dtype=c.dtype, device=c.device),
         ones=lambda: torch.ones(1, dtype=c.dtype, device=c.device),
         reduce=lambda p: dist.reduce(p, dst=root, op=dist.ReduceOp.SUM, group=group),
-        root=root, validate_full=_device_full_call_errors)
-
-
-def _device_full_call_errors(args, kw):
-    a, b, c = args[3], args[7], args[13]
-    lens = (a.shape[0], b.shape[0], c.shape[0])
-    sized = list(args)
-    sized[3], sized[7], sized[13] = (_Len(n) for n in lens)
-    return full_call_errors(tuple(sized), kw)
-
-
-class _Len:
-    """Stand-in exposing only len() for validation of device buffers."""
-
-    def __init__(self, n):
-        self.n = int(n)
-
-    def __len__(self):
-        return self.n
+        root=root, strategy=strategy)
