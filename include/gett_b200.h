@@ -273,6 +273,19 @@ int gett_zero_view_d_device(int rank, const int64_t* ext, const int64_t* inc, in
 int gett_zero_view_s_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset,
                             int64_t len, float* buf, void* stream);
 
+/* ---- pack: the addressed elements of a view in canonical packed order
+ * (dimension 0 fastest), a bit-exact copy of elem_bytes = 4, 8 or 16 per
+ * element (f32, f64 / c64, c128).  Replaces testkit.pack
+ * (/root/reference/pkg/src/gett/testkit.py:101-103, buf[view_offsets(view)]).
+ * gett_pack: host src (the whole buffer, view at `offset`) and host dst of
+ * prod(ext) elements; gett_pack_device: device pointers, stream-ordered.
+ * Returns 0 or GETT_E_INVALID_ARG (rank > 32, negative extent, footprint
+ * outside [0, len)). */
+int gett_pack(int rank, const int64_t* ext, const int64_t* inc, int64_t offset, int64_t len,
+              int elem_bytes, const void* src, void* dst);
+int gett_pack_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset, int64_t len,
+                     int elem_bytes, const void* src, void* dst, void* stream);
+
 /* ---- runtime control ---- */
 /* Kernel selection: "auto" (default), "ref" (reference-order kernel, bitwise
  * equal to the reference on all data), "tiled" (tensor-core / register-tiled

@@ -21,7 +21,7 @@ EXPORTS = (
     "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
     "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
-    "gett_multi_schedule",
+    "gett_multi_schedule", "gett_pack", "gett_pack_device",
 )
 
 ERR_INFO_WORDS = 6
@@ -63,6 +63,11 @@ def _load():
         ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
         ctypes.c_int, i64p, i64p, ctypes.c_int, i64p, ctypes.c_int, i64p,
         ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i32p, i64p, ctypes.c_int]
+    lib.gett_pack.restype = ctypes.c_int
+    lib.gett_pack.argtypes = [ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
+                              vp, vp]
+    lib.gett_pack_device.restype = ctypes.c_int
+    lib.gett_pack_device.argtypes = lib.gett_pack.argtypes + [vp]
     lib.gett_set_devices.restype = ctypes.c_int
     lib.gett_set_devices.argtypes = [ctypes.c_int, i32p]
     lib.gett_set_multi.restype = ctypes.c_int

@@ -1806,6 +1806,66 @@ int zero_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64
   return 0;
 }
 
+// pack: the view's addressed elements in canonical order (dimension 0
+// fastest).  Host form: H2D of the view's span, gather, D2H of the n packed
+// elements.
+int pack_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64_t off, int64_t len,
+              int elem_bytes, const void* src, void* dst, cudaStream_t stream) {
+  if (rank < 0 || rank > kPackMaxRank || off < 0 || len < 0 ||
+      (elem_bytes != 4 && elem_bytes != 8 && elem_bytes != 16) || (rank > 0 && (!ext || !inc))) {
+    t_last_error = "bad pack descriptor (rank <= 32, element of 4, 8 or 16 bytes)";
+    return GETT_E_INVALID_ARG;
+  }
+  int64_t n = 1;
+  for (int d = 0; d < rank; ++d) {
+    if (ext[d] < 0) {
+      t_last_error = "negative extent";
+      return GETT_E_INVALID_ARG;
+    }
+    n *= ext[d];
+  }
+  if (n == 0) return 0;
+  int64_t lo, hi;
+  footprint(rank, ext, inc, &lo, &hi);
+  if (off + lo < 0 || off + hi >= len) {
+    t_last_error = "view footprint outside the buffer";
+    return GETT_E_INVALID_ARG;
+  }
+  PackParams pp{};
+  pp.rank = rank;
+  pp.n = n;
+  for (int d = 0; d < rank; ++d) {
+    pp.ext[d] = ext[d];
+    pp.inc[d] = inc[d];
+    if (n < (1LL << 31)) pp.div[d] = FastDiv::make((int32_t)ext[d]);
+  }
+  int dev, rc;
+  if ((rc = current_device(&dev))) return rc;
+  DevState& ds = g_dev[dev];
+  std::lock_guard<std::mutex> lk(ds.mu);
+  const char* s8 = static_cast<const char*>(src);
+  if (!host) {
+    pp.src = s8 + off * elem_bytes;
+    pp.dst = dst;
+    CK(launch_pack(pp, elem_bytes, stream));
+    ++g_launches;
+    return 0;
+  }
+  Lane* Lp = nullptr;
+  if ((rc = get_lane(dev, 0, &Lp))) return rc;
+  Lane& L = *Lp;
+  const size_t span = (size_t)(hi - lo + 1) * elem_bytes, out = (size_t)n * elem_bytes;
+  if ((rc = ensure(L.a, span)) || (rc = ensure(L.c, out))) return rc;
+  CK(cudaMemcpyAsync(L.a.p, s8 + (off + lo) * elem_bytes, span, cudaMemcpyHostToDevice, L.stream));
+  pp.src = static_cast<const char*>(L.a.p) - lo * elem_bytes;
+  pp.dst = L.c.p;
+  CK(launch_pack(pp, elem_bytes, L.stream));
+  ++g_launches;
+  CK(cudaMemcpyAsync(dst, L.c.p, out, cudaMemcpyDeviceToHost, L.stream));
+  CK(cudaStreamSynchronize(L.stream));
+  return 0;
+}
+
 }  // namespace
 }  // namespace gett
 
@@ -2039,6 +2099,15 @@ int gett_zero_view_s_device(int rank, const int64_t* ext, const int64_t* inc, in
   return zero_impl<float>(false, rank, ext, inc, offset, len, buf, (cudaStream_t)stream);
 }
 
+int gett_pack(int rank, const int64_t* ext, const int64_t* inc, int64_t offset, int64_t len,
+              int elem_bytes, const void* src, void* dst) {
+  return pack_impl(true, rank, ext, inc, offset, len, elem_bytes, src, dst, nullptr);
+}
+int gett_pack_device(int rank, const int64_t* ext, const int64_t* inc, int64_t offset, int64_t len,
+                     int elem_bytes, const void* src, void* dst, void* stream) {
+  return pack_impl(false, rank, ext, inc, offset, len, elem_bytes, src, dst, (cudaStream_t)stream);
+}
+
 int gett_set_kernel(const char* name) {
   if (!name) return GETT_E_INVALID_ARG;
   if (!strcmp(name, "auto")) g_mode = Mode::Auto;
@@ -2123,7 +2192,8 @@ void gett_release_caches(void) {
 }
 
 // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed;
-// 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi
+// 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi,
+//       gett_multi_schedule, gett_pack[_device]
 int gett_abi_version(void) { return 104; }
 
 }  // extern "C"

@@ -762,6 +762,33 @@ __global__ void __launch_bounds__(256) gett_accum_view_kernel(const __grid_const
   }
 }
 
+template <typename E, bool SMALL>
+__global__ void __launch_bounds__(256) gett_pack_kernel(const __grid_constant__ PackParams p) {
+  const E* src = static_cast<const E*>(p.src);
+  E* dst = static_cast<E*>(p.dst);
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p.n; i += stride) {
+    int64_t off = 0;
+    if (SMALL) {
+      int32_t rem = (int32_t)i;
+      for (int d = 0; d < p.rank; ++d) {
+        int32_t q, r;
+        p.div[d].divmod(rem, q, r);
+        off += (int64_t)r * p.inc[d];
+        rem = q;
+      }
+    } else {
+      int64_t rem = i;
+      for (int d = 0; d < p.rank; ++d) {
+        const int64_t q = rem / p.ext[d];
+        off += (rem - q * p.ext[d]) * p.inc[d];
+        rem = q;
+      }
+    }
+    dst[i] = src[off];
+  }
+}
+
 // ---------------------------------------------------------------------------
 // launchers
 
@@ -930,6 +957,30 @@ cudaError_t launch_accum(const AccumParams<T>& p, cudaStream_t s) {
 }
 template cudaError_t launch_accum<double>(const AccumParams<double>&, cudaStream_t);
 template cudaError_t launch_accum<float>(const AccumParams<float>&, cudaStream_t);
+
+cudaError_t launch_pack(const PackParams& p, int elem_bytes, cudaStream_t s) {
+  if (p.n <= 0) return cudaSuccess;
+  int64_t blocks = (p.n + 255) / 256;
+  if (blocks > 148 * 16) blocks = 148 * 16;
+  const bool small = p.n < (1LL << 31);
+  switch (elem_bytes) {
+    case 4:
+      if (small) gett_pack_kernel<uint32_t, true><<<(unsigned)blocks, 256, 0, s>>>(p);
+      else gett_pack_kernel<uint32_t, false><<<(unsigned)blocks, 256, 0, s>>>(p);
+      break;
+    case 8:
+      if (small) gett_pack_kernel<uint64_t, true><<<(unsigned)blocks, 256, 0, s>>>(p);
+      else gett_pack_kernel<uint64_t, false><<<(unsigned)blocks, 256, 0, s>>>(p);
+      break;
+    case 16:
+      if (small) gett_pack_kernel<ulonglong2, true><<<(unsigned)blocks, 256, 0, s>>>(p);
+      else gett_pack_kernel<ulonglong2, false><<<(unsigned)blocks, 256, 0, s>>>(p);
+      break;
+    default:
+      return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
 
 int tiled_bm() { return tiled::BM; }
 int tiled_bn() { return tiled::BN; }

@@ -36,6 +36,20 @@ struct AccumParams {
 template <typename T>
 cudaError_t launch_accum(const AccumParams<T>& p, cudaStream_t s);
 
+// pack (testkit.pack, /root/reference/pkg/src/gett/testkit.py:101-103): dst[i]
+// = src[offset of packed index i], i in canonical order (dimension 0 fastest),
+// a bit-exact copy of elem_bytes (4, 8 or 16) per element.
+constexpr int kPackMaxRank = 32;
+struct PackParams {
+  const void* src;  // at the view's coordinate (0, ..., 0)
+  void* dst;
+  int rank;
+  int64_t n;
+  int64_t ext[kPackMaxRank], inc[kPackMaxRank];
+  FastDiv div[kPackMaxRank];  // used when n < 2^31
+};
+cudaError_t launch_pack(const PackParams& p, int elem_bytes, cudaStream_t s);
+
 template <typename T>
 cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s);
 

@@ -118,3 +118,26 @@ def cgett_device(*args, **kw):
 def zgett_device(*args, **kw):
     """complex128 xGETT on CUDA tensors (stream-ordered); see kernel.zgett."""
     return _gett_device("z", *args, **kw)
+
+
+def pack_device(view: TensorView, buf, stream=None):
+    """pack (kernel.pack) of a CUDA tensor: a new 1-D tensor of the view's
+    elements in canonical order (dimension 0 fastest), stream-ordered."""
+    import torch
+
+    if not isinstance(buf, torch.Tensor) or not buf.is_cuda or buf.dim() != 1 or buf.stride(0) != 1:
+        raise TypeError("buf must be a contiguous 1-D CUDA tensor")
+    n = 1
+    for e in view.extents:
+        n *= max(int(e), 0)
+    out = torch.empty(n, dtype=buf.dtype, device=buf.device)
+    if n == 0:
+        return out
+    if stream is None:
+        stream = torch.cuda.current_stream(buf.device)
+    with torch.cuda.device(buf.device):
+        _native.check(_native.LIB.gett_pack_device(
+            view.rank, _native.i64(view.extents), _native.i64(view.increments), view.base_offset,
+            buf.shape[0], buf.element_size(), buf.data_ptr(), out.data_ptr(),
+            ctypes.c_void_p(stream.cuda_stream)), "pack_device")
+    return out

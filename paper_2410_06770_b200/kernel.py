@@ -171,6 +171,35 @@ def zero_view(view: TensorView, buf: np.ndarray) -> None:
         buf[...] = w
 
 
+def pack(view: TensorView, buf) -> np.ndarray:
+    """The elements the view addresses, in canonical packed order (dimension
+    0 fastest) — testkit.pack's data (/root/reference/pkg/src/gett/testkit.py:101-103,
+    ``buf[view_offsets(view)]``), gathered on the GPU bit for bit."""
+    buf = np.asarray(buf)
+    if buf.ndim != 1:
+        raise TypeError("buf must be a flat 1-D buffer")
+    dtype_prefix(buf.dtype)  # s/d/c/z element types only
+    n = 1
+    for e in view.extents:
+        n *= max(int(e), 0)
+    out = np.empty(n, dtype=buf.dtype)
+    if n == 0:
+        return out
+    lo = hi = 0
+    for e, i in zip(view.extents, view.increments):
+        span = i * (e - 1)
+        lo, hi = (lo + span, hi) if span < 0 else (lo, hi + span)
+    if view.base_offset + lo < 0 or view.base_offset + hi >= buf.shape[0]:
+        raise IndexError(f"view addresses offsets {view.base_offset + lo}..{view.base_offset + hi} "
+                         f"outside a buffer of {buf.shape[0]} elements")
+    src = np.ascontiguousarray(buf)
+    _native.check(_native.LIB.gett_pack(view.rank, _native.i64(view.extents),
+                                        _native.i64(view.increments), view.base_offset,
+                                        src.shape[0], src.itemsize, src.ctypes.data,
+                                        out.ctypes.data), "pack")
+    return out
+
+
 def dtype_prefix(dtype) -> str:
     """The s/d/c/z tag for a numpy element type (kernel.py:203-209)."""
     dtype = np.dtype(dtype)

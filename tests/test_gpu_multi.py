@@ -182,3 +182,35 @@ def test_bad_device_ordinal_raises(multi):
     with pytest.raises(g.GettRuntimeError):
         g.dgett(1, (4,), (1,), a, 1, (4,), (1,), b, 1, (0,), (0,), (), (), c, devices=(0, 63))
     assert c[0] == 0.0
+
+
+# ---------------------------------------------------------------------------
+# pack (testkit.py:101-103) on the device
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64, np.complex64, np.complex128])
+def test_pack_equals_fancy_index(dtype):
+    rng = np.random.default_rng(5)
+    buf = rng.standard_normal(5000).astype(dtype)
+    if np.iscomplexobj(buf):
+        buf = buf + 1j * rng.standard_normal(5000).astype(dtype)
+    buf[7] = -0.0
+    for ext, inc, off in [((3, 4, 5), (1, 3, 12), 0), ((6, 7), (-9, 1), 60), ((5, 1, 4), (200, 0, -30), 100),
+                          ((), (), 17), ((0, 3), (1, 1), 0), ((8, 8, 8, 4), (2, 16, 128, 1024), 1)]:
+        v = g.TensorView(len(ext), ext, inc, off, len(buf))
+        got = g.pack(v, buf)
+        want = buf[view_offsets(ext, inc, off)] if ext else buf[off:off + 1]
+        assert got.tobytes() == want.tobytes(), (ext, inc, off)
+
+
+def test_pack_device_and_bounds():
+    import torch
+
+    from paper_2410_06770_b200.device import pack_device
+
+    buf = torch.arange(1000, dtype=torch.float64, device="cuda")
+    v = g.TensorView(2, (10, 7), (3, 100), 5, 1000)
+    got = pack_device(v, buf).cpu().numpy()
+    assert np.array_equal(got, np.arange(1000.0)[view_offsets((10, 7), (3, 100), 5)])
+    with pytest.raises(IndexError):
+        g.pack(g.TensorView(1, (10,), (200,), 0, 5000), np.zeros(1000))
