@@ -310,6 +310,13 @@ int gett_set_tma(int on);
  * split-K shapes with a K-major operand of >= 256 rows and a rows-major one of
  * <= 128 (e.g. c5); 0 = off (the default), 1 = on.  Also GETT_PAIR. */
 int gett_set_pair(int on);
+/* SGETT k-run kernel (one k-block = the TMEM operand's whole contiguous inner
+ * k run, <= 64 floats; dense TMA boxes; split-K reduced inside the kernel):
+ * 0 = off, 1 = automatic (runs < 64 on fewer tiles than SMs, the default),
+ * 2 = whenever it applies; + 4 = split-K partials reduced inside the kernel
+ * (tile counters; graph-replay safe) instead of by the separate reduce kernel
+ * (the default).  Also GETT_KR / GETT_KR_FUSED. */
+int gett_set_kr(int mode);
 /* cgett / zgett on the tensor-core kernels: 1 = one real GETT on a real
  * embedding of the smaller operand (the default), 0 = four real GETTs on the
  * re/im sub-views.  Also GETT_COMPLEX_EMBED. */

@@ -8,7 +8,7 @@ include/gett_b200.h); the planner and the kernels are C++/CUDA.
 """
 from . import _native
 from ._native import (GettRuntimeError, last_kernel, last_multi, launch_count, set_complex_embed,
-                      set_devices, set_kernel, set_multi, set_pipeline, set_pair, set_split_k,
+                      set_devices, set_kernel, set_kr, set_multi, set_pipeline, set_pair, set_split_k,
                       set_stream_k, set_tma)
 from .kernel import cgett, dgett, dtype_prefix, gett_for_dtype, pack, sgett, zero_view, zgett
 from .layout import TensorView, contiguous_increments, footprint, num_elements
@@ -29,5 +29,5 @@ __all__ = [
     "ContractionError", "ContractionSpec", "ErrorCode", "GettRuntimeError", "TensorView", "cgett", "zgett",
     "ValidationError", "contiguous_increments", "derive_output_extents", "dgett", "dtype_prefix",
     "footprint", "free_dims", "gett_for_dtype", "last_kernel", "last_multi", "launch_count", "num_elements",
-    "output_rank", "pack", "set_complex_embed", "set_devices", "set_kernel", "set_multi", "set_pair", "set_split_k", "set_stream_k", "set_tma", "sgett", "validate", "zero_view",
+    "output_rank", "pack", "set_complex_embed", "set_devices", "set_kernel", "set_kr", "set_multi", "set_pair", "set_split_k", "set_stream_k", "set_tma", "sgett", "validate", "zero_view",
 ]

@@ -21,7 +21,7 @@ EXPORTS = (
     "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
     "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
-    "gett_multi_schedule", "gett_pack", "gett_pack_device",
+    "gett_multi_schedule", "gett_pack", "gett_pack_device", "gett_set_kr",
 )
 
 ERR_INFO_WORDS = 6
@@ -99,6 +99,8 @@ def _load():
     lib.gett_set_stream_k.argtypes = [ctypes.c_int]
     lib.gett_set_tma.restype = ctypes.c_int
     lib.gett_set_tma.argtypes = [ctypes.c_int]
+    lib.gett_set_kr.restype = ctypes.c_int
+    lib.gett_set_kr.argtypes = [ctypes.c_int]
     lib.gett_set_pair.restype = ctypes.c_int
     lib.gett_set_pair.argtypes = [ctypes.c_int]
     lib.gett_set_complex_embed.restype = ctypes.c_int
@@ -188,6 +190,14 @@ def set_devices(devices) -> None:
     current device.  A device may repeat (devices=(0, 0): two lanes on one GPU)."""
     devs = [] if devices is None else [int(d) for d in devices]
     check(LIB.gett_set_devices(len(devs), i32(devs)), "set_devices")
+
+
+def set_kr(mode: str = "auto", fused: bool = False) -> None:
+    """SGETT k-run kernel: "off", "auto" (default) or "force" (whenever it
+    applies); fused=True reduces split-K partials inside the kernel instead of
+    with the separate reduce kernel (the default)."""
+    code = {"off": 0, "auto": 1, "force": 2}[mode] | (4 if fused else 0)
+    check(LIB.gett_set_kr(code), "set_kr")
 
 
 def set_multi(strategy: str, staged: bool = False) -> None:

@@ -44,6 +44,9 @@ bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=
 bool g_sk_small = true;    // DGETT: stream-K instead of split-K at 56-73 tiles (GETT_SK_SMALL=0: off)
 bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one embedded GETT (GETT_COMPLEX_EMBED=0)
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
+int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
+bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
+                          // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 int g_multi_stage = 0;      // multi-device split-K: 1 = stage partials by cudaMemcpyPeer instead of peer loads (GETT_MULTI_STAGE)
 std::vector<int> g_devices;  // default device list of the host entry points (gett_set_devices; empty = current device)
@@ -65,6 +68,10 @@ void read_env_once() {
   if (sks) g_sk_small = std::atoi(sks) != 0;
   const char* ce = std::getenv("GETT_COMPLEX_EMBED");
   if (ce) g_complex_4x = std::atoi(ce) == 0;
+  const char* krv = std::getenv("GETT_KR");
+  if (krv) g_kr = std::atoi(krv);
+  const char* krf = std::getenv("GETT_KR_FUSED");
+  if (krf) g_kr_fused = std::atoi(krf) != 0;
   const char* pv = std::getenv("GETT_PAIR");
   if (pv) g_pair = std::atoi(pv) != 0;
   const char* tv = std::getenv("GETT_TMA");
@@ -118,6 +125,18 @@ struct DevPlan {
   TmaParams pair_p{};
   const void* pair_base[2] = {nullptr, nullptr};
   GroupDev pgk{};      // dp.gk with its two tensors exchanged
+  // SGETT k-run kernel (sgett_kr.cu): decided once per plan; the tensor maps
+  // are re-encoded when the operand base pointers change
+  int kr_state = 0;    // 0 undecided, 1 usable, -1 not
+  int kr_x = 0;        // X (TMEM operand) is the plan's A' (0) or B' (1)
+  int kr_run = 0;      // KR
+  struct KrLayout {
+    uint64_t dims[5], strides[5];  // elements
+    uint32_t box[5];
+    int64_t base_off;
+  } kr_l[2];            // X, Y
+  KrParams kr_p{};
+  const void* kr_base[2] = {nullptr, nullptr};
   // used by a call captured into a CUDA graph: the graph holds raw pointers
   // into d_tab, so the LRU never evicts it (gett_release_caches still does)
   std::atomic<bool> pinned{false};
@@ -171,6 +190,7 @@ struct StreamWs {
   Scratch flags;      // stream-K publish flags (zeroed on allocation)
   Scratch cx;         // real embedding of a complex operand
   int32_t epoch = 0;  // stream-K launches so far on this stream
+  Scratch krsync;     // k-run kernel: tile counters, generations, slice claims (zeroed on allocation)
 };
 // A lane: one compute stream + two copy streams + the host path's device
 // staging of one device.  Lane 0 serves single-device calls; a multi-device
@@ -554,6 +574,339 @@ const TmaParams* sgett_tma(DevPlan& dp, const float* A, const float* B) {
   return &dp.tma_p;
 }
 
+// ---- SGETT k-run kernel (sgett_kr.cu) ----
+
+// The K group as affine dims shared by both tensors, inner first: the inner
+// mode, then the outer table cut wherever either tensor's offsets stop being
+// one arithmetic progression.  False unless every entry matches.
+bool joint_k_dims(const Group& gk, std::vector<int64_t>& ext, std::vector<int64_t> st[2]) {
+  ext.clear();
+  st[0].clear();
+  st[1].clear();
+  ext.push_back(gk.e_in);
+  st[0].push_back(gk.s_in[0]);
+  st[1].push_back(gk.s_in[1]);
+  const std::vector<int64_t>& T0 = gk.T[0];
+  const std::vector<int64_t>& T1 = gk.T[1];
+  const int64_t L = (int64_t)T0.size();
+  std::vector<int64_t> oe, os0, os1;
+  int64_t pos = 1;
+  while (pos < L) {
+    const int64_t a = T0[pos] - T0[0], b = T1[pos] - T1[0];
+    int64_t e = 1;
+    while (pos * e < L && T0[pos * e] - T0[0] == e * a && T1[pos * e] - T1[0] == e * b) ++e;
+    if (L % (pos * e) != 0) return false;
+    oe.push_back(e);
+    os0.push_back(a);
+    os1.push_back(b);
+    pos *= e;
+  }
+  for (int64_t q = 0; q < L; ++q) {
+    int64_t r = q, o0 = 0, o1 = 0;
+    for (size_t i = 0; i < oe.size(); ++i) {
+      o0 += (r % oe[i]) * os0[i];
+      o1 += (r % oe[i]) * os1[i];
+      r /= oe[i];
+    }
+    if (T0[q] - T0[0] != o0 || T1[q] - T1[0] != o1) return false;
+  }
+  for (size_t i = 0; i < oe.size(); ++i) {
+    ext.push_back(oe[i]);
+    st[0].push_back(os0[i]);
+    st[1].push_back(os1[i]);
+  }
+  return true;
+}
+
+// Box of up to `tile` rows over row dims R (inner first): how many dims it
+// spans, their box extents and the rows it covers (a whole number of inner
+// row runs when the inner extent is below `tile`: 50-row runs -> 100-row
+// boxes); 0 when the rows cannot be boxed.
+int row_box(const std::vector<AffDim>& R, int64_t tile, uint32_t* rb, int64_t* rows) {
+  if (R.empty()) return 0;
+  const int64_t r0 = R[0].ext;
+  if (r0 >= tile || R.size() == 1) {
+    rb[0] = (uint32_t)tile;
+    *rows = tile;
+    return 1;
+  }
+  const int64_t q = std::min<int64_t>(tile / r0, R[1].ext);
+  rb[0] = (uint32_t)r0;
+  rb[1] = (uint32_t)q;
+  *rows = r0 * q;
+  return 2;
+}
+
+// Decide (once per plan) whether the k-run kernel can run this SGETT, in
+// which orientation, and build its two tensor-map layouts.
+bool kr_decide(DevPlan& dp) {
+  const Plan& p = dp.plan;
+  std::vector<int64_t> kext, kst[2];
+  if (!joint_k_dims(p.gk, kext, kst)) return false;
+  for (int x = 0; x < 2; ++x) {
+    const int y = 1 - x;
+    const Group& gx = x == 0 ? p.gm : p.gn;
+    const Group& gy = x == 0 ? p.gn : p.gm;
+    if (kst[x][0] != 1 || kext[0] % 8 != 0) continue;
+    // k run: the whole inner run when <= 64, else the largest multiple of 8
+    // dividing it (the rest of the run becomes the innermost outer k digit)
+    int64_t KR = kext[0];
+    std::vector<int64_t> oe(kext.begin() + 1, kext.end()), os[2];
+    os[0].assign(kst[0].begin() + 1, kst[0].end());
+    os[1].assign(kst[1].begin() + 1, kst[1].end());
+    if (KR > 64) {
+      int64_t kr = 64;
+      while (kr >= 8 && KR % kr) kr -= 8;
+      if (kr < 8) continue;
+      oe.insert(oe.begin(), KR / kr);
+      os[0].insert(os[0].begin(), kr * kst[0][0]);
+      os[1].insert(os[1].begin(), kr * kst[1][0]);
+      KR = kr;
+    }
+    if (oe.size() > 2) continue;
+    std::vector<AffDim> RX, RY;
+    if (!affine_dims(gx, 0, RX) || !affine_dims(gy, 0, RY) || RX.empty() || RY.empty()) continue;
+    if (RY[0].stride != 1) continue;  // Y rows-major
+    bool pos_ok = kst[y][0] > 0;
+    for (int t = 0; t < 2; ++t)
+      for (int64_t v : os[t]) pos_ok = pos_ok && v > 0;
+    if (!pos_ok) continue;
+    const int64_t MX = gx.G, NY = gy.G;
+    uint32_t xb[2] = {1, 1}, yb[2] = {1, 1};
+    int64_t xrows = 0, yrows = 0;
+    const int nxb = row_box(RX, 128, xb, &xrows);
+    const int nyb = row_box(RY, NY <= 128 ? NY : 128, yb, &yrows);
+    if (!nxb || !nyb || yrows % 4 != 0) continue;
+    // one-dim boxes past the extent are zero-filled; a box of a multi-dim
+    // row group must hold whole inner runs (checked by row_box) or start on
+    // run boundaries (r0 a multiple of the box rows)
+    if (nyb == 1 && RY.size() > 1 && RY[0].ext % yrows != 0) continue;
+    if (nxb == 1 && RX.size() > 1 && RX[0].ext % xrows != 0) continue;
+    const int64_t NT = (yrows + 15) / 16 * 16;
+    const int nko = (int)oe.size();
+    if (1 + (int)RX.size() + nko > 5 || (int)RY.size() + 1 + nko > 5) continue;
+    struct D {
+      int64_t ext, stride;
+      uint32_t box;
+    };
+    std::vector<D> dx, dy;
+    KrParams& kp = dp.kr_p;
+    std::memset(&kp, 0, sizeof kp);
+    // X: [k run][rows...][outer k...]
+    dx.push_back({KR, 1, (uint32_t)(KR + 4)});  // (+4 zero-filled columns: conflict-free row pitch)
+    for (size_t i = 0; i < RX.size(); ++i) {
+      kp.xr_ext[i] = (int32_t)RX[i].ext;
+      kp.xr_pos[i] = (int32_t)dx.size();
+      dx.push_back({RX[i].ext, RX[i].stride, i < (size_t)nxb ? xb[i] : 1u});
+    }
+    // Y: [boxed rows][k run][other rows][outer k...]
+    for (int i = 0; i < nyb; ++i) {
+      kp.yr_ext[i] = (int32_t)RY[i].ext;
+      kp.yr_pos[i] = (int32_t)dy.size();
+      dy.push_back({RY[i].ext, RY[i].stride, yb[i]});
+    }
+    dy.push_back({KR, kst[y][0], (uint32_t)KR});
+    for (size_t i = nyb; i < RY.size(); ++i) {
+      kp.yr_ext[i] = (int32_t)RY[i].ext;
+      kp.yr_pos[i] = (int32_t)dy.size();
+      dy.push_back({RY[i].ext, RY[i].stride, 1u});
+    }
+    for (int j = 0; j < nko; ++j) {
+      kp.k_ext[j] = (int32_t)oe[j];
+      kp.xk_pos[j] = (int32_t)dx.size();
+      dx.push_back({oe[j], os[x][j], 1u});
+      kp.yk_pos[j] = (int32_t)dy.size();
+      dy.push_back({oe[j], os[y][j], 1u});
+    }
+    bool ok = true;
+    for (const std::vector<D>* dv : {&dx, &dy})
+      for (size_t i = 1; i < dv->size(); ++i)
+        ok = ok && (*dv)[i].stride % 4 == 0 && (*dv)[i].stride * 4 < (1LL << 40);
+    if (!ok || dy[0].stride != 1) continue;
+    for (int t = 0; t < 2; ++t) {
+      const std::vector<D>& dv = t == 0 ? dx : dy;
+      DevPlan::KrLayout& L = dp.kr_l[t];
+      for (int i = 0; i < 5; ++i) {
+        if (i < (int)dv.size()) {
+          L.dims[i] = (uint64_t)dv[i].ext;
+          L.strides[i] = (uint64_t)dv[i].stride;
+          L.box[i] = dv[i].box;
+        } else {
+          L.dims[i] = 1;
+          L.strides[i] = 4;
+          L.box[i] = 1;
+        }
+      }
+    }
+    dp.kr_l[0].base_off = gx.T[0][0] + p.gk.T[x][0];
+    dp.kr_l[1].base_off = gy.T[0][0] + p.gk.T[y][0];
+    kp.xnr = (int32_t)RX.size();
+    kp.ynr = (int32_t)RY.size();
+    kp.nko = nko;
+    kp.gx = x == 0 ? dp.gm : dp.gn;
+    kp.gy = x == 0 ? dp.gn : dp.gm;
+    kp.MX = (int32_t)MX;
+    kp.NY = (int32_t)NY;
+    kp.NT = (int32_t)NT;
+    kp.x_rows = (int32_t)xrows;
+    kp.y_rows = (int32_t)yrows;
+    kp.tiles_x = (int32_t)((MX + xrows - 1) / xrows);
+    kp.tiles_y = (int32_t)((NY + yrows - 1) / yrows);
+    kp.nkb = (int32_t)(p.gk.G / KR);
+    // shared memory: load slots [X raw 128 x (KR+4) | Y raw KR x NT] (freed
+    // right after the split) + operand slots [Y hi | Y lo] (freed by the MMA)
+    // + barriers, within 227 KB; TMEM: NT accumulator columns (rounded to 32)
+    // + 2 KR A columns (hi, lo) per A slot, within 512
+    auto up = [](int64_t v, int64_t a) { return (v + a - 1) / a * a; };
+    const int64_t xbytes = up(128 * (KR + 4) * 4, 1024), ybytes = up(KR * NT * 4, 1024);  // (box <= slot)
+    kp.lslot_bytes = (int32_t)(xbytes + ybytes);
+    kp.oslot_bytes = (int32_t)(2 * ybytes);
+    kp.a_col0 = (int32_t)up(NT, 32);
+    kp.aslots = (int32_t)std::min<int64_t>(8, (512 - kp.a_col0) / (2 * KR));
+    // as many load slots as fit beside two operand slots.  Ring sizes keep
+    // the mbarrier parity waits unambiguous (no waiter two phases ahead): the
+    // split warpgroups take alternate k-blocks, so with an even number of
+    // load slots and two operand slots each group has slots of its own;
+    // TMEM slots are freed in MMA order, so any count >= 2 works.
+    auto fits = [&](int l, int o) {
+      return (int64_t)l * kp.lslot_bytes + (int64_t)o * kp.oslot_bytes + 512 <= 227 * 1024;
+    };
+    const int so = 2;
+    int sl = 8;
+    while (sl > 2 && !fits(sl, so)) sl -= 2;
+    if (kp.aslots < 2 || !fits(sl, so)) continue;
+    kp.lslots = sl;
+    kp.oslots = so;
+    kp.o_off = sl * kp.lslot_bytes;
+    kp.bar_off = (int32_t)(kp.o_off + (int64_t)so * kp.oslot_bytes);
+    dp.kr_x = x;
+    dp.kr_run = (int)KR;
+    return true;
+  }
+  return false;
+}
+
+bool kr_encode(const DevPlan::KrLayout& L, const float* base, CUtensorMap* map) {
+  TmaEncodeFn enc = tma_encode_fn();
+  if (!enc) return false;
+  const float* g = base + L.base_off;
+  if ((uintptr_t)g % 16 != 0) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    dims[i] = L.dims[i];
+    box[i] = L.box[i];
+    if (i) strides[i - 1] = L.strides[i] * 4;
+  }
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(g), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, GETT_TMA_PROMO,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Run the SGETT on the k-run kernel when it applies.  Returns 1 when
+// launched, 0 when the call does not fit, < 0 on error.
+int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg, cudaStream_t stream,
+                 DevState& ds, StreamWs& sw) {
+  if (g_kr == 0 || !g_tma) return 0;
+  if (dp.kr_state == 0) {
+    dp.kr_state = kr_decide(dp) ? 1 : -1;
+    if (std::getenv("GETT_TMA_DEBUG")) {
+      std::fprintf(stderr, "gett kr: %s", dp.kr_state == 1 ? "on" : "off");
+      if (dp.kr_state == 1) {
+        std::fprintf(stderr, " X=%s KR %d MX %d NY %d NT %d nkb %d slots load %d operand %d tmem %d smem %d\n",
+                     dp.kr_x ? "B'" : "A'", dp.kr_run, dp.kr_p.MX, dp.kr_p.NY, dp.kr_p.NT, dp.kr_p.nkb,
+                     dp.kr_p.lslots, dp.kr_p.oslots, dp.kr_p.aslots, dp.kr_p.bar_off + 512);
+        for (int t = 0; t < 2; ++t) {
+          std::fprintf(stderr, "  %c base_off %lld dims", t ? 'Y' : 'X', (long long)dp.kr_l[t].base_off);
+          for (int i = 0; i < 5; ++i)
+            std::fprintf(stderr, " (%llu,%llu,%u)", (unsigned long long)dp.kr_l[t].dims[i],
+                         (unsigned long long)dp.kr_l[t].strides[i], dp.kr_l[t].box[i]);
+          std::fprintf(stderr, "\n");
+        }
+      } else {
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
+  if (dp.kr_state != 1) return 0;
+  KrParams kp = dp.kr_p;
+  const int64_t tiles = (int64_t)kp.tiles_x * kp.tiles_y;
+  if (!ds.sms) {
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  // automatic: the k-run kernel is for short runs (the SW32 boxes of the
+  // tiled kernel issue one 32 B line per row per 8 k) and split-K shapes
+  if (g_kr == 1 && !(dp.kr_run < 64 && tiles < ds.sms)) return 0;
+  const float* X = dp.kr_x == 0 ? A : B;
+  const float* Y = dp.kr_x == 0 ? B : A;
+  if (dp.kr_base[0] != X || dp.kr_base[1] != Y) {
+    if (!kr_encode(dp.kr_l[0], X, &dp.kr_p.mx) || !kr_encode(dp.kr_l[1], Y, &dp.kr_p.my)) {
+      dp.kr_base[0] = dp.kr_base[1] = nullptr;
+      return 0;
+    }
+    dp.kr_base[0] = X;
+    dp.kr_base[1] = Y;
+    kp.mx = dp.kr_p.mx;
+    kp.my = dp.kr_p.my;
+  }
+  int64_t splits = 1;
+  if (g_split > 0) splits = g_split;
+  else if (tiles < ds.sms && kp.nkb >= 4) splits = ds.sms / tiles;
+  if (splits > kp.nkb / 2) splits = kp.nkb / 2;
+  if (splits > KR_MAX_SPLITS) splits = KR_MAX_SPLITS;  // (the fused reduce's claim slots)
+  if (splits < 1) splits = 1;
+  const int64_t kpc = (kp.nkb + splits - 1) / splits;
+  splits = (kp.nkb + kpc - 1) / kpc;
+  kp.kpc = (int32_t)kpc;
+  kp.splits = (int32_t)splits;
+  kp.C = C;
+  kp.neg = neg;
+  kp.cnt = kp.gen = kp.claim = nullptr;
+  int rc;
+  if (splits > 1) {
+    if ((rc = ensure(sw.ws, (size_t)splits * kp.MX * kp.NY * sizeof(float)))) return rc;
+    kp.ws = (float*)sw.ws.p;
+    if (g_kr_fused && tiles <= KR_MAX_TILES) {
+      // counters, generations and claims: zeroed once on allocation; they
+      // return to a reusable state after every launch (graph replays too)
+      // (a fixed layout for every call: counters [0, 256), generations
+      // [256, 512), claims from 512 — slot t always belongs to tile t)
+      const size_t bytes = (size_t)(2 * KR_MAX_TILES + KR_MAX_TILES * KR_MAX_SPLITS) * sizeof(uint32_t);
+      if (sw.krsync.bytes < bytes) {
+        if ((rc = ensure(sw.krsync, bytes))) return rc;
+        CK(cudaMemsetAsync(sw.krsync.p, 0, sw.krsync.bytes, stream));
+      }
+      kp.cnt = (uint32_t*)sw.krsync.p;
+      kp.gen = kp.cnt + KR_MAX_TILES;
+      kp.claim = kp.gen + KR_MAX_TILES;
+      static const int64_t spin =
+          std::getenv("GETT_KR_SPIN_NS") ? std::atoll(std::getenv("GETT_KR_SPIN_NS")) : 200000;
+      kp.spin_ns = spin;
+    }
+  }
+  CK(launch_sgett_kr(kp, dp.kr_run, stream));
+  ++g_launches;
+  if (splits > 1 && kp.cnt == nullptr) {
+    TiledParams<float> tp{};
+    tp.C = C;
+    tp.gm = kp.gx;
+    tp.gn = kp.gy;
+    tp.M = kp.MX;
+    tp.N = kp.NY;
+    tp.splits = kp.splits;
+    tp.ws = kp.ws;
+    tp.neg = neg;
+    tp.ws_t = 1;
+    CK(launch_splitk_reduce<float>(tp, stream));
+    ++g_launches;
+  }
+  t_last_kernel = splits == 1 ? "sgett_tc3xtf32_kr"
+                              : (kp.cnt ? "sgett_tc3xtf32_kr_splitk_fused" : "sgett_tc3xtf32_kr_splitk");
+  return 1;
+}
+
 // CTA-pair SGETT (sgett_tc.cu pair kernel) on the swapped roles: M2 = the
 // plan's N (a K-major B', its rows 256 per pair in TMEM), N2 = the plan's M
 // (a rows-major A' of <= 128 rows, split across the pair).  Returns 1 when
@@ -775,6 +1128,12 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     bool bnd = V == 2 ? dp.bn_even2 : dp.bn_even4;
     a_vec = a_kf ? vec_ok(gkA, akd, dp.gm, amd, V, A) : vec_ok(dp.gm, amd, gkA, akd, V, A);
     b_vec = b_kf ? vec_ok(gkB, bkd, dp.gn, bnd, V, B) : vec_ok(dp.gn, bnd, gkB, bkd, V, B);
+  }
+  if (use_tc && sizeof(T) == 4) {
+    const int kr = try_sgett_kr(dp, reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B),
+                                reinterpret_cast<float*>(c), neg, stream, ds, sw);
+    if (kr < 0) return kr;
+    if (kr > 0) return 0;
   }
   if (use_tc && sizeof(T) == 4) {
     const int pr = try_sgett_pair(dp, reinterpret_cast<const float*>(A), reinterpret_cast<const float*>(B),
@@ -2150,6 +2509,13 @@ int gett_set_complex_embed(int on) {
   return 0;
 }
 
+int gett_set_kr(int mode) {
+  if (mode < 0 || (mode & 3) == 3 || mode > 6) return GETT_E_INVALID_ARG;
+  g_kr = mode & 3;
+  g_kr_fused = (mode & 4) != 0;
+  return 0;
+}
+
 int gett_set_tma(int on) {
   if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
   g_tma = on != 0;
@@ -2184,7 +2550,7 @@ void gett_release_caches(void) {
           s->bytes = 0;
         }
     for (auto& sv : ds.sws)
-      for (Scratch* s : {&sv.second.ws, &sv.second.part, &sv.second.flags, &sv.second.cx})
+      for (Scratch* s : {&sv.second.ws, &sv.second.part, &sv.second.flags, &sv.second.cx, &sv.second.krsync})
         if (s->p) cudaFree(s->p);
     ds.sws.clear();
   }
@@ -2193,7 +2559,7 @@ void gett_release_caches(void) {
 
 // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed;
 // 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi,
-//       gett_multi_schedule, gett_pack[_device]
+//       gett_multi_schedule, gett_pack[_device], gett_set_kr
 int gett_abi_version(void) { return 104; }
 
 }  // extern "C"

@@ -123,6 +123,46 @@ struct TmaParams {
   TmaOperand op[2];
 };
 
+// SGETT "k-run" kernel (sgett_kr.cu): the TMEM operand X has a contiguous
+// inner k run of KR floats (KR % 8 == 0, <= 64) — one k-block is one whole
+// run, loaded as a dense [rows][KR] TMA box (long contiguous lines instead of
+// 32 B SW32 boxes) and split straight into TMEM; Y is rows-major ([KR k][NT
+// rows] boxes) and transposed into K-major hi/lo tiles for the MMA's B.  The
+// accumulator is [128 X rows][NT Y rows].  With split-K the partials land in
+// ws [splits][NY][MX] (x fastest) and, when epoch != 0, the CTAs of a tile
+// reduce them themselves (each its slice, in split order), else the separate
+// reduce kernel does (CUDA-graph capture: the epoch would be baked in).
+constexpr int KR_MAX_SPLITS = 256;
+constexpr int KR_MAX_TILES = 256;  // fused split-K reduce: tiles of one call
+struct KrParams {
+  float* C;
+  GroupDev gx, gy;  // tensor 1 = C offsets of X rows / Y rows
+  int32_t MX, NY, NT;
+  int32_t x_rows, y_rows;  // rows one X / Y box covers (<= 128 / <= NT; a multiple of the inner row extent)
+  int32_t tiles_x, tiles_y;
+  int32_t nkb, kpc, splits;  // k-blocks (k runs) in all, per split, splits
+  float* ws;
+  // fused split-K reduce (null: the separate reduce kernel): per tile an
+  // arrival counter that wraps to 0 after `splits` arrivals (atomicInc), a
+  // generation bumped by the last arriver, and per slice the generation it
+  // was last claimed for — self-resetting, so CUDA-graph replays are safe
+  uint32_t* cnt;    // [tiles]
+  uint32_t* gen;    // [tiles]
+  uint32_t* claim;  // [tiles][KR_MAX_SPLITS]: slot (t, s) only ever holds tile t's generations
+  int32_t neg;
+  int64_t spin_ns;  // bounded wait of a split for its tile's other splits
+  // shared-memory / TMEM layout (host-computed for this NT): lslots load
+  // slots [X raw 128 x (KR+4) | Y raw KR x NT] of lslot_bytes from 0,
+  // oslots operand slots [Y hi | Y lo] of oslot_bytes from o_off, barriers
+  // at bar_off; aslots TMEM A slots of 2 KR columns from a_col0 (after the NT
+  // accumulator columns)
+  int32_t lslots, oslots, aslots, lslot_bytes, oslot_bytes, o_off, bar_off, a_col0;
+  int32_t xnr, ynr, nko;                   // row dims of X / Y, outer k dims
+  int32_t xr_ext[3], xr_pos[3], yr_ext[3], yr_pos[3];
+  int32_t k_ext[2], xk_pos[2], yk_pos[2];  // outer k digits (inner first)
+  CUtensorMap mx, my;
+};
+
 // the fused epilogue's update: C + acc, or C + (-acc) == C - acc for neg
 template <typename T>
 __device__ __forceinline__ T epi(T c, T acc, int32_t neg) {

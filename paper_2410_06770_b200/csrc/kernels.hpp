@@ -88,6 +88,10 @@ cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bo
 // operands TMA-fed: A' K-major, B' rows-major with NBH-row boxes); split-K
 cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s);
 
+// k-run SGETT (sgett_kr.cu); KR in {8, 16, ..., 64}
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, cudaStream_t s);
+int sgett_kr_max_nt();
+
 int tiled_bm();
 int tiled_bn();
 int tiled_bk(int elt_bytes);

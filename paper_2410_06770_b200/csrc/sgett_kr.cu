@@ -1,0 +1,636 @@
+// SGETT "k-run" kernel: 3xTF32 on tcgen05 for contractions whose TMEM-side
+// operand X has a short contiguous inner k run (c5: orig-A rows hold 40
+// contiguous k).  Replaces the fp32 hot loop (kernel.py:48-78 for sgett) for
+// such calls.
+//
+// One k-block = one whole k run of KR floats (KR % 8 == 0, <= 64), so the
+// loads follow the data's own contiguity:
+//   * X (the accumulator's 128 rows): one TMA box [KR][rows] per k-block, no
+//     swizzle, landing dense as [row][KR] — for c5 the box reads 8 runs of
+//     2.5 KB (orig-A's k run and its next free mode are adjacent), where the
+//     SW32 K-major boxes of sgett_tc.cu issued one 32 B line per row per 8 k.
+//     The split warps read each row and write hi (the raw value: the tensor
+//     core truncates to tf32) and lo = x - trunc(x) into TMEM with
+//     tcgen05.st: X never has to be in a UMMA shared-memory layout.
+//   * Y (N = NT <= 128 columns, a multiple of 16; c5: 96, no padding): rows-
+//     major boxes [KR k][NT rows], transposed by the split warps into K-major
+//     no-swizzle core matrices (hi in place, lo in a small ring).
+//   * MMA warp: per 8-k step, tcgen05.mma.kind::tf32 hi*hi, lo*hi, hi*lo,
+//     A from TMEM, B from shared memory, M = 128, N = NT.
+//   * Split-K (few output tiles, long K): partials [splits][NY][MX] (x
+//     fastest), then the CTAs of a tile reduce them themselves: each
+//     publishes its partial and counts in with one atomicInc on the tile's
+//     counter (it wraps back to 0 after the last of the `splits` arrivals, so
+//     nothing needs resetting between launches or graph replays); the last
+//     arriver bumps the tile's generation; a CTA that sees the bump (bounded
+//     wait) claims its own slice of the tile for that generation, and the
+//     last arriver then claims whatever slice is still unclaimed (no
+//     co-residency assumption: a CTA that timed out leaves its slice to it).
+//     Each element is summed from -0.0 over the splits in order and added to
+//     C once — bitwise what the separate reduce kernel
+//     (kernels.cu gett_splitk_reduce_t_kernel) computes.
+#include <cstdint>
+#include <cstdio>
+
+#include "device.cuh"
+#include "kernels.hpp"
+#include "tmem_io.cuh"
+
+// tuning builds only: skip the TMA loads (1), the X split (2), the Y split (4)
+#ifndef GETT_KR_ABLATE
+#define GETT_KR_ABLATE 0
+#endif
+
+namespace gett {
+namespace kr {
+
+constexpr int WG = 128;
+constexpr int SPLIT = 2 * WG;
+constexpr int MMA_WARP = (WG + SPLIT) / 32;  // warp 12
+constexpr int THREADS = WG + SPLIT + 32;
+constexpr int NT_MAX = 128;
+constexpr uint32_t TMEM_COLS = 512;
+
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+
+constexpr int MAX_SLOTS = 8;
+constexpr int BAR_BYTES = 512;
+constexpr int SMEM_MAX = 227 * 1024;
+
+template <int KR>
+struct Cfg {
+  // X staging [row][XP]: the box is KR + 4 wide (4 out-of-bounds, zero-filled
+  // columns) so the row pitch is an odd multiple of 16 B modulo 128 B and a
+  // quarter warp's 16-byte row reads hit 8 distinct bank groups
+  static constexpr int XP = KR + 4;
+  static constexpr int XB = 128 * XP * 4;
+  static constexpr int XB_AL = (XB + 1023) / 1024 * 1024;  // Y starts 1 KB aligned
+  static constexpr int CHK = KR / 4;           // 16-byte k chunks of a row
+  static constexpr uint32_t SBO = CHK * 128;   // bytes between 8-row groups (K-major no swizzle)
+  static_assert(KR % 8 == 0 && KR >= 8 && KR <= 64, "k run");
+  static_assert(5 * MAX_SLOTS + 1 + 1 + 8 <= BAR_BYTES / 8, "barrier area");
+};
+
+__device__ __forceinline__ void mbar_init(uint32_t a, uint32_t n) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(n));
+}
+__device__ __forceinline__ void mbar_arrive(uint32_t a) {
+  asm volatile("{\n\t.reg .b64 st;\n\tmbarrier.arrive.shared::cta.b64 st, [%0];\n\t}" ::"r"(a) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void commit(uint32_t bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void mma_tf32(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+// K-major no-swizzle shared-memory descriptor (sm_100 version bit 46)
+__device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
+         (1ull << 46);
+}
+__device__ __forceinline__ float tf32_lo(float x) {
+  return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+__device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int32_t* c, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// row coordinates of a tile's first row over up to 3 row dims (inner first)
+__device__ __forceinline__ void row_coords(int32_t* c, int row0, int nr, const int32_t* ext, const int32_t* pos) {
+  int q = row0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {
+    if (i < nr) {
+      const int v = q % ext[i];
+      q /= ext[i];
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (pos[i] == j) c[j] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ uint32_t ld_acquire_u32(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// claim a slice for generation g: true for exactly one caller per generation
+__device__ __forceinline__ bool claim_gen(uint32_t* p, uint32_t g) {
+  uint32_t cur = *reinterpret_cast<volatile uint32_t*>(p);
+  while (cur != g) {
+    const uint32_t prev = atomicCAS(p, cur, g);
+    if (prev == cur) return true;
+    cur = prev;
+  }
+  return false;
+}
+
+// sum of slice `sl` of tile (x0, y0) over the splits, added to C (threads t
+// of nthr).  Every partial of a thread's two elements is loaded before the
+// in-order sums (one L2 round trip per 32 splits instead of one per 8).
+__device__ __forceinline__ void reduce_slice(const KrParams& p, int x0, int y0, int sl, int t, int nthr) {
+  const int64_t E = (int64_t)128 * p.NT;  // tile grid: x = e & 127 (< x_rows), y = e >> 7 (< y_rows)
+  const int64_t e0 = E * sl / p.splits, e1 = E * (sl + 1) / p.splits;
+  const int64_t mn = (int64_t)p.MX * p.NY;
+  for (int64_t eb = e0 + t; eb < e1; eb += 2 * nthr) {
+    const float* w[2];
+    bool ok[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int64_t e = eb + u * nthr;
+      const int x = x0 + (int)(e & 127), y = y0 + (int)(e >> 7);
+      ok[u] = e < e1 && (int)(e & 127) < p.x_rows && (int)(e >> 7) < p.y_rows && x < p.MX && y < p.NY;
+      w[u] = ok[u] ? p.ws + (int64_t)y * p.MX + x : p.ws;
+    }
+    float s[2] = {-0.0f, -0.0f};
+    for (int sp0 = 0; sp0 < p.splits; sp0 += 32) {
+      float v[2][32];
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) v[u][j] = (ok[u] && sp0 + j < p.splits) ? __ldcg(w[u] + (sp0 + j) * mn) : 0.f;
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          if (sp0 + j < p.splits) s[u] = s[u] + v[u][j];
+    }
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      if (!ok[u]) continue;
+      const int64_t e = eb + u * nthr;
+      const int x = x0 + (int)(e & 127), y = y0 + (int)(e >> 7);
+      float* c = p.C + p.gx.off(1, x) + p.gy.off(1, y);
+      *c = epi(*c, s[u], p.neg);
+    }
+  }
+}
+
+template <int KR>
+__global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_constant__ KrParams p) {
+  using G = Cfg<KR>;
+  // three rings: load slots [X raw | Y raw] (TMA -> split; freed by the split
+  // warps as soon as they have read them, so the loads run ahead by SL
+  // k-blocks), operand slots [Y hi | Y lo] K-major (split -> MMA; freed by the
+  // MMA's commit) and TMEM A slots (hi, lo columns; freed by the commit).
+  // SL even and SO == 2 (host): each split warpgroup then waits only on its
+  // own load / operand slots, never on a barrier two phases ahead.
+  const int SL = p.lslots, SO = p.oslots, TA = p.aslots;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);  // [SL] TMA landed
+  uint64_t* lfree = full + MAX_SLOTS;                              // [SL] split read it
+  uint64_t* ready = lfree + MAX_SLOTS;                             // [SO] operands + TMEM A written
+  uint64_t* ofree = ready + MAX_SLOTS;                             // [SO] MMAs done with the operands
+  uint64_t* afree = ofree + MAX_SLOTS;                             // [TA] MMAs done with the TMEM A slot
+  uint64_t* done = afree + MAX_SLOTS;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  int* sh = reinterpret_cast<int*>(tmem_slot + 2);  // epilogue broadcast words
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+#ifdef GETT_KR_TRACE
+  const long long tr_c0 = clock64();
+  const unsigned long long tr_start = globaltimer();
+  unsigned long long tr_done = 0, tr_arr = 0, tr_own = 0;
+  int tr_n = 0;
+#endif
+
+  const int ntiles = p.tiles_x * p.tiles_y;
+  const int tile = blockIdx.x % ntiles, split = blockIdx.x / ntiles;
+  const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+  const int x0 = tx * p.x_rows, y0 = ty * p.y_rows;
+  const int kb0 = split * p.kpc;
+  const int nkb = max(0, min(p.nkb, kb0 + p.kpc) - kb0);
+  const uint32_t tile_bytes = (uint32_t)(KR * p.y_rows * 4);  // the Y box (raw [KR][y_rows])
+
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.mx) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&p.my) : "memory");
+    for (int s = 0; s < SL; ++s) {
+      mbar_init(smem_u32(full + s), 1);
+      mbar_init(smem_u32(lfree + s), 4);  // the 4 warps of the split warpgroup
+    }
+    for (int s = 0; s < SO; ++s) {
+      mbar_init(smem_u32(ready + s), 4);
+      mbar_init(smem_u32(ofree + s), 1);  // tcgen05.commit
+    }
+    for (int s = 0; s < TA; ++s) mbar_init(smem_u32(afree + s), 1);
+    mbar_init(smem_u32(done), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------- TMA producer (one thread) ----------------
+    if (lane == 0 && nkb > 0) {
+      int32_t cx[5] = {0, 0, 0, 0, 0}, cy[5] = {0, 0, 0, 0, 0};
+      row_coords(cx, x0, p.xnr, p.xr_ext, p.xr_pos);
+      row_coords(cy, y0, p.ynr, p.yr_ext, p.yr_pos);
+      int d0 = 0, d1 = 0;  // outer k digits of k-block kb0
+      if (p.nko > 0) {
+        d0 = kb0 % p.k_ext[0];
+        d1 = kb0 / p.k_ext[0];
+      }
+      const uint32_t sbase = smem_u32(smem);
+#ifdef GETT_KR_TRACE
+      long long w_empty = 0;
+#endif
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % SL, u = kb / SL;
+#ifdef GETT_KR_TRACE
+        const long long c0 = clock64();
+#endif
+        if (u > 0) mbar_wait(smem_u32(lfree + s), (u - 1) & 1);
+#ifdef GETT_KR_TRACE
+        w_empty += clock64() - c0;
+#endif
+        const uint32_t fb = smem_u32(full + s);
+        int32_t a[5], b[5];
+#pragma unroll
+        for (int j = 0; j < 5; ++j) {
+          a[j] = cx[j] + (p.nko > 0 && p.xk_pos[0] == j ? d0 : 0) + (p.nko > 1 && p.xk_pos[1] == j ? d1 : 0);
+          b[j] = cy[j] + (p.nko > 0 && p.yk_pos[0] == j ? d0 : 0) + (p.nko > 1 && p.yk_pos[1] == j ? d1 : 0);
+        }
+        if (GETT_KR_ABLATE & 1) {
+          mbar_arrive(fb);
+        } else {
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                       "r"((uint32_t)(p.x_rows * G::XP * 4) + tile_bytes)
+                       : "memory");
+          tma_load5(sbase + s * p.lslot_bytes, &p.mx, a, fb);
+          tma_load5(sbase + s * p.lslot_bytes + G::XB_AL, &p.my, b, fb);
+        }
+        if (p.nko > 0 && ++d0 == p.k_ext[0]) {
+          d0 = 0;
+          ++d1;
+        }
+      }
+#ifdef GETT_KR_TRACE
+      if (blockIdx.x < 2) printf("KRROLE blk %d producer wait_lfree %lld\n", blockIdx.x, w_empty);
+#endif
+    }
+  } else if (warp < 4) {
+    // idle
+  } else if (warp < MMA_WARP) {
+    // ---------------- split warpgroups (alternate k-blocks), then epilogue ----------------
+    const int h = (warp - 4) >> 2, wq = warp & 3, tw = (tid - WG) & (WG - 1);
+    // this thread's Y blocks (chunk c of 4 k, row quad rq): source byte offset
+    // in the [KR][NT] box, destination of the quad's first row in the K-major
+    // tiles, store rotation
+    constexpr int YU = (G::CHK * (NT_MAX / 4) + WG - 1) / WG;
+    uint32_t y_src[YU], y_dst[YU];
+    int y_rot[YU];
+    const int nq = p.y_rows >> 2;  // row quads of the box (y_rows % 4 == 0)
+    int ny_units = 0;
+#pragma unroll
+    for (int i = 0; i < YU; ++i) {
+      const int uu = tw + WG * i;
+      const int c = uu / nq, rq = uu - c * nq;
+      y_src[i] = (uint32_t)(4 * c * p.y_rows * 4 + rq * 16);
+      y_dst[i] = (uint32_t)(((4 * rq) >> 3) * G::SBO + c * 128 + ((4 * rq) & 7) * 16);
+      y_rot[i] = (rq >> 1) & 3;
+      if (uu < G::CHK * nq) ny_units = i + 1;
+    }
+#ifdef GETT_KR_TRACE
+    long long w_full = 0, w_lo = 0, t_x = 0, t_y = 0;
+#endif
+    for (int kb = h; kb < nkb; kb += 2) {
+      const int sl = kb % SL, so = kb % SO, sa = kb % TA;
+#ifdef GETT_KR_TRACE
+      long long c0 = clock64();
+#endif
+      mbar_wait(smem_u32(full + sl), (kb / SL) & 1);
+#ifdef GETT_KR_TRACE
+      w_full += clock64() - c0;
+      c0 = clock64();
+#endif
+      if (kb >= TA) mbar_wait(smem_u32(afree + sa), (kb / TA - 1) & 1);
+      if (kb >= SO) mbar_wait(smem_u32(ofree + so), (kb / SO - 1) & 1);
+#ifdef GETT_KR_TRACE
+      w_lo += clock64() - c0;
+      c0 = clock64();
+#endif
+      const uint8_t* st = smem + sl * p.lslot_bytes;
+      uint8_t* hi_t = smem + p.o_off + so * p.oslot_bytes;
+      uint8_t* lo_t = hi_t + p.oslot_bytes / 2;
+      // X row -> TMEM hi / lo columns of slot sa, 16 (then 8) columns at a time
+      if (!(GETT_KR_ABLATE & 2)) {
+        const int row = 32 * wq + lane;
+        const float4* xr = reinterpret_cast<const float4*>(st + row * G::XP * 4);
+        const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(p.a_col0 + sa * 2 * KR);
+#pragma unroll
+        for (int c = 0; c < KR; c += 16) {
+          constexpr int W = 16;
+          const int n = KR - c >= W ? W : 8;
+          uint32_t hv[W], lv[W];
+#pragma unroll
+          for (int q = 0; q < W / 4; ++q) {
+            if (4 * q < n) {
+              const float4 v = xr[c / 4 + q];
+              const float f[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int j = 0; j < 4; ++j) {
+                hv[4 * q + j] = __float_as_uint(f[j]);
+                lv[4 * q + j] = __float_as_uint(tf32_lo(f[j]));
+              }
+            }
+          }
+          if (n == W) {
+            tmemio::tst16(ta + c, hv);
+            tmemio::tst16(ta + KR + c, lv);
+          } else {
+            tmemio::tst8(ta + c, hv);
+            tmemio::tst8(ta + KR + c, lv);
+          }
+        }
+      }
+#ifdef GETT_KR_TRACE
+      t_x += clock64() - c0;
+      c0 = clock64();
+#endif
+      // Y [KR][NT] raw -> K-major hi + lo tiles of operand slot so, in 4 k x 4
+      // row blocks: four 16-byte row-quad loads (one per k), a register
+      // transpose, and per row one 16-byte store of 4 k to hi and to lo; the
+      // stores are rotated by the row quad so a quarter warp covers the 8
+      // rows of a core matrix (conflict-free)
+      if (!(GETT_KR_ABLATE & 4)) {
+        const uint8_t* yb = st + G::XB_AL;
+#pragma unroll
+        for (int i = 0; i < YU; ++i) {
+          if (i < ny_units) {
+            float4 v[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(yb + y_src[i] + j * p.y_rows * 4);
+            float4 rows[4];
+            rows[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+            rows[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+            rows[2] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+            rows[3] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+            const int rot = y_rot[i];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              float4 r = rows[0];
+              const int rq = (q + rot) & 3;
+              r = rq == 1 ? rows[1] : r;
+              r = rq == 2 ? rows[2] : r;
+              r = rq == 3 ? rows[3] : r;
+              const uint32_t o = y_dst[i] + rq * 16;
+              *reinterpret_cast<float4*>(hi_t + o) = r;
+              *reinterpret_cast<float4*>(lo_t + o) = make_float4(tf32_lo(r.x), tf32_lo(r.y), tf32_lo(r.z), tf32_lo(r.w));
+            }
+          }
+        }
+      }
+      // the load slot is free once every warp of the group has read it
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(lfree + sl));
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(ready + so));
+#ifdef GETT_KR_TRACE
+      t_y += clock64() - c0;
+#endif
+    }
+#ifdef GETT_KR_TRACE
+    if (blockIdx.x < 2 && (tid & 127) == 0)
+      printf("KRROLE blk %d split%d wait_full %lld wait_slots %lld x %lld y %lld\n", blockIdx.x, h, w_full, w_lo, t_x, t_y);
+#endif
+    if (nkb > 0) mbar_wait(smem_u32(done), 0);
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#ifdef GETT_KR_TRACE
+    tr_done = globaltimer();
+#endif
+    // ---------------- epilogue ----------------
+    // (rows >= x_rows and columns >= y_rows of the accumulator hold garbage:
+    // the boxes did not fill them)
+    const int row = 32 * wq + lane, x = row < p.x_rows ? x0 + row : p.MX;
+    const int half = p.NT >> 1, cbeg = h * half;
+    uint32_t rr[64];
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (8 * q < half)
+        tmemio::tld8(tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(cbeg + 8 * q), rr + 8 * q);
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#ifdef GETT_KR_TRACE
+    const unsigned long long tr_ld = globaltimer();
+    unsigned long long tr_st = 0, tr_fe = 0, tr_a0 = 0;
+#endif
+    if (p.splits == 1) {
+      if (x < p.MX) {
+        const int64_t ox = p.gx.off(1, x);
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int y = y0 + cbeg + i;
+          if (i < half && cbeg + i < p.y_rows && y < p.NY) {
+            float* c = p.C + ox + p.gy.off(1, y);
+            *c = epi(*c, nkb > 0 ? __uint_as_float(rr[i]) : -0.0f, p.neg);
+          }
+        }
+      }
+    } else {
+      const int64_t mn = (int64_t)p.MX * p.NY;
+      if (x < p.MX) {
+        float* w = p.ws + split * mn + x;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int y = y0 + cbeg + i;
+          if (i < half && cbeg + i < p.y_rows && y < p.NY)
+            __stcg(w + (int64_t)y * p.MX, nkb > 0 ? __uint_as_float(rr[i]) : -0.0f);
+        }
+      }
+      if (p.cnt != nullptr) {
+        // fused reduce: count in, then reduce the slices this CTA claims
+        const int t = tid - WG;  // 0..255 over the two warpgroups
+#ifdef GETT_KR_TRACE
+        tr_st = globaltimer();
+#endif
+        __threadfence();
+#ifdef GETT_KR_TRACE
+        tr_fe = globaltimer();
+#endif
+        asm volatile("bar.sync 3, %0;" ::"n"(SPLIT) : "memory");
+        uint32_t* claims = p.claim + (int64_t)tile * KR_MAX_SPLITS;
+        if (t == 0) {
+          // the generation before this launch's arrivals (the last arriver
+          // bumps it only after every split, this one included, arrived)
+          const uint32_t g0 = *reinterpret_cast<volatile uint32_t*>(p.gen + tile);
+          uint32_t old;
+          asm volatile("atom.acq_rel.gpu.global.inc.u32 %0, [%1], %2;" : "=r"(old) : "l"(p.cnt + tile), "r"((uint32_t)p.splits - 1) : "memory");
+#ifdef GETT_KR_TRACE
+          tr_a0 = globaltimer();
+#endif
+          int mine;
+          if (old == (uint32_t)p.splits - 1) {
+            asm volatile("red.release.gpu.global.add.u32 [%0], 1;" ::"l"(p.gen + tile) : "memory");
+            mine = 2;  // last arriver: own slice, then every unclaimed one
+          } else {
+            const unsigned long long t0 = globaltimer();
+            while (ld_acquire_u32(p.gen + tile) == g0) {
+              if (globaltimer() - t0 > (unsigned long long)p.spin_ns) break;
+              __nanosleep(32);
+            }
+            mine = ld_acquire_u32(p.gen + tile) != g0 ? 1 : 0;
+          }
+          sh[0] = mine;
+          sh[1] = (mine && claim_gen(claims + split, g0 + 1)) ? 1 : 0;
+          sh[2] = (int)(g0 + 1);
+        }
+        asm volatile("bar.sync 3, %0;" ::"n"(SPLIT) : "memory");
+        const int mine = sh[0];
+        const uint32_t g1 = (uint32_t)sh[2];
+#ifdef GETT_KR_TRACE
+        tr_arr = globaltimer();
+        tr_n = sh[1];
+#endif
+        if (sh[1]) reduce_slice(p, x0, y0, split, t, SPLIT);
+#ifdef GETT_KR_TRACE
+        tr_own = globaltimer();
+#endif
+        if (mine == 2) {
+          // after its own slice, the last arriver claims every slice still
+          // unclaimed (owners that timed out) in one parallel round: thread t
+          // tries slice t, the winners' bits gather in shared memory
+          uint32_t* won = reinterpret_cast<uint32_t*>(sh + 4);
+          if (t < 8) won[t] = 0;
+          asm volatile("bar.sync 3, %0;" ::"n"(SPLIT) : "memory");
+          for (int sl = t; sl < p.splits; sl += SPLIT)
+            if (sl != split && claim_gen(claims + sl, g1)) atomicOr(&won[(sl >> 5) & 7], 1u << (sl & 31));
+          asm volatile("bar.sync 3, %0;" ::"n"(SPLIT) : "memory");
+          for (int sl = 0; sl < p.splits && sl < 256; ++sl)
+            if ((won[sl >> 5] >> (sl & 31)) & 1u) {
+              reduce_slice(p, x0, y0, sl, t, SPLIT);
+#ifdef GETT_KR_TRACE
+              tr_n += 100;
+#endif
+            }
+        }
+#ifdef GETT_KR_TRACE
+        if (t == 0)
+          printf("KRTRACE blk %d tile %d split %d start %llu done %llu ld %llu st %llu fe %llu a0 %llu arr %llu own %llu end %llu mine %d n %d clk %lld\n",
+                 blockIdx.x, tile, split, tr_start, tr_done, tr_ld, tr_st, tr_fe, tr_a0, tr_arr, tr_own, globaltimer(), mine, tr_n, clock64() - tr_c0);
+#endif
+      }
+    }
+  } else {
+    // ---------------- MMA warp ----------------
+    if (lane == 0 && nkb > 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.NT >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t sbase = smem_u32(smem);
+#ifdef GETT_KR_TRACE
+      long long w_ready = 0, t_issue = 0;
+      unsigned long long g_first = 0;
+#endif
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int so = kb % SO, sa = kb % TA;
+#ifdef GETT_KR_TRACE
+        long long c0 = clock64();
+#endif
+        mbar_wait(smem_u32(ready + so), (kb / SO) & 1);
+#ifdef GETT_KR_TRACE
+        w_ready += clock64() - c0;
+        c0 = clock64();
+        if (kb == 0) g_first = globaltimer();
+#endif
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t hb = sbase + p.o_off + so * p.oslot_bytes;
+        const uint32_t lb = hb + p.oslot_bytes / 2;
+        const uint32_t ah0 = tmem + p.a_col0 + sa * 2 * KR;
+#pragma unroll
+        for (int j = 0; j < KR / 8; ++j) {
+          const uint64_t bh = sdesc(hb + 256 * j, 128, G::SBO);
+          const uint64_t bl = sdesc(lb + 256 * j, 128, G::SBO);
+          const uint32_t ah = ah0 + 8 * j, al = ah + KR;
+          // (hi*hi, hi*lo_Y, lo_X*hi: the tiled kernel's order when its TMEM
+          // operand is this kernel's Y — c5 — so both give the same bits there)
+          mma_tf32(tmem, ah, bh, idesc, (kb | j) != 0);
+          mma_tf32(tmem, ah, bl, idesc, 1);
+          mma_tf32(tmem, al, bh, idesc, 1);
+        }
+        commit(smem_u32(ofree + so));
+        commit(smem_u32(afree + sa));
+#ifdef GETT_KR_TRACE
+        t_issue += clock64() - c0;
+#endif
+      }
+      commit(smem_u32(done));
+#ifdef GETT_KR_TRACE
+      if (blockIdx.x < 4) printf("KRROLE blk %d mma wait_ready %lld issue %lld nkb %d first_ready_ns %llu loop_ns %llu since_start_ns %llu\n", blockIdx.x, w_ready, t_issue, nkb,
+                                 g_first - tr_start, globaltimer() - g_first, globaltimer() - tr_start);
+#endif
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == MMA_WARP)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+
+template <int KR>
+cudaError_t launch_t(const KrParams& p, cudaStream_t s) {
+  auto k = sgett_kr_kernel<KR>;
+  static unsigned long long configured = 0;
+  cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured);
+  if (e != cudaSuccess) return e;
+  k<<<(unsigned)(p.tiles_x * p.tiles_y * p.splits), THREADS, p.bar_off + BAR_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace kr
+
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, cudaStream_t s) {
+  switch (KR) {
+    case 8: return kr::launch_t<8>(p, s);
+    case 16: return kr::launch_t<16>(p, s);
+    case 24: return kr::launch_t<24>(p, s);
+    case 32: return kr::launch_t<32>(p, s);
+    case 40: return kr::launch_t<40>(p, s);
+    case 48: return kr::launch_t<48>(p, s);
+    case 56: return kr::launch_t<56>(p, s);
+    case 64: return kr::launch_t<64>(p, s);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+int sgett_kr_max_nt() { return kr::NT_MAX; }
+
+}  // namespace gett

@@ -16,10 +16,11 @@ def pytest_configure(config):
 @pytest.fixture
 def kernel_mode():
     """Set the native kernel family for one test, restoring auto after."""
-    from paper_2410_06770_b200 import (set_complex_embed, set_kernel, set_pair, set_pipeline, set_split_k,
-                                       set_stream_k, set_tma)
+    from paper_2410_06770_b200 import (set_complex_embed, set_kernel, set_kr, set_pair, set_pipeline,
+                                       set_split_k, set_stream_k, set_tma)
 
-    def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True):
+    def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
+            kr="auto", kr_fused=False):
         set_kernel(name)
         set_split_k(split)
         set_pipeline(pipeline)
@@ -27,6 +28,7 @@ def kernel_mode():
         set_tma(tma)
         set_pair(pair)
         set_complex_embed(complex_embed)
+        set_kr(kr, kr_fused)
 
     yield use
     set_kernel("auto")
@@ -36,3 +38,4 @@ def kernel_mode():
     set_tma(True)
     set_pair(False)
     set_complex_embed(True)
+    set_kr("auto")

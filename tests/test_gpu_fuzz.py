@@ -84,7 +84,9 @@ def test_random_descriptors(dtype, kernel_mode):
         c0 = rng.uniform(-1, 1, off_c + span_c + 4).astype(np_t)
         outs = []
         for tma in ((True, False) if dtype == "s" else (True,)):
-            kernel_mode("tiled", tma=tma)
+            # (the tcgen05 kernel's TMA and gather paths: same MMAs, same k
+            # order; the k-run kernel has its own tests, test_gpu_kr.py)
+            kernel_mode("tiled", tma=tma, kr="off")
             c = c0.copy()
             assert entry(len(ext_a), tuple(ext_a), inc_a, a, len(ext_b), tuple(ext_b), inc_b, b, conts, cont_a,
                          cont_b, perm, inc_c, c, offset_a=off_a, offset_b=off_b, offset_c=off_c) == []

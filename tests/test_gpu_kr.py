@@ -1,0 +1,151 @@
+"""The SGETT k-run kernel (sgett_kr.cu): one k-block = the TMEM operand's
+whole contiguous inner k run (<= 64 floats; longer runs are cut into 64-or-
+smaller pieces), dense [rows][KR+4] TMA boxes, the rows-major operand
+transposed into K-major hi/lo tiles, and split-K partials reduced either
+inside the kernel (tile counters, generations, slice claims) or by the
+separate reduce kernel.
+
+Every case: within the K-normalised fp32 bar of an fp64 contraction, bytes
+outside C's view untouched, and the fused and separate reduces bitwise equal
+(same partials, same order).  Shapes cover both operand orientations (C's
+fast mode in either operand), run lengths 8..64 and a cut 128-run, output
+widths that need N padding (40 -> 48) or several column tiles (200, 300),
+row counts off the 128 grid, and forced split counts."""
+import numpy as np
+import pytest
+
+import paper_2410_06770_b200 as g
+from paper_2410_06770_b200.workloads import C5
+
+pytestmark = pytest.mark.gpu
+
+
+def _strided(buf, ext, inc, off):
+    return np.lib.stride_tricks.as_strided(buf[off:], shape=ext, strides=[i * buf.itemsize for i in inc])
+
+
+def _case(m1, m2, kr, k2, n, c_m_fast, seed):
+    """A[m1][m2][k2][kr] (kr contiguous, padded rows), B[kr][k2][n] (n
+    contiguous), contract (k2, kr); C[m1][m2][n] with m2 or n fastest."""
+    rng = np.random.default_rng(seed)
+    ext_a = (m1, m2, k2, kr)
+    a_inc = (m2 * k2 * kr + 8, k2 * kr, kr, 1)
+    ext_b = (kr, k2, n)
+    nb = n + (4 - n % 4) % 4 + 4
+    b_inc = (k2 * nb, nb, 1)
+    if c_m_fast:
+        c_inc = (m2 + 4, 1, m1 * (m2 + 4) + 4)
+    else:
+        c_inc = (m2 * (n + 4), n + 4, 1)
+    span = lambda e, i: sum((x - 1) * y for x, y in zip(e, i)) + 1  # noqa: E731
+    a = rng.uniform(-1, 1, span(ext_a, a_inc) + 8).astype(np.float32)
+    b = rng.uniform(-1, 1, span(ext_b, b_inc) + 8).astype(np.float32)
+    off_c = 4
+    c = rng.uniform(-1, 1, off_c + span((m1, m2, n), c_inc) + 8).astype(np.float32)
+    pos = (4, ext_a, a_inc, a, 3, ext_b, b_inc, b, 2, (2, 3), (1, 0), (0, 1, 2), c_inc, c)
+    return pos, {"offset_c": off_c}
+
+
+def _check(pos, kw, c0):
+    (ra, ext_a, inc_a, a, rb, ext_b, inc_b, b, _, _, _, _, inc_c, c) = pos
+    A = _strided(a, ext_a, inc_a, 0).astype(np.float64)
+    B = _strided(b, ext_b, inc_b, 0).astype(np.float64)
+    ext_c = (ext_a[0], ext_a[1], ext_b[2])
+    want = _strided(c0, ext_c, inc_c, kw["offset_c"]).astype(np.float64) + np.einsum("abjk,kjn->abn", A, B)
+    got = _strided(c, ext_c, inc_c, kw["offset_c"]).astype(np.float64)
+    K = ext_a[2] * ext_a[3]
+    err = np.max(np.abs(got - want)) / (K * np.abs(a).max() * np.abs(b).max())
+    assert err <= 1e-5, err
+    mask = np.ones(len(c0), bool)
+    idx = kw["offset_c"] + sum(np.ix_(*[np.arange(e) * i for e, i in zip(ext_c, inc_c)]))
+    mask[np.asarray(idx).ravel()] = False
+    assert c[mask].tobytes() == c0[mask].tobytes()
+
+
+SHAPES = [
+    # (m1, m2, kr, k2, n)
+    (6, 16, 40, 24, 96),     # c5-like
+    (3, 50, 8, 64, 128),
+    (2, 64, 16, 30, 40),     # N padded 40 -> 48
+    (5, 40, 24, 20, 200),    # two column tiles
+    (1, 200, 32, 12, 300),   # three column tiles, 200 rows
+    (4, 32, 48, 10, 64),
+    (2, 48, 56, 9, 80),
+    (3, 33, 64, 8, 64),
+    (2, 64, 128, 6, 96),     # a 128-run cut into 64-float k-blocks
+]
+
+
+@pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("c_m_fast", [True, False])
+@pytest.mark.parametrize("split", [0, 1, 5])
+def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, kernel_mode):
+    m1, m2, kr, k2, n = shape
+    outs = []
+    for fused in (True, False):
+        pos, kw = _case(m1, m2, kr, k2, n, c_m_fast, seed=sum(shape) + split)
+        c0 = pos[13].copy()
+        kernel_mode("tiled", split=split, kr="force", kr_fused=fused)
+        assert g.sgett(*pos, **kw) == []
+        kname = g.last_kernel()
+        assert kname.startswith("sgett_tc3xtf32_kr"), kname
+        _check(pos, kw, c0)
+        outs.append(pos[13])
+    assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_kr_auto_on_c5_and_off_for_large_tilings(kernel_mode):
+    """Automatic choice: c5 (a 40-float run, 6 output tiles) takes the
+    k-run kernel; a 1024^3 GEMM (64 tiles, 64-float k-blocks) does not."""
+    kernel_mode("auto")
+    a, b, c = C5.buffers()
+    pos, kw = C5.args(a, b, c)
+    assert g.sgett(*pos, **kw) == []
+    assert g.last_kernel().startswith("sgett_tc3xtf32_kr")
+    rng = np.random.default_rng(1)
+    A = rng.uniform(-1, 1, 1024 * 1024).astype(np.float32)
+    B = rng.uniform(-1, 1, 1024 * 1024).astype(np.float32)
+    C = np.zeros(1024 * 1024, np.float32)
+    assert g.sgett(2, (1024, 1024), (1024, 1), A, 2, (1024, 1024), (1024, 1), B, 1, (1,), (0,), (0, 1),
+                   (1024, 1), C) == []
+    assert "kr" not in g.last_kernel()
+
+
+def test_kr_c5_equals_tiled_bitwise(kernel_mode):
+    """On c5 both tcgen05 kernels cut K at the same points (1280 = 32 runs of
+    40 = 80 blocks of 16) and issue the same MMAs in the same k order: the
+    results are bit-identical."""
+    outs = []
+    for kr in ("force", "off"):
+        kernel_mode("tiled", kr=kr)
+        a, b, c = C5.buffers()
+        pos, kw = C5.args(a, b, c)
+        assert g.sgett(*pos, **kw) == []
+        outs.append(c)
+    assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_kr_graph_replay_fused(kernel_mode):
+    """The fused reduce's counters reset themselves: a CUDA graph of a k-run
+    split-K call replays to the same bits as direct calls."""
+    import torch
+
+    from paper_2410_06770_b200.device import sgett_device
+    from paper_2410_06770_b200.graph import GettGraph
+
+    kernel_mode("tiled", kr="force")
+    w = C5.slice_free("A", 0, 0, 16)
+    a, b, c = w.buffers()
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    direct = torch.from_numpy(c).cuda()
+    pos, kw = w.args(ta, tb, direct)
+    for _ in range(3):
+        assert sgett_device(*pos, **kw) == []
+    tc = torch.from_numpy(c).cuda()
+    pos, kw = w.args(ta, tb, tc)
+    gg = GettGraph(sgett_device, *pos, **kw)
+    assert g.last_kernel().startswith("sgett_tc3xtf32_kr")
+    for _ in range(2):
+        gg.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(tc, direct)

@@ -99,7 +99,7 @@ def test_tma_matches_gathers_and_fp64(name, a_kf, b_kf, c_row, split, kernel_mod
                                                 c_row, 7)
     outs, kernels = [], []
     for tma in (True, False):
-        kernel_mode("tiled", split=split, tma=tma)
+        kernel_mode("tiled", split=split, tma=tma, kr="off")
         c = c0.copy()
         kernels.append(_contract(a, a_dims, a_inc, off_a, b, b_dims, b_inc, c, c_inc, off_c,
                                  len(cont_a), cont_a, cont_b))
@@ -129,7 +129,7 @@ def test_tma_matches_gathers_and_fp64(name, a_kf, b_kf, c_row, split, kernel_mod
 
 def test_tma_taken_for_affine_views(kernel_mode):
     """The gemm-shaped affine case runs the TMA kernel (evidence of the path)."""
-    kernel_mode("tiled")
+    kernel_mode("tiled", kr="off")
     a_dims, b_dims, cont_a, cont_b = CASES["gemm"]
     a_inc, _ = _inc(a_dims, [2, 1, 0])
     b_inc, _ = _inc(b_dims, [2, 1, 0])
@@ -142,7 +142,7 @@ def test_tma_taken_for_affine_views(kernel_mode):
 def test_tma_falls_back_on_negative_strides(kernel_mode):
     """A negative-stride A view is not a TMA box: the gathers run, and the
     result still matches fp64."""
-    kernel_mode("tiled")
+    kernel_mode("tiled", kr="off")
     a_dims, b_dims, cont_a, cont_b = CASES["gemm"]
     a_inc, _ = _inc(a_dims, [2, 1, 0])
     b_inc, _ = _inc(b_dims, [2, 1, 0])
@@ -174,7 +174,7 @@ def test_pair_kernel_matches_single_cta(M, N, K1, K2, kernel_mode):
     c0 = rng.uniform(-1, 1, (M + 4) * N + 8).astype(np.float32)
     outs, kernels = [], []
     for pair in (True, False):
-        kernel_mode("tiled", pair=pair)
+        kernel_mode("tiled", pair=pair, kr="off")
         c = c0.copy()
         assert g.sgett(3, a_dims, a_inc, a, 3, b_dims, b_inc, b, 2, (1, 2), (1, 2), (0, 1), (1, M + 4), c,
                        offset_c=2) == []

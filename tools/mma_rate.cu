@@ -149,9 +149,116 @@ void runp(long long* d) {
          "\"ideal\": 384, \"err\": \"%s\"}\n", ABASE, (int)COMMIT, (double)h / kb, cudaGetErrorString(e));
 }
 
+// the k-run kernel's pattern (sgett_kr.cu): per k-block KR/8 k-steps x 3
+// MMAs, M = 128, N = NT, A from TMEM, B K-major no-swizzle with SBO = KR/4 x 128
+template <int NT, int KR, bool RND, int FENCE = 0>
+__global__ void pattern_kr(long long* out, int kblocks) {
+  extern __shared__ __align__(1024) uint8_t sm[];
+  constexpr int STG = 4, TB = NT * KR * 4, SB = 2 * TB;
+  uint64_t* bar = (uint64_t*)(sm + STG * SB);
+  uint32_t* slot = (uint32_t*)(bar + STG + 1);
+  for (int i = threadIdx.x; i < STG * SB / 4; i += blockDim.x) {
+    uint32_t h = (uint32_t)i * 2654435761u + 12345u;
+    h ^= h >> 13;
+    h *= 0x5bd1e995u;
+    ((float*)sm)[i] = RND ? ((float)(h & 0xffffff) / 16777216.0f - 0.5f) : 0.f;
+  }
+  if (threadIdx.x == 0) {
+    for (int i = 0; i <= STG; ++i) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar + i)));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+  }
+  if (threadIdx.x < 32) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(su32(slot)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("fence.proxy.async.shared::cta;");
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *slot;
+  if (RND) {  // random A columns in TMEM (each warp its lane quarter)
+    const int w = threadIdx.x >> 5;
+    for (int c = 0; c < 384; c += 8) {
+      uint32_t v[8];
+      for (int j = 0; j < 8; ++j) {
+        uint32_t h = (uint32_t)(threadIdx.x * 977 + c * 131 + j * 7919) * 2654435761u;
+        h ^= h >> 15;
+        v[j] = __float_as_uint((float)(h & 0xffffff) / 16777216.0f - 0.5f);
+      }
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(tmem + ((uint32_t)(32 * w) << 16) + 128 + c),
+                   "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]) : "memory");
+    }
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;");
+    __syncthreads();
+    asm volatile("tcgen05.fence::after_thread_sync;");
+  }
+  constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
+  if (threadIdx.x == 0) {
+    const uint32_t base = su32(sm);
+    long long t0 = clock64();
+    for (int kb = 0; kb < kblocks; ++kb) {
+      const int s = kb % STG;
+      const uint32_t sb = base + s * SB;
+      // FENCE n: every n-th k-block waits on an (already completed) mbarrier
+      // phase and issues tcgen05.fence::after_thread_sync, as the kernels do
+      // after their `ready` waits
+      if (FENCE && kb % FENCE == 0) {
+        asm volatile("{\n\t.reg .pred P1;\nWF_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 1;\n\t@!P1 bra WF_%=;\n\t}" ::"r"(su32(bar + STG)));
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      }
+      for (int j = 0; j < KR / 8; ++j) {
+        const uint32_t ah = tmem + 128 + s * 2 * KR + 8 * j, al = ah + KR;
+        const uint64_t bh = sdesc(sb + 256 * j, 128, KR / 4 * 128), bl = sdesc(sb + TB + 256 * j, 128, KR / 4 * 128);
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                     "r"(ah), "l"(bh), "r"(IDESC), "r"((int)((kb | j) != 0)));
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                     "r"(al), "l"(bh), "r"(IDESC), "r"(1));
+        asm volatile("{\n\t.reg .pred p;\n\tsetp.ne.b32 p, %4, 0;\n\t"
+                     "tcgen05.mma.cta_group::1.kind::tf32 [%0], [%1], %2, %3, p;\n\t}" ::"r"(tmem),
+                     "r"(ah), "l"(bl), "r"(IDESC), "r"(1));
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + s)));
+    }
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + STG)));
+    asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W_%=;\n\t}" ::"r"(su32(bar + STG)));
+    out[blockIdx.x] = clock64() - t0;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+}
+
+template <int NT, int KR, bool RND = false, int FENCE = 0>
+void runkr(long long* d) {
+  auto k = pattern_kr<NT, KR, RND, FENCE>;
+  const int smem = 4 * 2 * NT * KR * 4 + 128;
+  cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int kb = 1024;
+  k<<<148, 128, smem>>>(d, kb);
+  cudaError_t e = cudaDeviceSynchronize();
+  long long h;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("{\"pattern\": \"sgett_kr k-block\", \"NT\": %d, \"KR\": %d, \"random_data\": %d, \"fence_every\": %d, \"cycles_per_kblock\": %.1f, "
+         "\"ideal\": %.1f, \"err\": \"%s\"}\n", NT, KR, (int)RND, FENCE, (double)h / kb, 3.0 * 128 * NT * KR / 2048.0,
+         cudaGetErrorString(e));
+}
+
 int main() {
   long long* d;
   cudaMalloc(&d, 8 * 148);
+  runkr<96, 40>(d);
+  runkr<96, 40, false, 1>(d);
+  runkr<96, 40, false, 2>(d);
+  runkr<96, 40, false, 4>(d);
+  runkr<96, 40, true>(d);
+  runkr<128, 40, true>(d);
+  runkr<128, 40>(d);
+  runkr<96, 16>(d);
+  runkr<128, 32>(d);
+  run<96, true, false>(d);
   run<64, false, false>(d);
   run<128, false, false>(d);
   run<256, false, false>(d);
