@@ -44,6 +44,7 @@ bool g_tma = true;        // SGETT: TMA-fed operands for affine views (GETT_TMA=
 bool g_sk_small = true;    // DGETT: stream-K instead of split-K at 56-73 tiles (GETT_SK_SMALL=0: off)
 bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one embedded GETT (GETT_COMPLEX_EMBED=0)
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
+bool g_dgett_tma = true;  // DGETT: TMA-fed operands for affine views (GETT_DGETT_TMA=0: cp.async gathers)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
 bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
                           // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
@@ -68,6 +69,8 @@ void read_env_once() {
   if (sks) g_sk_small = std::atoi(sks) != 0;
   const char* ce = std::getenv("GETT_COMPLEX_EMBED");
   if (ce) g_complex_4x = std::atoi(ce) == 0;
+  const char* dtv = std::getenv("GETT_DGETT_TMA");
+  if (dtv) g_dgett_tma = std::atoi(dtv) != 0;
   const char* krv = std::getenv("GETT_KR");
   if (krv) g_kr = std::atoi(krv);
   const char* krf = std::getenv("GETT_KR_FUSED");
@@ -127,6 +130,11 @@ struct DevPlan {
   GroupDev pgk{};      // dp.gk with its two tensors exchanged
   // SGETT k-run kernel (sgett_kr.cu): decided once per plan; the tensor maps
   // are re-encoded when the operand base pointers change
+  // DGETT TMA layouts (dgett_ws.cu TMA path)
+  int dtma_state = 0;  // 0 undecided, 1 both operands TMA-fed, -1 gathers
+  TmaLayout dtma_l[2];
+  TmaParams dtma_p{};
+  const void* dtma_base[2] = {nullptr, nullptr};
   int kr_state = 0;    // 0 undecided, 1 usable, -1 not
   int kr_x = 0;        // X (TMEM operand) is the plan's A' (0) or B' (1)
   int kr_run = 0;      // KR
@@ -907,6 +915,158 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
   return 1;
 }
 
+// ---- DGETT TMA layouts (dgett_ws.cu, TMA=true) ----
+//
+// Both operands of a DGETT tile are loaded as one 128B-swizzled box each per
+// 32-deep k-block when their row and k groups are affine: k-fast operands as
+// [16 k | 128 rows | 2 k-halves] boxes (smem [k/16][row][16 k]), rows-fast
+// ones as [16 rows | 32 k | 8 row-groups] (smem [row/16][k][16 rows]); the
+// inner k run must hold whole 32-blocks (k-fast) / K a multiple of 32, so no
+// k-block straddles a digit of the K group and there is no K tail (its -0.0
+// padding stays with the gather path).
+
+// one operand: rows from group gr (its tensor 0), k from the joint K dims
+bool dgett_tma_layout(const Group& gr, const std::vector<int64_t>& kext, const std::vector<int64_t>& kst,
+                      DevPlan::TmaLayout& L) {
+  std::vector<AffDim> R;
+  if (!affine_dims(gr, 0, R) || R.empty() || R.size() > 2) return false;
+  for (const AffDim& d : R)
+    if (d.stride <= 0) return false;
+  for (size_t i = 0; i < kst.size(); ++i)
+    if (kst[i] <= 0) return false;
+  struct D {
+    int64_t ext, stride;
+    uint32_t box;
+    int kind, idx;  // 0 row digit, 1 k digit
+  };
+  std::vector<D> dims;
+  std::vector<int64_t> rexp, kexp;  // the digit extents in mixed-radix order
+  // rows of a 128-row tile: one dim (extent a multiple of 128, or a single
+  // dim whose tail is zero-filled) or (r0, 128 / r0)
+  auto row_boxes = [&](int64_t inner_box_rows, int64_t r0ext) -> int {
+    (void)inner_box_rows;
+    if (r0ext % 128 == 0 || R.size() == 1) return 1;
+    if (128 % r0ext == 0 && R.size() == 2) return 2;
+    return 0;
+  };
+  const bool kf = kst[0] == 1;
+  if (kf) {
+    if (kext[0] % 32 != 0) return false;
+    const int nrb = row_boxes(128, R[0].ext);
+    if (!nrb) return false;
+    // k digits: (16, 1) (kext0 / 16, 16) outer...; rows: R0 [, R1]
+    dims.push_back({16, 1, 16u, 1, 0});
+    for (int i = 0; i < (int)R.size(); ++i)
+      dims.push_back({R[i].ext, R[i].stride, i < nrb ? (nrb == 1 ? 128u : (uint32_t)(i == 0 ? R[0].ext : 128 / R[0].ext)) : 1u, 0, i});
+    dims.push_back({kext[0] / 16, 16, 2u, 1, 1});
+    for (size_t i = 1; i < kext.size(); ++i) dims.push_back({kext[i], kst[i], 1u, 1, (int)i + 1});
+  } else {
+    if (R[0].stride != 1 || R[0].ext % 16 != 0 || kext[0] % 32 != 0) return false;
+    // rows: (16, 1) (R0 / 16, 16) [R1]; k: kext0 outer...
+    const int64_t g0 = R[0].ext / 16;
+    uint32_t gbox, r1box = 1;
+    if (g0 % 8 == 0 || R.size() == 1) gbox = 8;
+    else if (8 % g0 == 0 && R.size() == 2) {
+      gbox = (uint32_t)g0;
+      r1box = (uint32_t)(8 / g0);
+    } else {
+      return false;
+    }
+    dims.push_back({16, 1, 16u, 0, 0});
+    dims.push_back({kext[0], kst[0], 32u, 1, 0});
+    dims.push_back({g0, 16, gbox, 0, 1});
+    if (R.size() == 2) dims.push_back({R[1].ext, R[1].stride, r1box, 0, 2});
+    for (size_t i = 1; i < kext.size(); ++i) dims.push_back({kext[i], kst[i], 1u, 1, (int)i});
+  }
+  if (dims.size() > 5) return false;
+  for (size_t i = 1; i < dims.size(); ++i)
+    if (dims[i].stride % 2 != 0 || dims[i].stride * 8 >= (1LL << 40)) return false;
+  std::memset(&L.op, 0, sizeof L.op);
+  L.op.kf = kf ? 1 : 0;
+  int nr = 0, nk = 0;
+  for (int i = 0; i < 5; ++i) {
+    if (i < (int)dims.size()) {
+      L.dims[i] = (uint64_t)dims[i].ext;
+      L.strides[i] = (uint64_t)dims[i].stride;
+      L.box[i] = dims[i].box;
+      if (dims[i].kind == 0) {
+        L.op.r_ext[dims[i].idx] = (int32_t)dims[i].ext;
+        L.op.r_pos[dims[i].idx] = i;
+        nr = std::max(nr, dims[i].idx + 1);
+      } else {
+        L.op.k_ext[dims[i].idx] = (int32_t)dims[i].ext;
+        L.op.k_pos[dims[i].idx] = i;
+        nk = std::max(nk, dims[i].idx + 1);
+      }
+    } else {
+      L.dims[i] = 1;
+      L.strides[i] = 2;
+      L.box[i] = 1;
+    }
+  }
+  if (nr > 3 || nk > 3) return false;
+  L.op.nr = nr;
+  L.op.nk = nk;
+  return true;
+}
+
+bool dgett_tma_encode(const DevPlan::TmaLayout& L, const double* base, CUtensorMap* map) {
+  TmaEncodeFn enc = tma_encode_fn();
+  if (!enc) return false;
+  const double* g = base + L.base_off;
+  if ((uintptr_t)g % 16 != 0) return false;
+  cuuint64_t dims[5], strides[4];
+  cuuint32_t box[5], es[5] = {1, 1, 1, 1, 1};
+  for (int i = 0; i < 5; ++i) {
+    dims[i] = L.dims[i];
+    box[i] = L.box[i];
+    if (i) strides[i - 1] = L.strides[i] * 8;
+  }
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(g), dims, strides, box, es,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, GETT_TMA_PROMO,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Both DGETT operands TMA-fed?  Decided once per plan, tensor maps re-encoded
+// when the base pointers change.  Returns null for the gather path.
+const TmaParams* dgett_tma(DevPlan& dp, const double* A, const double* B) {
+  const Plan& p = dp.plan;
+  if (dp.dtma_state == 0) {
+    dp.dtma_state = -1;
+    std::vector<int64_t> kext, kst[2];
+    if (p.gk.G % 32 == 0 && p.gm.G > 1 && p.gn.G > 1 && joint_k_dims(p.gk, kext, kst) &&
+        dgett_tma_layout(p.gm, kext, kst[0], dp.dtma_l[0]) && dgett_tma_layout(p.gn, kext, kst[1], dp.dtma_l[1])) {
+      dp.dtma_l[0].base_off = p.gm.T[0][0] + p.gk.T[0][0];
+      dp.dtma_l[1].base_off = p.gn.T[0][0] + p.gk.T[1][0];
+      dp.dtma_state = 1;
+    }
+    if (std::getenv("GETT_TMA_DEBUG")) {
+      std::fprintf(stderr, "gett dgett tma: %s\n", dp.dtma_state == 1 ? "on" : "off");
+      for (int t = 0; dp.dtma_state == 1 && t < 2; ++t) {
+        const DevPlan::TmaLayout& L = dp.dtma_l[t];
+        std::fprintf(stderr, "  op %d kf %d base_off %lld dims", t, L.op.kf, (long long)L.base_off);
+        for (int i = 0; i < 5; ++i)
+          std::fprintf(stderr, " (%llu,%llu,%u)", (unsigned long long)L.dims[i],
+                       (unsigned long long)L.strides[i], L.box[i]);
+        std::fprintf(stderr, "\n");
+      }
+    }
+  }
+  if (dp.dtma_state != 1) return nullptr;
+  if (dp.dtma_base[0] != A || dp.dtma_base[1] != B) {
+    if (!dgett_tma_encode(dp.dtma_l[0], A, &dp.dtma_p.map[0]) ||
+        !dgett_tma_encode(dp.dtma_l[1], B, &dp.dtma_p.map[1])) {
+      dp.dtma_base[0] = dp.dtma_base[1] = nullptr;
+      return nullptr;
+    }
+    dp.dtma_p.op[0] = dp.dtma_l[0].op;
+    dp.dtma_p.op[1] = dp.dtma_l[1].op;
+    dp.dtma_base[0] = A;
+    dp.dtma_base[1] = B;
+  }
+  return &dp.dtma_p;
+}
+
 // CTA-pair SGETT (sgett_tc.cu pair kernel) on the swapped roles: M2 = the
 // plan's N (a K-major B', its rows 256 per pair in TMEM), N2 = the plan's M
 // (a rows-major A' of <= 128 rows, split across the pair).  Returns 1 when
@@ -1191,10 +1351,20 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
       sk.flags = (int32_t*)sw.flags.p;
       sk.epoch = sw.epoch;
     }
-    CK(launch_dgett_ws(*reinterpret_cast<TiledParams<double>*>(&tp), sk, a_kf, b_kf, a_vec,
+    const TmaParams* dtp =
+        g_tma && g_dgett_tma ? dgett_tma(dp, reinterpret_cast<const double*>(A), reinterpret_cast<const double*>(B))
+                             : nullptr;
+    if (dtp) {
+      a_kf = dtp->op[0].kf != 0;
+      b_kf = dtp->op[1].kf != 0;
+    }
+    CK(launch_dgett_ws(*reinterpret_cast<TiledParams<double>*>(&tp), sk, dtp, a_kf, b_kf, a_vec,
                        b_vec, stream));
     g_launches += splits > 1 ? 2 : 1;
-    t_last_kernel = splits > 1 ? "dgett_dmma_ws_splitk" : sk.enabled ? "dgett_dmma_ws_sk" : "dgett_dmma_ws";
+    if (dtp)
+      t_last_kernel = splits > 1 ? "dgett_dmma_ws_tma_splitk" : sk.enabled ? "dgett_dmma_ws_tma_sk" : "dgett_dmma_ws_tma";
+    else
+      t_last_kernel = splits > 1 ? "dgett_dmma_ws_splitk" : sk.enabled ? "dgett_dmma_ws_sk" : "dgett_dmma_ws";
     return 0;
   }
   CK(launch_tiled<T>(tp, a_kf, b_kf, a_vec, b_vec, stream));

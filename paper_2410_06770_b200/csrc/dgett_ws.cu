@@ -57,6 +57,15 @@ constexpr int STAGE_ELEMS = 2 * OPER_ELEMS;
 constexpr int BAR_BYTES = 64;
 constexpr int ROWOFF_BYTES = 2 * 128 * 8;
 constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8 + BAR_BYTES + ROWOFF_BYTES;
+// TMA-fed operands (both A' and B' affine boxes): 128 x 32 doubles per operand
+// per stage, SWIZZLE_128B, no padding: a k-fast operand lands as [k/16][row]
+// [16 k] (two 16-double halves of each row line), a rows-fast one as
+// [row/16][k][16 rows]; either way the 16-byte chunk index of a 128-byte line
+// is XORed with the line index mod 8, which keeps the DMMA fragment loads at 2
+// wavefronts (conflict-free).  One thread issues one box per operand.
+constexpr int T_OPER_BYTES = 128 * BK * 8;  // 32 KB
+constexpr int T_STAGE_BYTES = 2 * T_OPER_BYTES;
+constexpr int T_SMEM_BYTES = STAGES * T_STAGE_BYTES + BAR_BYTES + 1024;  // (+1 KB: 1024-byte alignment)
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
@@ -237,22 +246,69 @@ __device__ __forceinline__ void tile_origin(const TiledParams<double>& p, int ti
   n0 = (in_group / gsize) * BN;
 }
 
-template <bool AKF, bool BKF, bool AVEC, bool BVEC>
+// TMA box coordinates of one operand for a tile and a k-block: the mixed-radix
+// digits of the tile's first row over the row dims and of the k-block's first
+// k over the k dims, placed at their tensor-map dims (TmaOperand, built by the
+// host: capi.cu dgett_tma_layout)
+__device__ __forceinline__ void dtma_coords(const TmaOperand& op, int row0, int k0, int32_t* c) {
+#pragma unroll
+  for (int j = 0; j < 5; ++j) c[j] = 0;
+  int q = row0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (i < op.nr) {
+      const int v = q % op.r_ext[i];
+      q /= op.r_ext[i];
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (op.r_pos[i] == j) c[j] = v;
+    }
+  q = k0;
+#pragma unroll
+  for (int i = 0; i < 3; ++i)
+    if (i < op.nk) {
+      const int v = q % op.k_ext[i];
+      q /= op.k_ext[i];
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        if (op.k_pos[i] == j) c[j] = v;
+    }
+}
+
+__device__ __forceinline__ void dtma_load(uint32_t dst, const CUtensorMap* map, const int32_t* c, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar)
+      : "memory");
+}
+
+template <bool AKF, bool BKF, bool AVEC, bool BVEC, bool TMA>
 __global__ void __launch_bounds__(THREADS, 1)
     dgett_ws_kernel(const __grid_constant__ TiledParams<double> p,
-                    const __grid_constant__ SkParams sk) {
+                    const __grid_constant__ SkParams sk, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double* smem = reinterpret_cast<double*>(smem_raw);
-  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + STAGES * STAGE_ELEMS * 8);
+  // (TMA: stages 1024-byte aligned for the 128-byte swizzle pattern)
+  unsigned char* sbase_ptr =
+      TMA ? smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023) : smem_raw;
+  double* smem = reinterpret_cast<double*>(sbase_ptr);
+  constexpr int RING_BYTES = TMA ? STAGES * T_STAGE_BYTES : STAGES * STAGE_ELEMS * 8;
+  constexpr int SOPER = TMA ? T_OPER_BYTES / 8 : OPER_ELEMS;    // doubles per operand tile
+  constexpr int SSTAGE = TMA ? T_STAGE_BYTES / 8 : STAGE_ELEMS;  // doubles per stage
+  uint64_t* full = reinterpret_cast<uint64_t*>(sbase_ptr + RING_BYTES);
   uint64_t* empty = full + STAGES;
-  int64_t* rowoff_a = reinterpret_cast<int64_t*>(smem_raw + STAGES * STAGE_ELEMS * 8 + BAR_BYTES);
+  int64_t* rowoff_a = reinterpret_cast<int64_t*>(sbase_ptr + RING_BYTES + BAR_BYTES);
   int64_t* rowoff_b = rowoff_a + 128;
 
   const int tid = threadIdx.x;
   const int warp = tid >> 5, lane = tid & 31;
   if (tid == 0) {
+    if (TMA) {
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[0]) : "memory");
+      asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[1]) : "memory");
+    }
     for (int s = 0; s < STAGES; ++s) {
-      mbar_init(smem_u32(full + s), 2 * PW * 32);  // per producer lane: cp.async + plain arrival
+      // per producer lane: cp.async + plain arrival; TMA: the expect_tx arrival
+      mbar_init(smem_u32(full + s), TMA ? 1 : 2 * PW * 32);
       mbar_init(smem_u32(empty + s), CW);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -263,6 +319,31 @@ __global__ void __launch_bounds__(THREADS, 1)
   seg_init(p, sk, it);
   Seg sg;
 
+  if (TMA && warp >= CW) {
+    // ---------------- TMA producer: one thread, one box per operand ----------------
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+    if (warp != CW || lane != 0) return;
+    uint32_t g = 0;
+    const uint32_t ring = smem_u32(smem);
+    while (seg_next(p, sk, it, sg)) {
+      int m0, n0;
+      tile_origin(p, sg.tile, m0, n0);
+      for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
+        const int s = g % STAGES, u = g / STAGES;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        const uint32_t fb = smem_u32(full + s);
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(T_STAGE_BYTES)
+                     : "memory");
+        const int k0 = sg.kbase + kb * BK;
+        int32_t c[5];
+        dtma_coords(tp.op[0], m0, k0, c);
+        dtma_load(ring + s * T_STAGE_BYTES, &tp.map[0], c, fb);
+        dtma_coords(tp.op[1], n0, k0, c);
+        dtma_load(ring + s * T_STAGE_BYTES + T_OPER_BYTES, &tp.map[1], c, fb);
+      }
+    }
+    return;
+  }
   if (warp >= CW) {
     // ---------------- producer warpgroup ----------------
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
@@ -283,8 +364,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
         const int s = g % STAGES, u = g / STAGES;
         if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
-        double* sa = smem + s * STAGE_ELEMS;
-        double* sb = sa + OPER_ELEMS;
+        double* sa = smem + s * SSTAGE;
+        double* sb = sa + SOPER;
         const int k0 = sg.kbase + kb * BK;
         produce<AKF, AVEC, true>(sa, p.A, rowoff_a, mvalid, p.gk, 0, k0, sg.kend, pw, lane);
         produce<BKF, BVEC, false>(sb, p.B, rowoff_b, nvalid, p.gk, 1, k0, sg.kend, pw, lane);
@@ -303,15 +384,35 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     int r = wm0 + i * 8 + (lane >> 2);
-    aoff[i] = AKF ? r * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + r;
+    if (TMA) aoff[i] = AKF ? r * 16 : (r >> 4) * (BK * 16) + (lane & 3) * 16;
+    else aoff[i] = AKF ? r * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + r;
   }
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     int c = wn0 + j * 8 + (lane >> 2);
-    boff[j] = BKF ? c * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + c;
+    if (TMA) boff[j] = BKF ? c * 16 : (c >> 4) * (BK * 16) + (lane & 3) * 16;
+    else boff[j] = BKF ? c * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + c;
   }
   constexpr int AKS = AKF ? 4 : 4 * RF_PITCH;
   constexpr int BKS = BKF ? 4 : 4 * RF_PITCH;
+  // TMA layouts (in doubles): k-fast (row, k) at (k/16)*2048 + row*16 +
+  // 2*(((k%16)/2) ^ (row%8)) + k%2; rows-fast (row, k) at (row/16)*512 + k*16 +
+  // 2*(((row%16)/2) ^ (k%8)) + row%2.  For a fragment (row = 8i + lane/4 +
+  // base, k = 4 ks + lane%4) the swizzle term depends on ks % 4 (k-fast) or on
+  // (i % 2, ks % 2) (rows-fast): per-thread constants.
+  int kx[4], rx[2][2];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) kx[q] = 2 * (((2 * q + ((lane >> 1) & 1)) ^ (lane >> 2)) & 7) + (lane & 1);
+#pragma unroll
+  for (int i2 = 0; i2 < 2; ++i2)
+#pragma unroll
+    for (int k2 = 0; k2 < 2; ++k2)
+      rx[i2][k2] = 2 * (((4 * i2 + (lane >> 3)) ^ (4 * k2 + (lane & 3))) & 7) + ((lane >> 2) & 1);
+  // fragment (i or j, ks) offset in an operand tile
+  auto toff = [&](int base, int idx, int ks, bool kf) -> int {
+    if (kf) return base + (ks >> 2) * 2048 + kx[ks & 3];
+    return base + ks * 64 + rx[idx & 1][ks & 1];
+  };
 
   uint32_t g = 0;
   TR_DECL(cw = 0, cc = 0, ce = 0, cx = 0)
@@ -332,21 +433,23 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = g % STAGES, u = g / STAGES;
       mbar_wait(smem_u32(full + s), u & 1);
       TR_ADD(cw)
-      const double* As = smem + s * STAGE_ELEMS;
-      const double* Bs = As + OPER_ELEMS;
+      const double* As = smem + s * SSTAGE;
+      const double* Bs = As + SOPER;
       double a[2][MI], b[2][NJ];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[0][i] = As[aoff[i]];
+      for (int i = 0; i < MI; ++i) a[0][i] = As[TMA ? toff(aoff[i], i, 0, AKF) : aoff[i]];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) b[0][j] = Bs[boff[j]];
+      for (int j = 0; j < NJ; ++j) b[0][j] = Bs[TMA ? toff(boff[j], j, 0, BKF) : boff[j]];
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         const int cur = ks & 1;
         if (ks + 1 < BK / 4) {
 #pragma unroll
-          for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[aoff[i] + (ks + 1) * AKS];
+          for (int i = 0; i < MI; ++i)
+            a[cur ^ 1][i] = As[TMA ? toff(aoff[i], i, ks + 1, AKF) : aoff[i] + (ks + 1) * AKS];
 #pragma unroll
-          for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[boff[j] + (ks + 1) * BKS];
+          for (int j = 0; j < NJ; ++j)
+            b[cur ^ 1][j] = Bs[TMA ? toff(boff[j], j, ks + 1, BKF) : boff[j] + (ks + 1) * BKS];
         }
 #pragma unroll
         for (int i = 0; i < MI; ++i)
@@ -448,39 +551,42 @@ __global__ void __launch_bounds__(THREADS, 1)
              blockIdx.x, nseg, cw, cc, ce, cx);
 }
 
-template <bool AKF, bool BKF, bool AV, bool BV>
-cudaError_t launch4(const TiledParams<double>& p, const SkParams& sk, unsigned grid,
-                    cudaStream_t s) {
-  auto k = dgett_ws_kernel<AKF, BKF, AV, BV>;
+template <bool AKF, bool BKF, bool AV, bool BV, bool TMA>
+cudaError_t launch5(const TiledParams<double>& p, const SkParams& sk, const TmaParams& tp,
+                    unsigned grid, cudaStream_t s) {
+  auto k = dgett_ws_kernel<AKF, BKF, AV, BV, TMA>;
   static unsigned long long configured = 0;
-  cudaError_t e = ensure_dyn_smem(k, SMEM_BYTES, configured);
+  constexpr int smem = TMA ? T_SMEM_BYTES : SMEM_BYTES;
+  cudaError_t e = ensure_dyn_smem(k, smem, configured);
   if (e != cudaSuccess) return e;
-  k<<<grid, THREADS, SMEM_BYTES, s>>>(p, sk);
+  k<<<grid, THREADS, smem, s>>>(p, sk, tp);
   return cudaGetLastError();
 }
 
 template <bool AKF, bool BKF>
-cudaError_t launch2(const TiledParams<double>& p, const SkParams& sk, unsigned grid, bool av,
-                    bool bv, cudaStream_t s) {
-  if (av && bv) return launch4<AKF, BKF, true, true>(p, sk, grid, s);
-  if (av) return launch4<AKF, BKF, true, false>(p, sk, grid, s);
-  if (bv) return launch4<AKF, BKF, false, true>(p, sk, grid, s);
-  return launch4<AKF, BKF, false, false>(p, sk, grid, s);
+cudaError_t launch2(const TiledParams<double>& p, const SkParams& sk, const TmaParams* tp,
+                    unsigned grid, bool av, bool bv, cudaStream_t s) {
+  if (tp) return launch5<AKF, BKF, false, false, true>(p, sk, *tp, grid, s);
+  static const TmaParams none{};
+  if (av && bv) return launch5<AKF, BKF, true, true, false>(p, sk, none, grid, s);
+  if (av) return launch5<AKF, BKF, true, false, false>(p, sk, none, grid, s);
+  if (bv) return launch5<AKF, BKF, false, true, false>(p, sk, none, grid, s);
+  return launch5<AKF, BKF, false, false, false>(p, sk, none, grid, s);
 }
 
 }  // namespace ws
 
 int dgett_ws_tiles_k(int K) { return (K + ws::BK - 1) / ws::BK; }
 
-cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, bool a_kf,
-                            bool b_kf, bool a_vec, bool b_vec, cudaStream_t s) {
+cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, const TmaParams* tp,
+                            bool a_kf, bool b_kf, bool a_vec, bool b_vec, cudaStream_t s) {
   const unsigned grid = sk.enabled ? (unsigned)sk.grid
                                    : (unsigned)(p.tiles_m * p.tiles_n * p.splits);
   cudaError_t e;
-  if (a_kf && b_kf) e = ws::launch2<true, true>(p, sk, grid, a_vec, b_vec, s);
-  else if (a_kf) e = ws::launch2<true, false>(p, sk, grid, a_vec, b_vec, s);
-  else if (b_kf) e = ws::launch2<false, true>(p, sk, grid, a_vec, b_vec, s);
-  else e = ws::launch2<false, false>(p, sk, grid, a_vec, b_vec, s);
+  if (a_kf && b_kf) e = ws::launch2<true, true>(p, sk, tp, grid, a_vec, b_vec, s);
+  else if (a_kf) e = ws::launch2<true, false>(p, sk, tp, grid, a_vec, b_vec, s);
+  else if (b_kf) e = ws::launch2<false, true>(p, sk, tp, grid, a_vec, b_vec, s);
+  else e = ws::launch2<false, false>(p, sk, tp, grid, a_vec, b_vec, s);
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_splitk_reduce<double>(p, s);
 }

@@ -76,8 +76,9 @@ template <typename R>
 cudaError_t launch_expand_complex(const ExpandParams<R>& p, cudaStream_t s);
 
 // DGETT warp-specialised (producer warp + DMMA consumer warps), dgett_ws.cu
-cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, bool a_kf,
-                            bool b_kf, bool a_vec, bool b_vec, cudaStream_t s);
+// tp != nullptr: both operands TMA-fed (128B-swizzled boxes; capi.cu dgett_tma)
+cudaError_t launch_dgett_ws(const TiledParams<double>& p, const SkParams& sk, const TmaParams* tp,
+                            bool a_kf, bool b_kf, bool a_vec, bool b_vec, cudaStream_t s);
 int dgett_ws_tiles_k(int K);  // k-blocks per tile
 
 // SGETT 3xTF32 on tcgen05 (sgett_tc.cu); tp != nullptr: both operands TMA-fed
