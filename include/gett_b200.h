@@ -236,6 +236,32 @@ int gett_cgett_device(int rank_a, const int64_t* ext_a, const int64_t* inc_a, co
                       int64_t len_c, void* stream,
                       int32_t* err_codes, int64_t* err_info, int max_errs);
 
+/* ---- plan once, execute many (d and s) ----
+ * gett_plan_create validates a descriptor exactly like gett_dgett (same
+ * codes; the C view is footprint-checked against offset_c / len_c) and, when
+ * it is valid, returns a handle holding the device plan.  gett_execute (host
+ * buffers, synchronous) and gett_execute_device (device pointers, stream-
+ * ordered) then run C += contract(A, B) on buffers of the planned lengths at
+ * the planned offsets, without validation, descriptor hashing or plan lookup:
+ * the per-call host cost of a small contraction.  The same call semantics
+ * as the reference's dgett/sgett (kernel.py:158-184) minus its per-call
+ * argument processing (kernel.py:124-155).  dtype: 'd' or 's'.  Returns the
+ * validation error count (> 0: *out = NULL) or a negative status; a handle
+ * with an empty iteration space executes to nothing.  n_dev/devices: as
+ * gett_dgett_multi (0 = the current device).  A handle may be executed from
+ * any thread; destroy it once. */
+typedef struct gett_plan_s* gett_plan_t;
+int gett_plan_create(char dtype, int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
+                     int64_t len_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,
+                     int64_t offset_b, int64_t len_b, int conts, const int64_t* cont_a,
+                     const int64_t* cont_b, int perm_len, const int64_t* perm, int inc_c_len,
+                     const int64_t* inc_c, int64_t offset_c, int64_t len_c, int n_dev,
+                     const int32_t* devices, gett_plan_t* out, int32_t* err_codes, int64_t* err_info,
+                     int max_errs);
+int gett_execute(gett_plan_t plan, const void* a, const void* b, void* c);
+int gett_execute_device(gett_plan_t plan, const void* a, const void* b, void* c, void* stream);
+void gett_plan_destroy(gett_plan_t plan);
+
 /* ---- planning helpers ---- */
 /* Validation only.  c_mode selects how the output view takes part:
  *   GETT_CHECK_C_NONE     plan.validate(a, b, spec, inc_c)           (plan.py:162-234)

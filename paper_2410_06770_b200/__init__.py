@@ -10,6 +10,7 @@ from . import _native
 from ._native import (GettRuntimeError, last_kernel, last_multi, launch_count, set_complex_embed,
                       set_devices, set_kernel, set_kr, set_multi, set_pipeline, set_pair, set_split_k,
                       set_stream_k, set_tma)
+from .handle import GettPlan, dgett_plan, sgett_plan
 from .kernel import cgett, dgett, dtype_prefix, gett_for_dtype, pack, sgett, zero_view, zgett
 from .layout import TensorView, contiguous_increments, footprint, num_elements
 from .plan import (
@@ -26,7 +27,8 @@ from .plan import (
 __version__ = "0.1.0"
 
 __all__ = [
-    "ContractionError", "ContractionSpec", "ErrorCode", "GettRuntimeError", "TensorView", "cgett", "zgett",
+    "ContractionError", "ContractionSpec", "ErrorCode", "GettPlan", "GettRuntimeError", "TensorView", "cgett",
+    "dgett_plan", "sgett_plan", "zgett",
     "ValidationError", "contiguous_increments", "derive_output_extents", "dgett", "dtype_prefix",
     "footprint", "free_dims", "gett_for_dtype", "last_kernel", "last_multi", "launch_count", "num_elements",
     "output_rank", "pack", "set_complex_embed", "set_devices", "set_kernel", "set_kr", "set_multi", "set_pair", "set_split_k", "set_stream_k", "set_tma", "sgett", "validate", "zero_view",

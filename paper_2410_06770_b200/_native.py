@@ -22,6 +22,7 @@ EXPORTS = (
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
     "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
     "gett_multi_schedule", "gett_pack", "gett_pack_device", "gett_set_kr",
+    "gett_plan_create", "gett_execute", "gett_execute_device", "gett_plan_destroy",
 )
 
 ERR_INFO_WORDS = 6
@@ -63,6 +64,19 @@ def _load():
         ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
         ctypes.c_int, i64p, i64p, ctypes.c_int, i64p, ctypes.c_int, i64p,
         ctypes.c_int64, ctypes.c_int64, ctypes.c_int, ctypes.c_int, i64p, i32p, i64p, ctypes.c_int]
+    lib.gett_plan_create.restype = ctypes.c_int
+    lib.gett_plan_create.argtypes = [
+        ctypes.c_char, ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64,
+        ctypes.c_int, i64p, i64p, ctypes.c_int, i64p, ctypes.c_int, i64p,
+        ctypes.c_int64, ctypes.c_int64, ctypes.c_int, i32p, ctypes.POINTER(ctypes.c_void_p), i32p, i64p,
+        ctypes.c_int]
+    lib.gett_execute.restype = ctypes.c_int
+    lib.gett_execute.argtypes = [vp, vp, vp, vp]
+    lib.gett_execute_device.restype = ctypes.c_int
+    lib.gett_execute_device.argtypes = [vp, vp, vp, vp, vp]
+    lib.gett_plan_destroy.restype = None
+    lib.gett_plan_destroy.argtypes = [vp]
     lib.gett_pack.restype = ctypes.c_int
     lib.gett_pack.argtypes = [ctypes.c_int, i64p, i64p, ctypes.c_int64, ctypes.c_int64, ctypes.c_int,
                               vp, vp]

@@ -1941,6 +1941,62 @@ int check_devices(int n_dev, const int32_t* devices, std::vector<int>* out) {
   return 0;
 }
 
+// Run a validated, non-empty call on its plan (gett_impl after validation,
+// and gett_execute on a plan handle): multi-device host calls, else the
+// current device's lane 0 — device pointers stream-ordered, host buffers
+// through the (pipelined) copy path.
+template <typename T>
+int execute_plan(bool host, DevPlan& dpr, const View& va, const View& vb, const Spec& sp, const T* a,
+                 const T* b, T* c, int64_t off_a, int64_t off_b, int64_t off_c, int64_t len_c,
+                 cudaStream_t stream, const std::vector<int>& devs) {
+  int rc = 0;
+  const Plan& p = dpr.plan;
+  if (host && devs.size() > 1) {
+    for (int d : devs) {
+      cudaError_t e = cudaSetDevice(d);
+      if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice(devices[i])");
+    }
+    rc = host_multi<T>(p, va, vb, sp, a, b, c, off_c, len_c, devs);
+    if (rc != kNotPipelined) return rc;
+    CK(cudaSetDevice(devs[0]));
+  }
+  int dev;
+  if ((rc = current_device(&dev))) return rc;
+  DevState& ds = g_dev[dev];
+  std::lock_guard<std::mutex> lk(ds.mu);
+  if (!host) {
+    CaptureScope cs(stream);
+    if (t_capturing) dpr.pinned = true;
+    return run_device<T>(dpr, a + off_a, b + off_b, c + off_c, stream, ds);
+  }
+  Lane* Lp = nullptr;
+  if ((rc = get_lane(dev, 0, &Lp))) return rc;
+  Lane& L = *Lp;
+  rc = host_pipelined<T>(dpr, va, vb, sp, a, b, c, off_c, len_c, ds, L);
+  if (rc != kNotPipelined) return rc;
+  // host buffers: copy the addressed spans in, run, copy C's span back
+  // (the plan is cached by descriptor only: spans use this call's offsets)
+  const int64_t lo_a = off_a + p.fp_lo[0], lo_b = off_b + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
+  size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
+  size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
+  size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
+  if ((rc = ensure(L.a, na * sizeof(T))) || (rc = ensure(L.b, nb * sizeof(T))) ||
+      (rc = ensure(L.c, nc * sizeof(T))))
+    return rc;
+  T* da = (T*)L.a.p;
+  T* db = (T*)L.b.p;
+  T* dc = (T*)L.c.p;
+  cudaStream_t s = L.stream;
+  CK(cudaMemcpyAsync(da, a + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(db, b + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(dc, c + lo_c, nc * sizeof(T), cudaMemcpyHostToDevice, s));
+  rc = run_device<T>(dpr, da - p.fp_lo[0], db - p.fp_lo[1], dc - p.fp_lo[2], s, ds);
+  if (rc) return rc;
+  CK(cudaMemcpyAsync(c + lo_c, dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s));
+  CK(cudaStreamSynchronize(s));
+  return 0;
+}
+
 template <typename T>
 int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a, const T* a,
               int64_t off_a, int64_t len_a, int rank_b, const int64_t* ext_b,
@@ -2004,51 +2060,7 @@ int gett_impl(bool host, int rank_a, const int64_t* ext_a, const int64_t* inc_a,
     g_last.dp = dp;
   }
   if (set_err != cudaSuccess) return cuda_fail(set_err, "cudaSetDevice(devices[0])");
-  const Plan& p = dp->plan;
-  if (host && devs.size() > 1) {
-    for (int d : devs) {
-      cudaError_t e = cudaSetDevice(d);
-      if (e != cudaSuccess) return cuda_fail(e, "cudaSetDevice(devices[i])");
-    }
-    rc = host_multi<T>(p, va, vb, sp, a, b, c, off_c, len_c, devs);
-    if (rc != kNotPipelined) return rc;
-    CK(cudaSetDevice(devs[0]));
-  }
-  int dev;
-  if ((rc = current_device(&dev))) return rc;
-  DevState& ds = g_dev[dev];
-  std::lock_guard<std::mutex> lk(ds.mu);
-  Lane* Lp = nullptr;
-  if ((rc = get_lane(dev, 0, &Lp))) return rc;
-  Lane& L = *Lp;
-  if (!host) {
-    CaptureScope cs(stream);
-    if (t_capturing) dp->pinned = true;
-    return run_device<T>(*dp, a + off_a, b + off_b, c + off_c, stream, ds);
-  }
-  rc = host_pipelined<T>(*dp, va, vb, sp, a, b, c, off_c, len_c, ds, L);
-  if (rc != kNotPipelined) return rc;
-  // host buffers: copy the addressed spans in, run, copy C's span back
-  // (the plan is cached by descriptor only: spans use this call's offsets)
-  const int64_t lo_a = off_a + p.fp_lo[0], lo_b = off_b + p.fp_lo[1], lo_c = off_c + p.fp_lo[2];
-  size_t na = (size_t)(p.fp_hi[0] - p.fp_lo[0] + 1);
-  size_t nb = (size_t)(p.fp_hi[1] - p.fp_lo[1] + 1);
-  size_t nc = (size_t)(p.fp_hi[2] - p.fp_lo[2] + 1);
-  if ((rc = ensure(L.a, na * sizeof(T))) || (rc = ensure(L.b, nb * sizeof(T))) ||
-      (rc = ensure(L.c, nc * sizeof(T))))
-    return rc;
-  T* da = (T*)L.a.p;
-  T* db = (T*)L.b.p;
-  T* dc = (T*)L.c.p;
-  cudaStream_t s = L.stream;
-  CK(cudaMemcpyAsync(da, a + lo_a, na * sizeof(T), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(db, b + lo_b, nb * sizeof(T), cudaMemcpyHostToDevice, s));
-  CK(cudaMemcpyAsync(dc, c + lo_c, nc * sizeof(T), cudaMemcpyHostToDevice, s));
-  rc = run_device<T>(*dp, da - p.fp_lo[0], db - p.fp_lo[1], dc - p.fp_lo[2], s, ds);
-  if (rc) return rc;
-  CK(cudaMemcpyAsync(c + lo_c, dc, nc * sizeof(T), cudaMemcpyDeviceToHost, s));
-  CK(cudaStreamSynchronize(s));
-  return 0;
+  return execute_plan<T>(host, *dp, va, vb, sp, a, b, c, off_a, off_b, off_c, len_c, stream, devs);
 }
 
 // Complex contraction as ONE real GETT on a real embedding.  The operand with
@@ -2398,6 +2410,48 @@ int pack_impl(bool host, int rank, const int64_t* ext, const int64_t* inc, int64
 }  // namespace
 }  // namespace gett
 
+// A validated, planned call (gett_plan_create): the descriptor, its device
+// plan and the device it lives on; gett_execute* skip validation, the
+// descriptor key and plan lookup.
+struct gett_plan_s {
+  char dtype = 'd';
+  bool empty = false;  // empty iteration space: executing writes nothing
+  int device = 0;
+  std::vector<int64_t> ext_a, inc_a, ext_b, inc_b, cont_a, cont_b, perm, inc_c;
+  int64_t off_a = 0, off_b = 0, off_c = 0, len_a = 0, len_b = 0, len_c = 0;
+  std::vector<int> devs;
+  std::shared_ptr<gett::DevPlan> dp;
+  gett::View va() const { return gett::View{(int)ext_a.size(), ext_a.data(), inc_a.data(), off_a, len_a}; }
+  gett::View vb() const { return gett::View{(int)ext_b.size(), ext_b.data(), inc_b.data(), off_b, len_b}; }
+  gett::Spec sp() const {
+    return gett::Spec{(int)cont_a.size(), cont_a.data(), cont_b.data(), (int)perm.size(), perm.data(),
+                      (int)inc_c.size(), inc_c.data()};
+  }
+};
+
+namespace gett {
+namespace {
+template <typename T>
+int execute_handle(gett_plan_s* h, bool host, const void* a, const void* b, void* c, cudaStream_t stream) {
+  read_env();
+  t_last_kernel = "none";
+  std::snprintf(t_last_multi, sizeof t_last_multi, "none");
+  if (h->empty) return 0;
+  int cur = -1;
+  CK(cudaGetDevice(&cur));
+  if (cur != h->device) CK(cudaSetDevice(h->device));
+  const View va = h->va(), vb = h->vb();
+  const Spec sp = h->sp();
+  static const std::vector<int> none;
+  const int rc = execute_plan<T>(host, *h->dp, va, vb, sp, static_cast<const T*>(a), static_cast<const T*>(b),
+                                 static_cast<T*>(c), h->off_a, h->off_b, h->off_c, h->len_c, stream,
+                                 host ? h->devs : none);
+  if (cur != h->device) cudaSetDevice(cur);
+  return rc;
+}
+}  // namespace
+}  // namespace gett
+
 using namespace gett;
 
 extern "C" {
@@ -2637,6 +2691,73 @@ int gett_pack_device(int rank, const int64_t* ext, const int64_t* inc, int64_t o
   return pack_impl(false, rank, ext, inc, offset, len, elem_bytes, src, dst, (cudaStream_t)stream);
 }
 
+int gett_plan_create(char dtype, int rank_a, const int64_t* ext_a, const int64_t* inc_a, int64_t offset_a,
+                     int64_t len_a, int rank_b, const int64_t* ext_b, const int64_t* inc_b,
+                     int64_t offset_b, int64_t len_b, int conts, const int64_t* cont_a,
+                     const int64_t* cont_b, int perm_len, const int64_t* perm, int inc_c_len,
+                     const int64_t* inc_c, int64_t offset_c, int64_t len_c, int n_dev,
+                     const int32_t* devices, gett_plan_t* out, int32_t* err_codes, int64_t* err_info,
+                     int max_errs) {
+  if (!out || (dtype != 'd' && dtype != 's') || rank_a < 0 || rank_b < 0 || conts < 0 || perm_len < 0 ||
+      inc_c_len < 0 || offset_a < 0 || offset_b < 0 || offset_c < 0 || len_a < 0 || len_b < 0 ||
+      len_c < 0 || n_dev < 0) {
+    t_last_error = "bad gett_plan_create arguments (dtype 'd' or 's')";
+    return GETT_E_INVALID_ARG;
+  }
+  *out = nullptr;
+  read_env();
+  std::vector<int> devs;
+  int rc = check_devices(n_dev, devices, &devs);
+  if (rc) return rc;
+  View va{rank_a, ext_a, inc_a, offset_a, len_a};
+  View vb{rank_b, ext_b, inc_b, offset_b, len_b};
+  Spec sp{conts, cont_a, cont_b, perm_len, perm, inc_c_len, inc_c};
+  View vc{0, nullptr, nullptr, offset_c, len_c};
+  std::vector<Error> errs = validate(va, vb, sp, CMode::Derived, vc);
+  if (!errs.empty()) return fill_errors(errs, err_codes, err_info, max_errs);
+  std::unique_ptr<gett_plan_s> h(new gett_plan_s());
+  h->dtype = dtype;
+  h->ext_a.assign(ext_a, ext_a + rank_a);
+  h->inc_a.assign(inc_a, inc_a + rank_a);
+  h->ext_b.assign(ext_b, ext_b + rank_b);
+  h->inc_b.assign(inc_b, inc_b + rank_b);
+  h->cont_a.assign(cont_a, cont_a + conts);
+  h->cont_b.assign(cont_b, cont_b + conts);
+  h->perm.assign(perm, perm + perm_len);
+  h->inc_c.assign(inc_c, inc_c + inc_c_len);
+  h->off_a = offset_a;
+  h->off_b = offset_b;
+  h->off_c = offset_c;
+  h->len_a = len_a;
+  h->len_b = len_b;
+  h->len_c = len_c;
+  h->devs = devs;
+  for (int d = 0; d < rank_a; ++d) h->empty = h->empty || ext_a[d] == 0;
+  for (int d = 0; d < rank_b; ++d) h->empty = h->empty || ext_b[d] == 0;
+  if (!h->empty) {
+    DeviceGuard guard;
+    if (!devs.empty()) CK(cudaSetDevice(devs[0]));
+    CK(cudaGetDevice(&h->device));
+    if ((rc = get_plan(dtype, h->va(), h->vb(), h->sp(), offset_c, len_c, &h->dp))) return rc;
+  }
+  *out = h.release();
+  return 0;
+}
+
+int gett_execute(gett_plan_t plan, const void* a, const void* b, void* c) {
+  if (!plan) return GETT_E_INVALID_ARG;
+  return plan->dtype == 'd' ? execute_handle<double>(plan, true, a, b, c, nullptr)
+                            : execute_handle<float>(plan, true, a, b, c, nullptr);
+}
+
+int gett_execute_device(gett_plan_t plan, const void* a, const void* b, void* c, void* stream) {
+  if (!plan) return GETT_E_INVALID_ARG;
+  return plan->dtype == 'd' ? execute_handle<double>(plan, false, a, b, c, (cudaStream_t)stream)
+                            : execute_handle<float>(plan, false, a, b, c, (cudaStream_t)stream);
+}
+
+void gett_plan_destroy(gett_plan_t plan) { delete plan; }
+
 int gett_set_kernel(const char* name) {
   if (!name) return GETT_E_INVALID_ARG;
   if (!strcmp(name, "auto")) g_mode = Mode::Auto;
@@ -2729,7 +2850,8 @@ void gett_release_caches(void) {
 
 // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed;
 // 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi,
-//       gett_multi_schedule, gett_pack[_device], gett_set_kr
-int gett_abi_version(void) { return 104; }
+//       gett_multi_schedule, gett_pack[_device], gett_set_kr,
+// 1.05: gett_plan_create / gett_execute[_device] / gett_plan_destroy
+int gett_abi_version(void) { return 105; }
 
 }  // extern "C"

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert _native.LIB.gett_abi_version() == 104
+    assert _native.LIB.gett_abi_version() == 105
 
 
 @pytest.mark.parametrize("case", load_validation(), ids=lambda c: c["label"])
@@ -224,3 +224,27 @@ def test_readonly_c_returns_phase_two_errors():
     c.flags.writeable = False
     with pytest.raises(ValueError):
         g.dgett(2, (2, 3), (3, 1), a, 2, (3, 4), (4, 1), b, 1, (1,), (0,), (0, 1), (4, 1), c)
+
+
+def test_plan_handle_validates_like_the_entry_without_device():
+    """dgett_plan reports exactly dgett's validation errors (no GPU needed),
+    and an empty iteration space plans to a no-op."""
+    n = 0
+    for case in load_validation():
+        if "raises" in case or not case["errors"]:
+            continue
+        args, kw = case["args"], case["kw"]
+        want = g.dgett(*args, **kw)
+        p = g.dgett_plan(*args, **kw)
+        assert [(e.code, e.message) for e in p.errors] == [(e.code, e.message) for e in want]
+        assert p(args[3] if isinstance(args[3], np.ndarray) else np.asarray(args[3]),
+                 np.asarray(args[7]), args[13]) == p.errors
+        p.close()
+        n += 1
+    assert n > 100
+    c = np.full(4, 3.0)
+    p = g.dgett_plan(1, (0,), (1,), np.array([1.0]), 1, (1,), (1,), np.array([2.0]), 0, (), (), (0, 1),
+                     (1, 1), c)
+    assert p.errors == [] and p(np.array([1.0]), np.array([2.0]), c) == [] and np.all(c == 3.0)
+    with pytest.raises(TypeError):
+        g.GettPlan("z", 0, (), (), 1, 0, (), (), 1, 0, (), (), (), (), 1)

@@ -56,9 +56,27 @@ def main():
         ref = per_call(lambda: nat(*args), n)
         g.set_kernel("auto")
         empty = per_call(lambda: torch.cuda.current_stream(), n)
+        # plan handle: device tensors (stream-ordered) and the bare execute
+        plan = (g.dgett_plan if w.dtype == "d" else g.sgett_plan)(
+            *w.args(a, b, c)[0], **w.args(a, b, c)[1])
+        pdev = per_call(lambda: plan.device(ta, tb, tc), n)
+        h, ex = plan._h, _native.LIB.gett_execute_device
+        pa, pb, pc = ta.data_ptr(), tb.data_ptr(), tc.data_ptr()
+        pnat = per_call(lambda: ex(h, pa, pb, pc, stream), n)
+        # host buffers, synchronous end to end (pinned): dgett vs the plan
+        ha, hb, hc = (torch.from_numpy(x).pin_memory().numpy() for x in (a, b, c))
+        hpos, hkw = w.args(ha, hb, hc)
+        entry = g.dgett if w.dtype == "d" else g.sgett
+        host_full = per_call(lambda: entry(*hpos, **hkw), n)
+        host_plan = per_call(lambda: plan(ha, hb, hc), n)
+        plan.close()
         print(json.dumps({"config": name, "us_per_call_python_entry": round(full, 2),
                           "us_per_call_native": round(native, 2),
                           "us_per_call_native_ref_kernel": round(ref, 2),
+                          "us_per_call_plan_device": round(pdev, 2),
+                          "us_per_call_plan_native_execute": round(pnat, 2),
+                          "us_per_call_host_dgett_sync": round(host_full, 2),
+                          "us_per_call_host_plan_sync": round(host_plan, 2),
                           "us_current_stream": round(empty, 2), "kernel": g.last_kernel()}),
               flush=True)
 
