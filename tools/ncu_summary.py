@@ -1,12 +1,21 @@
 """Summarise one kernel of an ncu report (--page raw) into a small JSON file
 for profiles/.  Usage:
     python tools/ncu_summary.py REPORT.ncu-rep OUT.json [note...]
+The summary records the sha256 prefix of the libgett_b200.so in the tree
+(the build the capture must have been taken on; bench.py reports the capture's
+traffic only when it matches the library it runs) and algorithmic figures when
+GETT_ALG_BYTES / GETT_ALG_FLOPS are set.
 """
 import csv
+import hashlib
 import io
 import json
+import os
 import subprocess
 import sys
+
+LIB = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2410_06770_b200",
+                   "libgett_b200.so")
 
 KEYS = {
     "gpu__time_duration.sum": "gpu_time",
@@ -32,9 +41,13 @@ SCALE = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1, "ms": 1e-3, "us": 
 
 
 def main():
-    rep, out = sys.argv[1], sys.argv[2]
-    note = " ".join(sys.argv[3:])
-    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+    args = sys.argv[1:]
+    kfilter = []
+    if args and args[0].startswith("--kernel="):
+        kfilter = ["-k", "regex:" + args.pop(0).split("=", 1)[1]]
+    rep, out = args[0], args[1]
+    note = " ".join(args[2:])
+    raw = subprocess.run(["ncu", "-i", rep] + kfilter + ["--page", "raw", "--csv"], capture_output=True,
                          text=True, check=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     h, u, v = rows[0], rows[1], rows[2]
@@ -56,6 +69,13 @@ def main():
             stalls[name.split("stalled_")[1].split("_per")[0]] = round(x, 3)
     if "dram_bytes_read" in d:
         d["dram_bytes_per_launch"] = d["dram_bytes_read"] + d.get("dram_bytes_write", 0.0)
+    with open(LIB, "rb") as f:
+        d["so_sha16"] = hashlib.sha256(f.read()).hexdigest()[:16]
+    for env, key in (("GETT_ALG_BYTES", "algorithmic_bytes_per_launch"), ("GETT_ALG_FLOPS", "algorithmic_flops_per_launch")):
+        if os.environ.get(env):
+            d[key] = float(os.environ[env])
+    if d.get("algorithmic_bytes_per_launch") and d.get("dram_bytes_per_launch"):
+        d["traffic_over_algorithmic"] = round(d["dram_bytes_per_launch"] / d["algorithmic_bytes_per_launch"], 3)
     d["top_stalls_per_issue"] = stalls
     with open(out, "w") as f:
         json.dump(d, f, indent=1)
