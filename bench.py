@@ -67,9 +67,9 @@ C2 = W.C2
 METRIC = "xGETT GFLOP/s (2·|C|·|K|/s), DGETT c2 4096^3 strided GEMM-shaped subtensor"
 WORKLOAD = ("c2: DGETT A[4096,4096] view of f64 [4100,4224], B[4096,4096] view of [4096,4160], "
             "contract A1-B0, identity PERM, C += into [4096,4200] parent (BASELINE configs[1])")
-FP64_PEAK_TFLOPS = 37.151  # measured DMMA m16n8k4 loop, profiles/peaks_r01.jsonl
-FP64_PEAK_SRC = ("measured FP64 DMMA peak (tools/peaks.cu, profiles/peaks_r01.jsonl); "
-                 "MEASURED_PEAKS.json has no FP64 figure")
+FP64_PEAK_TFLOPS = 37.116  # best DMMA loop, profiles/r02/peaks/peaks.jsonl (SM clock 1965 MHz: clocks.csv)
+FP64_PEAK_SRC = ("measured FP64 DMMA peak (tools/peaks.cu via tools/peaks_with_clocks.sh, "
+                 "profiles/r02/peaks/{peaks.jsonl,clocks.csv}); MEASURED_PEAKS.json has no FP64 figure")
 
 
 def env_rank():
@@ -550,7 +550,7 @@ def splitk_c5(dist, dev, args):
 
 
 # fp32 via 3xTF32: a third of the tf32 MMA rate measured by tools/mma_rate.cu
-# (2046 MAC/clk/SM x 148 SMs x 1.965 GHz)
+# (2046 MAC/clk/SM x 148 SMs x 1.965 GHz; profiles/r02/peaks/mma_rate.jsonl)
 TF32X3_PEAK_TFLOPS = 2 * 2046 * 148 * 1.965e9 / 3 / 1e12
 
 
