@@ -168,19 +168,38 @@ def lib_sha16():
         return None
 
 
+def src_sha16():
+    """sha256 prefix of the native sources the library is built from (nvcc's
+    output bytes differ between identical builds, so a capture is matched to
+    a build by its sources when the binary hash differs)."""
+    h = hashlib.sha256()
+    csrc = os.path.join(ROOT, "paper_2410_06770_b200", "csrc")
+    files = sorted(os.path.join(csrc, f) for f in os.listdir(csrc)
+                   if f.endswith((".cu", ".cuh", ".hpp", ".cpp")) or f == "Makefile")
+    files.append(os.path.join(ROOT, "include", "gett_b200.h"))
+    for fn in files:
+        h.update(os.path.basename(fn).encode())
+        with open(fn, "rb") as f:
+            h.update(f.read())
+    return h.hexdigest()[:16]
+
+
 def traffic_from_profiles():
     """dram bytes per launch of the DGETT kernel from the committed ncu capture
     — only when the capture was taken on THIS build of libgett_b200.so (the
-    capture records the library's sha256 prefix); else None."""
+    capture records the library's sha256 prefix, and the sha256 prefix of its
+    sources); else None."""
     p = os.path.join(ROOT, "profiles", "ncu_dgett_c2.json")
     if not os.path.exists(p):
         return None, "no capture"
     with open(p) as f:
         d = json.load(f)
-    have, want = lib_sha16(), d.get("so_sha16")
-    if want is None or have != want:
-        return None, f"capture so_sha16 {want} != this build {have}"
-    return d.get("dram_bytes_per_launch"), f"profiles/ncu_dgett_c2.json (so_sha16 {want})"
+    if d.get("so_sha16") and d["so_sha16"] == lib_sha16():
+        return d.get("dram_bytes_per_launch"), f"profiles/ncu_dgett_c2.json (same binary, so_sha16 {d['so_sha16']})"
+    if d.get("src_sha16") and d["src_sha16"] == src_sha16():
+        return d.get("dram_bytes_per_launch"), (f"profiles/ncu_dgett_c2.json (same sources, src_sha16 "
+                                                f"{d['src_sha16']}; binary rebuilt)")
+    return None, f"capture so/src {d.get('so_sha16')}/{d.get('src_sha16')} != this build {lib_sha16()}/{src_sha16()}"
 
 
 # ---------------------------------------------------------------------------
@@ -494,7 +513,8 @@ def run_ours(args):
                      "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s",
                      "frac": round(achieved / FP64_PEAK_TFLOPS, 4),
                      "traffic": traffic, "traffic_source": traffic_src,
-                     "peak_source": FP64_PEAK_SRC, "kernel": kname, "so_sha16": lib_sha16()},
+                     "peak_source": FP64_PEAK_SRC, "kernel": kname, "so_sha16": lib_sha16(),
+                     "src_sha16": src_sha16()},
         "clocks": clocks.summary(),
         "e2e": {"value": round(e2e_value, 2), "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
                 "d2h_bytes_per_step": int(d2h),

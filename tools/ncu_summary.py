@@ -71,6 +71,11 @@ def main():
         d["dram_bytes_per_launch"] = d["dram_bytes_read"] + d.get("dram_bytes_write", 0.0)
     with open(LIB, "rb") as f:
         d["so_sha16"] = hashlib.sha256(f.read()).hexdigest()[:16]
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    sys.argv = sys.argv[:1]
+    import bench  # noqa: E402  (only for src_sha16; bench imports no GPU code at import time)
+
+    d["src_sha16"] = bench.src_sha16()
     for env, key in (("GETT_ALG_BYTES", "algorithmic_bytes_per_launch"), ("GETT_ALG_FLOPS", "algorithmic_flops_per_launch")):
         if os.environ.get(env):
             d[key] = float(os.environ[env])
