@@ -46,6 +46,8 @@ bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one 
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 bool g_dgett_tma = true;  // DGETT: TMA-fed operands for affine views (GETT_DGETT_TMA=0: cp.async gathers)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
+bool g_kr_pair = false;   // k-run kernel as CTA pairs (cta_group::2) when the tiling allows (GETT_KR_PAIR=1;
+                          // c5: 48.2 vs 48.1 us single — the MMA issue, not shared memory, binds)
 bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
                           // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
@@ -73,6 +75,8 @@ void read_env_once() {
   if (dtv) g_dgett_tma = std::atoi(dtv) != 0;
   const char* krv = std::getenv("GETT_KR");
   if (krv) g_kr = std::atoi(krv);
+  const char* krp = std::getenv("GETT_KR_PAIR");
+  if (krp) g_kr_pair = std::atoi(krp) != 0;
   const char* krf = std::getenv("GETT_KR_FUSED");
   if (krf) g_kr_fused = std::atoi(krf) != 0;
   const char* pv = std::getenv("GETT_PAIR");
@@ -145,6 +149,11 @@ struct DevPlan {
   } kr_l[2];            // X, Y
   KrParams kr_p{};
   const void* kr_base[2] = {nullptr, nullptr};
+  // CTA-pair form: X tiles in pairs, each CTA loads half of Y's NT rows
+  bool kr_pair_ok = false;
+  KrLayout kr_ly_pair;  // the Y layout with NT/2-row boxes
+  CUtensorMap kr_my_pair;
+  const void* kr_base_pair = nullptr;
   // used by a call captured into a CUDA graph: the graph holds raw pointers
   // into d_tab, so the LRU never evicts it (gett_release_caches still does)
   std::atomic<bool> pinned{false};
@@ -770,7 +779,10 @@ bool kr_decide(DevPlan& dp) {
     kp.lslot_bytes = (int32_t)(xbytes + ybytes);
     kp.oslot_bytes = (int32_t)(2 * ybytes);
     kp.a_col0 = (int32_t)up(NT, 32);
-    kp.aslots = (int32_t)std::min<int64_t>(8, (512 - kp.a_col0) / (2 * KR));
+    // two TMEM A slots, like the operand slots: each split warpgroup owns one
+    // of each and one commit frees both (a second commit per k-block costs
+    // ~46 clk of MMA issue, tools/mma_rate.cu)
+    kp.aslots = (int32_t)std::min<int64_t>(2, (512 - kp.a_col0) / (2 * KR));
     // as many load slots as fit beside two operand slots.  Ring sizes keep
     // the mbarrier parity waits unambiguous (no waiter two phases ahead): the
     // split warpgroups take alternate k-blocks, so with an even number of
@@ -789,6 +801,12 @@ bool kr_decide(DevPlan& dp) {
     kp.bar_off = (int32_t)(kp.o_off + (int64_t)so * kp.oslot_bytes);
     dp.kr_x = x;
     dp.kr_run = (int)KR;
+    // pairs: an even number of X tiles, one Y box dim covering exactly NT rows
+    dp.kr_pair_ok = kp.tiles_x % 2 == 0 && yrows == NT && NT % 16 == 0 && nyb == 1;
+    if (dp.kr_pair_ok) {
+      dp.kr_ly_pair = dp.kr_l[1];
+      dp.kr_ly_pair.box[0] = (uint32_t)(NT / 2);
+    }
     return true;
   }
   return false;
@@ -894,7 +912,13 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
       kp.spin_ns = spin;
     }
   }
-  CK(launch_sgett_kr(kp, dp.kr_run, stream));
+  bool pair = g_kr_pair && dp.kr_pair_ok;
+  if (pair && dp.kr_base_pair != Y) {
+    if (kr_encode(dp.kr_ly_pair, Y, &dp.kr_my_pair)) dp.kr_base_pair = Y;
+    else pair = false;
+  }
+  if (pair) kp.my = dp.kr_my_pair;
+  CK(launch_sgett_kr(kp, dp.kr_run, pair, stream));
   ++g_launches;
   if (splits > 1 && kp.cnt == nullptr) {
     TiledParams<float> tp{};
@@ -910,8 +934,12 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
     CK(launch_splitk_reduce<float>(tp, stream));
     ++g_launches;
   }
-  t_last_kernel = splits == 1 ? "sgett_tc3xtf32_kr"
-                              : (kp.cnt ? "sgett_tc3xtf32_kr_splitk_fused" : "sgett_tc3xtf32_kr_splitk");
+  if (pair)
+    t_last_kernel = splits == 1 ? "sgett_tc3xtf32_kr_pair"
+                                : (kp.cnt ? "sgett_tc3xtf32_kr_pair_splitk_fused" : "sgett_tc3xtf32_kr_pair_splitk");
+  else
+    t_last_kernel = splits == 1 ? "sgett_tc3xtf32_kr"
+                                : (kp.cnt ? "sgett_tc3xtf32_kr_splitk_fused" : "sgett_tc3xtf32_kr_splitk");
   return 1;
 }
 
@@ -2801,9 +2829,10 @@ int gett_set_complex_embed(int on) {
 }
 
 int gett_set_kr(int mode) {
-  if (mode < 0 || (mode & 3) == 3 || mode > 6) return GETT_E_INVALID_ARG;
+  if (mode < 0 || (mode & 3) == 3 || mode > 15) return GETT_E_INVALID_ARG;
   g_kr = mode & 3;
   g_kr_fused = (mode & 4) != 0;
+  g_kr_pair = (mode & 8) != 0;
   return 0;
 }
 

@@ -90,7 +90,8 @@ cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bo
 cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s);
 
 // k-run SGETT (sgett_kr.cu); KR in {8, 16, ..., 64}
-cudaError_t launch_sgett_kr(const KrParams& p, int KR, cudaStream_t s);
+// pair: clusters of 2 (cta_group::2, M = 256; tiles_x even, y_rows == NT)
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, bool pair, cudaStream_t s);
 int sgett_kr_max_nt();
 
 int tiled_bm();

@@ -101,6 +101,43 @@ __device__ __forceinline__ void mma_tf32(uint32_t d, uint32_t a_tmem, uint64_t b
       : "memory");
 }
 // K-major no-swizzle shared-memory descriptor (sm_100 version bit 46)
+// CTA-pair helpers (cta_group::2): the leader (rank 0) issues the pair MMAs;
+// both CTAs' split warps arrive on the leader's ready barrier, its commits
+// are multicast to the same barrier offsets in both CTAs
+__device__ __forceinline__ void arrive_leader(uint32_t local_bar) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, 0;" : "=r"(remote) : "r"(local_bar));
+  asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(remote) : "memory");
+}
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t a, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n\t"
+      "}" ::"r"(a),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void mma_tf32_pair(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::tf32 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void commit_pair(uint32_t bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
+      "h"((uint16_t)3)
+      : "memory");
+}
+__device__ __forceinline__ void cluster_sync2() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)(lbo >> 4) << 16) | ((uint64_t)(sbo >> 4) << 32) |
          (1ull << 46);
@@ -197,7 +234,12 @@ __device__ __forceinline__ void reduce_slice(const KrParams& p, int x0, int y0, 
   }
 }
 
-template <int KR>
+// PAIR: clusters of 2 CTAs (cta_group::2, M = 256): each CTA holds its own
+// 128 X rows in TMEM and half of Y's NT rows (Y rows rank * NT/2 ...) as the
+// K-major operand in its shared memory; the leader issues one pair MMA per
+// (k-step, product) for both — per SM half the Y bytes (loads, split,
+// B-operand reads) and half the MMA instructions of the one-CTA form.
+template <int KR, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_constant__ KrParams p) {
   using G = Cfg<KR>;
   // three rings: load slots [X raw | Y raw] (TMA -> split; freed by the split
@@ -225,12 +267,29 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
 #endif
 
   const int ntiles = p.tiles_x * p.tiles_y;
-  const int tile = blockIdx.x % ntiles, split = blockIdx.x / ntiles;
-  const int tx = tile % p.tiles_x, ty = tile / p.tiles_x;
+  uint32_t rank = 0;
+  if (PAIR) asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  int tile, split, tx, ty;
+  if (PAIR) {
+    // cluster c covers X tiles (2 tp, 2 tp + 1) of column tile ty, K slice split
+    const int tx2 = p.tiles_x >> 1, cl = blockIdx.x >> 1;
+    const int tpair = cl % (tx2 * p.tiles_y);
+    split = cl / (tx2 * p.tiles_y);
+    tx = 2 * (tpair % tx2) + (int)rank;
+    ty = tpair / tx2;
+    tile = ty * p.tiles_x + tx;
+  } else {
+    tile = blockIdx.x % ntiles;
+    split = blockIdx.x / ntiles;
+    tx = tile % p.tiles_x;
+    ty = tile / p.tiles_x;
+  }
+  // rows of Y this CTA loads and splits (its half of the pair's N = NT)
+  const int yrows_me = PAIR ? p.NT / 2 : p.y_rows;
   const int x0 = tx * p.x_rows, y0 = ty * p.y_rows;
   const int kb0 = split * p.kpc;
   const int nkb = max(0, min(p.nkb, kb0 + p.kpc) - kb0);
-  const uint32_t tile_bytes = (uint32_t)(KR * p.y_rows * 4);  // the Y box (raw [KR][y_rows])
+  const uint32_t tile_bytes = (uint32_t)(KR * yrows_me * 4);  // the Y box (raw [KR][rows])
 
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&p.mx) : "memory");
@@ -240,7 +299,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       mbar_init(smem_u32(lfree + s), 4);  // the 4 warps of the split warpgroup
     }
     for (int s = 0; s < SO; ++s) {
-      mbar_init(smem_u32(ready + s), 4);
+      mbar_init(smem_u32(ready + s), PAIR ? 8 : 4);  // (pair: the leader's, 4 warps of each CTA)
       mbar_init(smem_u32(ofree + s), 1);  // tcgen05.commit
     }
     for (int s = 0; s < TA; ++s) mbar_init(smem_u32(afree + s), 1);
@@ -248,12 +307,19 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == MMA_WARP) {
-    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
-                 "r"(TMEM_COLS));
-    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    if (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+    } else {
+      asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(TMEM_COLS));
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  if (PAIR) cluster_sync2();  // both CTAs' barriers initialised before any remote arrival
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
 
@@ -262,7 +328,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
     if (lane == 0 && nkb > 0) {
       int32_t cx[5] = {0, 0, 0, 0, 0}, cy[5] = {0, 0, 0, 0, 0};
       row_coords(cx, x0, p.xnr, p.xr_ext, p.xr_pos);
-      row_coords(cy, y0, p.ynr, p.yr_ext, p.yr_pos);
+      row_coords(cy, y0 + (PAIR ? (int)rank * yrows_me : 0), p.ynr, p.yr_ext, p.yr_pos);
       int d0 = 0, d1 = 0;  // outer k digits of k-block kb0
       if (p.nko > 0) {
         d0 = kb0 % p.k_ext[0];
@@ -317,13 +383,13 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
     constexpr int YU = (G::CHK * (NT_MAX / 4) + WG - 1) / WG;
     uint32_t y_src[YU], y_dst[YU];
     int y_rot[YU];
-    const int nq = p.y_rows >> 2;  // row quads of the box (y_rows % 4 == 0)
+    const int nq = yrows_me >> 2;  // row quads of the box (rows % 4 == 0)
     int ny_units = 0;
 #pragma unroll
     for (int i = 0; i < YU; ++i) {
       const int uu = tw + WG * i;
       const int c = uu / nq, rq = uu - c * nq;
-      y_src[i] = (uint32_t)(4 * c * p.y_rows * 4 + rq * 16);
+      y_src[i] = (uint32_t)(4 * c * yrows_me * 4 + rq * 16);
       y_dst[i] = (uint32_t)(((4 * rq) >> 3) * G::SBO + c * 128 + ((4 * rq) & 7) * 16);
       y_rot[i] = (rq >> 1) & 3;
       if (uu < G::CHK * nq) ny_units = i + 1;
@@ -341,8 +407,9 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       w_full += clock64() - c0;
       c0 = clock64();
 #endif
-      if (kb >= TA) mbar_wait(smem_u32(afree + sa), (kb / TA - 1) & 1);
+      // (SO == TA: one commit frees a k-block's operand slot and TMEM slot)
       if (kb >= SO) mbar_wait(smem_u32(ofree + so), (kb / SO - 1) & 1);
+      if (TA != SO && kb >= TA) mbar_wait(smem_u32(afree + sa), (kb / TA - 1) & 1);
 #ifdef GETT_KR_TRACE
       w_lo += clock64() - c0;
       c0 = clock64();
@@ -397,7 +464,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           if (i < ny_units) {
             float4 v[4];
 #pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(yb + y_src[i] + j * p.y_rows * 4);
+            for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(yb + y_src[i] + j * yrows_me * 4);
             float4 rows[4];
             rows[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
             rows[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
@@ -425,7 +492,10 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
       __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(ready + so));
+      if (lane == 0) {
+        if (PAIR) arrive_leader(smem_u32(ready + so));
+        else mbar_arrive(smem_u32(ready + so));
+      }
 #ifdef GETT_KR_TRACE
       t_y += clock64() - c0;
 #endif
@@ -551,9 +621,10 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       }
     }
   } else {
-    // ---------------- MMA warp ----------------
-    if (lane == 0 && nkb > 0) {
-      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.NT >> 3) << 17) | ((128u >> 4) << 24);
+    // ---------------- MMA warp (pair: the leader's only) ----------------
+    if (lane == 0 && nkb > 0 && rank == 0) {
+      const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.NT >> 3) << 17) |
+                             ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
       const uint32_t sbase = smem_u32(smem);
 #ifdef GETT_KR_TRACE
       long long w_ready = 0, t_issue = 0;
@@ -564,7 +635,8 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
 #ifdef GETT_KR_TRACE
         long long c0 = clock64();
 #endif
-        mbar_wait(smem_u32(ready + so), (kb / SO) & 1);
+        if (PAIR) mbar_wait_cluster(smem_u32(ready + so), (kb / SO) & 1);
+        else mbar_wait(smem_u32(ready + so), (kb / SO) & 1);
 #ifdef GETT_KR_TRACE
         w_ready += clock64() - c0;
         c0 = clock64();
@@ -581,17 +653,29 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           const uint32_t ah = ah0 + 8 * j, al = ah + KR;
           // (hi*hi, hi*lo_Y, lo_X*hi: the tiled kernel's order when its TMEM
           // operand is this kernel's Y — c5 — so both give the same bits there)
-          mma_tf32(tmem, ah, bh, idesc, (kb | j) != 0);
-          mma_tf32(tmem, ah, bl, idesc, 1);
-          mma_tf32(tmem, al, bh, idesc, 1);
+          if (PAIR) {
+            mma_tf32_pair(tmem, ah, bh, idesc, (kb | j) != 0);
+            mma_tf32_pair(tmem, ah, bl, idesc, 1);
+            mma_tf32_pair(tmem, al, bh, idesc, 1);
+          } else {
+            mma_tf32(tmem, ah, bh, idesc, (kb | j) != 0);
+            mma_tf32(tmem, ah, bl, idesc, 1);
+            mma_tf32(tmem, al, bh, idesc, 1);
+          }
         }
-        commit(smem_u32(ofree + so));
-        commit(smem_u32(afree + sa));
+        if (PAIR) {
+          commit_pair(smem_u32(ofree + so));
+          if (TA != SO) commit_pair(smem_u32(afree + sa));
+        } else {
+          commit(smem_u32(ofree + so));
+          if (TA != SO) commit(smem_u32(afree + sa));
+        }
 #ifdef GETT_KR_TRACE
         t_issue += clock64() - c0;
 #endif
       }
-      commit(smem_u32(done));
+      if (PAIR) commit_pair(smem_u32(done));
+      else commit(smem_u32(done));
 #ifdef GETT_KR_TRACE
       if (blockIdx.x < 4) printf("KRROLE blk %d mma wait_ready %lld issue %lld nkb %d first_ready_ns %llu loop_ns %llu since_start_ns %llu\n", blockIdx.x, w_ready, t_issue, nkb,
                                  g_first - tr_start, globaltimer() - g_first, globaltimer() - tr_start);
@@ -601,32 +685,56 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
-  if (warp == MMA_WARP)
+  if (PAIR) {
+    cluster_sync2();  // the peer's MMAs (issued by the leader) are done with this CTA's smem
+    if (warp == MMA_WARP)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  } else if (warp == MMA_WARP) {
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+  }
 }
 
 template <int KR>
-cudaError_t launch_t(const KrParams& p, cudaStream_t s) {
-  auto k = sgett_kr_kernel<KR>;
-  static unsigned long long configured = 0;
-  cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured);
+cudaError_t launch_t(const KrParams& p, bool pair, cudaStream_t s) {
+  if (!pair) {
+    auto k = sgett_kr_kernel<KR, false>;
+    static unsigned long long configured = 0;
+    cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured);
+    if (e != cudaSuccess) return e;
+    k<<<(unsigned)(p.tiles_x * p.tiles_y * p.splits), THREADS, p.bar_off + BAR_BYTES, s>>>(p);
+    return cudaGetLastError();
+  }
+  auto k = sgett_kr_kernel<KR, true>;
+  static unsigned long long configured2 = 0;
+  cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured2);
   if (e != cudaSuccess) return e;
-  k<<<(unsigned)(p.tiles_x * p.tiles_y * p.splits), THREADS, p.bar_off + BAR_BYTES, s>>>(p);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(p.tiles_x * p.tiles_y * p.splits));  // tiles_x even: 2 CTAs per X-tile pair
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = p.bar_off + BAR_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, p);
 }
 
 }  // namespace kr
 
-cudaError_t launch_sgett_kr(const KrParams& p, int KR, cudaStream_t s) {
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, bool pair, cudaStream_t s) {
   switch (KR) {
-    case 8: return kr::launch_t<8>(p, s);
-    case 16: return kr::launch_t<16>(p, s);
-    case 24: return kr::launch_t<24>(p, s);
-    case 32: return kr::launch_t<32>(p, s);
-    case 40: return kr::launch_t<40>(p, s);
-    case 48: return kr::launch_t<48>(p, s);
-    case 56: return kr::launch_t<56>(p, s);
-    case 64: return kr::launch_t<64>(p, s);
+    case 8: return kr::launch_t<8>(p, pair, s);
+    case 16: return kr::launch_t<16>(p, pair, s);
+    case 24: return kr::launch_t<24>(p, pair, s);
+    case 32: return kr::launch_t<32>(p, pair, s);
+    case 40: return kr::launch_t<40>(p, pair, s);
+    case 48: return kr::launch_t<48>(p, pair, s);
+    case 56: return kr::launch_t<56>(p, pair, s);
+    case 64: return kr::launch_t<64>(p, pair, s);
     default: return cudaErrorInvalidValue;
   }
 }

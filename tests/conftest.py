@@ -20,7 +20,7 @@ def kernel_mode():
                                        set_split_k, set_stream_k, set_tma)
 
     def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
-            kr="auto", kr_fused=False):
+            kr="auto", kr_fused=False, kr_pair=False):
         set_kernel(name)
         set_split_k(split)
         set_pipeline(pipeline)
@@ -28,7 +28,7 @@ def kernel_mode():
         set_tma(tma)
         set_pair(pair)
         set_complex_embed(complex_embed)
-        set_kr(kr, kr_fused)
+        set_kr(kr, kr_fused, kr_pair)
 
     yield use
     set_kernel("auto")

@@ -80,18 +80,23 @@ SHAPES = [
 @pytest.mark.parametrize("c_m_fast", [True, False])
 @pytest.mark.parametrize("split", [0, 1, 5])
 def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, kernel_mode):
+    """single CTAs and CTA pairs (where the tiling allows), fused and separate
+    reduce: all four bitwise equal (same MMAs, same order), within the bar."""
     m1, m2, kr, k2, n = shape
-    outs = []
-    for fused in (True, False):
-        pos, kw = _case(m1, m2, kr, k2, n, c_m_fast, seed=sum(shape) + split)
-        c0 = pos[13].copy()
-        kernel_mode("tiled", split=split, kr="force", kr_fused=fused)
-        assert g.sgett(*pos, **kw) == []
-        kname = g.last_kernel()
-        assert kname.startswith("sgett_tc3xtf32_kr"), kname
-        _check(pos, kw, c0)
-        outs.append(pos[13])
-    assert outs[0].tobytes() == outs[1].tobytes()
+    outs, names = [], []
+    for pair in (True, False):
+        for fused in (True, False):
+            pos, kw = _case(m1, m2, kr, k2, n, c_m_fast, seed=sum(shape) + split)
+            c0 = pos[13].copy()
+            kernel_mode("tiled", split=split, kr="force", kr_fused=fused, kr_pair=pair)
+            assert g.sgett(*pos, **kw) == []
+            kname = g.last_kernel()
+            assert kname.startswith("sgett_tc3xtf32_kr"), kname
+            _check(pos, kw, c0)
+            outs.append(pos[13])
+            names.append(kname)
+    assert all(o.tobytes() == outs[0].tobytes() for o in outs[1:]), names
+    assert not any("pair" in k for k in names[2:]), names
 
 
 def test_kr_auto_on_c5_and_off_for_large_tilings(kernel_mode):
@@ -149,3 +154,11 @@ def test_kr_graph_replay_fused(kernel_mode):
         gg.replay()
     torch.cuda.synchronize()
     assert torch.equal(tc, direct)
+
+
+def test_kr_pair_taken_on_c5(kernel_mode):
+    kernel_mode("auto", kr_pair=True)
+    a, b, c = C5.buffers()
+    pos, kw = C5.args(a, b, c)
+    assert g.sgett(*pos, **kw) == []
+    assert g.last_kernel().startswith("sgett_tc3xtf32_kr_pair"), g.last_kernel()

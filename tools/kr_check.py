@@ -17,7 +17,8 @@ from oracle import oracle  # noqa: E402
 from paper_2410_06770_b200.device import sgett_device  # noqa: E402
 from paper_2410_06770_b200.workloads import CONFIGS  # noqa: E402
 
-MODES = [("tiled", dict(kr="off")), ("kr_fused", dict(kr="force", fused=True)), ("kr_sep", dict(kr="force"))]
+MODES = [("tiled", dict(kr="off")), ("kr_fused", dict(kr="force", fused=True)), ("kr_sep", dict(kr="force")),
+         ("kr_pair", dict(kr="force", pair=True))]
 
 
 def main(names):
@@ -31,7 +32,7 @@ def main(names):
         ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
         outs = {}
         for mode, kw in MODES:
-            g.set_kr(kw["kr"], kw.get("fused", False))
+            g.set_kr(kw["kr"], kw.get("fused", False), kw.get("pair", False))
             tc = torch.from_numpy(c).cuda()
             pos, kwa = w.args(ta, tb, tc)
             assert sgett_device(*pos, **kwa) == []

@@ -151,7 +151,10 @@ void runp(long long* d) {
 
 // the k-run kernel's pattern (sgett_kr.cu): per k-block KR/8 k-steps x 3
 // MMAs, M = 128, N = NT, A from TMEM, B K-major no-swizzle with SBO = KR/4 x 128
-template <int NT, int KR, bool RND, int FENCE = 0>
+// COMMIT2: two commits per k-block (the kernel frees an operand slot and a
+// TMEM slot); STW: the other three warps keep writing TMEM columns (the split
+// warps' tcgen05.st traffic) while the MMAs run
+template <int NT, int KR, bool RND, int FENCE = 0, bool COMMIT2 = false, bool STW = false>
 __global__ void pattern_kr(long long* out, int kblocks) {
   extern __shared__ __align__(1024) uint8_t sm[];
   constexpr int STG = 4, TB = NT * KR * 4, SB = 2 * TB;
@@ -194,6 +197,21 @@ __global__ void pattern_kr(long long* out, int kblocks) {
     asm volatile("tcgen05.fence::after_thread_sync;");
   }
   constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(NT >> 3) << 17) | ((128u >> 4) << 24);
+  volatile __shared__ int stop;
+  if (threadIdx.x == 0) stop = 0;
+  __syncthreads();
+  if (STW && threadIdx.x >= 32) {
+    // warps 1-3: tcgen05.st 32x32b.x16 into columns 448.. (not read by the MMAs)
+    const int w = threadIdx.x >> 5;
+    uint32_t v[16];
+    for (int j = 0; j < 16; ++j) v[j] = threadIdx.x * 16 + j;
+    while (!stop) {
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(tmem + ((uint32_t)(32 * w) << 16) + 448u),
+                   "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]),
+                   "r"(v[8]), "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15]) : "memory");
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    }
+  }
   if (threadIdx.x == 0) {
     const uint32_t base = su32(sm);
     long long t0 = clock64();
@@ -221,19 +239,22 @@ __global__ void pattern_kr(long long* out, int kblocks) {
                      "r"(ah), "l"(bl), "r"(IDESC), "r"(1));
       }
       asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + s)));
+      if (COMMIT2)
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + (s + 1) % STG)));
     }
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(su32(bar + STG)));
     asm volatile("{\n\t.reg .pred P1;\nW_%=:\n\tmbarrier.try_wait.parity.shared::cta.b64 P1, [%0], 0;\n\t@!P1 bra W_%=;\n\t}" ::"r"(su32(bar + STG)));
     out[blockIdx.x] = clock64() - t0;
+    stop = 1;
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
   if (threadIdx.x < 32) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
 }
 
-template <int NT, int KR, bool RND = false, int FENCE = 0>
+template <int NT, int KR, bool RND = false, int FENCE = 0, bool COMMIT2 = false, bool STW = false>
 void runkr(long long* d) {
-  auto k = pattern_kr<NT, KR, RND, FENCE>;
+  auto k = pattern_kr<NT, KR, RND, FENCE, COMMIT2, STW>;
   const int smem = 4 * 2 * NT * KR * 4 + 128;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int kb = 1024;
@@ -241,8 +262,8 @@ void runkr(long long* d) {
   cudaError_t e = cudaDeviceSynchronize();
   long long h;
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-  printf("{\"pattern\": \"sgett_kr k-block\", \"NT\": %d, \"KR\": %d, \"random_data\": %d, \"fence_every\": %d, \"cycles_per_kblock\": %.1f, "
-         "\"ideal\": %.1f, \"err\": \"%s\"}\n", NT, KR, (int)RND, FENCE, (double)h / kb, 3.0 * 128 * NT * KR / 2048.0,
+  printf("{\"pattern\": \"sgett_kr k-block\", \"NT\": %d, \"KR\": %d, \"random_data\": %d, \"fence_every\": %d, \"commit2\": %d, \"tmem_st_warps\": %d, \"cycles_per_kblock\": %.1f, "
+         "\"ideal\": %.1f, \"err\": \"%s\"}\n", NT, KR, (int)RND, FENCE, (int)COMMIT2, STW ? 3 : 0, (double)h / kb, 3.0 * 128 * NT * KR / 2048.0,
          cudaGetErrorString(e));
 }
 
@@ -253,6 +274,9 @@ int main() {
   runkr<96, 40, false, 1>(d);
   runkr<96, 40, false, 2>(d);
   runkr<96, 40, false, 4>(d);
+  runkr<96, 40, false, 0, true>(d);
+  runkr<96, 40, false, 0, false, true>(d);
+  runkr<96, 40, false, 1, true, true>(d);
   runkr<96, 40, true>(d);
   runkr<128, 40, true>(d);
   runkr<128, 40>(d);
