@@ -341,9 +341,10 @@ int gett_set_pair(int on);
  * 0 = off, 1 = automatic (runs < 64 on fewer tiles than SMs, the default),
  * 2 = whenever it applies; + 4 = split-K partials reduced inside the kernel
  * (tile counters; graph-replay safe) instead of by the separate reduce kernel
- * (the default); + 8 = pairs of X tiles as cta_group::2 clusters, each CTA
- * holding half of the other operand, when the tiling allows (off by default:
- * same speed on c5).  Also GETT_KR / GETT_KR_FUSED / GETT_KR_PAIR. */
+ * (the default); + 8 = never as CTA pairs (by default pairs of X tiles run as
+ * cta_group::2 clusters, each CTA holding half of the other operand, with two
+ * k runs per k-block when they fit).  Also GETT_KR / GETT_KR_FUSED /
+ * GETT_KR_PAIR. */
 int gett_set_kr(int mode);
 /* cgett / zgett on the tensor-core kernels: 1 = one real GETT on a real
  * embedding of the smaller operand (the default), 0 = four real GETTs on the

@@ -206,12 +206,13 @@ def set_devices(devices) -> None:
     check(LIB.gett_set_devices(len(devs), i32(devs)), "set_devices")
 
 
-def set_kr(mode: str = "auto", fused: bool = False, pair: bool = False) -> None:
+def set_kr(mode: str = "auto", fused: bool = False, pair: bool = True) -> None:
     """SGETT k-run kernel: "off", "auto" (default) or "force" (whenever it
     applies); fused=True reduces split-K partials inside the kernel instead of
-    with the separate reduce kernel (the default); pair=True runs pairs of X
-    tiles as cta_group::2 clusters when the tiling allows."""
-    code = {"off": 0, "auto": 1, "force": 2}[mode] | (4 if fused else 0) | (8 if pair else 0)
+    with the separate reduce kernel (the default); pair=False never runs pairs
+    of X tiles as cta_group::2 clusters (the default does when the tiling
+    allows, with two k runs per k-block when they fit)."""
+    code = {"off": 0, "auto": 1, "force": 2}[mode] | (4 if fused else 0) | (0 if pair else 8)
     check(LIB.gett_set_kr(code), "set_kr")
 
 

@@ -46,8 +46,8 @@ bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one 
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 bool g_dgett_tma = true;  // DGETT: TMA-fed operands for affine views (GETT_DGETT_TMA=0: cp.async gathers)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
-bool g_kr_pair = false;   // k-run kernel as CTA pairs (cta_group::2) when the tiling allows (GETT_KR_PAIR=1;
-                          // c5: 48.2 vs 48.1 us single — the MMA issue, not shared memory, binds)
+bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the tiling allows, two k runs per
+                          // k-block when they fit (c5: 46.1 vs 48.1 us; GETT_KR_PAIR=0: one CTA per tile)
 bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
                           // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
@@ -149,11 +149,16 @@ struct DevPlan {
   } kr_l[2];            // X, Y
   KrParams kr_p{};
   const void* kr_base[2] = {nullptr, nullptr};
-  // CTA-pair form: X tiles in pairs, each CTA loads half of Y's NT rows
-  bool kr_pair_ok = false;
-  KrLayout kr_ly_pair;  // the Y layout with NT/2-row boxes
-  CUtensorMap kr_my_pair;
-  const void* kr_base_pair = nullptr;
+  // launch configurations: [0] one CTA per tile, one k run per k-block;
+  // [1] CTA pairs (cta_group::2), two runs per k-block when they fit
+  struct KrCfg {
+    bool valid = false, pair = false;
+    int krn = 1;
+    KrParams kp{};       // slot / TMEM layout, tile counts (maps filled at launch)
+    KrLayout lx, ly;     // the two tensor-map layouts
+    CUtensorMap mx, my;
+    const void* base[2] = {nullptr, nullptr};
+  } krc[2];
   // used by a call captured into a CUDA graph: the graph holds raw pointers
   // into d_tab, so the LRU never evicts it (gett_release_caches still does)
   std::atomic<bool> pinned{false};
@@ -755,8 +760,6 @@ bool kr_decide(DevPlan& dp) {
         }
       }
     }
-    dp.kr_l[0].base_off = gx.T[0][0] + p.gk.T[x][0];
-    dp.kr_l[1].base_off = gy.T[0][0] + p.gk.T[y][0];
     kp.xnr = (int32_t)RX.size();
     kp.ynr = (int32_t)RY.size();
     kp.nko = nko;
@@ -770,43 +773,60 @@ bool kr_decide(DevPlan& dp) {
     kp.tiles_x = (int32_t)((MX + xrows - 1) / xrows);
     kp.tiles_y = (int32_t)((NY + yrows - 1) / yrows);
     kp.nkb = (int32_t)(p.gk.G / KR);
-    // shared memory: load slots [X raw 128 x (KR+4) | Y raw KR x NT] (freed
-    // right after the split) + operand slots [Y hi | Y lo] (freed by the MMA)
-    // + barriers, within 227 KB; TMEM: NT accumulator columns (rounded to 32)
-    // + 2 KR A columns (hi, lo) per A slot, within 512
-    auto up = [](int64_t v, int64_t a) { return (v + a - 1) / a * a; };
-    const int64_t xbytes = up(128 * (KR + 4) * 4, 1024), ybytes = up(KR * NT * 4, 1024);  // (box <= slot)
-    kp.lslot_bytes = (int32_t)(xbytes + ybytes);
-    kp.oslot_bytes = (int32_t)(2 * ybytes);
-    kp.a_col0 = (int32_t)up(NT, 32);
-    // two TMEM A slots, like the operand slots: each split warpgroup owns one
-    // of each and one commit frees both (a second commit per k-block costs
-    // ~46 clk of MMA issue, tools/mma_rate.cu)
-    kp.aslots = (int32_t)std::min<int64_t>(2, (512 - kp.a_col0) / (2 * KR));
-    // as many load slots as fit beside two operand slots.  Ring sizes keep
-    // the mbarrier parity waits unambiguous (no waiter two phases ahead): the
-    // split warpgroups take alternate k-blocks, so with an even number of
-    // load slots and two operand slots each group has slots of its own;
-    // TMEM slots are freed in MMA order, so any count >= 2 works.
-    auto fits = [&](int l, int o) {
-      return (int64_t)l * kp.lslot_bytes + (int64_t)o * kp.oslot_bytes + 512 <= 227 * 1024;
-    };
-    const int so = 2;
-    int sl = 8;
-    while (sl > 2 && !fits(sl, so)) sl -= 2;
-    if (kp.aslots < 2 || !fits(sl, so)) continue;
-    kp.lslots = sl;
-    kp.oslots = so;
-    kp.o_off = sl * kp.lslot_bytes;
-    kp.bar_off = (int32_t)(kp.o_off + (int64_t)so * kp.oslot_bytes);
+    kp.kpc = 0;
     dp.kr_x = x;
     dp.kr_run = (int)KR;
-    // pairs: an even number of X tiles, one Y box dim covering exactly NT rows
-    dp.kr_pair_ok = kp.tiles_x % 2 == 0 && yrows == NT && NT % 16 == 0 && nyb == 1;
-    if (dp.kr_pair_ok) {
-      dp.kr_ly_pair = dp.kr_l[1];
-      dp.kr_ly_pair.box[0] = (uint32_t)(NT / 2);
-    }
+    dp.kr_l[0].base_off = gx.T[0][0] + p.gk.T[x][0];
+    dp.kr_l[1].base_off = gy.T[0][0] + p.gk.T[y][0];
+    // launch configurations.  Shared memory: load slots [X raw KRN x 128 x
+    // (KR+4) | Y raw KE x rows] (freed right after the split) + two operand
+    // slots [Y hi | Y lo] (freed by the MMA) + barriers, within 227 KB; TMEM:
+    // NT accumulator columns (rounded to 32) + two A slots of 2 KE columns.
+    // Ring sizes keep the mbarrier parity waits unambiguous (no waiter two
+    // phases ahead): the split warpgroups take alternate k-blocks, so with an
+    // even number of load slots and two operand slots each group has slots of
+    // its own; one commit frees a k-block's operand and TMEM slots (a second
+    // commit per k-block costs ~46 clk of MMA issue, tools/mma_rate.cu).
+    auto up = [](int64_t v, int64_t a) { return (v + a - 1) / a * a; };
+    auto make = [&](DevPlan::KrCfg& c, int krn, bool pair) -> bool {
+      c.valid = false;
+      if (krn == 2 && (KR > 40 || nko < 1 || oe[0] % 2 != 0)) return false;
+      if (pair && !(kp.tiles_x % 2 == 0 && yrows == NT && NT % 16 == 0 && nyb == 1)) return false;
+      const int64_t KE = krn * KR, yr = pair ? NT / 2 : NT;
+      KrParams q = kp;
+      const int64_t xbytes = up(krn * 128 * (KR + 4) * 4, 1024), ybytes = up(KE * yr * 4, 1024);
+      q.lslot_bytes = (int32_t)(xbytes + ybytes);
+      q.oslot_bytes = (int32_t)(2 * ybytes);
+      q.a_col0 = (int32_t)up(NT, 32);
+      q.aslots = 2;
+      if (q.a_col0 + 2 * 2 * KE > 512) return false;
+      auto fits = [&](int l, int o) {
+        return (int64_t)l * q.lslot_bytes + (int64_t)o * q.oslot_bytes + 512 <= 227 * 1024;
+      };
+      int sl = 8;
+      while (sl > 2 && !fits(sl, 2)) sl -= 2;
+      if (!fits(sl, 2)) return false;
+      q.lslots = sl;
+      q.oslots = 2;
+      q.o_off = sl * q.lslot_bytes;
+      q.bar_off = (int32_t)(q.o_off + 2LL * q.oslot_bytes);
+      q.nkb = (int32_t)(p.gk.G / KE);
+      c.kp = q;
+      c.lx = dp.kr_l[0];
+      c.ly = dp.kr_l[1];
+      if (krn == 2) {
+        c.lx.box[kp.xk_pos[0]] = 2;
+        c.ly.box[kp.yk_pos[0]] = 2;
+      }
+      if (pair) c.ly.box[0] = (uint32_t)(NT / 2);
+      c.krn = krn;
+      c.pair = pair;
+      c.base[0] = c.base[1] = nullptr;
+      c.valid = true;
+      return true;
+    };
+    if (!make(dp.krc[0], 1, false)) continue;
+    if (!make(dp.krc[1], 2, true)) make(dp.krc[1], 1, true);
     return true;
   }
   return false;
@@ -839,15 +859,21 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
     if (std::getenv("GETT_TMA_DEBUG")) {
       std::fprintf(stderr, "gett kr: %s", dp.kr_state == 1 ? "on" : "off");
       if (dp.kr_state == 1) {
-        std::fprintf(stderr, " X=%s KR %d MX %d NY %d NT %d nkb %d slots load %d operand %d tmem %d smem %d\n",
-                     dp.kr_x ? "B'" : "A'", dp.kr_run, dp.kr_p.MX, dp.kr_p.NY, dp.kr_p.NT, dp.kr_p.nkb,
-                     dp.kr_p.lslots, dp.kr_p.oslots, dp.kr_p.aslots, dp.kr_p.bar_off + 512);
-        for (int t = 0; t < 2; ++t) {
-          std::fprintf(stderr, "  %c base_off %lld dims", t ? 'Y' : 'X', (long long)dp.kr_l[t].base_off);
-          for (int i = 0; i < 5; ++i)
-            std::fprintf(stderr, " (%llu,%llu,%u)", (unsigned long long)dp.kr_l[t].dims[i],
-                         (unsigned long long)dp.kr_l[t].strides[i], dp.kr_l[t].box[i]);
-          std::fprintf(stderr, "\n");
+        std::fprintf(stderr, " X=%s KR %d MX %d NY %d NT %d\n", dp.kr_x ? "B'" : "A'", dp.kr_run,
+                     dp.kr_p.MX, dp.kr_p.NY, dp.kr_p.NT);
+        for (int ci = 0; ci < 2; ++ci) {
+          const DevPlan::KrCfg& c = dp.krc[ci];
+          if (!c.valid) continue;
+          std::fprintf(stderr, "  cfg %d: pair %d runs/k-block %d nkb %d slots load %d operand 2 smem %d\n", ci,
+                       (int)c.pair, c.krn, c.kp.nkb, c.kp.lslots, c.kp.bar_off + 512);
+          for (int t = 0; t < 2; ++t) {
+            const DevPlan::KrLayout& L = t ? c.ly : c.lx;
+            std::fprintf(stderr, "    %c base_off %lld dims", t ? 'Y' : 'X', (long long)L.base_off);
+            for (int i = 0; i < 5; ++i)
+              std::fprintf(stderr, " (%llu,%llu,%u)", (unsigned long long)L.dims[i],
+                           (unsigned long long)L.strides[i], L.box[i]);
+            std::fprintf(stderr, "\n");
+          }
         }
       } else {
         std::fprintf(stderr, "\n");
@@ -855,7 +881,8 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
     }
   }
   if (dp.kr_state != 1) return 0;
-  KrParams kp = dp.kr_p;
+  DevPlan::KrCfg& cfg = (g_kr_pair && dp.krc[1].valid) ? dp.krc[1] : dp.krc[0];
+  KrParams kp = cfg.kp;
   const int64_t tiles = (int64_t)kp.tiles_x * kp.tiles_y;
   if (!ds.sms) {
     int dev = 0;
@@ -867,16 +894,16 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
   if (g_kr == 1 && !(dp.kr_run < 64 && tiles < ds.sms)) return 0;
   const float* X = dp.kr_x == 0 ? A : B;
   const float* Y = dp.kr_x == 0 ? B : A;
-  if (dp.kr_base[0] != X || dp.kr_base[1] != Y) {
-    if (!kr_encode(dp.kr_l[0], X, &dp.kr_p.mx) || !kr_encode(dp.kr_l[1], Y, &dp.kr_p.my)) {
-      dp.kr_base[0] = dp.kr_base[1] = nullptr;
+  if (cfg.base[0] != X || cfg.base[1] != Y) {
+    if (!kr_encode(cfg.lx, X, &cfg.mx) || !kr_encode(cfg.ly, Y, &cfg.my)) {
+      cfg.base[0] = cfg.base[1] = nullptr;
       return 0;
     }
-    dp.kr_base[0] = X;
-    dp.kr_base[1] = Y;
-    kp.mx = dp.kr_p.mx;
-    kp.my = dp.kr_p.my;
+    cfg.base[0] = X;
+    cfg.base[1] = Y;
   }
+  kp.mx = cfg.mx;
+  kp.my = cfg.my;
   int64_t splits = 1;
   if (g_split > 0) splits = g_split;
   else if (tiles < ds.sms && kp.nkb >= 4) splits = ds.sms / tiles;
@@ -912,13 +939,8 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
       kp.spin_ns = spin;
     }
   }
-  bool pair = g_kr_pair && dp.kr_pair_ok;
-  if (pair && dp.kr_base_pair != Y) {
-    if (kr_encode(dp.kr_ly_pair, Y, &dp.kr_my_pair)) dp.kr_base_pair = Y;
-    else pair = false;
-  }
-  if (pair) kp.my = dp.kr_my_pair;
-  CK(launch_sgett_kr(kp, dp.kr_run, pair, stream));
+  const bool pair = cfg.pair;
+  CK(launch_sgett_kr(kp, dp.kr_run, cfg.krn, pair, stream));
   ++g_launches;
   if (splits > 1 && kp.cnt == nullptr) {
     TiledParams<float> tp{};
@@ -2832,7 +2854,7 @@ int gett_set_kr(int mode) {
   if (mode < 0 || (mode & 3) == 3 || mode > 15) return GETT_E_INVALID_ARG;
   g_kr = mode & 3;
   g_kr_fused = (mode & 4) != 0;
-  g_kr_pair = (mode & 8) != 0;
+  g_kr_pair = (mode & 8) == 0;
   return 0;
 }
 

@@ -91,7 +91,8 @@ cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& t
 
 // k-run SGETT (sgett_kr.cu); KR in {8, 16, ..., 64}
 // pair: clusters of 2 (cta_group::2, M = 256; tiles_x even, y_rows == NT)
-cudaError_t launch_sgett_kr(const KrParams& p, int KR, bool pair, cudaStream_t s);
+// KRN: k runs per k-block (1, or 2 for KR <= 40)
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, int KRN, bool pair, cudaStream_t s);
 int sgett_kr_max_nt();
 
 int tiled_bm();

@@ -57,17 +57,22 @@ constexpr int MAX_SLOTS = 8;
 constexpr int BAR_BYTES = 512;
 constexpr int SMEM_MAX = 227 * 1024;
 
-template <int KR>
+// KRN runs per k-block (1, or 2 for runs <= 40: the k-block is then two
+// consecutive runs, the next outer k digit boxed 2 wide): twice the MMAs per
+// ready wait + fence + commit, which cost ~350 clk of MMA issue per k-block
+// (tools/mma_rate.cu: 15 MMAs 1159 clk, 30 MMAs 1836 clk)
+template <int KR, int KRN = 1>
 struct Cfg {
-  // X staging [row][XP]: the box is KR + 4 wide (4 out-of-bounds, zero-filled
-  // columns) so the row pitch is an odd multiple of 16 B modulo 128 B and a
-  // quarter warp's 16-byte row reads hit 8 distinct bank groups
+  // X staging [run][row][XP]: the box is KR + 4 wide (4 out-of-bounds,
+  // zero-filled columns) so the row pitch is an odd multiple of 16 B modulo
+  // 128 B and a quarter warp's 16-byte row reads hit 8 distinct bank groups
   static constexpr int XP = KR + 4;
-  static constexpr int XB = 128 * XP * 4;
+  static constexpr int XB = KRN * 128 * XP * 4;
   static constexpr int XB_AL = (XB + 1023) / 1024 * 1024;  // Y starts 1 KB aligned
-  static constexpr int CHK = KR / 4;           // 16-byte k chunks of a row
+  static constexpr int KE = KRN * KR;          // k per k-block
+  static constexpr int CHK = KE / 4;           // 16-byte k chunks of an operand row
   static constexpr uint32_t SBO = CHK * 128;   // bytes between 8-row groups (K-major no swizzle)
-  static_assert(KR % 8 == 0 && KR >= 8 && KR <= 64, "k run");
+  static_assert(KR % 8 == 0 && KR >= 8 && KR <= 64 && (KRN == 1 || (KRN == 2 && KR <= 40)), "k run");
   static_assert(5 * MAX_SLOTS + 1 + 1 + 8 <= BAR_BYTES / 8, "barrier area");
 };
 
@@ -239,9 +244,10 @@ __device__ __forceinline__ void reduce_slice(const KrParams& p, int x0, int y0, 
 // K-major operand in its shared memory; the leader issues one pair MMA per
 // (k-step, product) for both — per SM half the Y bytes (loads, split,
 // B-operand reads) and half the MMA instructions of the one-CTA form.
-template <int KR, bool PAIR>
+template <int KR, int KRN, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_constant__ KrParams p) {
-  using G = Cfg<KR>;
+  using G = Cfg<KR, KRN>;
+  constexpr int KE = G::KE;
   // three rings: load slots [X raw | Y raw] (TMA -> split; freed by the split
   // warps as soon as they have read them, so the loads run ahead by SL
   // k-blocks), operand slots [Y hi | Y lo] K-major (split -> MMA; freed by the
@@ -289,7 +295,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
   const int x0 = tx * p.x_rows, y0 = ty * p.y_rows;
   const int kb0 = split * p.kpc;
   const int nkb = max(0, min(p.nkb, kb0 + p.kpc) - kb0);
-  const uint32_t tile_bytes = (uint32_t)(KR * yrows_me * 4);  // the Y box (raw [KR][rows])
+  const uint32_t tile_bytes = (uint32_t)(KE * yrows_me * 4);  // the Y box (raw [KE][rows])
 
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&p.mx) : "memory");
@@ -331,10 +337,14 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       row_coords(cy, y0 + (PAIR ? (int)rank * yrows_me : 0), p.ynr, p.yr_ext, p.yr_pos);
       int d0 = 0, d1 = 0;  // outer k digits of k-block kb0
       if (p.nko > 0) {
-        d0 = kb0 % p.k_ext[0];
-        d1 = kb0 / p.k_ext[0];
+        d0 = (kb0 * KRN) % p.k_ext[0];
+        d1 = (kb0 * KRN) / p.k_ext[0];
       }
       const uint32_t sbase = smem_u32(smem);
+      // a pair's second Y half can lie wholly past NY (NY = 189: rows 192..255
+      // of the second column tile): such a box faults (illegal instruction),
+      // so it is not loaded — its columns are never stored
+      const bool y_live = !PAIR || y0 + (int)rank * yrows_me < p.NY;
 #ifdef GETT_KR_TRACE
       long long w_empty = 0;
 #endif
@@ -358,12 +368,12 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           mbar_arrive(fb);
         } else {
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
-                       "r"((uint32_t)(p.x_rows * G::XP * 4) + tile_bytes)
+                       "r"((uint32_t)(KRN * p.x_rows * G::XP * 4) + (y_live ? tile_bytes : 0u))
                        : "memory");
           tma_load5(sbase + s * p.lslot_bytes, &p.mx, a, fb);
-          tma_load5(sbase + s * p.lslot_bytes + G::XB_AL, &p.my, b, fb);
+          if (y_live) tma_load5(sbase + s * p.lslot_bytes + G::XB_AL, &p.my, b, fb);
         }
-        if (p.nko > 0 && ++d0 == p.k_ext[0]) {
+        if (p.nko > 0 && (d0 += KRN) == p.k_ext[0]) {  // (k_ext[0] % KRN == 0, host)
           d0 = 0;
           ++d1;
         }
@@ -417,11 +427,14 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       const uint8_t* st = smem + sl * p.lslot_bytes;
       uint8_t* hi_t = smem + p.o_off + so * p.oslot_bytes;
       uint8_t* lo_t = hi_t + p.oslot_bytes / 2;
-      // X row -> TMEM hi / lo columns of slot sa, 16 (then 8) columns at a time
+      // X row -> TMEM hi / lo columns of slot sa (run q at columns q KR), 16
+      // (then 8) columns at a time
       if (!(GETT_KR_ABLATE & 2)) {
+#pragma unroll
+        for (int q = 0; q < KRN; ++q) {
         const int row = 32 * wq + lane;
-        const float4* xr = reinterpret_cast<const float4*>(st + row * G::XP * 4);
-        const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(p.a_col0 + sa * 2 * KR);
+        const float4* xr = reinterpret_cast<const float4*>(st + (q * p.x_rows + row) * G::XP * 4);
+        const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(p.a_col0 + sa * 2 * KE + q * KR);
 #pragma unroll
         for (int c = 0; c < KR; c += 16) {
           constexpr int W = 16;
@@ -441,11 +454,12 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           }
           if (n == W) {
             tmemio::tst16(ta + c, hv);
-            tmemio::tst16(ta + KR + c, lv);
+            tmemio::tst16(ta + KE + c, lv);
           } else {
             tmemio::tst8(ta + c, hv);
-            tmemio::tst8(ta + KR + c, lv);
+            tmemio::tst8(ta + KE + c, lv);
           }
+        }
         }
       }
 #ifdef GETT_KR_TRACE
@@ -645,12 +659,12 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
         const uint32_t hb = sbase + p.o_off + so * p.oslot_bytes;
         const uint32_t lb = hb + p.oslot_bytes / 2;
-        const uint32_t ah0 = tmem + p.a_col0 + sa * 2 * KR;
+        const uint32_t ah0 = tmem + p.a_col0 + sa * 2 * KE;
 #pragma unroll
-        for (int j = 0; j < KR / 8; ++j) {
+        for (int j = 0; j < KE / 8; ++j) {
           const uint64_t bh = sdesc(hb + 256 * j, 128, G::SBO);
           const uint64_t bl = sdesc(lb + 256 * j, 128, G::SBO);
-          const uint32_t ah = ah0 + 8 * j, al = ah + KR;
+          const uint32_t ah = ah0 + 8 * j, al = ah + KE;
           // (hi*hi, hi*lo_Y, lo_X*hi: the tiled kernel's order when its TMEM
           // operand is this kernel's Y — c5 — so both give the same bits there)
           if (PAIR) {
@@ -694,17 +708,17 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
   }
 }
 
-template <int KR>
+template <int KR, int KRN>
 cudaError_t launch_t(const KrParams& p, bool pair, cudaStream_t s) {
   if (!pair) {
-    auto k = sgett_kr_kernel<KR, false>;
+    auto k = sgett_kr_kernel<KR, KRN, false>;
     static unsigned long long configured = 0;
     cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured);
     if (e != cudaSuccess) return e;
     k<<<(unsigned)(p.tiles_x * p.tiles_y * p.splits), THREADS, p.bar_off + BAR_BYTES, s>>>(p);
     return cudaGetLastError();
   }
-  auto k = sgett_kr_kernel<KR, true>;
+  auto k = sgett_kr_kernel<KR, KRN, true>;
   static unsigned long long configured2 = 0;
   cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured2);
   if (e != cudaSuccess) return e;
@@ -725,16 +739,26 @@ cudaError_t launch_t(const KrParams& p, bool pair, cudaStream_t s) {
 
 }  // namespace kr
 
-cudaError_t launch_sgett_kr(const KrParams& p, int KR, bool pair, cudaStream_t s) {
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, int KRN, bool pair, cudaStream_t s) {
+  if (KRN == 2) {
+    switch (KR) {
+      case 8: return kr::launch_t<8, 2>(p, pair, s);
+      case 16: return kr::launch_t<16, 2>(p, pair, s);
+      case 24: return kr::launch_t<24, 2>(p, pair, s);
+      case 32: return kr::launch_t<32, 2>(p, pair, s);
+      case 40: return kr::launch_t<40, 2>(p, pair, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
   switch (KR) {
-    case 8: return kr::launch_t<8>(p, pair, s);
-    case 16: return kr::launch_t<16>(p, pair, s);
-    case 24: return kr::launch_t<24>(p, pair, s);
-    case 32: return kr::launch_t<32>(p, pair, s);
-    case 40: return kr::launch_t<40>(p, pair, s);
-    case 48: return kr::launch_t<48>(p, pair, s);
-    case 56: return kr::launch_t<56>(p, pair, s);
-    case 64: return kr::launch_t<64>(p, pair, s);
+    case 8: return kr::launch_t<8, 1>(p, pair, s);
+    case 16: return kr::launch_t<16, 1>(p, pair, s);
+    case 24: return kr::launch_t<24, 1>(p, pair, s);
+    case 32: return kr::launch_t<32, 1>(p, pair, s);
+    case 40: return kr::launch_t<40, 1>(p, pair, s);
+    case 48: return kr::launch_t<48, 1>(p, pair, s);
+    case 56: return kr::launch_t<56, 1>(p, pair, s);
+    case 64: return kr::launch_t<64, 1>(p, pair, s);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -20,7 +20,7 @@ def kernel_mode():
                                        set_split_k, set_stream_k, set_tma)
 
     def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
-            kr="auto", kr_fused=False, kr_pair=False):
+            kr="auto", kr_fused=False, kr_pair=True):
         set_kernel(name)
         set_split_k(split)
         set_pipeline(pipeline)

@@ -80,11 +80,13 @@ SHAPES = [
 @pytest.mark.parametrize("c_m_fast", [True, False])
 @pytest.mark.parametrize("split", [0, 1, 5])
 def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, kernel_mode):
-    """single CTAs and CTA pairs (where the tiling allows), fused and separate
-    reduce: all four bitwise equal (same MMAs, same order), within the bar."""
+    """single CTAs and CTA pairs (where the tiling allows; pairs may take two
+    k runs per k-block, which moves the split-K cuts), fused and separate
+    reduce: each within the bar, fused == separate bitwise for each form."""
     m1, m2, kr, k2, n = shape
-    outs, names = [], []
+    names = []
     for pair in (True, False):
+        outs = []
         for fused in (True, False):
             pos, kw = _case(m1, m2, kr, k2, n, c_m_fast, seed=sum(shape) + split)
             c0 = pos[13].copy()
@@ -95,7 +97,7 @@ def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, ke
             _check(pos, kw, c0)
             outs.append(pos[13])
             names.append(kname)
-    assert all(o.tobytes() == outs[0].tobytes() for o in outs[1:]), names
+        assert outs[0].tobytes() == outs[1].tobytes(), names
     assert not any("pair" in k for k in names[2:]), names
 
 
@@ -117,12 +119,12 @@ def test_kr_auto_on_c5_and_off_for_large_tilings(kernel_mode):
 
 
 def test_kr_c5_equals_tiled_bitwise(kernel_mode):
-    """On c5 both tcgen05 kernels cut K at the same points (1280 = 32 runs of
-    40 = 80 blocks of 16) and issue the same MMAs in the same k order: the
-    results are bit-identical."""
+    """On c5 both tcgen05 kernels (one-CTA form) cut K at the same points
+    (1280 = 32 runs of 40 = 80 blocks of 16) and issue the same MMAs in the
+    same k order: the results are bit-identical."""
     outs = []
     for kr in ("force", "off"):
-        kernel_mode("tiled", kr=kr)
+        kernel_mode("tiled", kr=kr, kr_pair=False)
         a, b, c = C5.buffers()
         pos, kw = C5.args(a, b, c)
         assert g.sgett(*pos, **kw) == []
@@ -157,8 +159,32 @@ def test_kr_graph_replay_fused(kernel_mode):
 
 
 def test_kr_pair_taken_on_c5(kernel_mode):
-    kernel_mode("auto", kr_pair=True)
+    kernel_mode("auto")
     a, b, c = C5.buffers()
     pos, kw = C5.args(a, b, c)
     assert g.sgett(*pos, **kw) == []
     assert g.last_kernel().startswith("sgett_tc3xtf32_kr_pair"), g.last_kernel()
+
+
+@pytest.mark.parametrize("ny", [189, 193, 320])
+def test_kr_pair_second_column_tile_half_out_of_range(ny, kernel_mode):
+    """CTA pairs split each 128-column tile in two halves; with NY = 189 the
+    second tile's second half (rows 192..255) is wholly past the tensor — its
+    box is not loaded (a fully out-of-bounds box faults) and its columns are
+    never stored."""
+    kernel_mode("tiled", kr="force")
+    rng = np.random.default_rng(ny)
+    na, nb, k = ny, 175, 16
+    inc_a, inc_b = (1, na + 7 + (4 - (na + 7) % 4) % 4), (k + 4, 1)
+    a = rng.uniform(-1, 1, inc_a[1] * k + 8).astype(np.float32)
+    b = rng.uniform(-1, 1, (k + 4) * nb + 8).astype(np.float32)
+    c0 = rng.uniform(-1, 1, 3 + (nb + 1) * na + 8).astype(np.float32)
+    c = c0.copy()
+    assert g.sgett(2, (na, k), inc_a, a, 2, (nb, k), inc_b, b, 1, (1,), (1,), (0, 1), (nb + 1, 1), c,
+                   offset_c=3) == []
+    assert g.last_kernel().startswith("sgett_tc3xtf32_kr"), g.last_kernel()
+    A = _strided(a, (na, k), inc_a, 0).astype(np.float64)
+    B = _strided(b, (nb, k), inc_b, 0).astype(np.float64)
+    want = _strided(c0, (na, nb), (nb + 1, 1), 3).astype(np.float64) + A @ B.T
+    got = _strided(c, (na, nb), (nb + 1, 1), 3).astype(np.float64)
+    assert np.abs(got - want).max() / (k * np.abs(a).max() * np.abs(b).max()) <= 1e-5

@@ -17,8 +17,8 @@ from oracle import oracle  # noqa: E402
 from paper_2410_06770_b200.device import sgett_device  # noqa: E402
 from paper_2410_06770_b200.workloads import CONFIGS  # noqa: E402
 
-MODES = [("tiled", dict(kr="off")), ("kr_fused", dict(kr="force", fused=True)), ("kr_sep", dict(kr="force")),
-         ("kr_pair", dict(kr="force", pair=True))]
+MODES = [("tiled", dict(kr="off")), ("kr_fused", dict(kr="force", fused=True)), ("kr_pair", dict(kr="force")),
+         ("kr_single", dict(kr="force", pair=False))]
 
 
 def main(names):
@@ -32,7 +32,7 @@ def main(names):
         ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
         outs = {}
         for mode, kw in MODES:
-            g.set_kr(kw["kr"], kw.get("fused", False), kw.get("pair", False))
+            g.set_kr(kw["kr"], kw.get("fused", False), kw.get("pair", True))
             tc = torch.from_numpy(c).cuda()
             pos, kwa = w.args(ta, tb, tc)
             assert sgett_device(*pos, **kwa) == []
@@ -57,7 +57,7 @@ def main(names):
                               "gflops": round(w.flops / ms / 1e6, 1),
                               "hbm_frac": round(w.alg_bytes / (ms * 1e-3) / 6546.2e9, 3)}), flush=True)
         if "kr_fused" in outs:
-            print(json.dumps({"config": name, "fused_eq_sep": outs["kr_fused"].tobytes() == outs["kr_sep"].tobytes()}))
+            print(json.dumps({"config": name, "fused_eq_sep": outs["kr_fused"].tobytes() == outs["kr_pair"].tobytes()}))
         g.set_kr("auto")
 
 

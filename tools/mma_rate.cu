@@ -157,7 +157,7 @@ void runp(long long* d) {
 template <int NT, int KR, bool RND, int FENCE = 0, bool COMMIT2 = false, bool STW = false>
 __global__ void pattern_kr(long long* out, int kblocks) {
   extern __shared__ __align__(1024) uint8_t sm[];
-  constexpr int STG = 4, TB = NT * KR * 4, SB = 2 * TB;
+  constexpr int STG = KR > 40 ? 2 : 4, TB = NT * KR * 4, SB = 2 * TB;
   uint64_t* bar = (uint64_t*)(sm + STG * SB);
   uint32_t* slot = (uint32_t*)(bar + STG + 1);
   for (int i = threadIdx.x; i < STG * SB / 4; i += blockDim.x) {
@@ -255,7 +255,7 @@ __global__ void pattern_kr(long long* out, int kblocks) {
 template <int NT, int KR, bool RND = false, int FENCE = 0, bool COMMIT2 = false, bool STW = false>
 void runkr(long long* d) {
   auto k = pattern_kr<NT, KR, RND, FENCE, COMMIT2, STW>;
-  const int smem = 4 * 2 * NT * KR * 4 + 128;
+  const int smem = (KR > 40 ? 2 : 4) * 2 * NT * KR * 4 + 128;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   const int kb = 1024;
   k<<<148, 128, smem>>>(d, kb);
@@ -277,6 +277,8 @@ int main() {
   runkr<96, 40, false, 0, true>(d);
   runkr<96, 40, false, 0, false, true>(d);
   runkr<96, 40, false, 1, true, true>(d);
+  runkr<96, 40, false, 1, false, true>(d);
+  runkr<96, 80, false, 1, false, true>(d);
   runkr<96, 40, true>(d);
   runkr<128, 40, true>(d);
   runkr<128, 40>(d);
