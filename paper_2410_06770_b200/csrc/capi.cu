@@ -967,13 +967,15 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
 
 // ---- DGETT TMA layouts (dgett_ws.cu, TMA=true) ----
 //
-// Both operands of a DGETT tile are loaded as one 128B-swizzled box each per
-// 32-deep k-block when their row and k groups are affine: k-fast operands as
-// [16 k | 128 rows | 2 k-halves] boxes (smem [k/16][row][16 k]), rows-fast
-// ones as [16 rows | 32 k | 8 row-groups] (smem [row/16][k][16 rows]); the
-// inner k run must hold whole 32-blocks (k-fast) / K a multiple of 32, so no
-// k-block straddles a digit of the K group and there is no K tail (its -0.0
-// padding stays with the gather path).
+// Both operands of a DGETT tile are loaded as one box each per 32-deep
+// k-block when their row and k groups are affine, into the same padded
+// layouts the gathers write: a k-fast operand as [36 k | 128 rows] (smem
+// [row][36]: the k run is cut into 32-wide digits, so k 32..35 of the box are
+// out of bounds and zero-filled), a rows-fast one as [132 rows | 32 k] (smem
+// [k][132]; its inner rows cut into 128-row digits, or one dim of at most 128
+// rows).  The inner k run must hold whole 32-blocks and K be a multiple of
+// 32, so no k-block straddles a digit of the K group and there is no K tail
+// (its -0.0 padding stays with the gather path).
 
 // one operand: rows from group gr (its tensor 0), k from the joint K dims
 bool dgett_tma_layout(const Group& gr, const std::vector<int64_t>& kext, const std::vector<int64_t>& kst,
@@ -984,48 +986,42 @@ bool dgett_tma_layout(const Group& gr, const std::vector<int64_t>& kext, const s
     if (d.stride <= 0) return false;
   for (size_t i = 0; i < kst.size(); ++i)
     if (kst[i] <= 0) return false;
+  if (kext[0] % 32 != 0) return false;
   struct D {
     int64_t ext, stride;
     uint32_t box;
     int kind, idx;  // 0 row digit, 1 k digit
   };
   std::vector<D> dims;
-  std::vector<int64_t> rexp, kexp;  // the digit extents in mixed-radix order
-  // rows of a 128-row tile: one dim (extent a multiple of 128, or a single
-  // dim whose tail is zero-filled) or (r0, 128 / r0)
-  auto row_boxes = [&](int64_t inner_box_rows, int64_t r0ext) -> int {
-    (void)inner_box_rows;
-    if (r0ext % 128 == 0 || R.size() == 1) return 1;
-    if (128 % r0ext == 0 && R.size() == 2) return 2;
-    return 0;
-  };
   const bool kf = kst[0] == 1;
   if (kf) {
-    if (kext[0] % 32 != 0) return false;
-    const int nrb = row_boxes(128, R[0].ext);
-    if (!nrb) return false;
-    // k digits: (16, 1) (kext0 / 16, 16) outer...; rows: R0 [, R1]
-    dims.push_back({16, 1, 16u, 1, 0});
-    for (int i = 0; i < (int)R.size(); ++i)
-      dims.push_back({R[i].ext, R[i].stride, i < nrb ? (nrb == 1 ? 128u : (uint32_t)(i == 0 ? R[0].ext : 128 / R[0].ext)) : 1u, 0, i});
-    dims.push_back({kext[0] / 16, 16, 2u, 1, 1});
-    for (size_t i = 1; i < kext.size(); ++i) dims.push_back({kext[i], kst[i], 1u, 1, (int)i + 1});
-  } else {
-    if (R[0].stride != 1 || R[0].ext % 16 != 0 || kext[0] % 32 != 0) return false;
-    // rows: (16, 1) (R0 / 16, 16) [R1]; k: kext0 outer...
-    const int64_t g0 = R[0].ext / 16;
-    uint32_t gbox, r1box = 1;
-    if (g0 % 8 == 0 || R.size() == 1) gbox = 8;
-    else if (8 % g0 == 0 && R.size() == 2) {
-      gbox = (uint32_t)g0;
-      r1box = (uint32_t)(8 / g0);
+    // k digits: (32, 1) box 36, (kext0 / 32, 32), outer...; rows: a 128-row box
+    dims.push_back({32, 1, 36u, 1, 0});
+    if (R[0].ext % 128 == 0 || R.size() == 1) {
+      dims.push_back({R[0].ext, R[0].stride, 128u, 0, 0});
+      if (R.size() == 2) dims.push_back({R[1].ext, R[1].stride, 1u, 0, 1});
+    } else if (128 % R[0].ext == 0) {
+      dims.push_back({R[0].ext, R[0].stride, (uint32_t)R[0].ext, 0, 0});
+      dims.push_back({R[1].ext, R[1].stride, (uint32_t)(128 / R[0].ext), 0, 1});
     } else {
       return false;
     }
-    dims.push_back({16, 1, 16u, 0, 0});
-    dims.push_back({kext[0], kst[0], 32u, 1, 0});
-    dims.push_back({g0, 16, gbox, 0, 1});
-    if (R.size() == 2) dims.push_back({R[1].ext, R[1].stride, r1box, 0, 2});
+    dims.push_back({kext[0] / 32, 32, 1u, 1, 1});
+    for (size_t i = 1; i < kext.size(); ++i) dims.push_back({kext[i], kst[i], 1u, 1, (int)i + 1});
+  } else {
+    if (R[0].stride != 1) return false;
+    // rows: (128, 1) box 132 [(R0 / 128, 128)] [R1]; k: kext0 box 32, outer...
+    if (R[0].ext <= 128 && R.size() == 1) {
+      dims.push_back({R[0].ext, 1, 132u, 0, 0});
+      dims.push_back({kext[0], kst[0], 32u, 1, 0});
+    } else if (R[0].ext % 128 == 0) {
+      dims.push_back({128, 1, 132u, 0, 0});
+      dims.push_back({kext[0], kst[0], 32u, 1, 0});
+      dims.push_back({R[0].ext / 128, 128, 1u, 0, 1});
+      if (R.size() == 2) dims.push_back({R[1].ext, R[1].stride, 1u, 0, 2});
+    } else {
+      return false;
+    }
     for (size_t i = 1; i < kext.size(); ++i) dims.push_back({kext[i], kst[i], 1u, 1, (int)i});
   }
   if (dims.size() > 5) return false;
@@ -1073,7 +1069,7 @@ bool dgett_tma_encode(const DevPlan::TmaLayout& L, const double* base, CUtensorM
     if (i) strides[i - 1] = L.strides[i] * 8;
   }
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 5, const_cast<double*>(g), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, GETT_TMA_PROMO,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, GETT_TMA_PROMO,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 

@@ -57,15 +57,16 @@ constexpr int STAGE_ELEMS = 2 * OPER_ELEMS;
 constexpr int BAR_BYTES = 64;
 constexpr int ROWOFF_BYTES = 2 * 128 * 8;
 constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8 + BAR_BYTES + ROWOFF_BYTES;
-// TMA-fed operands (both A' and B' affine boxes): 128 x 32 doubles per operand
-// per stage, SWIZZLE_128B, no padding: a k-fast operand lands as [k/16][row]
-// [16 k] (two 16-double halves of each row line), a rows-fast one as
-// [row/16][k][16 rows]; either way the 16-byte chunk index of a 128-byte line
-// is XORed with the line index mod 8, which keeps the DMMA fragment loads at 2
-// wavefronts (conflict-free).  One thread issues one box per operand.
-constexpr int T_OPER_BYTES = 128 * BK * 8;  // 32 KB
-constexpr int T_STAGE_BYTES = 2 * T_OPER_BYTES;
-constexpr int T_SMEM_BYTES = STAGES * T_STAGE_BYTES + BAR_BYTES + 1024;  // (+1 KB: 1024-byte alignment)
+// TMA-fed operands (both A' and B' affine boxes) land in exactly the padded
+// layouts the gathers write — [row][k] pitch 36 or [k][row] pitch 132 — so the
+// consumers are unchanged: each box is 4 elements wider than the tile along
+// its fast dimension, and the host cuts that dimension into tile-sized
+// digits, so the 4 extra columns are out of bounds and zero-filled.  (128B-
+// swizzled dense boxes gave the DMMA fragment loads 2-way bank conflicts.)
+// One thread issues one box per operand.
+constexpr int T_KF_BYTES = 128 * KF_PITCH * 8;  // a k-fast box: 128 rows x 36
+constexpr int T_RF_BYTES = BK * RF_PITCH * 8;   // a rows-fast box: 32 k x 132
+
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
@@ -287,13 +288,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     dgett_ws_kernel(const __grid_constant__ TiledParams<double> p,
                     const __grid_constant__ SkParams sk, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  // (TMA: stages 1024-byte aligned for the 128-byte swizzle pattern)
-  unsigned char* sbase_ptr =
-      TMA ? smem_raw + ((1024 - (smem_u32(smem_raw) & 1023)) & 1023) : smem_raw;
+  unsigned char* sbase_ptr = smem_raw;
   double* smem = reinterpret_cast<double*>(sbase_ptr);
-  constexpr int RING_BYTES = TMA ? STAGES * T_STAGE_BYTES : STAGES * STAGE_ELEMS * 8;
-  constexpr int SOPER = TMA ? T_OPER_BYTES / 8 : OPER_ELEMS;    // doubles per operand tile
-  constexpr int SSTAGE = TMA ? T_STAGE_BYTES / 8 : STAGE_ELEMS;  // doubles per stage
+  constexpr int RING_BYTES = STAGES * STAGE_ELEMS * 8;
+  constexpr int SOPER = OPER_ELEMS;    // doubles per operand tile
+  constexpr int SSTAGE = STAGE_ELEMS;  // doubles per stage
   uint64_t* full = reinterpret_cast<uint64_t*>(sbase_ptr + RING_BYTES);
   uint64_t* empty = full + STAGES;
   int64_t* rowoff_a = reinterpret_cast<int64_t*>(sbase_ptr + RING_BYTES + BAR_BYTES);
@@ -332,14 +331,15 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int s = g % STAGES, u = g / STAGES;
         if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
         const uint32_t fb = smem_u32(full + s);
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(T_STAGE_BYTES)
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
+                     "r"((AKF ? T_KF_BYTES : T_RF_BYTES) + (BKF ? T_KF_BYTES : T_RF_BYTES))
                      : "memory");
         const int k0 = sg.kbase + kb * BK;
         int32_t c[5];
         dtma_coords(tp.op[0], m0, k0, c);
-        dtma_load(ring + s * T_STAGE_BYTES, &tp.map[0], c, fb);
+        dtma_load(ring + s * STAGE_ELEMS * 8, &tp.map[0], c, fb);
         dtma_coords(tp.op[1], n0, k0, c);
-        dtma_load(ring + s * T_STAGE_BYTES + T_OPER_BYTES, &tp.map[1], c, fb);
+        dtma_load(ring + s * STAGE_ELEMS * 8 + OPER_ELEMS * 8, &tp.map[1], c, fb);
       }
     }
     return;
@@ -384,36 +384,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
   for (int i = 0; i < MI; ++i) {
     int r = wm0 + i * 8 + (lane >> 2);
-    if (TMA) aoff[i] = AKF ? r * 16 : (r >> 4) * (BK * 16) + (lane & 3) * 16;
-    else aoff[i] = AKF ? r * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + r;
+    aoff[i] = AKF ? r * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + r;
   }
 #pragma unroll
   for (int j = 0; j < NJ; ++j) {
     int c = wn0 + j * 8 + (lane >> 2);
-    if (TMA) boff[j] = BKF ? c * 16 : (c >> 4) * (BK * 16) + (lane & 3) * 16;
-    else boff[j] = BKF ? c * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + c;
+    boff[j] = BKF ? c * KF_PITCH + (lane & 3) : (lane & 3) * RF_PITCH + c;
   }
   constexpr int AKS = AKF ? 4 : 4 * RF_PITCH;
   constexpr int BKS = BKF ? 4 : 4 * RF_PITCH;
-  // TMA layouts (in doubles): k-fast (row, k) at (k/16)*2048 + row*16 +
-  // 2*(((k%16)/2) ^ (row%8)) + k%2; rows-fast (row, k) at (row/16)*512 + k*16 +
-  // 2*(((row%16)/2) ^ (k%8)) + row%2.  For a fragment (row = 8i + lane/4 +
-  // base, k = 4 ks + lane%4) the swizzle term depends on ks % 4 (k-fast) or on
-  // (i % 2, ks % 2) (rows-fast): per-thread constants.
-  int kx[4], rx[2][2];
-#pragma unroll
-  for (int q = 0; q < 4; ++q) kx[q] = 2 * (((2 * q + ((lane >> 1) & 1)) ^ (lane >> 2)) & 7) + (lane & 1);
-#pragma unroll
-  for (int i2 = 0; i2 < 2; ++i2)
-#pragma unroll
-    for (int k2 = 0; k2 < 2; ++k2)
-      rx[i2][k2] = 2 * (((4 * i2 + (lane >> 3)) ^ (4 * k2 + (lane & 3))) & 7) + ((lane >> 2) & 1);
-  // fragment (i or j, ks) offset in an operand tile
-  auto toff = [&](int base, int idx, int ks, bool kf) -> int {
-    if (kf) return base + (ks >> 2) * 2048 + kx[ks & 3];
-    return base + ks * 64 + rx[idx & 1][ks & 1];
-  };
-
   uint32_t g = 0;
   TR_DECL(cw = 0, cc = 0, ce = 0, cx = 0)
   TR_T0()
@@ -437,19 +416,17 @@ __global__ void __launch_bounds__(THREADS, 1)
       const double* Bs = As + SOPER;
       double a[2][MI], b[2][NJ];
 #pragma unroll
-      for (int i = 0; i < MI; ++i) a[0][i] = As[TMA ? toff(aoff[i], i, 0, AKF) : aoff[i]];
+      for (int i = 0; i < MI; ++i) a[0][i] = As[aoff[i]];
 #pragma unroll
-      for (int j = 0; j < NJ; ++j) b[0][j] = Bs[TMA ? toff(boff[j], j, 0, BKF) : boff[j]];
+      for (int j = 0; j < NJ; ++j) b[0][j] = Bs[boff[j]];
 #pragma unroll
       for (int ks = 0; ks < BK / 4; ++ks) {
         const int cur = ks & 1;
         if (ks + 1 < BK / 4) {
 #pragma unroll
-          for (int i = 0; i < MI; ++i)
-            a[cur ^ 1][i] = As[TMA ? toff(aoff[i], i, ks + 1, AKF) : aoff[i] + (ks + 1) * AKS];
+          for (int i = 0; i < MI; ++i) a[cur ^ 1][i] = As[aoff[i] + (ks + 1) * AKS];
 #pragma unroll
-          for (int j = 0; j < NJ; ++j)
-            b[cur ^ 1][j] = Bs[TMA ? toff(boff[j], j, ks + 1, BKF) : boff[j] + (ks + 1) * BKS];
+          for (int j = 0; j < NJ; ++j) b[cur ^ 1][j] = Bs[boff[j] + (ks + 1) * BKS];
         }
 #pragma unroll
         for (int i = 0; i < MI; ++i)
@@ -556,7 +533,7 @@ cudaError_t launch5(const TiledParams<double>& p, const SkParams& sk, const TmaP
                     unsigned grid, cudaStream_t s) {
   auto k = dgett_ws_kernel<AKF, BKF, AV, BV, TMA>;
   static unsigned long long configured = 0;
-  constexpr int smem = TMA ? T_SMEM_BYTES : SMEM_BYTES;
+  constexpr int smem = SMEM_BYTES;
   cudaError_t e = ensure_dyn_smem(k, smem, configured);
   if (e != cudaSuccess) return e;
   k<<<grid, THREADS, smem, s>>>(p, sk, tp);

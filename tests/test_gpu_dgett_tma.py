@@ -1,7 +1,8 @@
 """TMA-fed DGETT (dgett_ws.cu TMA path, capi.cu dgett_tma_layout): when both
 operands' row and k groups are affine boxes (K and the inner k run multiples
-of 32; a 128-row tile = one box) each k-block arrives as one 128B-swizzled box
-per operand, issued by one thread.  Every case runs with TMA on and off: the
+of 32; a 128-row tile = one box) each k-block arrives as one box per operand,
+issued by one thread, into the gathers' padded layouts (4 zero-filled
+out-of-bounds columns).  Every case runs with TMA on and off: the
 same values reach the same DMMAs in the same order, so C must be bitwise
 identical, within the fp64 K-normalised bar of an fp64 contraction, and bytes
 outside C's view untouched."""
@@ -52,7 +53,7 @@ def _run(M, N, K1, K2, a_kfast, b_kfast, c_nfast, seed, kernel_mode, tma, split=
 
 
 @pytest.mark.parametrize("a_kfast,b_kfast,c_nfast", list(itertools.product([True, False], repeat=3)))
-@pytest.mark.parametrize("shape", [(304, 208, 32, 5), (128, 384, 64, 2), (528, 144, 96, 3)])
+@pytest.mark.parametrize("shape", [(384, 256, 32, 5), (128, 384, 64, 2), (640, 128, 96, 3), (100, 90, 32, 2)])
 def test_dgett_tma_equals_gathers(shape, a_kfast, b_kfast, c_nfast, kernel_mode):
     M, N, K1, K2 = shape
     seed = M + N + K1
@@ -77,8 +78,9 @@ def test_dgett_tma_split_and_stream_k(split, stream_k, kernel_mode):
 
 def test_dgett_tma_not_taken_for_k_tails_or_ragged_rows(kernel_mode):
     """K not a multiple of 32 (a -0.0-padded K tail), or a rows-fast operand
-    whose inner row extent is not a multiple of 16 (its 16-row box lines would
-    run into the next row group), stays on the gathers."""
+    of more than 128 rows whose inner row extent is not a multiple of 128 (its
+    padded 132-row box lines would run into the next rows), stays on the
+    gathers."""
     _, k = _run(200, 200, 24, 3, True, True, True, 3, kernel_mode, True)
     assert "_tma" not in k, k
     _, k = _run(300, 200, 32, 5, True, False, True, 3, kernel_mode, True)
