@@ -332,6 +332,12 @@ int gett_set_stream_k(int on);
 /* SGETT operands fed by TMA tensor maps when both views are affine boxes
  * (1 = on, the default; 0 = cp.async gathers only).  Also GETT_TMA. */
 int gett_set_tma(int on);
+/* DGETT epilogue C += acc as bulk shared->global f64 add reductions of whole
+ * 32-element C row runs (cp.reduce.async.bulk; 1 = when C's N runs are
+ * contiguous, even-aligned and C is 16-byte aligned, the default; 0 = one
+ * red.add per element).  Both add each element once at L2: bitwise equal
+ * results.  Also GETT_DGETT_BULK. */
+int gett_set_bulk(int on);
 /* SGETT CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256 per pair) for
  * split-K shapes with a K-major operand of >= 256 rows and a rows-major one of
  * <= 128 (e.g. c5); 0 = off (the default), 1 = on.  Also GETT_PAIR. */

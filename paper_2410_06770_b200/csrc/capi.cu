@@ -45,6 +45,7 @@ bool g_sk_small = true;    // DGETT: stream-K instead of split-K at 56-73 tiles 
 bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one embedded GETT (GETT_COMPLEX_EMBED=0)
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 bool g_dgett_tma = true;  // DGETT: TMA-fed operands for affine views (GETT_DGETT_TMA=0: cp.async gathers)
+bool g_dgett_bulk = true; // DGETT: C += acc as bulk shared->global adds of 32-wide row runs (GETT_DGETT_BULK=0: red.add per element)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
 bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the tiling allows, two k runs per
                           // k-block when they fit (c5: 46.1 vs 48.1 us; GETT_KR_PAIR=0: one CTA per tile)
@@ -73,6 +74,8 @@ void read_env_once() {
   if (ce) g_complex_4x = std::atoi(ce) == 0;
   const char* dtv = std::getenv("GETT_DGETT_TMA");
   if (dtv) g_dgett_tma = std::atoi(dtv) != 0;
+  const char* dbv = std::getenv("GETT_DGETT_BULK");
+  if (dbv) g_dgett_bulk = std::atoi(dbv) != 0;
   const char* krv = std::getenv("GETT_KR");
   if (krv) g_kr = std::atoi(krv);
   const char* krp = std::getenv("GETT_KR_PAIR");
@@ -115,6 +118,8 @@ struct DevPlan {
   // residues used by the vector-load checks: every table entry divisible by 2 / 4
   bool am_even2 = false, am_even4 = false, ak_even2 = false, ak_even4 = false;
   bool bn_even2 = false, bn_even4 = false, bk_even2 = false, bk_even4 = false;
+  // C offsets: every row offset even, and the N group's 32-aligned runs contiguous with even starts
+  bool c_bulk_rows = false, c_bulk_cols = false;
   // SGETT TMA operand layouts (sgett_tc.cu): decided once per plan, tensor
   // maps re-encoded when the operand base pointers change
   int tma_state = 0;  // 0: not decided, 1: both operands TMA-fed, -1: gathers
@@ -356,6 +361,8 @@ int get_plan(char dtype, const View& a, const View& b, const Spec& s, int64_t of
   dp->ak_even2 = all_div(p.gk.T[0], 2); dp->ak_even4 = all_div(p.gk.T[0], 4);
   dp->bn_even2 = all_div(p.gn.T[0], 2); dp->bn_even4 = all_div(p.gn.T[0], 4);
   dp->bk_even2 = all_div(p.gk.T[1], 2); dp->bk_even4 = all_div(p.gk.T[1], 4);
+  dp->c_bulk_rows = all_div(p.gm.T[1], 2) && (p.gm.e_in == 1 || p.gm.s_in[1] % 2 == 0);
+  dp->c_bulk_cols = all_div(p.gn.T[1], 2) && p.gn.s_in[1] == 1 && p.gn.e_in % 32 == 0;
   g_plans.lru.push_front(key);
   g_plans.map[key] = {dp, g_plans.lru.begin()};
   evict_plans();
@@ -1397,6 +1404,9 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
       sk.flags = (int32_t*)sw.flags.p;
       sk.epoch = sw.epoch;
     }
+    // C += acc as bulk adds of whole 32-wide row runs staged in shared memory
+    tp.c_bulk = g_dgett_bulk && dp.c_bulk_rows && dp.c_bulk_cols &&
+                (reinterpret_cast<uintptr_t>(c) & 15) == 0;
     const TmaParams* dtp =
         g_tma && g_dgett_tma ? dgett_tma(dp, reinterpret_cast<const double*>(A), reinterpret_cast<const double*>(B))
                              : nullptr;
@@ -1407,10 +1417,13 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     CK(launch_dgett_ws(*reinterpret_cast<TiledParams<double>*>(&tp), sk, dtp, a_kf, b_kf, a_vec,
                        b_vec, stream));
     g_launches += splits > 1 ? 2 : 1;
-    if (dtp)
-      t_last_kernel = splits > 1 ? "dgett_dmma_ws_tma_splitk" : sk.enabled ? "dgett_dmma_ws_tma_sk" : "dgett_dmma_ws_tma";
-    else
-      t_last_kernel = splits > 1 ? "dgett_dmma_ws_splitk" : sk.enabled ? "dgett_dmma_ws_sk" : "dgett_dmma_ws";
+    // [tma][schedule: one CTA per tile, stream-K, split-K][bulk-add epilogue]
+    static const char* const names[2][3][2] = {
+        {{"dgett_dmma_ws", "dgett_dmma_ws_bulk"}, {"dgett_dmma_ws_sk", "dgett_dmma_ws_sk_bulk"},
+         {"dgett_dmma_ws_splitk", "dgett_dmma_ws_splitk"}},
+        {{"dgett_dmma_ws_tma", "dgett_dmma_ws_tma_bulk"}, {"dgett_dmma_ws_tma_sk", "dgett_dmma_ws_tma_sk_bulk"},
+         {"dgett_dmma_ws_tma_splitk", "dgett_dmma_ws_tma_splitk"}}};
+    t_last_kernel = names[dtp ? 1 : 0][splits > 1 ? 2 : sk.enabled ? 1 : 0][tp.c_bulk ? 1 : 0];
     return 0;
   }
   CK(launch_tiled<T>(tp, a_kf, b_kf, a_vec, b_vec, stream));
@@ -2860,6 +2873,12 @@ int gett_set_tma(int on) {
   return 0;
 }
 
+int gett_set_bulk(int on) {
+  if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
+  g_dgett_bulk = on != 0;
+  return 0;
+}
+
 const char* gett_last_kernel(void) { return t_last_kernel; }
 const char* gett_last_error(void) { return t_last_error.c_str(); }
 int64_t gett_launch_count(void) { return g_launches; }
@@ -2898,7 +2917,7 @@ void gett_release_caches(void) {
 // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed;
 // 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi,
 //       gett_multi_schedule, gett_pack[_device], gett_set_kr,
-// 1.05: gett_plan_create / gett_execute[_device] / gett_plan_destroy
-int gett_abi_version(void) { return 105; }
+// 1.05: gett_plan_create / gett_execute[_device] / gett_plan_destroy; 1.06: gett_set_bulk
+int gett_abi_version(void) { return 106; }
 
 }  // extern "C"

@@ -88,6 +88,8 @@ struct TiledParams {
   T* ws;            // [splits][M][N] partial tiles when splits > 1 ([splits][N][M] if ws_t)
   int32_t neg = 0;  // epilogue C += -acc (the a.im*b.im term of a complex contraction)
   int32_t ws_t = 0; // split-K workspace transposed (tcgen05 SGETT epilogue: m fastest)
+  int32_t c_bulk = 0; // C's N group: unit inner stride, inner extent a multiple of 32, every
+                      // offset even and C 16-B aligned (DGETT bulk-add epilogue, dgett_ws.cu)
 };
 
 // Persistent stream-K schedule of the DGETT kernel (dgett_ws.cu); enabled == 0

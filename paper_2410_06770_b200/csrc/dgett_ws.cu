@@ -24,10 +24,11 @@ namespace ws {
 // Optional per-role cycle accounting (tuning builds only: make variant
 // EXTRA=-DGETT_WS_TRACE); blocks 0 and gridDim.x-1 printf their totals.
 #ifdef GETT_WS_TRACE
+__device__ __forceinline__ int smid() { int r; asm volatile("mov.u32 %0, %%smid;" : "=r"(r)); return r; }
 #define TR_DECL(...) long long __VA_ARGS__;
 #define TR_T0() long long _tr0 = clock64();
 #define TR_ADD(v) { long long _tr1 = clock64(); v += _tr1 - _tr0; _tr0 = _tr1; }
-#define TR_PRINT(...) do { if (blockIdx.x == 0 || blockIdx.x == gridDim.x - 1) printf(__VA_ARGS__); } while (0)
+#define TR_PRINT(...) do { printf(__VA_ARGS__); } while (0)
 #else
 #define TR_DECL(...)
 #define TR_T0()
@@ -66,6 +67,22 @@ constexpr int SMEM_BYTES = STAGES * STAGE_ELEMS * 8 + BAR_BYTES + ROWOFF_BYTES;
 // One thread issues one box per operand.
 constexpr int T_KF_BYTES = 128 * KF_PITCH * 8;  // a k-fast box: 128 rows x 36
 constexpr int T_RF_BYTES = BK * RF_PITCH * 8;   // a rows-fast box: 32 k x 132
+// Bulk-add epilogue (p.c_bulk): each consumer warp stages its 64 x 32 block
+// as 8-row chunks, [row][34] (the 16-byte row shift spreads a warp's
+// fragment stores over all banks), and adds each 32-wide row run into C with
+// one cp.reduce.async.bulk .add.f64 — done at L2 like red.add: one IEEE
+// round-to-nearest add per element, the same result, and a 256-byte request
+// instead of 32 scattered 8-byte ones.  The staging buffer is the ring slot
+// after the tile's last k-block, which carries no data for it: the producer
+// completes that slot's `full` phase once all consumer warps have released
+// its previous k-block (so no warp still reads it — warps leave the k loop
+// up to a k-block apart), and the consumers release it after the bulk reads.
+// Four chunks per pass: 8 warps x 4 x 8 rows x 272 B fit a slot.
+constexpr int EP_PITCH = 34;
+constexpr int EP_CHUNKS = 4;
+constexpr int EP_WARP_ELEMS = EP_CHUNKS * 8 * EP_PITCH;
+static_assert(CW * EP_WARP_ELEMS <= STAGE_ELEMS, "bulk-add staging exceeds a stage");
+static_assert(MI % EP_CHUNKS == 0 && WN == 32, "bulk-add staging shape");
 
 
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
@@ -236,6 +253,12 @@ __device__ __forceinline__ bool seg_next(const TiledParams<double>& p, const SkP
   return false;
 }
 
+// C += acc of this segment goes through the bulk-add epilogue, which takes
+// one extra (data-less) ring slot after the segment's k-blocks
+__device__ __forceinline__ bool bulk_epilogue(const TiledParams<double>& p, const Seg& sg) {
+  return p.c_bulk && (sg.kind == SEG_FULL || sg.kind == SEG_HEAD) && sg.kb1 > sg.kb0;
+}
+
 __device__ __forceinline__ void tile_origin(const TiledParams<double>& p, int tile, int& m0,
                                             int& n0) {
   const int per_group = GROUP_M * p.tiles_n;
@@ -341,6 +364,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         dtma_coords(tp.op[1], n0, k0, c);
         dtma_load(ring + s * STAGE_ELEMS * 8 + OPER_ELEMS * 8, &tp.map[1], c, fb);
       }
+      if (bulk_epilogue(p, sg)) {
+        // the epilogue's staging slot: completes its `full` phase without data
+        // once the consumers have released the slot's previous k-block
+        const int s = g % STAGES, u = g / STAGES;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        mbar_arrive(smem_u32(full + s));
+        ++g;
+      }
     }
     return;
   }
@@ -372,6 +403,14 @@ __global__ void __launch_bounds__(THREADS, 1)
         mbar_arrive_cpasync(smem_u32(full + s));  // fires when this lane's copies land
         mbar_arrive(smem_u32(full + s));          // publishes this lane's padding stores
       }
+      if (bulk_epilogue(p, sg)) {
+        // the epilogue's staging slot (see the TMA producer)
+        const int s = g % STAGES, u = g / STAGES;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        mbar_arrive(smem_u32(full + s));
+        mbar_arrive(smem_u32(full + s));
+        ++g;
+      }
     }
     cp_async_wait<0>();
     return;
@@ -399,6 +438,10 @@ __global__ void __launch_bounds__(THREADS, 1)
   int nseg = 0;
   while (seg_next(p, sk, it, sg)) {
     ++nseg;
+#ifdef GETT_WS_TRACE_SEGS
+    if (blockIdx.x == 0 && lane == 0 && (warp == 0 || warp == CW / 2) && nseg <= 12)
+      printf("seg %d warp %d clk %lld kind %d kb %d..%d\n", nseg, warp, clock64(), (int)sg.kind, sg.kb0, sg.kb1);
+#endif
     int m0, n0;
     tile_origin(p, sg.tile, m0, n0);
     double acc[MI][NJ][2];
@@ -483,6 +526,53 @@ __global__ void __launch_bounds__(THREADS, 1)
           }
       }
     }
+    if (bulk_epilogue(p, sg)) {
+      // C's 32-wide row runs are contiguous and 16-byte aligned (host check).
+      // The ring slot after the tile's last k-block carries no data: the
+      // producer signals its `full` phase once every warp has released the
+      // slot's previous k-block, so no warp still reads what is staged here.
+      // Stage, then lane l adds row l of the pass with one bulk reduction.
+      const int sx = g % STAGES;
+      mbar_wait(smem_u32(full + sx), (g / STAGES) & 1);
+      double* stg = smem + sx * SSTAGE + warp * EP_WARP_ELEMS;
+      const uint32_t stg_u = smem_u32(stg);
+      const int nb = n0 + wn0;
+      const int64_t cb = nb < p.N ? p.gn.off(1, nb) : 0;
+#pragma unroll
+      for (int pass = 0; pass < MI / EP_CHUNKS; ++pass) {
+        if (pass > 0) {
+          asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+          __syncwarp();
+        }
+#pragma unroll
+        for (int ii = 0; ii < EP_CHUNKS; ++ii) {
+          const int i = pass * EP_CHUNKS + ii;
+#pragma unroll
+          for (int j = 0; j < NJ; ++j) {
+            const double x0 = p.neg ? -acc[i][j][0] : acc[i][j][0];
+            const double x1 = p.neg ? -acc[i][j][1] : acc[i][j][1];
+            *reinterpret_cast<double2*>(stg + (ii * 8 + (lane >> 2)) * EP_PITCH + j * 8 + 2 * (lane & 3)) =
+                make_double2(x0, x1);
+          }
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        const int m = m0 + wm0 + pass * EP_CHUNKS * 8 + lane;
+        if (nb < p.N && m < p.M && !GETT_WS_NO_EPI) {
+          const double* dst = p.C + p.gm.off(1, m) + cb;
+          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                       "r"(stg_u + lane * EP_PITCH * 8), "n"(WN * 8)
+                       : "memory");
+        }
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+      }
+      asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(smem_u32(empty + sx));
+      ++g;
+      TR_ADD(ce)
+      continue;
+    }
     const bool to_c = sg.kind != SEG_SPLITK;
     int64_t coff[NJ * 2];
     bool cok[NJ * 2];
@@ -523,9 +613,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     TR_ADD(ce)
   }
+  if (p.c_bulk) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (warp == 0 && lane == 0)
-    TR_PRINT("blk %d consumer0: segs %d wait_full %lld compute %lld epilogue %lld tail_publish %lld\n",
-             blockIdx.x, nseg, cw, cc, ce, cx);
+    TR_PRINT("blk %d consumer0: segs %d wait_full %lld compute %lld epilogue %lld tail_publish %lld sm %d\n",
+             blockIdx.x, nseg, cw, cc, ce, cx, smid());
 }
 
 template <bool AKF, bool BKF, bool AV, bool BV, bool TMA>

@@ -16,12 +16,13 @@ def pytest_configure(config):
 @pytest.fixture
 def kernel_mode():
     """Set the native kernel family for one test, restoring auto after."""
-    from paper_2410_06770_b200 import (set_complex_embed, set_kernel, set_kr, set_pair, set_pipeline,
-                                       set_split_k, set_stream_k, set_tma)
+    from paper_2410_06770_b200 import (set_bulk, set_complex_embed, set_kernel, set_kr, set_pair,
+                                       set_pipeline, set_split_k, set_stream_k, set_tma)
 
     def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
-            kr="auto", kr_fused=False, kr_pair=True):
+            kr="auto", kr_fused=False, kr_pair=True, bulk=True):
         set_kernel(name)
+        set_bulk(bulk)
         set_split_k(split)
         set_pipeline(pipeline)
         set_stream_k(stream_k)
@@ -39,3 +40,4 @@ def kernel_mode():
     set_pair(False)
     set_complex_embed(True)
     set_kr("auto")
+    set_bulk(True)
