@@ -1405,8 +1405,11 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
       sk.epoch = sw.epoch;
     }
     // C += acc as bulk adds of whole 32-wide row runs staged in shared memory
-    tp.c_bulk = g_dgett_bulk && dp.c_bulk_rows && dp.c_bulk_cols &&
-                (reinterpret_cast<uintptr_t>(c) & 15) == 0;
+    tp.c_bulk = 0;
+    if (g_dgett_bulk && dp.c_bulk_rows && dp.c_bulk_cols && (reinterpret_cast<uintptr_t>(c) & 15) == 0) {
+      tp.c_bulk = 1;
+      if (dp.gm.e_in.d % 32 == 0) tp.c_bulk |= 2;
+    }
     const TmaParams* dtp =
         g_tma && g_dgett_tma ? dgett_tma(dp, reinterpret_cast<const double*>(A), reinterpret_cast<const double*>(B))
                              : nullptr;

@@ -88,8 +88,11 @@ struct TiledParams {
   T* ws;            // [splits][M][N] partial tiles when splits > 1 ([splits][N][M] if ws_t)
   int32_t neg = 0;  // epilogue C += -acc (the a.im*b.im term of a complex contraction)
   int32_t ws_t = 0; // split-K workspace transposed (tcgen05 SGETT epilogue: m fastest)
-  int32_t c_bulk = 0; // C's N group: unit inner stride, inner extent a multiple of 32, every
-                      // offset even and C 16-B aligned (DGETT bulk-add epilogue, dgett_ws.cu)
+  int32_t c_bulk = 0; // DGETT bulk-add epilogue (dgett_ws.cu), bits: 1 = C's N group has a unit
+                      // inner stride and an inner extent a multiple of 32, every offset even and
+                      // C 16-B aligned; 2 = also C's M group's inner extent a multiple of 32 (32
+                      // consecutive rows from a 32-aligned start are affine: one thread issues
+                      // their adds)
 };
 
 // Persistent stream-K schedule of the DGETT kernel (dgett_ws.cu); enabled == 0

@@ -85,6 +85,15 @@ static_assert(CW * EP_WARP_ELEMS <= STAGE_ELEMS, "bulk-add staging exceeds a sta
 static_assert(MI % EP_CHUNKS == 0 && WN == 32, "bulk-add staging shape");
 
 
+// one lane of the (converged) warp: true for it, false for the others
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred p;\n\telect.sync _|p, 0xffffffff;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+      : "=r"(pred));
+  return pred != 0;
+}
+
 __device__ __forceinline__ void mbar_init(uint32_t addr, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(addr), "r"(count));
 }
@@ -433,7 +442,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   constexpr int AKS = AKF ? 4 : 4 * RF_PITCH;
   constexpr int BKS = BKF ? 4 : 4 * RF_PITCH;
   uint32_t g = 0;
-  TR_DECL(cw = 0, cc = 0, ce = 0, cx = 0)
+  TR_DECL(cw = 0, cc = 0, ce = 0, cx = 0, e_slot = 0, e_st = 0, e_iss = 0, e_rd = 0, e_fin = 0, cw_first = 0, cw_seg0 = 0)
   TR_T0()
   int nseg = 0;
   while (seg_next(p, sk, it, sg)) {
@@ -454,6 +463,11 @@ __global__ void __launch_bounds__(THREADS, 1)
     for (int kb = sg.kb0; kb < sg.kb1; ++kb, ++g) {
       const int s = g % STAGES, u = g / STAGES;
       mbar_wait(smem_u32(full + s), u & 1);
+#ifdef GETT_WS_TRACE
+      if (g == 0) TR_ADD(cw_first)
+      else if (kb == sg.kb0) TR_ADD(cw_seg0)
+      else
+#endif
       TR_ADD(cw)
       const double* As = smem + s * SSTAGE;
       const double* Bs = As + SOPER;
@@ -533,7 +547,9 @@ __global__ void __launch_bounds__(THREADS, 1)
       // slot's previous k-block, so no warp still reads what is staged here.
       // Stage, then lane l adds row l of the pass with one bulk reduction.
       const int sx = g % STAGES;
+      TR_ADD(ce)
       mbar_wait(smem_u32(full + sx), (g / STAGES) & 1);
+      TR_ADD(e_slot)
       double* stg = smem + sx * SSTAGE + warp * EP_WARP_ELEMS;
       const uint32_t stg_u = smem_u32(stg);
       const int nb = n0 + wn0;
@@ -543,6 +559,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (pass > 0) {
           asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
           __syncwarp();
+          TR_ADD(e_rd)
         }
 #pragma unroll
         for (int ii = 0; ii < EP_CHUNKS; ++ii) {
@@ -557,20 +574,43 @@ __global__ void __launch_bounds__(THREADS, 1)
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
-        const int m = m0 + wm0 + pass * EP_CHUNKS * 8 + lane;
-        if (nb < p.N && m < p.M && !GETT_WS_NO_EPI) {
-          const double* dst = p.C + p.gm.off(1, m) + cb;
-          asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
-                       "r"(stg_u + lane * EP_PITCH * 8), "n"(WN * 8)
-                       : "memory");
+        TR_ADD(e_st)
+        const int mf = m0 + wm0 + pass * EP_CHUNKS * 8;
+        if (p.c_bulk & 2) {
+          // rows mf .. mf+31 lie in one inner run of C's M group: row l's run
+          // starts at row mf's + l * stride; one thread issues all the adds
+          // from warp-uniform operands (no per-lane issue loop)
+          const int nrows = __shfl_sync(0xffffffffu, min(32, p.M - mf), 0);
+          const int64_t base = __shfl_sync(0xffffffffu, mf < p.M ? p.gm.off(1, mf) + cb : 0, 0);
+          const uint32_t src = __shfl_sync(0xffffffffu, stg_u, 0);
+          if (nb < p.N && !GETT_WS_NO_EPI && elect_one()) {
+            const int64_t rs = p.gm.s_in[1];
+            const double* dst = p.C + base;
+#pragma unroll 4
+            for (int l = 0; l < nrows; ++l)
+              asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
+                               dst + l * rs),
+                           "r"(src + l * EP_PITCH * 8), "n"(WN * 8)
+                           : "memory");
+          }
+        } else {
+          const int m = mf + lane;
+          if (nb < p.N && m < p.M && !GETT_WS_NO_EPI) {
+            const double* dst = p.C + p.gm.off(1, m) + cb;
+            asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(dst),
+                         "r"(stg_u + lane * EP_PITCH * 8), "n"(WN * 8)
+                         : "memory");
+          }
         }
         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        __syncwarp();
+        TR_ADD(e_iss)
       }
       asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
       __syncwarp();
       if (lane == 0) mbar_arrive(smem_u32(empty + sx));
       ++g;
-      TR_ADD(ce)
+      TR_ADD(e_fin)
       continue;
     }
     const bool to_c = sg.kind != SEG_SPLITK;
@@ -615,8 +655,9 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
   if (p.c_bulk) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
   if (warp == 0 && lane == 0)
-    TR_PRINT("blk %d consumer0: segs %d wait_full %lld compute %lld epilogue %lld tail_publish %lld sm %d\n",
-             blockIdx.x, nseg, cw, cc, ce, cx, smid());
+    TR_PRINT("blk %d consumer0: segs %d wait_full %lld compute %lld epilogue %lld tail_publish %lld sm %d "
+             "bulk: slot %lld store %lld issue %lld read %lld final %lld first_wait %lld seg0_wait %lld\n",
+             blockIdx.x, nseg, cw, cc, ce, cx, smid(), e_slot, e_st, e_iss, e_rd, e_fin, cw_first, cw_seg0);
 }
 
 template <bool AKF, bool BKF, bool AV, bool BV, bool TMA>
