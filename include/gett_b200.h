@@ -338,6 +338,12 @@ int gett_set_tma(int on);
  * red.add per element).  Both add each element once at L2: bitwise equal
  * results.  Also GETT_DGETT_BULK. */
 int gett_set_bulk(int on);
+/* SGETT wide CTA-pair kernel (tcgen05.mma.cta_group::2, a 256 x 256 output
+ * tile per cluster of 2, half the shared-memory traffic per MAC of the
+ * 128 x 128 kernel): 0 = off, 1 = automatic (tilings that fill at least half
+ * the SMs, the default), 2 = whenever both operands are TMA-fed and M, N >=
+ * 256.  Also GETT_WIDE. */
+int gett_set_wide(int mode);
 /* SGETT CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256 per pair) for
  * split-K shapes with a K-major operand of >= 256 rows and a rows-major one of
  * <= 128 (e.g. c5); 0 = off (the default), 1 = on.  Also GETT_PAIR. */

@@ -18,7 +18,7 @@ EXPORTS = (
     "gett_zgett", "gett_cgett", "gett_zgett_device", "gett_cgett_device",
     "gett_validate", "gett_derive_output_extents",
     "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
-    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_bulk", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
+    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_bulk", "gett_set_wide", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
     "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
     "gett_multi_schedule", "gett_pack", "gett_pack_device", "gett_set_kr",
@@ -115,6 +115,8 @@ def _load():
     lib.gett_set_tma.argtypes = [ctypes.c_int]
     lib.gett_set_bulk.restype = ctypes.c_int
     lib.gett_set_bulk.argtypes = [ctypes.c_int]
+    lib.gett_set_wide.restype = ctypes.c_int
+    lib.gett_set_wide.argtypes = [ctypes.c_int]
     lib.gett_set_kr.restype = ctypes.c_int
     lib.gett_set_kr.argtypes = [ctypes.c_int]
     lib.gett_set_pair.restype = ctypes.c_int
@@ -186,6 +188,15 @@ def set_bulk(on: bool) -> None:
     """DGETT bulk-add epilogue (whole C row runs per request) on (default) / off."""
     if LIB.gett_set_bulk(1 if on else 0) != 0:
         raise ValueError(f"bad bulk switch {on}")
+
+
+_WIDE = {"off": 0, "auto": 1, "force": 2}
+
+
+def set_wide(mode: str = "auto") -> None:
+    """SGETT wide CTA-pair kernel (256 x 256 per cluster): "off", "auto" (default), "force"."""
+    if mode not in _WIDE or LIB.gett_set_wide(_WIDE[mode]) != 0:
+        raise ValueError(f"bad wide mode {mode!r}")
 
 
 def set_pair(on: bool) -> None:

@@ -46,6 +46,7 @@ bool g_complex_4x = false; // cgett/zgett tiled: four real GETTs instead of one 
 bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes (GETT_PAIR=1: on)
 bool g_dgett_tma = true;  // DGETT: TMA-fed operands for affine views (GETT_DGETT_TMA=0: cp.async gathers)
 bool g_dgett_bulk = true; // DGETT: C += acc as bulk shared->global adds of 32-wide row runs (GETT_DGETT_BULK=0: red.add per element)
+int g_wide = 1;           // SGETT wide CTA-pair kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_WIDE)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
 bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the tiling allows, two k runs per
                           // k-block when they fit (c5: 46.1 vs 48.1 us; GETT_KR_PAIR=0: one CTA per tile)
@@ -76,6 +77,8 @@ void read_env_once() {
   if (dtv) g_dgett_tma = std::atoi(dtv) != 0;
   const char* dbv = std::getenv("GETT_DGETT_BULK");
   if (dbv) g_dgett_bulk = std::atoi(dbv) != 0;
+  const char* wdv = std::getenv("GETT_WIDE");
+  if (wdv) g_wide = std::atoi(wdv);
   const char* krv = std::getenv("GETT_KR");
   if (krv) g_kr = std::atoi(krv);
   const char* krp = std::getenv("GETT_KR_PAIR");
@@ -1361,6 +1364,45 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
     if (tma) {
       a_kf = tma->op[0].kf != 0;
       b_kf = tma->op[1].kf != 0;
+    }
+    if (tma && g_wide > 0 && M >= 256 && N >= 256) {
+      // wide CTA-pair kernel (256 x 256 per pair): half the shared-memory
+      // traffic per MAC; automatic when the pair tiles fill at least half the
+      // SMs without split-K, or K is long enough to split them
+      if (!ds.sms) {
+        int dev = 0;
+        CK(cudaGetDevice(&dev));
+        CK(cudaDeviceGetAttribute(&ds.sms, cudaDevAttrMultiProcessorCount, dev));
+      }
+      TiledParams<T> tw = tp;
+      tw.tiles_m = (int32_t)((M + 255) / 256);
+      tw.tiles_n = (int32_t)((N + 255) / 256);
+      const int64_t pairs = (int64_t)tw.tiles_m * tw.tiles_n;
+      const int64_t kb16 = K / 16;
+      int64_t ws_split = g_split > 0 ? g_split : 1;
+      if (g_split <= 0 && 2 * pairs < ds.sms && kb16 >= 64) {
+        ws_split = ds.sms / (2 * pairs);
+        if (ws_split > kb16 / 32) ws_split = kb16 / 32;  // >= 32 k-blocks per slice
+        if (ws_split < 1) ws_split = 1;
+      }
+      const bool take = g_wide == 2 || (2 * pairs * ws_split >= ds.sms / 2 && kb16 >= 32);
+      if (take) {
+        const int64_t kchunk = ((kb16 + ws_split - 1) / ws_split) * 16;
+        ws_split = (K + kchunk - 1) / kchunk;
+        tw.k_chunk = (int32_t)kchunk;
+        tw.splits = (int32_t)ws_split;
+        tw.ws = nullptr;
+        tw.ws_t = 1;
+        if (ws_split > 1) {
+          int rc = ensure(sw.ws, (size_t)ws_split * M * N * sizeof(T));
+          if (rc) return rc;
+          tw.ws = (T*)sw.ws.p;
+        }
+        CK(launch_sgett_tc_wide(*reinterpret_cast<TiledParams<float>*>(&tw), *tma, a_kf, b_kf, stream));
+        g_launches += ws_split > 1 ? 2 : 1;
+        t_last_kernel = ws_split > 1 ? "sgett_tc3xtf32_wide_splitk" : "sgett_tc3xtf32_wide";
+        return 0;
+      }
     }
     CK(launch_sgett_tc(*reinterpret_cast<TiledParams<float>*>(&tp), tma, a_kf, b_kf, a_vec, b_vec,
                        stream));
@@ -2876,6 +2918,12 @@ int gett_set_tma(int on) {
   return 0;
 }
 
+int gett_set_wide(int mode) {
+  if (mode < 0 || mode > 2) return GETT_E_INVALID_ARG;
+  g_wide = mode;
+  return 0;
+}
+
 int gett_set_bulk(int on) {
   if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
   g_dgett_bulk = on != 0;
@@ -2920,7 +2968,7 @@ void gett_release_caches(void) {
 // 1.02: gett_set_tma, gett_set_pair; 1.03: gett_set_complex_embed;
 // 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi,
 //       gett_multi_schedule, gett_pack[_device], gett_set_kr,
-// 1.05: gett_plan_create / gett_execute[_device] / gett_plan_destroy; 1.06: gett_set_bulk
+// 1.05: gett_plan_create / gett_execute[_device] / gett_plan_destroy; 1.06: gett_set_bulk, gett_set_wide
 int gett_abi_version(void) { return 106; }
 
 }  // extern "C"

@@ -89,6 +89,11 @@ cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bo
 // operands TMA-fed: A' K-major, B' rows-major with NBH-row boxes); split-K
 cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s);
 
+// wide CTA-pair SGETT (256 x 256 tile per pair; both operands TMA-fed);
+// p.tiles_m / tiles_n count pair tiles; split-K partials [split][N][M]
+cudaError_t launch_sgett_tc_wide(const TiledParams<float>& p, const TmaParams& tp, bool a_kf, bool b_kf,
+                                 cudaStream_t s);
+
 // k-run SGETT (sgett_kr.cu); KR in {8, 16, ..., 64}
 // pair: clusters of 2 (cta_group::2, M = 256; tiles_x even, y_rows == NT)
 // KRN: k runs per k-block (1, or 2 for KR <= 40)

@@ -1084,6 +1084,265 @@ cudaError_t launch2(const TiledParams<float>& p, const TmaParams* tp, bool av, b
   return launch4<AKF, BKF, false, false, false>(p, none, s);
 }
 
+
+// ---------------------------------------------------------------------------
+// Wide CTA-pair variant for large tilings (tcgen05.mma.cta_group::2, a
+// 256 x 256 output tile per pair): CTA r of the cluster holds rows
+// 128r..128r+127 of the pair's 256 A' rows in its TMEM and rows 128r..128r+127
+// of the pair's 256 B' rows in its shared memory; the pair MMA (M = 256, N =
+// 256) reads A from each CTA's TMEM and B split N-wise across the two CTAs
+// (tools/umma_2cta_test.cu), so every B' byte staged, split and read by the
+// tensor core feeds twice the MACs of the single-CTA kernel: per k-block a CTA
+// moves the same 16 KB loaded + 16-24 KB split + 24 KB MMA reads as a
+// 128 x 128 tile but for 128 x 256 of output, which takes the kernel from the
+// shared-memory bound (sgett_tc_kernel at 2048^3: ~500 cycles of smem traffic
+// against 384 of MMA per k-block) back under the MMA time.  Loads, split and
+// lo ring are those of the single-CTA TMA kernel (same boxes: 128 rows per
+// operand per CTA); the split warps of both CTAs arrive on the leader's ready
+// barrier, the leader issues the pair MMAs and multicasts each commit.  TMEM:
+// a 256-column accumulator + 8 stages x (A hi, A lo).  A CTA whose A' or B'
+// rows lie wholly past the view skips that box (a fully out-of-bounds box
+// faults) and expects fewer bytes; those accumulator rows / columns are never
+// stored.
+namespace wide {
+constexpr int STAGESW = 8;
+constexpr int ACCW = 256;                               // fp32 accumulator columns
+constexpr int LO_OFFW = STAGESW * STAGE_BYTES;
+constexpr int BAR_OFFW = LO_OFFW + LO_BUFS * TILE_BYTES;
+constexpr int SMEMW_BYTES = BAR_OFFW + BAR_BYTES;
+static_assert(ACCW + STAGESW * A_COLS <= TMEM_COLS, "TMEM budget");
+static_assert(2 * BM * EPI_PITCH * 4 <= STAGESW * STAGE_BYTES, "epilogue staging fits the stage ring");
+static_assert(SMEMW_BYTES <= 227 * 1024, "shared memory budget");
+// D f32, A/B tf32, K-major, N = 256, M = 256 (the pair)
+constexpr uint32_t IDESCW = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                            ((uint32_t)(256 >> 4) << 24);
+
+// grid: 2 x (pair tiles x splits), clusters of 2; p.tiles_m / tiles_n count 256-row pair tiles
+template <bool AKF, bool BKF>
+__global__ void __launch_bounds__(THREADS, 1)
+    sgett_tc_wide_kernel(const __grid_constant__ TiledParams<float> p, const __grid_constant__ TmaParams tp) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + BAR_OFFW);  // this CTA's boxes landed
+  uint64_t* ready = full + STAGESW;    // leader: 8 split-warp arrivals (4 per CTA)
+  uint64_t* empty = ready + STAGESW;   // pair commit (multicast)
+  uint64_t* done = empty + STAGESW;
+  uint64_t* lofree = done + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(lofree + LO_BUFS);
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  uint32_t rank;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+  const int ntiles = p.tiles_m * p.tiles_n;
+  const int cl = blockIdx.x >> 1;
+  const int tile = cl % ntiles, split = cl / ntiles;
+  int tm, tn;
+  {
+    const int per_group = GROUP_M * p.tiles_n;
+    const int group = tile / per_group, first_m = group * GROUP_M;
+    const int gsize = min(p.tiles_m - first_m, GROUP_M);
+    const int in_group = tile % per_group;
+    tm = first_m + in_group % gsize;
+    tn = in_group / gsize;
+  }
+  const int m0 = tm * 256 + 128 * (int)rank;  // this CTA's A' rows (accumulator rows)
+  const int nb0 = tn * 256;                    // the pair's B' rows (accumulator columns)
+  const int n0 = nb0 + 128 * (int)rank;        // this CTA's B' rows
+  const bool a_live = m0 < p.M, b_live = n0 < p.N;
+  const int kbeg = split * p.k_chunk;
+  const int kend = min(p.K, kbeg + p.k_chunk);
+  const int nkb = kend > kbeg ? (kend - kbeg) / BK : 0;  // K % 16 == 0 on the TMA path
+  if (tid == 0) {
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[0]) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[1]) : "memory");
+    for (int s = 0; s < STAGESW; ++s) {
+      mbar_init(smem_u32(full + s), 1);
+      mbar_init(smem_u32(ready + s), 8);
+      mbar_init(smem_u32(empty + s), 1);
+    }
+    mbar_init(smem_u32(done), 1);
+    for (int l = 0; l < LO_BUFS; ++l) mbar_init(smem_u32(lofree + l), 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == MMA_WARP) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  pair::cluster_sync2();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp < 4) {
+    // producer: lanes 0-1 A' boxes (k 0-7 / 8-15), lanes 2-3 B' boxes
+    if (warp == 0 && lane < 4) {
+      const int t = lane >> 1, h = lane & 1;
+      const bool live = t ? b_live : a_live;
+      TmaCoord cc;
+      if (t) cc.init(tp.op[1], live ? n0 : 0, kbeg + 8 * h);
+      else cc.init(tp.op[0], live ? m0 : 0, kbeg + 8 * h);
+      const CUtensorMap* map = t ? &tp.map[1] : &tp.map[0];
+      const uint32_t dst0 = smem_u32(smem) + t * TILE_BYTES + 4096 * h;
+      const uint32_t bytes = (a_live ? TILE_BYTES : 0) + (b_live ? TILE_BYTES : 0);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGESW, u = kb / STAGESW;
+        if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
+        const uint32_t fb = smem_u32(full + s);
+        if (lane == 0)
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb), "r"(bytes) : "memory");
+        int32_t c[5];
+        cc.coords(c);
+        if (live) tma_load5(dst0 + s * STAGE_BYTES, map, c, fb);
+        cc.step();
+      }
+    }
+  } else if (warp < MMA_WARP) {
+    // ---------------- split warpgroups (alternate k-blocks), then epilogue ----------------
+    const int h = (warp - 4) >> 2, wq = warp & 3, tw = (tid - WG) & (WG - 1);
+    constexpr int ALAY = AKF ? 2 : 1;
+    for (int kb = h; kb < nkb; kb += 2) {
+      const int s = kb % STAGESW, u = kb / STAGESW;
+      mbar_wait(smem_u32(full + s), u & 1);
+      const int lb = kb % LO_BUFS, lu = kb / LO_BUFS;
+      if (lu > 0) mbar_wait(smem_u32(lofree + lb), (lu - 1) & 1);
+      uint8_t* st = smem + s * STAGE_BYTES;
+      uint8_t* lo = smem + LO_OFFW + lb * TILE_BYTES;
+      split_a_tmem<ALAY>(st, tmem, ACCW + s * A_COLS, wq, lane);
+      if (!BKF) split_tile_rv(st + TILE_BYTES, lo, tw, h);
+      else split_tile(st + TILE_BYTES, lo, tw);
+      asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) pair::arrive_leader(smem_u32(ready + s));
+    }
+    if (nkb > 0) mbar_wait(smem_u32(done), 0);
+    asm volatile("griddepcontrol.launch_dependents;");
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    // thread = accumulator row 32 wq + lane of this CTA; warpgroup h takes
+    // columns 128h..128h+127 of the pair's 256, in two halves of 64
+    const int lane_row = 32 * wq + lane;
+    const int m = m0 + lane_row;
+    const bool mok = m < p.M;
+    float* tb = reinterpret_cast<float*>(smem) + h * (BM * EPI_PITCH);
+    for (int half = 0; half < 2; ++half) {
+      const int cbeg = 128 * h + 64 * half;
+      uint32_t rr[64];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint32_t taddr = tmem + ((uint32_t)(wq * 32) << 16) + (uint32_t)(cbeg + 16 * q);
+        uint32_t* r = rr + 16 * q;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+            : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+              "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+            : "r"(taddr));
+      }
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (p.splits > 1) {
+        // partials [split][N][M] (m fastest: a warp's 32 rows are 32 consecutive floats)
+        if (!mok) continue;
+        float* wcol = p.ws + (int64_t)split * p.M * p.N + m;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) {
+          const int n = nb0 + cbeg + i;
+          if (n < p.N) wcol[(int64_t)n * p.M] = __uint_as_float(r_or_zero(rr[i], nkb));
+        }
+        continue;
+      }
+      // C += acc staged through the (idle) stage ring, [128 rows][65], so each
+      // warp's C loads and stores cover 32 consecutive n
+      if (half) asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(WG) : "memory");  // previous half read
+#pragma unroll
+      for (int i = 0; i < 64; ++i) tb[lane_row * EPI_PITCH + i] = __uint_as_float(r_or_zero(rr[i], nkb));
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "r"(WG) : "memory");
+      int64_t con[2];
+      bool nok[2];
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int n = nb0 + cbeg + 32 * j + lane;
+        nok[j] = n < p.N;
+        con[j] = nok[j] ? p.gn.off(1, n) : 0;
+      }
+      for (int r0 = wq; r0 < BM; r0 += 4 * EPI_ROWS) {
+        float cv[EPI_ROWS][2];
+        int64_t co[EPI_ROWS][2];
+#pragma unroll
+        for (int t = 0; t < EPI_ROWS; ++t) {
+          const int mm = m0 + r0 + 4 * t;
+          const bool rok = mm < p.M;
+          const int64_t rof = rok ? p.gm.off(1, mm) : 0;
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            co[t][j] = rof + con[j];
+            cv[t][j] = (rok && nok[j]) ? p.C[co[t][j]] : 0.f;
+          }
+        }
+#pragma unroll
+        for (int t = 0; t < EPI_ROWS; ++t) {
+          const int r = r0 + 4 * t;
+          if (m0 + r >= p.M) continue;
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            if (nok[j]) p.C[co[t][j]] = epi(cv[t][j], tb[r * EPI_PITCH + 32 * j + lane], p.neg);
+        }
+      }
+    }
+  } else if (rank == 0) {
+    // ---------------- MMA issue (leader CTA) ----------------
+    if (lane == 0) {
+      const uint32_t base = smem_u32(smem);
+      for (int kb = 0; kb < nkb; ++kb) {
+        const int s = kb % STAGESW, u = kb / STAGESW;
+        pair::mbar_wait_cluster(smem_u32(ready + s), u & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        const uint32_t sb = base + s * STAGE_BYTES;
+        const uint32_t lob = base + LO_OFFW + (kb % LO_BUFS) * TILE_BYTES;
+#pragma unroll
+        for (int j = 0; j < BK / 8; ++j) {
+          const uint32_t ah = tmem + ACCW + s * A_COLS + 8 * j, al = ah + BK;
+          const uint64_t bh = BKF ? sdesc_sw32(sb + TILE_BYTES + 4096 * j) : sdesc(sb + TILE_BYTES + 256 * j);
+          const uint64_t bl = BKF ? sdesc_sw32(lob + 4096 * j) : sdesc(lob + 256 * j);
+          pair::mma_pair(tmem, ah, bh, IDESCW, (kb | j) != 0);
+          pair::mma_pair(tmem, al, bh, IDESCW, 1);
+          pair::mma_pair(tmem, ah, bl, IDESCW, 1);
+        }
+        pair::commit_pair(smem_u32(empty + s));
+        pair::commit_pair(smem_u32(lofree + kb % LO_BUFS));
+      }
+      pair::commit_pair(smem_u32(done));
+    }
+    __syncwarp();
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  pair::cluster_sync2();
+  if (warp == MMA_WARP)
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
+}
+}  // namespace wide
+
+template <bool AKF, bool BKF>
+cudaError_t launch_wide_t(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
+  auto k = wide::sgett_tc_wide_kernel<AKF, BKF>;
+  static unsigned long long configured = 0;
+  cudaError_t e = ensure_dyn_smem(k, wide::SMEMW_BYTES, configured);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(2 * p.tiles_m * p.tiles_n * p.splits));
+  cfg.blockDim = dim3(THREADS);
+  cfg.dynamicSmemBytes = wide::SMEMW_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, k, p, tp);
+}
+
 }  // namespace tc
 
 cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bool a_kf, bool b_kf,
@@ -1100,6 +1359,18 @@ cudaError_t launch_sgett_tc(const TiledParams<float>& p, const TmaParams* tp, bo
 cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
   cudaError_t e = tc::launch_pair(p, tp, s);
   if (e != cudaSuccess) return e;
+  return launch_splitk_reduce<float>(p, s);
+}
+
+// wide CTA-pair SGETT: p.tiles_m / tiles_n in 256-row pair tiles
+cudaError_t launch_sgett_tc_wide(const TiledParams<float>& p, const TmaParams& tp, bool a_kf, bool b_kf,
+                                 cudaStream_t s) {
+  cudaError_t e;
+  if (a_kf && b_kf) e = tc::launch_wide_t<true, true>(p, tp, s);
+  else if (a_kf) e = tc::launch_wide_t<true, false>(p, tp, s);
+  else if (b_kf) e = tc::launch_wide_t<false, true>(p, tp, s);
+  else e = tc::launch_wide_t<false, false>(p, tp, s);
+  if (e != cudaSuccess || p.splits == 1) return e;
   return launch_splitk_reduce<float>(p, s);
 }
 

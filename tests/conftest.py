@@ -17,12 +17,13 @@ def pytest_configure(config):
 def kernel_mode():
     """Set the native kernel family for one test, restoring auto after."""
     from paper_2410_06770_b200 import (set_bulk, set_complex_embed, set_kernel, set_kr, set_pair,
-                                       set_pipeline, set_split_k, set_stream_k, set_tma)
+                                       set_pipeline, set_split_k, set_stream_k, set_tma, set_wide)
 
     def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
-            kr="auto", kr_fused=False, kr_pair=True, bulk=True):
+            kr="auto", kr_fused=False, kr_pair=True, bulk=True, wide="auto"):
         set_kernel(name)
         set_bulk(bulk)
+        set_wide(wide)
         set_split_k(split)
         set_pipeline(pipeline)
         set_stream_k(stream_k)
@@ -41,3 +42,4 @@ def kernel_mode():
     set_complex_embed(True)
     set_kr("auto")
     set_bulk(True)
+    set_wide("auto")

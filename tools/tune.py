@@ -32,6 +32,16 @@ def main():
                          len_a=4096 * 4096, ext_b=(4096, 4096), inc_b=(4096, 1),
                          len_b=4096 * 4096, inc_c=(4096, 1), len_c=4096 * 4096),
     }
+    for n in (2048, 4096):
+        # row-major A[m,k], B[k,n]: A' K-major, B' rows-major (N fast)
+        extra[f"sgemm{n}"] = replace(CONFIGS["c2"], name=f"sgemm{n}", dtype="s", ext_a=(n, n), inc_a=(n, 1),
+                                     len_a=n * n, ext_b=(n, n), inc_b=(n, 1), len_b=n * n, inc_c=(n, 1),
+                                     len_c=n * n)
+        # the same product with the operands exchanged: the first operand is
+        # B[k,n] (contracted mode 0), the second A[m,k]; perm puts m first in C
+        extra[f"sgemm{n}_sw"] = replace(CONFIGS["c2"], name=f"sgemm{n}_sw", dtype="s", ext_a=(n, n),
+                                        inc_a=(n, 1), len_a=n * n, ext_b=(n, n), inc_b=(n, 1), len_b=n * n,
+                                        cont_a=(0,), cont_b=(1,), perm=(1, 0), inc_c=(n, 1), len_c=n * n)
     for name in names:
         w = extra[name] if name in extra else CONFIGS[name]
         a, b, c = w.buffers()
