@@ -788,15 +788,14 @@ bool kr_decide(DevPlan& dp) {
     dp.kr_run = (int)KR;
     dp.kr_l[0].base_off = gx.T[0][0] + p.gk.T[x][0];
     dp.kr_l[1].base_off = gy.T[0][0] + p.gk.T[y][0];
-    // launch configurations.  Shared memory: load slots [X raw KRN x 128 x
-    // (KR+4) | Y raw KE x rows] (freed right after the split) + two operand
-    // slots [Y hi | Y lo] (freed by the MMA) + barriers, within 227 KB; TMEM:
-    // NT accumulator columns (rounded to 32) + two A slots of 2 KE columns.
-    // Ring sizes keep the mbarrier parity waits unambiguous (no waiter two
-    // phases ahead): the split warpgroups take alternate k-blocks, so with an
-    // even number of load slots and two operand slots each group has slots of
-    // its own; one commit frees a k-block's operand and TMEM slots (a second
-    // commit per k-block costs ~46 clk of MMA issue, tools/mma_rate.cu).
+    // launch configurations.  Shared memory: load slots [X raw 128 x (KR+4) |
+    // Y raw KR x rows] of one k run each (freed right after the split) + two
+    // operand slots [Y hi | Y lo] of a k-block = KRN runs (freed by the MMA) +
+    // barriers, within 227 KB; TMEM: NT accumulator columns (rounded to 32) +
+    // two A slots of 2 KE columns.  At least 2 KRN load slots keep the
+    // mbarrier parity waits unambiguous (sgett_kr.cu, ring comment); one commit
+    // frees a k-block's operand and TMEM slots (a second commit per k-block
+    // costs ~46 clk of MMA issue, tools/mma_rate.cu).
     auto up = [](int64_t v, int64_t a) { return (v + a - 1) / a * a; };
     auto make = [&](DevPlan::KrCfg& c, int krn, bool pair) -> bool {
       c.valid = false;
@@ -804,9 +803,9 @@ bool kr_decide(DevPlan& dp) {
       if (pair && !(kp.tiles_x % 2 == 0 && yrows == NT && NT % 16 == 0 && nyb == 1)) return false;
       const int64_t KE = krn * KR, yr = pair ? NT / 2 : NT;
       KrParams q = kp;
-      const int64_t xbytes = up(krn * 128 * (KR + 4) * 4, 1024), ybytes = up(KE * yr * 4, 1024);
+      const int64_t xbytes = up(128 * (KR + 4) * 4, 1024), ybytes = up(KR * yr * 4, 128);
       q.lslot_bytes = (int32_t)(xbytes + ybytes);
-      q.oslot_bytes = (int32_t)(2 * ybytes);
+      q.oslot_bytes = (int32_t)(2 * up(KE * yr * 4, 1024));
       q.a_col0 = (int32_t)up(NT, 32);
       q.aslots = 2;
       if (q.a_col0 + 2 * 2 * KE > 512) return false;
@@ -814,7 +813,7 @@ bool kr_decide(DevPlan& dp) {
         return (int64_t)l * q.lslot_bytes + (int64_t)o * q.oslot_bytes + 512 <= 227 * 1024;
       };
       int sl = 8;
-      while (sl > 2 && !fits(sl, 2)) sl -= 2;
+      while (sl > 2 * krn && !fits(sl, 2)) --sl;
       if (!fits(sl, 2)) return false;
       q.lslots = sl;
       q.oslots = 2;
@@ -824,10 +823,6 @@ bool kr_decide(DevPlan& dp) {
       c.kp = q;
       c.lx = dp.kr_l[0];
       c.ly = dp.kr_l[1];
-      if (krn == 2) {
-        c.lx.box[kp.xk_pos[0]] = 2;
-        c.ly.box[kp.yk_pos[0]] = 2;
-      }
       if (pair) c.ly.box[0] = (uint32_t)(NT / 2);
       c.krn = krn;
       c.pair = pair;

@@ -67,10 +67,11 @@ struct Cfg {
   // zero-filled columns) so the row pitch is an odd multiple of 16 B modulo
   // 128 B and a quarter warp's 16-byte row reads hit 8 distinct bank groups
   static constexpr int XP = KR + 4;
-  static constexpr int XB = KRN * 128 * XP * 4;
+  static constexpr int XB = 128 * XP * 4;      // one run's X box (a multiple of 1 KB: KR + 4 is even)
   static constexpr int XB_AL = (XB + 1023) / 1024 * 1024;  // Y starts 1 KB aligned
   static constexpr int KE = KRN * KR;          // k per k-block
   static constexpr int CHK = KE / 4;           // 16-byte k chunks of an operand row
+  static constexpr int CHR = KR / 4;           // ... of one run
   static constexpr uint32_t SBO = CHK * 128;   // bytes between 8-row groups (K-major no swizzle)
   static_assert(KR % 8 == 0 && KR >= 8 && KR <= 64 && (KRN == 1 || (KRN == 2 && KR <= 40)), "k run");
   static_assert(5 * MAX_SLOTS + 1 + 1 + 8 <= BAR_BYTES / 8, "barrier area");
@@ -248,12 +249,15 @@ template <int KR, int KRN, bool PAIR>
 __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_constant__ KrParams p) {
   using G = Cfg<KR, KRN>;
   constexpr int KE = G::KE;
-  // three rings: load slots [X raw | Y raw] (TMA -> split; freed by the split
-  // warps as soon as they have read them, so the loads run ahead by SL
-  // k-blocks), operand slots [Y hi | Y lo] K-major (split -> MMA; freed by the
-  // MMA's commit) and TMEM A slots (hi, lo columns; freed by the commit).
-  // SL even and SO == 2 (host): each split warpgroup then waits only on its
-  // own load / operand slots, never on a barrier two phases ahead.
+  // three rings: load slots [X raw | Y raw] of ONE k run each (TMA -> split;
+  // freed by the split warps as soon as they have read them, so the loads run
+  // ahead by SL runs whatever the k-block size), operand slots [Y hi | Y lo]
+  // K-major of one k-block = KRN runs (split -> MMA; freed by the MMA's commit)
+  // and TMEM A slots (hi, lo columns; freed by the commit).  SO == 2 and
+  // SL >= 2 KRN (host): a split warpgroup first waits for the commit of its
+  // previous k-block (kb - 2), which implies every run up to k-block kb - 2 has
+  // landed and been read, and the run that last used any of its load slots is
+  // at least 2 KRN runs back — so no full-barrier wait is two phases ahead.
   const int SL = p.lslots, SO = p.oslots, TA = p.aslots;
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + p.bar_off);  // [SL] TMA landed
@@ -295,7 +299,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
   const int x0 = tx * p.x_rows, y0 = ty * p.y_rows;
   const int kb0 = split * p.kpc;
   const int nkb = max(0, min(p.nkb, kb0 + p.kpc) - kb0);
-  const uint32_t tile_bytes = (uint32_t)(KE * yrows_me * 4);  // the Y box (raw [KE][rows])
+  const uint32_t tile_bytes = (uint32_t)(KR * yrows_me * 4);  // one run's Y box (raw [KR][rows])
 
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&p.mx) : "memory");
@@ -348,8 +352,8 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
 #ifdef GETT_KR_TRACE
       long long w_empty = 0;
 #endif
-      for (int kb = 0; kb < nkb; ++kb) {
-        const int s = kb % SL, u = kb / SL;
+      for (int r = 0; r < nkb * KRN; ++r) {
+        const int s = r % SL, u = r / SL;
 #ifdef GETT_KR_TRACE
         const long long c0 = clock64();
 #endif
@@ -368,12 +372,12 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           mbar_arrive(fb);
         } else {
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
-                       "r"((uint32_t)(KRN * p.x_rows * G::XP * 4) + (y_live ? tile_bytes : 0u))
+                       "r"((uint32_t)(p.x_rows * G::XP * 4) + (y_live ? tile_bytes : 0u))
                        : "memory");
           tma_load5(sbase + s * p.lslot_bytes, &p.mx, a, fb);
           if (y_live) tma_load5(sbase + s * p.lslot_bytes + G::XB_AL, &p.my, b, fb);
         }
-        if (p.nko > 0 && (d0 += KRN) == p.k_ext[0]) {  // (k_ext[0] % KRN == 0, host)
+        if (p.nko > 0 && ++d0 == p.k_ext[0]) {
           d0 = 0;
           ++d1;
         }
@@ -390,7 +394,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
     // this thread's Y blocks (chunk c of 4 k, row quad rq): source byte offset
     // in the [KR][NT] box, destination of the quad's first row in the K-major
     // tiles, store rotation
-    constexpr int YU = (G::CHK * (NT_MAX / 4) + WG - 1) / WG;
+    constexpr int YU = (G::CHR * (NT_MAX / 4) + WG - 1) / WG;  // per run
     uint32_t y_src[YU], y_dst[YU];
     int y_rot[YU];
     const int nq = yrows_me >> 2;  // row quads of the box (rows % 4 == 0)
@@ -402,106 +406,114 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       y_src[i] = (uint32_t)(4 * c * yrows_me * 4 + rq * 16);
       y_dst[i] = (uint32_t)(((4 * rq) >> 3) * G::SBO + c * 128 + ((4 * rq) & 7) * 16);
       y_rot[i] = (rq >> 1) & 3;
-      if (uu < G::CHK * nq) ny_units = i + 1;
+      if (uu < G::CHR * nq) ny_units = i + 1;
     }
 #ifdef GETT_KR_TRACE
     long long w_full = 0, w_lo = 0, t_x = 0, t_y = 0;
 #endif
     for (int kb = h; kb < nkb; kb += 2) {
-      const int sl = kb % SL, so = kb % SO, sa = kb % TA;
+      const int so = kb % SO, sa = kb % TA;
 #ifdef GETT_KR_TRACE
       long long c0 = clock64();
 #endif
-      mbar_wait(smem_u32(full + sl), (kb / SL) & 1);
-#ifdef GETT_KR_TRACE
-      w_full += clock64() - c0;
-      c0 = clock64();
-#endif
-      // (SO == TA: one commit frees a k-block's operand slot and TMEM slot)
+      // (first: see the ring comment above; SO == TA: one commit frees a
+      // k-block's operand slot and TMEM slot)
       if (kb >= SO) mbar_wait(smem_u32(ofree + so), (kb / SO - 1) & 1);
       if (TA != SO && kb >= TA) mbar_wait(smem_u32(afree + sa), (kb / TA - 1) & 1);
 #ifdef GETT_KR_TRACE
       w_lo += clock64() - c0;
-      c0 = clock64();
 #endif
-      const uint8_t* st = smem + sl * p.lslot_bytes;
       uint8_t* hi_t = smem + p.o_off + so * p.oslot_bytes;
       uint8_t* lo_t = hi_t + p.oslot_bytes / 2;
-      // X row -> TMEM hi / lo columns of slot sa (run q at columns q KR), 16
-      // (then 8) columns at a time
-      if (!(GETT_KR_ABLATE & 2)) {
 #pragma unroll
-        for (int q = 0; q < KRN; ++q) {
-        const int row = 32 * wq + lane;
-        const float4* xr = reinterpret_cast<const float4*>(st + (q * p.x_rows + row) * G::XP * 4);
-        const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(p.a_col0 + sa * 2 * KE + q * KR);
+      for (int q = 0; q < KRN; ++q) {
+        const int r = kb * KRN + q, sl = r % SL;
+#ifdef GETT_KR_TRACE
+        c0 = clock64();
+#endif
+        mbar_wait(smem_u32(full + sl), (r / SL) & 1);
+#ifdef GETT_KR_TRACE
+        w_full += clock64() - c0;
+        c0 = clock64();
+#endif
+        const uint8_t* st = smem + sl * p.lslot_bytes;
+        // X row -> TMEM hi / lo columns of slot sa (run q at columns q KR), 16
+        // (then 8) columns at a time
+        if (!(GETT_KR_ABLATE & 2)) {
+          const int row = 32 * wq + lane;
+          const float4* xr = reinterpret_cast<const float4*>(st + row * G::XP * 4);
+          const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + (uint32_t)(p.a_col0 + sa * 2 * KE + q * KR);
 #pragma unroll
-        for (int c = 0; c < KR; c += 16) {
-          constexpr int W = 16;
-          const int n = KR - c >= W ? W : 8;
-          uint32_t hv[W], lv[W];
+          for (int c = 0; c < KR; c += 16) {
+            constexpr int W = 16;
+            const int n = KR - c >= W ? W : 8;
+            uint32_t hv[W], lv[W];
 #pragma unroll
-          for (int q = 0; q < W / 4; ++q) {
-            if (4 * q < n) {
-              const float4 v = xr[c / 4 + q];
-              const float f[4] = {v.x, v.y, v.z, v.w};
+            for (int q4 = 0; q4 < W / 4; ++q4) {
+              if (4 * q4 < n) {
+                const float4 v = xr[c / 4 + q4];
+                const float f[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-              for (int j = 0; j < 4; ++j) {
-                hv[4 * q + j] = __float_as_uint(f[j]);
-                lv[4 * q + j] = __float_as_uint(tf32_lo(f[j]));
+                for (int j = 0; j < 4; ++j) {
+                  hv[4 * q4 + j] = __float_as_uint(f[j]);
+                  lv[4 * q4 + j] = __float_as_uint(tf32_lo(f[j]));
+                }
+              }
+            }
+            if (n == W) {
+              tmemio::tst16(ta + c, hv);
+              tmemio::tst16(ta + KE + c, lv);
+            } else {
+              tmemio::tst8(ta + c, hv);
+              tmemio::tst8(ta + KE + c, lv);
+            }
+          }
+        }
+#ifdef GETT_KR_TRACE
+        t_x += clock64() - c0;
+        c0 = clock64();
+#endif
+        // Y [KR][NT] raw -> K-major hi + lo tiles of operand slot so (run q at
+        // k chunks q KR/4 ...), in 4 k x 4 row blocks: four 16-byte row-quad
+        // loads (one per k), a register transpose, and per row one 16-byte
+        // store of 4 k to hi and to lo; the stores are rotated by the row quad
+        // so a quarter warp covers the 8 rows of a core matrix (conflict-free)
+        if (!(GETT_KR_ABLATE & 4)) {
+          const uint8_t* yb = st + G::XB_AL;
+#pragma unroll
+          for (int i = 0; i < YU; ++i) {
+            if (i < ny_units) {
+              float4 v[4];
+#pragma unroll
+              for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(yb + y_src[i] + j * yrows_me * 4);
+              float4 rows[4];
+              rows[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+              rows[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+              rows[2] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+              rows[3] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+              const int rot = y_rot[i];
+#pragma unroll
+              for (int q4 = 0; q4 < 4; ++q4) {
+                float4 rw = rows[0];
+                const int rq = (q4 + rot) & 3;
+                rw = rq == 1 ? rows[1] : rw;
+                rw = rq == 2 ? rows[2] : rw;
+                rw = rq == 3 ? rows[3] : rw;
+                const uint32_t o = y_dst[i] + q * (G::CHR * 128) + rq * 16;
+                *reinterpret_cast<float4*>(hi_t + o) = rw;
+                *reinterpret_cast<float4*>(lo_t + o) =
+                    make_float4(tf32_lo(rw.x), tf32_lo(rw.y), tf32_lo(rw.z), tf32_lo(rw.w));
               }
             }
           }
-          if (n == W) {
-            tmemio::tst16(ta + c, hv);
-            tmemio::tst16(ta + KE + c, lv);
-          } else {
-            tmemio::tst8(ta + c, hv);
-            tmemio::tst8(ta + KE + c, lv);
-          }
         }
-        }
-      }
+        // the load slot is free once every warp of the group has read it
+        __syncwarp();
+        if (lane == 0) mbar_arrive(smem_u32(lfree + sl));
 #ifdef GETT_KR_TRACE
-      t_x += clock64() - c0;
-      c0 = clock64();
+        t_y += clock64() - c0;
 #endif
-      // Y [KR][NT] raw -> K-major hi + lo tiles of operand slot so, in 4 k x 4
-      // row blocks: four 16-byte row-quad loads (one per k), a register
-      // transpose, and per row one 16-byte store of 4 k to hi and to lo; the
-      // stores are rotated by the row quad so a quarter warp covers the 8
-      // rows of a core matrix (conflict-free)
-      if (!(GETT_KR_ABLATE & 4)) {
-        const uint8_t* yb = st + G::XB_AL;
-#pragma unroll
-        for (int i = 0; i < YU; ++i) {
-          if (i < ny_units) {
-            float4 v[4];
-#pragma unroll
-            for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(yb + y_src[i] + j * yrows_me * 4);
-            float4 rows[4];
-            rows[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
-            rows[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
-            rows[2] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
-            rows[3] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
-            const int rot = y_rot[i];
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-              float4 r = rows[0];
-              const int rq = (q + rot) & 3;
-              r = rq == 1 ? rows[1] : r;
-              r = rq == 2 ? rows[2] : r;
-              r = rq == 3 ? rows[3] : r;
-              const uint32_t o = y_dst[i] + rq * 16;
-              *reinterpret_cast<float4*>(hi_t + o) = r;
-              *reinterpret_cast<float4*>(lo_t + o) = make_float4(tf32_lo(r.x), tf32_lo(r.y), tf32_lo(r.z), tf32_lo(r.w));
-            }
-          }
-        }
       }
-      // the load slot is free once every warp of the group has read it
-      __syncwarp();
-      if (lane == 0) mbar_arrive(smem_u32(lfree + sl));
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -510,9 +522,6 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
         if (PAIR) arrive_leader(smem_u32(ready + so));
         else mbar_arrive(smem_u32(ready + so));
       }
-#ifdef GETT_KR_TRACE
-      t_y += clock64() - c0;
-#endif
     }
 #ifdef GETT_KR_TRACE
     if (blockIdx.x < 2 && (tid & 127) == 0)
