@@ -344,6 +344,13 @@ int gett_set_bulk(int on);
  * the SMs, the default), 2 = whenever both operands are TMA-fed and M, N >=
  * 256.  Also GETT_WIDE. */
 int gett_set_wide(int mode);
+/* Programmatic dependent launch of the k-run SGETT kernel and of the split-K
+ * reduce kernels (cudaLaunchAttributeProgrammaticStreamSerialization): each is
+ * scheduled while its predecessor in the stream drains — barrier / TMEM set-up
+ * and launch latency overlap the predecessor's tail — and executes
+ * griddepcontrol.wait before it touches global memory.  1 = on (the default),
+ * 0 = ordinary launches.  Also GETT_PDL.  c5 back to back 38.5 -> 35.1 us. */
+int gett_set_pdl(int on);
 /* SGETT CTA-pair kernel (tcgen05.mma.cta_group::2, M = 256 per pair) for
  * split-K shapes with a K-major operand of >= 256 rows and a rows-major one of
  * <= 128 (e.g. c5); 0 = off (the default), 1 = on.  Also GETT_PAIR. */
@@ -355,8 +362,12 @@ int gett_set_pair(int on);
  * (tile counters; graph-replay safe) instead of by the separate reduce kernel
  * (the default); + 8 = never as CTA pairs (by default pairs of X tiles run as
  * cta_group::2 clusters, each CTA holding half of the other operand, with two
- * k runs per k-block when they fit).  Also GETT_KR / GETT_KR_FUSED /
- * GETT_KR_PAIR. */
+ * k runs per k-block when they fit); + 16 = three tf32 MMAs per 8 k (3xTF32,
+ * truncation split) instead of the default mixed split: one tf32 MMA hi * hi
+ * (hi rounded to tf32) and one bf16 MMA carrying both cross terms
+ * ([bf16(x) | bf16(x_lo)] . [bf16(y_lo) ; bf16(y)]) — at least as accurate
+ * (tools/umma_mixed_test.cu) at two thirds of the tensor work.  Also GETT_KR /
+ * GETT_KR_FUSED / GETT_KR_PAIR / GETT_KR_MIX. */
 int gett_set_kr(int mode);
 /* cgett / zgett on the tensor-core kernels: 1 = one real GETT on a real
  * embedding of the smaller operand (the default), 0 = four real GETTs on the

@@ -18,7 +18,7 @@ EXPORTS = (
     "gett_zgett", "gett_cgett", "gett_zgett_device", "gett_cgett_device",
     "gett_validate", "gett_derive_output_extents",
     "gett_zero_view_d", "gett_zero_view_s", "gett_zero_view_d_device", "gett_zero_view_s_device",
-    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_bulk", "gett_set_wide", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
+    "gett_set_kernel", "gett_set_split_k", "gett_set_pipeline", "gett_set_stream_k", "gett_set_tma", "gett_set_bulk", "gett_set_wide", "gett_set_pdl", "gett_set_pair", "gett_set_complex_embed", "gett_last_kernel", "gett_last_error",
     "gett_launch_count", "gett_release_caches", "gett_abi_version",
     "gett_dgett_multi", "gett_sgett_multi", "gett_set_devices", "gett_set_multi", "gett_last_multi",
     "gett_multi_schedule", "gett_pack", "gett_pack_device", "gett_set_kr",
@@ -117,6 +117,8 @@ def _load():
     lib.gett_set_bulk.argtypes = [ctypes.c_int]
     lib.gett_set_wide.restype = ctypes.c_int
     lib.gett_set_wide.argtypes = [ctypes.c_int]
+    lib.gett_set_pdl.restype = ctypes.c_int
+    lib.gett_set_pdl.argtypes = [ctypes.c_int]
     lib.gett_set_kr.restype = ctypes.c_int
     lib.gett_set_kr.argtypes = [ctypes.c_int]
     lib.gett_set_pair.restype = ctypes.c_int
@@ -190,6 +192,14 @@ def set_bulk(on: bool) -> None:
         raise ValueError(f"bad bulk switch {on}")
 
 
+def set_pdl(on: bool) -> None:
+    """Programmatic dependent launch of the k-run SGETT kernel and the split-K
+    reduce (each scheduled while its predecessor in the stream drains) on
+    (default) / off."""
+    if LIB.gett_set_pdl(1 if on else 0) != 0:
+        raise ValueError(f"bad PDL switch {on}")
+
+
 _WIDE = {"off": 0, "auto": 1, "force": 2}
 
 
@@ -225,13 +235,16 @@ def set_devices(devices) -> None:
     check(LIB.gett_set_devices(len(devs), i32(devs)), "set_devices")
 
 
-def set_kr(mode: str = "auto", fused: bool = False, pair: bool = True) -> None:
+def set_kr(mode: str = "auto", fused: bool = False, pair: bool = True, mixed: bool = True) -> None:
     """SGETT k-run kernel: "off", "auto" (default) or "force" (whenever it
     applies); fused=True reduces split-K partials inside the kernel instead of
     with the separate reduce kernel (the default); pair=False never runs pairs
     of X tiles as cta_group::2 clusters (the default does when the tiling
-    allows, with two k runs per k-block when they fit)."""
-    code = {"off": 0, "auto": 1, "force": 2}[mode] | (4 if fused else 0) | (0 if pair else 8)
+    allows, with two k runs per k-block when they fit); mixed=False issues the
+    three tf32 MMAs of the 3xTF32 truncation split instead of one tf32 + one
+    bf16 MMA per 8 k (the default)."""
+    code = ({"off": 0, "auto": 1, "force": 2}[mode] | (4 if fused else 0) | (0 if pair else 8)
+            | (0 if mixed else 16))
     check(LIB.gett_set_kr(code), "set_kr")
 
 

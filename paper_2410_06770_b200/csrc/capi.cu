@@ -50,6 +50,10 @@ int g_wide = 1;           // SGETT wide CTA-pair kernel: 0 off, 1 automatic, 2 w
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
 bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the tiling allows, two k runs per
                           // k-block when they fit (c5: 46.1 vs 48.1 us; GETT_KR_PAIR=0: one CTA per tile)
+}  // namespace
+int g_launch_pdl = 1;     // programmatic dependent launches of the k-run SGETT kernel and the split-K reduce (GETT_PDL)
+namespace {
+bool g_kr_mix = true;     // k-run kernel: mixed split, one tf32 + one bf16 MMA per 8 k (GETT_KR_MIX=0: three tf32 MMAs)
 bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
                           // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
@@ -83,6 +87,10 @@ void read_env_once() {
   if (krv) g_kr = std::atoi(krv);
   const char* krp = std::getenv("GETT_KR_PAIR");
   if (krp) g_kr_pair = std::atoi(krp) != 0;
+  const char* pdl = std::getenv("GETT_PDL");
+  if (pdl) g_launch_pdl = std::atoi(pdl) != 0;
+  const char* krm = std::getenv("GETT_KR_MIX");
+  if (krm) g_kr_mix = std::atoi(krm) != 0;
   const char* krf = std::getenv("GETT_KR_FUSED");
   if (krf) g_kr_fused = std::atoi(krf) != 0;
   const char* pv = std::getenv("GETT_PAIR");
@@ -945,7 +953,8 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
     }
   }
   const bool pair = cfg.pair;
-  CK(launch_sgett_kr(kp, dp.kr_run, cfg.krn, pair, stream));
+  const bool mix = g_kr_mix;
+  CK(launch_sgett_kr(kp, dp.kr_run, cfg.krn, pair, mix, stream));
   ++g_launches;
   if (splits > 1 && kp.cnt == nullptr) {
     TiledParams<float> tp{};
@@ -961,12 +970,13 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
     CK(launch_splitk_reduce<float>(tp, stream));
     ++g_launches;
   }
-  if (pair)
-    t_last_kernel = splits == 1 ? "sgett_tc3xtf32_kr_pair"
-                                : (kp.cnt ? "sgett_tc3xtf32_kr_pair_splitk_fused" : "sgett_tc3xtf32_kr_pair_splitk");
-  else
-    t_last_kernel = splits == 1 ? "sgett_tc3xtf32_kr"
-                                : (kp.cnt ? "sgett_tc3xtf32_kr_splitk_fused" : "sgett_tc3xtf32_kr_splitk");
+  // [mix][pair][one pass, split-K, split-K reduced in the kernel]
+  static const char* const kr_names[2][2][3] = {
+      {{"sgett_tc3xtf32_kr", "sgett_tc3xtf32_kr_splitk", "sgett_tc3xtf32_kr_splitk_fused"},
+       {"sgett_tc3xtf32_kr_pair", "sgett_tc3xtf32_kr_pair_splitk", "sgett_tc3xtf32_kr_pair_splitk_fused"}},
+      {{"sgett_tctf32bf16_kr", "sgett_tctf32bf16_kr_splitk", "sgett_tctf32bf16_kr_splitk_fused"},
+       {"sgett_tctf32bf16_kr_pair", "sgett_tctf32bf16_kr_pair_splitk", "sgett_tctf32bf16_kr_pair_splitk_fused"}}};
+  t_last_kernel = kr_names[mix ? 1 : 0][pair ? 1 : 0][splits == 1 ? 0 : (kp.cnt ? 2 : 1)];
   return 1;
 }
 
@@ -2900,10 +2910,11 @@ int gett_set_complex_embed(int on) {
 }
 
 int gett_set_kr(int mode) {
-  if (mode < 0 || (mode & 3) == 3 || mode > 15) return GETT_E_INVALID_ARG;
+  if (mode < 0 || (mode & 3) == 3 || mode > 31) return GETT_E_INVALID_ARG;
   g_kr = mode & 3;
   g_kr_fused = (mode & 4) != 0;
   g_kr_pair = (mode & 8) == 0;
+  g_kr_mix = (mode & 16) == 0;
   return 0;
 }
 
@@ -2916,6 +2927,12 @@ int gett_set_tma(int on) {
 int gett_set_wide(int mode) {
   if (mode < 0 || mode > 2) return GETT_E_INVALID_ARG;
   g_wide = mode;
+  return 0;
+}
+
+int gett_set_pdl(int on) {
+  if (on != 0 && on != 1) return GETT_E_INVALID_ARG;
+  g_launch_pdl = on;
   return 0;
 }
 
@@ -2964,6 +2981,7 @@ void gett_release_caches(void) {
 // 1.04: gett_{d,s}gett_multi, gett_set_devices, gett_set_multi, gett_last_multi,
 //       gett_multi_schedule, gett_pack[_device], gett_set_kr,
 // 1.05: gett_plan_create / gett_execute[_device] / gett_plan_destroy; 1.06: gett_set_bulk, gett_set_wide
-int gett_abi_version(void) { return 106; }
+// 1.07: gett_set_pdl; gett_set_kr + 16 (three tf32 MMAs instead of the mixed tf32 + bf16 split)
+int gett_abi_version(void) { return 107; }
 
 }  // extern "C"

@@ -30,9 +30,6 @@ namespace tiled {
 constexpr int BM = 128;
 constexpr int BN = 128;
 constexpr int PAD = 4;
-#ifndef GETT_PDL
-#define GETT_PDL 0  // programmatic dependent launch of the reduce: measured slower on c5 (0.0545 vs 0.0498 ms)
-#endif
 #ifndef GETT_REDUCE_T
 #define GETT_REDUCE_T 1  // transposed-partials reduce through a shared-memory tile (0: element per thread)
 #endif
@@ -692,8 +689,9 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
   // C's element (offset tables, then its value) does not depend on the
   // partials: fetched first, so its two round trips overlap the partials'
   T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
-  const T c0 = *c;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  const T c0 = *c;
   // the slices' partials in a fixed order; loads batched 8 at a time so their
   // latencies overlap
   T s = T(-0.0);
@@ -723,8 +721,11 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_t_kernel(const __grid_
   const int mw = m0 + t / 8, nw = n0 + t % 8;
   const bool okw = mw < p.M && nw < p.N;
   T* c = okw ? p.C + p.gm.off(1, mw) + p.gn.off(1, nw) : nullptr;
-  const T c0 = okw ? *c : T(0);
+  // (a programmatic dependent of this grid may be scheduled right away: it
+  // waits for this grid's completion itself)
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  const T c0 = okw ? *c : T(0);
   const int mr = m0 + t % 32, nr = n0 + t / 32;
   if (mr < p.M && nr < p.N) {
     const int64_t idx = (int64_t)nr * p.M + mr;
@@ -844,7 +845,7 @@ cudaError_t launch_splitk_reduce(const TiledParams<T>& p, cudaStream_t s) {
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = GETT_PDL ? 1 : 0;
+  cfg.numAttrs = g_launch_pdl ? 1 : 0;
   const int64_t mt = (p.M + 31) / 32;
   if (GETT_REDUCE_T && p.ws_t && mt <= 65535) {
     cfg.gridDim = dim3((unsigned)((p.N + 7) / 8), (unsigned)mt);

@@ -7,6 +7,13 @@
 
 namespace gett {
 
+// Programmatic dependent launch (capi.cu; GETT_PDL / gett_set_pdl): the k-run
+// SGETT kernel and the split-K reduce are launched with
+// cudaLaunchAttributeProgrammaticStreamSerialization, so each is scheduled while
+// its predecessor in the stream drains (both wait on griddepcontrol.wait before
+// touching global memory the predecessor may still use).
+extern int g_launch_pdl;
+
 template <typename T>
 cudaError_t launch_tiled(const TiledParams<T>& p, bool a_kf, bool b_kf, bool a_vec, bool b_vec,
                          cudaStream_t s);
@@ -97,7 +104,9 @@ cudaError_t launch_sgett_tc_wide(const TiledParams<float>& p, const TmaParams& t
 // k-run SGETT (sgett_kr.cu); KR in {8, 16, ..., 64}
 // pair: clusters of 2 (cta_group::2, M = 256; tiles_x even, y_rows == NT)
 // KRN: k runs per k-block (1, or 2 for KR <= 40)
-cudaError_t launch_sgett_kr(const KrParams& p, int KR, int KRN, bool pair, cudaStream_t s);
+// mix: per 8 k one tf32 MMA (hi * hi) + one bf16 MMA (both cross terms)
+// instead of three tf32 MMAs
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, int KRN, bool pair, bool mix, cudaStream_t s);
 int sgett_kr_max_nt();
 
 int tiled_bm();

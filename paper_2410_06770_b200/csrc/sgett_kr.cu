@@ -29,6 +29,8 @@
 //     Each element is summed from -0.0 over the splits in order and added to
 //     C once — bitwise what the separate reduce kernel
 //     (kernels.cu gett_splitk_reduce_t_kernel) computes.
+#include <cuda_bf16.h>
+
 #include <cstdint>
 #include <cstdio>
 
@@ -151,6 +153,35 @@ __device__ __forceinline__ uint64_t sdesc(uint32_t saddr, uint32_t lbo, uint32_t
 __device__ __forceinline__ float tf32_lo(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
 }
+// mixed split: hi = x rounded to tf32 (half up in magnitude; the tensor core's
+// truncation of it is then a no-op), lo = x - hi exactly
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+// two floats -> bf16x2 (a in the low half: the even k of a TMEM column / the
+// first k of a shared-memory pair)
+__device__ __forceinline__ uint32_t bf16x2(float a, float b) {
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&v);
+}
+__device__ __forceinline__ void mma_bf16(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
+__device__ __forceinline__ void mma_bf16_pair(uint32_t d, uint32_t a_tmem, uint64_t b, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(d),
+      "r"(a_tmem), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void tma_load5(uint32_t dst, const CUtensorMap* map, const int32_t* c, uint32_t bar) {
   asm volatile(
       "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(dst),
@@ -245,7 +276,13 @@ __device__ __forceinline__ void reduce_slice(const KrParams& p, int x0, int y0, 
 // K-major operand in its shared memory; the leader issues one pair MMA per
 // (k-step, product) for both — per SM half the Y bytes (loads, split,
 // B-operand reads) and half the MMA instructions of the one-CTA form.
-template <int KR, int KRN, bool PAIR>
+// MIX: the mixed split (tools/umma_mixed_test.cu) — per 8 k one tf32 MMA
+// hi * hi (hi rounded to tf32) and ONE bf16 MMA (K = 16) whose 16 k are
+// [bf16(x) | bf16(x_lo)] against [bf16(y_lo) ; bf16(y)]: both cross terms at
+// the bf16 rate, 2 MMAs per 8 k instead of 3.  The lo TMEM columns and the lo
+// shared-memory tile hold the bf16 operands in the same geometry (8 columns /
+// two 16-byte chunks per 8 k).
+template <int KR, int KRN, bool PAIR, bool MIX>
 __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_constant__ KrParams p) {
   using G = Cfg<KR, KRN>;
   constexpr int KE = G::KE;
@@ -336,6 +373,10 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
   if (warp == 0) {
     // ---------------- TMA producer (one thread) ----------------
     if (lane == 0 && nkb > 0) {
+      // launched as a programmatic dependent (g_launch_pdl): the prologue above
+      // overlapped the previous kernel's tail; its results (and its reads of the
+      // split-K workspace) are complete from here on (a no-op otherwise)
+      asm volatile("griddepcontrol.wait;" ::: "memory");
       int32_t cx[5] = {0, 0, 0, 0, 0}, cy[5] = {0, 0, 0, 0, 0};
       row_coords(cx, x0, p.xnr, p.xr_ext, p.xr_pos);
       row_coords(cy, y0 + (PAIR ? (int)rank * yrows_me : 0), p.ynr, p.yr_ext, p.yr_pos);
@@ -399,15 +440,31 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
     int y_rot[YU];
     const int nq = yrows_me >> 2;  // row quads of the box (rows % 4 == 0)
     int ny_units = 0;
+    // (MIX: lanes l and l ^ 8 hold the two 4-k chunks of one 8-k step for the
+    // same row quad and exchange halves, so each stores whole 16-byte bf16
+    // chunks — the even chunk's lane the y_lo chunk, the odd one's the y chunk;
+    // a quarter warp still covers 8 consecutive row quads of one chunk)
+    bool y_ok[YU];
 #pragma unroll
     for (int i = 0; i < YU; ++i) {
       const int uu = tw + WG * i;
-      const int c = uu / nq, rq = uu - c * nq;
+      int c, rq;
+      if (MIX) {
+        const int pp = ((uu >> 4) << 3) | (uu & 7), e = (uu >> 3) & 1;
+        const int cp = pp / nq;
+        rq = pp - cp * nq;
+        c = 2 * cp + e;
+      } else {
+        c = uu / nq;
+        rq = uu - c * nq;
+      }
+      y_ok[i] = c < G::CHR;
       y_src[i] = (uint32_t)(4 * c * yrows_me * 4 + rq * 16);
       y_dst[i] = (uint32_t)(((4 * rq) >> 3) * G::SBO + c * 128 + ((4 * rq) & 7) * 16);
       y_rot[i] = (rq >> 1) & 3;
-      if (uu < G::CHR * nq) ny_units = i + 1;
+      if (y_ok[i]) ny_units = i + 1;
     }
+    if (MIX) ny_units = __reduce_max_sync(0xffffffffu, ny_units);  // (warp-uniform: the exchange is a shuffle)
 #ifdef GETT_KR_TRACE
     long long w_full = 0, w_lo = 0, t_x = 0, t_y = 0;
 #endif
@@ -453,10 +510,26 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
               if (4 * q4 < n) {
                 const float4 v = xr[c / 4 + q4];
                 const float f[4] = {v.x, v.y, v.z, v.w};
+                if (MIX) {
+                  float xl[4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                  hv[4 * q4 + j] = __float_as_uint(f[j]);
-                  lv[4 * q4 + j] = __float_as_uint(tf32_lo(f[j]));
+                  for (int j = 0; j < 4; ++j) {
+                    const float xh = tf32_rn(f[j]);
+                    hv[4 * q4 + j] = __float_as_uint(xh);
+                    xl[j] = f[j] - xh;
+                  }
+                  // 8-k step g = q4 / 2: columns 8g + (0..3) bf16(x), 8g + (4..7) bf16(x_lo)
+                  const int cb = 8 * (q4 >> 1) + 2 * (q4 & 1);
+                  lv[cb] = bf16x2(f[0], f[1]);
+                  lv[cb + 1] = bf16x2(f[2], f[3]);
+                  lv[cb + 4] = bf16x2(xl[0], xl[1]);
+                  lv[cb + 5] = bf16x2(xl[2], xl[3]);
+                } else {
+#pragma unroll
+                  for (int j = 0; j < 4; ++j) {
+                    hv[4 * q4 + j] = __float_as_uint(f[j]);
+                    lv[4 * q4 + j] = __float_as_uint(tf32_lo(f[j]));
+                  }
                 }
               }
             }
@@ -483,26 +556,72 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < YU; ++i) {
             if (i < ny_units) {
+              const bool ok = y_ok[i];
               float4 v[4];
 #pragma unroll
-              for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(yb + y_src[i] + j * yrows_me * 4);
+              for (int j = 0; j < 4; ++j)
+                v[j] = ok ? *reinterpret_cast<const float4*>(yb + y_src[i] + j * yrows_me * 4)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
               float4 rows[4];
               rows[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
               rows[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
               rows[2] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
               rows[3] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
               const int rot = y_rot[i];
+              const uint32_t ob = y_dst[i] + q * (G::CHR * 128);
+              if (MIX) {
+                // hi rounded to tf32; this lane's half (2 words per row) of the
+                // bf16 chunks: the partner's y_lo half goes to the even-chunk
+                // lane, the partner's y half to the odd-chunk lane
+                const bool odd = ((tw >> 3) & 1) != 0;
+                uint2 mine[4], other[4];
 #pragma unroll
-              for (int q4 = 0; q4 < 4; ++q4) {
-                float4 rw = rows[0];
-                const int rq = (q4 + rot) & 3;
-                rw = rq == 1 ? rows[1] : rw;
-                rw = rq == 2 ? rows[2] : rw;
-                rw = rq == 3 ? rows[3] : rw;
-                const uint32_t o = y_dst[i] + q * (G::CHR * 128) + rq * 16;
-                *reinterpret_cast<float4*>(hi_t + o) = rw;
-                *reinterpret_cast<float4*>(lo_t + o) =
-                    make_float4(tf32_lo(rw.x), tf32_lo(rw.y), tf32_lo(rw.z), tf32_lo(rw.w));
+                for (int r4 = 0; r4 < 4; ++r4) {
+                  const float4 y = rows[r4];
+                  const float4 yh = make_float4(tf32_rn(y.x), tf32_rn(y.y), tf32_rn(y.z), tf32_rn(y.w));
+                  rows[r4] = yh;
+                  const uint2 yb2 = make_uint2(bf16x2(y.x, y.y), bf16x2(y.z, y.w));
+                  const uint2 yl2 = make_uint2(bf16x2(y.x - yh.x, y.y - yh.y), bf16x2(y.z - yh.z, y.w - yh.w));
+                  mine[r4] = odd ? yb2 : yl2;
+                  const uint2 send = odd ? yl2 : yb2;
+                  other[r4].x = __shfl_xor_sync(0xffffffffu, send.x, 8);
+                  other[r4].y = __shfl_xor_sync(0xffffffffu, send.y, 8);
+                }
+                if (ok) {
+#pragma unroll
+                  for (int q4 = 0; q4 < 4; ++q4) {
+                    const int rq = (q4 + rot) & 3;
+                    float4 rw = rows[0];
+                    uint2 m2 = mine[0], o2 = other[0];
+                    rw = rq == 1 ? rows[1] : rw;
+                    m2 = rq == 1 ? mine[1] : m2;
+                    o2 = rq == 1 ? other[1] : o2;
+                    rw = rq == 2 ? rows[2] : rw;
+                    m2 = rq == 2 ? mine[2] : m2;
+                    o2 = rq == 2 ? other[2] : o2;
+                    rw = rq == 3 ? rows[3] : rw;
+                    m2 = rq == 3 ? mine[3] : m2;
+                    o2 = rq == 3 ? other[3] : o2;
+                    const uint32_t o = ob + rq * 16;
+                    *reinterpret_cast<float4*>(hi_t + o) = rw;
+                    // (k order inside the chunk: the even 4-k chunk first)
+                    *reinterpret_cast<uint4*>(lo_t + o) =
+                        odd ? make_uint4(o2.x, o2.y, m2.x, m2.y) : make_uint4(m2.x, m2.y, o2.x, o2.y);
+                  }
+                }
+              } else {
+#pragma unroll
+                for (int q4 = 0; q4 < 4; ++q4) {
+                  float4 rw = rows[0];
+                  const int rq = (q4 + rot) & 3;
+                  rw = rq == 1 ? rows[1] : rw;
+                  rw = rq == 2 ? rows[2] : rw;
+                  rw = rq == 3 ? rows[3] : rw;
+                  const uint32_t o = ob + rq * 16;
+                  *reinterpret_cast<float4*>(hi_t + o) = rw;
+                  *reinterpret_cast<float4*>(lo_t + o) =
+                      make_float4(tf32_lo(rw.x), tf32_lo(rw.y), tf32_lo(rw.z), tf32_lo(rw.w));
+                }
               }
             }
           }
@@ -528,6 +647,10 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
       printf("KRROLE blk %d split%d wait_full %lld wait_slots %lld x %lld y %lld\n", blockIdx.x, h, w_full, w_lo, t_x, t_y);
 #endif
     if (nkb > 0) mbar_wait(smem_u32(done), 0);
+    else asm volatile("griddepcontrol.wait;" ::: "memory");  // (no producer ran: order the stores below)
+    // the split-K reduce (or whatever follows as a programmatic dependent) may
+    // be scheduled now; it waits for this grid's completion before reading
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 #ifdef GETT_KR_TRACE
     tr_done = globaltimer();
@@ -648,6 +771,9 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
     if (lane == 0 && nkb > 0 && rank == 0) {
       const uint32_t idesc = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(p.NT >> 3) << 17) |
                              ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
+      // kind::f16 with bf16 operands (format 1), fp32 accumulate
+      const uint32_t idesc_b = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(p.NT >> 3) << 17) |
+                               ((uint32_t)((PAIR ? 256 : 128) >> 4) << 24);
       const uint32_t sbase = smem_u32(smem);
 #ifdef GETT_KR_TRACE
       long long w_ready = 0, t_issue = 0;
@@ -676,7 +802,15 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           const uint32_t ah = ah0 + 8 * j, al = ah + KE;
           // (hi*hi, hi*lo_Y, lo_X*hi: the tiled kernel's order when its TMEM
           // operand is this kernel's Y — c5 — so both give the same bits there)
-          if (PAIR) {
+          if (MIX) {
+            if (PAIR) {
+              mma_tf32_pair(tmem, ah, bh, idesc, (kb | j) != 0);
+              mma_bf16_pair(tmem, al, bl, idesc_b, 1);
+            } else {
+              mma_tf32(tmem, ah, bh, idesc, (kb | j) != 0);
+              mma_bf16(tmem, al, bl, idesc_b, 1);
+            }
+          } else if (PAIR) {
             mma_tf32_pair(tmem, ah, bh, idesc, (kb | j) != 0);
             mma_tf32_pair(tmem, ah, bl, idesc, 1);
             mma_tf32_pair(tmem, al, bh, idesc, 1);
@@ -717,17 +851,26 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
   }
 }
 
-template <int KR, int KRN>
+template <int KR, int KRN, bool MIX>
 cudaError_t launch_t(const KrParams& p, bool pair, cudaStream_t s) {
   if (!pair) {
-    auto k = sgett_kr_kernel<KR, KRN, false>;
+    auto k = sgett_kr_kernel<KR, KRN, false, MIX>;
     static unsigned long long configured = 0;
     cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured);
     if (e != cudaSuccess) return e;
-    k<<<(unsigned)(p.tiles_x * p.tiles_y * p.splits), THREADS, p.bar_off + BAR_BYTES, s>>>(p);
-    return cudaGetLastError();
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(p.tiles_x * p.tiles_y * p.splits));
+    cfg.blockDim = dim3(THREADS);
+    cfg.dynamicSmemBytes = p.bar_off + BAR_BYTES;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_launch_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, k, p);
   }
-  auto k = sgett_kr_kernel<KR, KRN, true>;
+  auto k = sgett_kr_kernel<KR, KRN, true, MIX>;
   static unsigned long long configured2 = 0;
   cudaError_t e = ensure_dyn_smem(k, SMEM_MAX, configured2);
   if (e != cudaSuccess) return e;
@@ -736,40 +879,47 @@ cudaError_t launch_t(const KrParams& p, bool pair, cudaStream_t s) {
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = p.bar_off + BAR_BYTES;
   cfg.stream = s;
-  cudaLaunchAttribute attr[1];
+  cudaLaunchAttribute attr[2];
   attr[0].id = cudaLaunchAttributeClusterDimension;
   attr[0].val.clusterDim.x = 2;
   attr[0].val.clusterDim.y = 1;
   attr[0].val.clusterDim.z = 1;
+  attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = g_launch_pdl ? 2 : 1;
   return cudaLaunchKernelEx(&cfg, k, p);
 }
 
-}  // namespace kr
-
-cudaError_t launch_sgett_kr(const KrParams& p, int KR, int KRN, bool pair, cudaStream_t s) {
+template <bool MIX>
+cudaError_t launch_m(const KrParams& p, int KR, int KRN, bool pair, cudaStream_t s) {
   if (KRN == 2) {
     switch (KR) {
-      case 8: return kr::launch_t<8, 2>(p, pair, s);
-      case 16: return kr::launch_t<16, 2>(p, pair, s);
-      case 24: return kr::launch_t<24, 2>(p, pair, s);
-      case 32: return kr::launch_t<32, 2>(p, pair, s);
-      case 40: return kr::launch_t<40, 2>(p, pair, s);
+      case 8: return launch_t<8, 2, MIX>(p, pair, s);
+      case 16: return launch_t<16, 2, MIX>(p, pair, s);
+      case 24: return launch_t<24, 2, MIX>(p, pair, s);
+      case 32: return launch_t<32, 2, MIX>(p, pair, s);
+      case 40: return launch_t<40, 2, MIX>(p, pair, s);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (KR) {
-    case 8: return kr::launch_t<8, 1>(p, pair, s);
-    case 16: return kr::launch_t<16, 1>(p, pair, s);
-    case 24: return kr::launch_t<24, 1>(p, pair, s);
-    case 32: return kr::launch_t<32, 1>(p, pair, s);
-    case 40: return kr::launch_t<40, 1>(p, pair, s);
-    case 48: return kr::launch_t<48, 1>(p, pair, s);
-    case 56: return kr::launch_t<56, 1>(p, pair, s);
-    case 64: return kr::launch_t<64, 1>(p, pair, s);
+    case 8: return launch_t<8, 1, MIX>(p, pair, s);
+    case 16: return launch_t<16, 1, MIX>(p, pair, s);
+    case 24: return launch_t<24, 1, MIX>(p, pair, s);
+    case 32: return launch_t<32, 1, MIX>(p, pair, s);
+    case 40: return launch_t<40, 1, MIX>(p, pair, s);
+    case 48: return launch_t<48, 1, MIX>(p, pair, s);
+    case 56: return launch_t<56, 1, MIX>(p, pair, s);
+    case 64: return launch_t<64, 1, MIX>(p, pair, s);
     default: return cudaErrorInvalidValue;
   }
+}
+
+}  // namespace kr
+
+cudaError_t launch_sgett_kr(const KrParams& p, int KR, int KRN, bool pair, bool mix, cudaStream_t s) {
+  return mix ? kr::launch_m<true>(p, KR, KRN, pair, s) : kr::launch_m<false>(p, KR, KRN, pair, s);
 }
 
 int sgett_kr_max_nt() { return kr::NT_MAX; }

@@ -20,7 +20,7 @@ def kernel_mode():
                                        set_pipeline, set_split_k, set_stream_k, set_tma, set_wide)
 
     def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
-            kr="auto", kr_fused=False, kr_pair=True, bulk=True, wide="auto"):
+            kr="auto", kr_fused=False, kr_pair=True, bulk=True, wide="auto", kr_mixed=True):
         set_kernel(name)
         set_bulk(bulk)
         set_wide(wide)
@@ -30,7 +30,7 @@ def kernel_mode():
         set_tma(tma)
         set_pair(pair)
         set_complex_embed(complex_embed)
-        set_kr(kr, kr_fused, kr_pair)
+        set_kr(kr, kr_fused, kr_pair, kr_mixed)
 
     yield use
     set_kernel("auto")

@@ -33,7 +33,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version():
-    assert _native.LIB.gett_abi_version() == 106
+    assert _native.LIB.gett_abi_version() == 107
 
 
 @pytest.mark.parametrize("case", load_validation(), ids=lambda c: c["label"])

@@ -79,10 +79,12 @@ SHAPES = [
 @pytest.mark.parametrize("shape", SHAPES, ids=lambda s: "x".join(map(str, s)))
 @pytest.mark.parametrize("c_m_fast", [True, False])
 @pytest.mark.parametrize("split", [0, 1, 5])
-def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, kernel_mode):
+@pytest.mark.parametrize("mixed", [True, False], ids=["tf32bf16", "3xtf32"])
+def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, mixed, kernel_mode):
     """single CTAs and CTA pairs (where the tiling allows; pairs may take two
     k runs per k-block, which moves the split-K cuts), fused and separate
-    reduce: each within the bar, fused == separate bitwise for each form."""
+    reduce, the mixed (tf32 + bf16) and the 3xTF32 split: each within the bar,
+    fused == separate bitwise for each form."""
     m1, m2, kr, k2, n = shape
     names = []
     for pair in (True, False):
@@ -90,10 +92,10 @@ def test_kr_kernel_matches_fp64_fused_equals_separate(shape, c_m_fast, split, ke
         for fused in (True, False):
             pos, kw = _case(m1, m2, kr, k2, n, c_m_fast, seed=sum(shape) + split)
             c0 = pos[13].copy()
-            kernel_mode("tiled", split=split, kr="force", kr_fused=fused, kr_pair=pair)
+            kernel_mode("tiled", split=split, kr="force", kr_fused=fused, kr_pair=pair, kr_mixed=mixed)
             assert g.sgett(*pos, **kw) == []
             kname = g.last_kernel()
-            assert kname.startswith("sgett_tc3xtf32_kr"), kname
+            assert kname.startswith("sgett_tctf32bf16_kr" if mixed else "sgett_tc3xtf32_kr"), kname
             _check(pos, kw, c0)
             outs.append(pos[13])
             names.append(kname)
@@ -108,7 +110,7 @@ def test_kr_auto_on_c5_and_off_for_large_tilings(kernel_mode):
     a, b, c = C5.buffers()
     pos, kw = C5.args(a, b, c)
     assert g.sgett(*pos, **kw) == []
-    assert g.last_kernel().startswith("sgett_tc3xtf32_kr")
+    assert g.last_kernel().startswith(("sgett_tc3xtf32_kr", "sgett_tctf32bf16_kr"))
     rng = np.random.default_rng(1)
     A = rng.uniform(-1, 1, 1024 * 1024).astype(np.float32)
     B = rng.uniform(-1, 1, 1024 * 1024).astype(np.float32)
@@ -119,12 +121,12 @@ def test_kr_auto_on_c5_and_off_for_large_tilings(kernel_mode):
 
 
 def test_kr_c5_equals_tiled_bitwise(kernel_mode):
-    """On c5 both tcgen05 kernels (one-CTA form) cut K at the same points
+    """On c5 both tcgen05 kernels (one-CTA form, three tf32 MMAs) cut K at the same points
     (1280 = 32 runs of 40 = 80 blocks of 16) and issue the same MMAs in the
     same k order: the results are bit-identical."""
     outs = []
     for kr in ("force", "off"):
-        kernel_mode("tiled", kr=kr, kr_pair=False)
+        kernel_mode("tiled", kr=kr, kr_pair=False, kr_mixed=False)
         a, b, c = C5.buffers()
         pos, kw = C5.args(a, b, c)
         assert g.sgett(*pos, **kw) == []
@@ -151,7 +153,7 @@ def test_kr_graph_replay_fused(kernel_mode):
     tc = torch.from_numpy(c).cuda()
     pos, kw = w.args(ta, tb, tc)
     gg = GettGraph(sgett_device, *pos, **kw)
-    assert g.last_kernel().startswith("sgett_tc3xtf32_kr")
+    assert g.last_kernel().startswith(("sgett_tc3xtf32_kr", "sgett_tctf32bf16_kr"))
     for _ in range(2):
         gg.replay()
     torch.cuda.synchronize()
@@ -163,7 +165,7 @@ def test_kr_pair_taken_on_c5(kernel_mode):
     a, b, c = C5.buffers()
     pos, kw = C5.args(a, b, c)
     assert g.sgett(*pos, **kw) == []
-    assert g.last_kernel().startswith("sgett_tc3xtf32_kr_pair"), g.last_kernel()
+    assert g.last_kernel().startswith("sgett_tctf32bf16_kr_pair"), g.last_kernel()
 
 
 @pytest.mark.parametrize("ny", [189, 193, 320])
@@ -182,9 +184,46 @@ def test_kr_pair_second_column_tile_half_out_of_range(ny, kernel_mode):
     c = c0.copy()
     assert g.sgett(2, (na, k), inc_a, a, 2, (nb, k), inc_b, b, 1, (1,), (1,), (0, 1), (nb + 1, 1), c,
                    offset_c=3) == []
-    assert g.last_kernel().startswith("sgett_tc3xtf32_kr"), g.last_kernel()
+    assert g.last_kernel().startswith(("sgett_tc3xtf32_kr", "sgett_tctf32bf16_kr")), g.last_kernel()
     A = _strided(a, (na, k), inc_a, 0).astype(np.float64)
     B = _strided(b, (nb, k), inc_b, 0).astype(np.float64)
     want = _strided(c0, (na, nb), (nb + 1, 1), 3).astype(np.float64) + A @ B.T
     got = _strided(c, (na, nb), (nb + 1, 1), 3).astype(np.float64)
     assert np.abs(got - want).max() / (k * np.abs(a).max() * np.abs(b).max()) <= 1e-5
+
+
+def test_kr_mixed_split_at_least_as_accurate_as_3xtf32(kernel_mode):
+    """The mixed split (one tf32 MMA of tf32-rounded hi parts + one bf16 MMA
+    carrying both cross terms) against the three-MMA truncation split on c5
+    and on a short-K case: its error against fp64 is no larger than 1.25x the
+    3xTF32 error (it is smaller on c5: rounding the hi parts removes the
+    truncation split's one-signed lo*lo term), and on integer data both are
+    exact."""
+    from oracle import oracle
+
+    def err_of(w, mixed):
+        a, b, c = w.buffers()
+        ref = oracle.einsum_check(w.ext_a, w.inc_a, a, w.off_a, w.ext_b, w.inc_b, b, w.off_b,
+                                  w.conts, w.cont_a, w.cont_b, w.perm)
+        ref = ref + oracle.strided(c, w.ext_c, w.inc_c, w.off_c).astype(np.float64)
+        kernel_mode("tiled", kr="force", kr_mixed=mixed)
+        pos, kw = w.args(a, b, c)
+        assert g.sgett(*pos, **kw) == []
+        assert ("tf32bf16" in g.last_kernel()) == mixed, g.last_kernel()
+        return np.max(np.abs(oracle.strided(c, w.ext_c, w.inc_c, w.off_c) - ref))
+
+    for w in (C5, C5.slice_free("A", 0, 0, 16)):
+        e_mix, e_3x = err_of(w, True), err_of(w, False)
+        assert e_mix <= 1.25 * e_3x, (w.name, e_mix, e_3x)
+    # integer data (|x| <= 8): hi parts exact, lo parts zero -> exact sums
+    pos, kw = _case(3, 50, 8, 64, 128, True, seed=5)
+    pos = list(pos)
+    for i in (3, 7, 13):
+        pos[i] = np.rint(pos[i] * 8).astype(np.float32)
+    outs = []
+    for mixed in (True, False):
+        c = pos[13].copy()
+        kernel_mode("tiled", kr="force", kr_mixed=mixed)
+        assert g.sgett(*pos[:13], c, **kw) == []
+        outs.append(c)
+    assert outs[0].tobytes() == outs[1].tobytes()

@@ -87,4 +87,4 @@ def test_layout_matrix(dtype, kmodes, split, M, N, kernel_mode):
         idx = off_c + np.add.outer(np.arange(M) * c_inc[0], np.arange(N) * c_inc[1]).ravel()
         mask[idx] = False
         assert c[mask].tobytes() == c0[mask].tobytes()
-        assert g.last_kernel().startswith("sgett_tc3xtf32" if dtype == "s" else "dgett_dmma")
+        assert g.last_kernel().startswith(("sgett_tc3xtf32", "sgett_tctf32bf16") if dtype == "s" else "dgett_dmma")
