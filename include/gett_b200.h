@@ -342,7 +342,11 @@ int gett_set_bulk(int on);
  * tile per cluster of 2, half the shared-memory traffic per MAC of the
  * 128 x 128 kernel): 0 = off, 1 = automatic (tilings that fill at least half
  * the SMs, the default), 2 = whenever both operands are TMA-fed and M, N >=
- * 256.  Also GETT_WIDE. */
+ * 256; + 4 = the mixed split (one tf32 MMA hi * hi + one bf16 MMA carrying
+ * both cross terms per 8 k, as the k-run kernel's; see gett_set_kr) instead of
+ * the default three tf32 MMAs (3xTF32 truncation split, bitwise equal to the
+ * 128 x 128 kernel without split-K): same accuracy, no faster while the
+ * kernel is bound by its 32-byte TMA lines.  Also GETT_WIDE / GETT_WIDE_MIX. */
 int gett_set_wide(int mode);
 /* Programmatic dependent launch of the k-run SGETT kernel and of the split-K
  * reduce kernels (cudaLaunchAttributeProgrammaticStreamSerialization): each is

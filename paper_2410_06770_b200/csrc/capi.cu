@@ -47,6 +47,10 @@ bool g_pair = false;      // SGETT: CTA-pair kernel for narrow-N split-K shapes 
 bool g_dgett_tma = true;  // DGETT: TMA-fed operands for affine views (GETT_DGETT_TMA=0: cp.async gathers)
 bool g_dgett_bulk = true; // DGETT: C += acc as bulk shared->global adds of 32-wide row runs (GETT_DGETT_BULK=0: red.add per element)
 int g_wide = 1;           // SGETT wide CTA-pair kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_WIDE)
+bool g_wide_k16 = true;   // wide kernel: K-major operands as one 16-k SWIZZLE_64B box per k-block (GETT_WIDE_K16=0: two SW32 boxes)
+int g_l2hint = 0;          // DGETT TMA producer / bulk epilogue L2 policies (SkParams::l2hint; GETT_WS_L2HINT)
+bool g_wide_mix = false;  // wide kernel: mixed split, one tf32 + one bf16 MMA per 8 k (GETT_WIDE_MIX=1; 4096^3 229 vs 236 TF:
+                          // the kernel is bound by the TMA line rate of its 32-byte K-major boxes, not by the MMAs)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
 bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the tiling allows, two k runs per
                           // k-block when they fit (c5: 46.1 vs 48.1 us; GETT_KR_PAIR=0: one CTA per tile)
@@ -83,6 +87,12 @@ void read_env_once() {
   if (dbv) g_dgett_bulk = std::atoi(dbv) != 0;
   const char* wdv = std::getenv("GETT_WIDE");
   if (wdv) g_wide = std::atoi(wdv);
+  const char* l2v = std::getenv("GETT_WS_L2HINT");
+  if (l2v) g_l2hint = std::atoi(l2v);
+  const char* wkv = std::getenv("GETT_WIDE_K16");
+  if (wkv) g_wide_k16 = std::atoi(wkv) != 0;
+  const char* wmv = std::getenv("GETT_WIDE_MIX");
+  if (wmv) g_wide_mix = std::atoi(wmv) != 0;
   const char* krv = std::getenv("GETT_KR");
   if (krv) g_kr = std::atoi(krv);
   const char* krp = std::getenv("GETT_KR_PAIR");
@@ -142,6 +152,11 @@ struct DevPlan {
   } tma_l[2];
   TmaParams tma_p{};
   const void* tma_base[2] = {nullptr, nullptr};
+  // the wide kernel's maps: K-major operands as one [16 k][128 rows]
+  // SWIZZLE_64B box per k-block (half the TMA lines of two SW32 boxes)
+  int tma64_state = 0;  // 0 undecided, 1 usable, -1 not
+  TmaParams tma64_p{};
+  const void* tma64_base[2] = {nullptr, nullptr};
   // CTA-pair SGETT on swapped roles (A2 = B' K-major, B2 = A' rows-major)
   int pair_state = 0;  // 0 undecided, 1 usable, -1 not
   TmaLayout pair_l[2];
@@ -561,7 +576,9 @@ TmaEncodeFn tma_encode_fn() {
   return fn;
 }
 
-bool tma_encode(const DevPlan::TmaLayout& L, const float* base, CUtensorMap* map) {
+// k16: a K-major operand's boxes are 16 k wide with SWIZZLE_64B (the wide
+// kernel) instead of 8 k with SWIZZLE_32B
+bool tma_encode(const DevPlan::TmaLayout& L, const float* base, CUtensorMap* map, bool k16 = false) {
   TmaEncodeFn enc = tma_encode_fn();
   if (!enc) return false;
   const float* g = base + L.base_off;
@@ -573,10 +590,13 @@ bool tma_encode(const DevPlan::TmaLayout& L, const float* base, CUtensorMap* map
     box[i] = L.box[i];
     if (i) strides[i - 1] = L.strides[i] * 4;
   }
+  CUtensorMapSwizzle sw = CU_TENSOR_MAP_SWIZZLE_NONE;
+  if (L.op.kf) {
+    sw = k16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+    if (k16) box[0] = 16;
+  }
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, const_cast<float*>(g), dims, strides, box, es,
-             CU_TENSOR_MAP_INTERLEAVE_NONE,
-             L.op.kf ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE,
-             GETT_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, GETT_TMA_PROMO, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Both SGETT operands TMA-fed? (K a multiple of the 16-wide k-block; both
@@ -612,6 +632,37 @@ const TmaParams* sgett_tma(DevPlan& dp, const float* A, const float* B) {
     dp.tma_base[1] = B;
   }
   return &dp.tma_p;
+}
+
+// The wide kernel's tensor maps: as sgett_tma, with every K-major operand
+// loaded as one 16-k SWIZZLE_64B box per k-block (its inner k extent must be a
+// multiple of 16).  Null when some K-major operand cannot (the caller then
+// uses the SW32 maps).
+const TmaParams* sgett_tma64(DevPlan& dp, const float* A, const float* B) {
+  if (dp.tma_state != 1) return nullptr;
+  if (dp.tma64_state == 0) {
+    dp.tma64_state = 1;
+    bool any = false;
+    for (int t = 0; t < 2; ++t)
+      if (dp.tma_l[t].op.kf) {
+        any = true;
+        if (dp.tma_l[t].dims[0] % 16 != 0) dp.tma64_state = -1;
+      }
+    if (!any) dp.tma64_state = -1;
+  }
+  if (dp.tma64_state != 1) return nullptr;
+  if (dp.tma64_base[0] != A || dp.tma64_base[1] != B) {
+    if (!tma_encode(dp.tma_l[0], A, &dp.tma64_p.map[0], true) ||
+        !tma_encode(dp.tma_l[1], B, &dp.tma64_p.map[1], true)) {
+      dp.tma64_base[0] = dp.tma64_base[1] = nullptr;
+      return nullptr;
+    }
+    dp.tma64_p.op[0] = dp.tma_l[0].op;
+    dp.tma64_p.op[1] = dp.tma_l[1].op;
+    dp.tma64_base[0] = A;
+    dp.tma64_base[1] = B;
+  }
+  return &dp.tma64_p;
 }
 
 // ---- SGETT k-run kernel (sgett_kr.cu) ----
@@ -1403,9 +1454,14 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
           if (rc) return rc;
           tw.ws = (T*)sw.ws.p;
         }
-        CK(launch_sgett_tc_wide(*reinterpret_cast<TiledParams<float>*>(&tw), *tma, a_kf, b_kf, stream));
+        const TmaParams* t64 = g_wide_k16 ? sgett_tma64(dp, reinterpret_cast<const float*>(A),
+                                                        reinterpret_cast<const float*>(B))
+                                          : nullptr;
+        CK(launch_sgett_tc_wide(*reinterpret_cast<TiledParams<float>*>(&tw), t64 ? *t64 : *tma, a_kf, b_kf,
+                                g_wide_mix, t64 != nullptr, stream));
         g_launches += ws_split > 1 ? 2 : 1;
-        t_last_kernel = ws_split > 1 ? "sgett_tc3xtf32_wide_splitk" : "sgett_tc3xtf32_wide";
+        if (g_wide_mix) t_last_kernel = ws_split > 1 ? "sgett_tctf32bf16_wide_splitk" : "sgett_tctf32bf16_wide";
+        else t_last_kernel = ws_split > 1 ? "sgett_tc3xtf32_wide_splitk" : "sgett_tc3xtf32_wide";
         return 0;
       }
     }
@@ -1418,6 +1474,7 @@ int run_device(DevPlan& dp, const T* a, const T* b, T* c, cudaStream_t stream, D
   }
   if (sizeof(T) == 8 && g_dgett_ws) {
     SkParams sk;
+    sk.l2hint = g_l2hint;
     if (!ds.sms) {
       int dev = 0;
       CK(cudaGetDevice(&dev));
@@ -2925,8 +2982,9 @@ int gett_set_tma(int on) {
 }
 
 int gett_set_wide(int mode) {
-  if (mode < 0 || mode > 2) return GETT_E_INVALID_ARG;
-  g_wide = mode;
+  if (mode < 0 || (mode & 3) == 3 || mode > 7) return GETT_E_INVALID_ARG;
+  g_wide = mode & 3;
+  g_wide_mix = (mode & 4) != 0;
   return 0;
 }
 

@@ -106,6 +106,10 @@ struct SkParams {
   double* part = nullptr; // [grid][128*128] tail partials
   int32_t* flags = nullptr;  // [grid] "part published" epochs
   int32_t epoch = 0;
+  // L2 cache-policy hints (TMA producer, bulk-add epilogue): bit 0 A' boxes
+  // evict_last, bit 1 B' boxes evict_first, bit 2 the C bulk adds evict_first,
+  // bit 3 exchanges the A' / B' policies
+  int32_t l2hint = 0;
 };
 
 

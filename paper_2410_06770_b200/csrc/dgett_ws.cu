@@ -315,6 +315,24 @@ __device__ __forceinline__ void dtma_load(uint32_t dst, const CUtensorMap* map, 
       : "memory");
 }
 
+__device__ __forceinline__ void dtma_load_hint(uint32_t dst, const CUtensorMap* map, const int32_t* c, uint32_t bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.tensor.5d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1, {%2, %3, %4, %5, %6}], [%7], %8;" ::"r"(dst),
+      "l"(map), "r"(c[0]), "r"(c[1]), "r"(c[2]), "r"(c[3]), "r"(c[4]), "r"(bar), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+__device__ __forceinline__ uint64_t policy_evict_first() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
+
 template <bool AKF, bool BKF, bool AVEC, bool BVEC, bool TMA>
 __global__ void __launch_bounds__(THREADS, 1)
     dgett_ws_kernel(const __grid_constant__ TiledParams<double> p,
@@ -356,6 +374,10 @@ __global__ void __launch_bounds__(THREADS, 1)
     if (warp != CW || lane != 0) return;
     uint32_t g = 0;
     const uint32_t ring = smem_u32(smem);
+    const uint64_t pol_last = policy_evict_last(), pol_first = policy_evict_first();
+    const bool swap = (sk.l2hint & 8) != 0;
+    const int hint_a = swap ? ((sk.l2hint & 2) ? 2 : 0) : ((sk.l2hint & 1) ? 1 : 0);  // 1 evict_last, 2 evict_first
+    const int hint_b = swap ? ((sk.l2hint & 1) ? 1 : 0) : ((sk.l2hint & 2) ? 2 : 0);
     while (seg_next(p, sk, it, sg)) {
       int m0, n0;
       tile_origin(p, sg.tile, m0, n0);
@@ -369,9 +391,13 @@ __global__ void __launch_bounds__(THREADS, 1)
         const int k0 = sg.kbase + kb * BK;
         int32_t c[5];
         dtma_coords(tp.op[0], m0, k0, c);
-        dtma_load(ring + s * STAGE_ELEMS * 8, &tp.map[0], c, fb);
+        if (hint_a) dtma_load_hint(ring + s * STAGE_ELEMS * 8, &tp.map[0], c, fb, hint_a == 1 ? pol_last : pol_first);
+        else dtma_load(ring + s * STAGE_ELEMS * 8, &tp.map[0], c, fb);
         dtma_coords(tp.op[1], n0, k0, c);
-        dtma_load(ring + s * STAGE_ELEMS * 8 + OPER_ELEMS * 8, &tp.map[1], c, fb);
+        if (hint_b)
+          dtma_load_hint(ring + s * STAGE_ELEMS * 8 + OPER_ELEMS * 8, &tp.map[1], c, fb,
+                         hint_b == 1 ? pol_last : pol_first);
+        else dtma_load(ring + s * STAGE_ELEMS * 8 + OPER_ELEMS * 8, &tp.map[1], c, fb);
       }
       if (bulk_epilogue(p, sg)) {
         // the epilogue's staging slot: completes its `full` phase without data
@@ -586,12 +612,24 @@ __global__ void __launch_bounds__(THREADS, 1)
           if (nb < p.N && !GETT_WS_NO_EPI && elect_one()) {
             const int64_t rs = p.gm.s_in[1];
             const double* dst = p.C + base;
+            if (sk.l2hint & 4) {
+              // C's lines are touched once per call: let them leave L2 first
+              const uint64_t pol = policy_evict_first();
 #pragma unroll 4
-            for (int l = 0; l < nrows; ++l)
-              asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
-                               dst + l * rs),
-                           "r"(src + l * EP_PITCH * 8), "n"(WN * 8)
-                           : "memory");
+              for (int l = 0; l < nrows; ++l)
+                asm volatile(
+                    "cp.reduce.async.bulk.global.shared::cta.bulk_group.L2::cache_hint.add.f64 [%0], [%1], %2, %3;" ::"l"(
+                        dst + l * rs),
+                    "r"(src + l * EP_PITCH * 8), "n"(WN * 8), "l"(pol)
+                    : "memory");
+            } else {
+#pragma unroll 4
+              for (int l = 0; l < nrows; ++l)
+                asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f64 [%0], [%1], %2;" ::"l"(
+                                 dst + l * rs),
+                             "r"(src + l * EP_PITCH * 8), "n"(WN * 8)
+                             : "memory");
+            }
           }
         } else {
           const int m = mf + lane;

@@ -98,8 +98,12 @@ cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& t
 
 // wide CTA-pair SGETT (256 x 256 tile per pair; both operands TMA-fed);
 // p.tiles_m / tiles_n count pair tiles; split-K partials [split][N][M]
+// mix: per 8 k one tf32 MMA (hi * hi) + one bf16 MMA (both cross terms) instead
+// of three tf32 MMAs
+// k16: tp's K-major operands are one [16 k][128 rows] SWIZZLE_64B box per
+// k-block (capi.cu sgett_tma64) instead of two SW32 boxes
 cudaError_t launch_sgett_tc_wide(const TiledParams<float>& p, const TmaParams& tp, bool a_kf, bool b_kf,
-                                 cudaStream_t s);
+                                 bool mix, bool k16, cudaStream_t s);
 
 // k-run SGETT (sgett_kr.cu); KR in {8, 16, ..., 64}
 // pair: clusters of 2 (cta_group::2, M = 256; tiles_x even, y_rows == NT)

@@ -31,6 +31,7 @@
 // Accuracy: each product misses lo*lo and lo's own truncation (< 2^-19
 // relative), fp32 accumulation in TMEM; checked against the fp64 oracle and
 // the reference (tests/).
+#include <cuda_bf16.h>
 #include <cstdint>
 #include <cstdio>
 #include <type_traits>
@@ -160,6 +161,20 @@ __device__ __forceinline__ void commit(uint32_t bar) {
 // truncation: < 2^-19 relative per product (accuracy checked in tests/).
 __device__ __forceinline__ float tf32_lo(float x) {
   return x - __uint_as_float(__float_as_uint(x) & 0xffffe000u);
+}
+// Mixed split (tools/umma_mixed_test.cu; MIX kernels): per 8 k one tf32 MMA
+// hi * hi plus ONE kind::f16 (bf16) MMA whose 16 k are [bf16(x) | bf16(x_lo)]
+// against [bf16(y_lo) ; bf16(y)] — both cross terms at the bf16 rate, two MMAs
+// per 8 k instead of three, at least as accurate as the truncation split.
+// hi = x rounded to tf32 where the split writes it (TMEM A', transposed B'),
+// the raw value (truncated by the tensor core) where a landed tile is used in
+// place; lo = x - hi exactly either way.
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+__device__ __forceinline__ uint32_t bf16x2(float a, float b) {  // a in the low half (the first k)
+  const __nv_bfloat162 v = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&v);
 }
 
 // cp.async with zero fill: sz = 0 writes zeros and reads nothing (the source
@@ -384,6 +399,116 @@ __device__ __forceinline__ void split_tile(const uint8_t* hi_s, uint8_t* lo_s, i
   }
 }
 
+// byte offset of (row r, 16-byte k chunk c = k / 4) in one SWIZZLE_64B box of
+// 128 rows x 16 floats: row r's 64 B at 64 r, its chunk index XORed with
+// (r >> 1) & 3 (address bits 4-5 ^ bits 7-8) — the TMA SW64 write pattern and
+// the UMMA K-major SW64 layout
+__device__ __forceinline__ uint32_t sw64_off(int r, int c) {
+  return (uint32_t)(r * 64 + ((c ^ (r >> 1)) & 3) * 16);
+}
+// SWIZZLE_64B K-major descriptor: SBO 512 B (8 rows x 64 B), LBO unused; the
+// 8-k steps of a box start 32 B apart (the swizzle applies to absolute
+// shared-memory address bits, the box is 512 B aligned)
+__device__ __forceinline__ uint64_t sdesc_sw64(uint32_t saddr) {
+  return (uint64_t)((saddr >> 4) & 0x3FFFu) | ((uint64_t)1 << 16) | ((uint64_t)(512 >> 4) << 32) |
+         (1ull << 46) | (4ull << 61);
+}
+
+// MIX, K-major B' landed as ONE SW64 box [16 k][128 rows]: the box stays the
+// tf32 hi operand; the bf16 tile is written in the SW32 geometry of
+// split_tile_mix (one 4 KB box per 8-k step).  Thread tw takes row tw; a
+// quarter warp's reads of one logical chunk cover 8 distinct 16-byte bank
+// groups (4 (r & 1) + (c ^ (r >> 1) & 3)).
+__device__ __forceinline__ void split_tile_mix64(const uint8_t* hi_s, uint8_t* lo_s, int tw) {
+  const uint32_t sw = (uint32_t)((tw >> 2) & 1) << 4;
+#pragma unroll
+  for (int j = 0; j < BK / 8; ++j) {
+    const float4 a = *reinterpret_cast<const float4*>(hi_s + sw64_off(tw, 2 * j));      // k 0-3 of the step
+    const float4 b = *reinterpret_cast<const float4*>(hi_s + sw64_off(tw, 2 * j + 1));  // k 4-7
+    const uint4 yl = make_uint4(bf16x2(tf32_lo(a.x), tf32_lo(a.y)), bf16x2(tf32_lo(a.z), tf32_lo(a.w)),
+                                bf16x2(tf32_lo(b.x), tf32_lo(b.y)), bf16x2(tf32_lo(b.z), tf32_lo(b.w)));
+    const uint4 yy = make_uint4(bf16x2(a.x, a.y), bf16x2(a.z, a.w), bf16x2(b.x, b.y), bf16x2(b.z, b.w));
+    const uint32_t o = 4096u * j + 32u * tw;
+    *reinterpret_cast<uint4*>(lo_s + o + sw) = yl;
+    *reinterpret_cast<uint4*>(lo_s + o + (sw ^ 16)) = yy;
+  }
+}
+
+// MIX, K-major B' landed as two TMA SW32 boxes (k 0-7, k 8-15; row r's 32 B at
+// 32 r, its two 16-byte halves exchanged when (r >> 2) is odd): the boxes stay
+// the tf32 hi operand (truncated by the tensor core); the second tile gets, in
+// the same SW32 geometry, row r's bf16 operand [bf16(y_lo) x 8 | bf16(y) x 8].
+// Thread tw takes row tw of both boxes; reading / writing the logical first
+// half first makes a quarter warp cover 8 distinct 16-byte bank groups.
+__device__ __forceinline__ void split_tile_mix(const uint8_t* hi_s, uint8_t* lo_s, int tw) {
+  const uint32_t sw = (uint32_t)((tw >> 2) & 1) << 4;
+#pragma unroll
+  for (int j = 0; j < BK / 8; ++j) {
+    const uint32_t o = 4096u * j + 32u * tw;
+    const float4 a = *reinterpret_cast<const float4*>(hi_s + o + sw);         // k 0-3 of the step
+    const float4 b = *reinterpret_cast<const float4*>(hi_s + o + (sw ^ 16));  // k 4-7
+    const uint4 yl = make_uint4(bf16x2(tf32_lo(a.x), tf32_lo(a.y)), bf16x2(tf32_lo(a.z), tf32_lo(a.w)),
+                                bf16x2(tf32_lo(b.x), tf32_lo(b.y)), bf16x2(tf32_lo(b.z), tf32_lo(b.w)));
+    const uint4 yy = make_uint4(bf16x2(a.x, a.y), bf16x2(a.z, a.w), bf16x2(b.x, b.y), bf16x2(b.z, b.w));
+    *reinterpret_cast<uint4*>(lo_s + o + sw) = yl;
+    *reinterpret_cast<uint4*>(lo_s + o + (sw ^ 16)) = yy;
+  }
+}
+
+// MIX, rows-major B' staged [k][row]: thread tw takes one 4-k x 4-row unit
+// (chunk c of 4 k, row quad rq; lanes l and l ^ 8 hold the two chunks of one
+// 8-k step), transposes it in registers, and after the warpgroup barrier (the
+// K-major hi tile overwrites the staged tile) stores per row the 16-byte chunk
+// of tf32-rounded hi values and — after exchanging halves with its partner — a
+// whole 16-byte bf16 chunk: the even chunk's lane the y_lo chunk, the odd
+// one's the y chunk; stores rotated by the row quad (conflict-free).
+__device__ __forceinline__ void split_tile_rv_mix(uint8_t* hi_s, uint8_t* lo_s, int tw, int h) {
+  const int e = (tw >> 3) & 1, pp = ((tw >> 4) << 3) | (tw & 7);
+  const int c = 2 * (pp >> 5) + e, rq = pp & 31;
+  float4 v[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) v[j] = *reinterpret_cast<const float4*>(hi_s + (4 * c + j) * 512 + rq * 16);
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + h), "n"(WG) : "memory");
+  float4 rows[4];
+  rows[0] = make_float4(v[0].x, v[1].x, v[2].x, v[3].x);
+  rows[1] = make_float4(v[0].y, v[1].y, v[2].y, v[3].y);
+  rows[2] = make_float4(v[0].z, v[1].z, v[2].z, v[3].z);
+  rows[3] = make_float4(v[0].w, v[1].w, v[2].w, v[3].w);
+  const bool odd = e != 0;
+  uint2 mine[4], other[4];
+#pragma unroll
+  for (int r4 = 0; r4 < 4; ++r4) {
+    const float4 y = rows[r4];
+    const float4 yh = make_float4(tf32_rn(y.x), tf32_rn(y.y), tf32_rn(y.z), tf32_rn(y.w));
+    rows[r4] = yh;
+    const uint2 yb2 = make_uint2(bf16x2(y.x, y.y), bf16x2(y.z, y.w));
+    const uint2 yl2 = make_uint2(bf16x2(y.x - yh.x, y.y - yh.y), bf16x2(y.z - yh.z, y.w - yh.w));
+    mine[r4] = odd ? yb2 : yl2;
+    const uint2 send = odd ? yl2 : yb2;
+    other[r4].x = __shfl_xor_sync(0xffffffffu, send.x, 8);
+    other[r4].y = __shfl_xor_sync(0xffffffffu, send.y, 8);
+  }
+  const int rot = (rq >> 1) & 3;
+#pragma unroll
+  for (int q4 = 0; q4 < 4; ++q4) {
+    const int r4 = (q4 + rot) & 3;
+    float4 rw = rows[0];
+    uint2 m2 = mine[0], o2 = other[0];
+    rw = r4 == 1 ? rows[1] : rw;
+    m2 = r4 == 1 ? mine[1] : m2;
+    o2 = r4 == 1 ? other[1] : o2;
+    rw = r4 == 2 ? rows[2] : rw;
+    m2 = r4 == 2 ? mine[2] : m2;
+    o2 = r4 == 2 ? other[2] : o2;
+    rw = r4 == 3 ? rows[3] : rw;
+    m2 = r4 == 3 ? mine[3] : m2;
+    o2 = r4 == 3 ? other[3] : o2;
+    const uint32_t o = toff(4 * rq + r4, c);
+    *reinterpret_cast<float4*>(hi_s + o) = rw;
+    *reinterpret_cast<uint4*>(lo_s + o) = odd ? make_uint4(o2.x, o2.y, m2.x, m2.y) : make_uint4(m2.x, m2.y, o2.x, o2.y);
+  }
+}
+
 // byte offset of (row r, k) in one SWIZZLE_32B box of 128 rows x 8 floats
 // (the TMA SW32 write pattern = the UMMA K-major SW32 layout; checked by
 // tools/umma_tma_test.cu)
@@ -395,9 +520,9 @@ __device__ __forceinline__ uint32_t sw32_off(int r, int k) {
 // 32 wq + l (TMEM lane quarter wq = warp % 4) and all BK k of the k-block,
 // read from the staging tile — LAYOUT 0: K-major no-swizzle core matrices (4
 // 16-byte chunks), 1: [k][row] (16 words, consecutive lanes on consecutive
-// words), 2: two TMA SW32 boxes — and writes the raw values (hi) and lo with
+// words), 2: two TMA SW32 boxes, 3: one TMA SW64 box — and writes the raw values (hi) and lo with
 // tcgen05.st into the stage's A columns.
-template <int LAYOUT>
+template <int LAYOUT, bool MIX = false>
 __device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, uint32_t col, int wq,
                                              int lane) {
   const int row = 32 * wq + lane;
@@ -408,16 +533,36 @@ __device__ __forceinline__ void split_a_tmem(const uint8_t* st, uint32_t tmem, u
   } else {
 #pragma unroll
     for (int c = 0; c < BK / 4; ++c) {
-      const uint32_t o = LAYOUT == 0 ? toff(row, c) : 4096 * (c >> 1) + sw32_off(row, 4 * (c & 1));
+      const uint32_t o = LAYOUT == 0   ? toff(row, c)
+                         : LAYOUT == 3 ? sw64_off(row, c)
+                                       : 4096 * (c >> 1) + sw32_off(row, 4 * (c & 1));
       const float4 x = *reinterpret_cast<const float4*>(st + o);
       v[4 * c] = x.x; v[4 * c + 1] = x.y; v[4 * c + 2] = x.z; v[4 * c + 3] = x.w;
     }
   }
   uint32_t hi[BK], lo[BK];
+  if (MIX) {
+    // lo columns of 8-k step g: 8g + (0..3) bf16(x) pairs, 8g + (4..7) bf16(x_lo) pairs
+    float xl[BK];
 #pragma unroll
-  for (int i = 0; i < BK; ++i) {
-    hi[i] = __float_as_uint(v[i]);
-    lo[i] = __float_as_uint(tf32_lo(v[i]));
+    for (int i = 0; i < BK; ++i) {
+      const float xh = tf32_rn(v[i]);
+      hi[i] = __float_as_uint(xh);
+      xl[i] = v[i] - xh;
+    }
+#pragma unroll
+    for (int g = 0; g < BK / 8; ++g)
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        lo[8 * g + i] = bf16x2(v[8 * g + 2 * i], v[8 * g + 2 * i + 1]);
+        lo[8 * g + 4 + i] = bf16x2(xl[8 * g + 2 * i], xl[8 * g + 2 * i + 1]);
+      }
+  } else {
+#pragma unroll
+    for (int i = 0; i < BK; ++i) {
+      hi[i] = __float_as_uint(v[i]);
+      lo[i] = __float_as_uint(tf32_lo(v[i]));
+    }
   }
   const uint32_t ta = tmem + ((uint32_t)(32 * wq) << 16) + col;
   asm volatile(
@@ -874,6 +1019,16 @@ __device__ __forceinline__ void mma_pair(uint32_t tmem_d, uint32_t tmem_a, uint6
       "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
       : "memory");
 }
+__device__ __forceinline__ void mma_pair_bf16(uint32_t tmem_d, uint32_t tmem_a, uint64_t b, uint32_t idesc,
+                                              uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::2.kind::f16 [%0], [%1], %2, %3, p;\n\t"
+      "}" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(b), "r"(idesc), "r"(acc)
+      : "memory");
+}
 __device__ __forceinline__ void commit_pair(uint32_t bar) {
   asm volatile(
       "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(bar),
@@ -1116,9 +1271,15 @@ static_assert(SMEMW_BYTES <= 227 * 1024, "shared memory budget");
 // D f32, A/B tf32, K-major, N = 256, M = 256 (the pair)
 constexpr uint32_t IDESCW = (1u << 4) | (2u << 7) | (2u << 10) | ((uint32_t)(256 >> 3) << 17) |
                             ((uint32_t)(256 >> 4) << 24);
+// the same shape for kind::f16 with bf16 operands (format 1)
+constexpr uint32_t IDESCW_BF = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(256 >> 3) << 17) |
+                               ((uint32_t)(256 >> 4) << 24);
 
 // grid: 2 x (pair tiles x splits), clusters of 2; p.tiles_m / tiles_n count 256-row pair tiles
-template <bool AKF, bool BKF>
+// MIX: the mixed split (above) — 4 instead of 6 pair MMAs per k-block
+// W64: K-major operands arrive as one SWIZZLE_64B box [16 k][128 rows] per
+// k-block (half the TMA lines of two SW32 boxes)
+template <bool AKF, bool BKF, bool MIX, bool W64>
 __global__ void __launch_bounds__(THREADS, 1)
     sgett_tc_wide_kernel(const __grid_constant__ TiledParams<float> p, const __grid_constant__ TmaParams tp) {
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -1177,7 +1338,8 @@ __global__ void __launch_bounds__(THREADS, 1)
     // producer: lanes 0-1 A' boxes (k 0-7 / 8-15), lanes 2-3 B' boxes
     if (warp == 0 && lane < 4) {
       const int t = lane >> 1, h = lane & 1;
-      const bool live = t ? b_live : a_live;
+      // (a K-major operand's single 16-k box is issued by the h = 0 lane)
+      const bool live = (t ? b_live : a_live) && !(W64 && h == 1 && (t ? BKF : AKF));
       TmaCoord cc;
       if (t) cc.init(tp.op[1], live ? n0 : 0, kbeg + 8 * h);
       else cc.init(tp.op[0], live ? m0 : 0, kbeg + 8 * h);
@@ -1199,7 +1361,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp < MMA_WARP) {
     // ---------------- split warpgroups (alternate k-blocks), then epilogue ----------------
     const int h = (warp - 4) >> 2, wq = warp & 3, tw = (tid - WG) & (WG - 1);
-    constexpr int ALAY = AKF ? 2 : 1;
+    constexpr int ALAY = AKF ? (W64 ? 3 : 2) : 1;
     for (int kb = h; kb < nkb; kb += 2) {
       const int s = kb % STAGESW, u = kb / STAGESW;
       mbar_wait(smem_u32(full + s), u & 1);
@@ -1207,9 +1369,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       if (lu > 0) mbar_wait(smem_u32(lofree + lb), (lu - 1) & 1);
       uint8_t* st = smem + s * STAGE_BYTES;
       uint8_t* lo = smem + LO_OFFW + lb * TILE_BYTES;
-      split_a_tmem<ALAY>(st, tmem, ACCW + s * A_COLS, wq, lane);
-      if (!BKF) split_tile_rv(st + TILE_BYTES, lo, tw, h);
-      else split_tile(st + TILE_BYTES, lo, tw);
+      split_a_tmem<ALAY, MIX>(st, tmem, ACCW + s * A_COLS, wq, lane);
+      if (MIX) {
+        if (!BKF) split_tile_rv_mix(st + TILE_BYTES, lo, tw, h);
+        else if (W64) split_tile_mix64(st + TILE_BYTES, lo, tw);
+        else split_tile_mix(st + TILE_BYTES, lo, tw);
+      } else {
+        if (!BKF) split_tile_rv(st + TILE_BYTES, lo, tw, h);
+        else split_tile(st + TILE_BYTES, lo, tw);
+      }
       asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -1301,11 +1469,20 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
         for (int j = 0; j < BK / 8; ++j) {
           const uint32_t ah = tmem + ACCW + s * A_COLS + 8 * j, al = ah + BK;
-          const uint64_t bh = BKF ? sdesc_sw32(sb + TILE_BYTES + 4096 * j) : sdesc(sb + TILE_BYTES + 256 * j);
-          const uint64_t bl = BKF ? sdesc_sw32(lob + 4096 * j) : sdesc(lob + 256 * j);
+          const uint64_t bh = !BKF ? sdesc(sb + TILE_BYTES + 256 * j)
+                              : W64 ? sdesc_sw64(sb + TILE_BYTES + 32 * j)
+                                    : sdesc_sw32(sb + TILE_BYTES + 4096 * j);
+          // (the 3xTF32 lo tile mirrors the hi layout; the bf16 tile is SW32 boxes)
+          const uint64_t bl = !BKF ? sdesc(lob + 256 * j)
+                              : (W64 && !MIX) ? sdesc_sw64(lob + 32 * j)
+                                              : sdesc_sw32(lob + 4096 * j);
           pair::mma_pair(tmem, ah, bh, IDESCW, (kb | j) != 0);
-          pair::mma_pair(tmem, al, bh, IDESCW, 1);
-          pair::mma_pair(tmem, ah, bl, IDESCW, 1);
+          if (MIX) {
+            pair::mma_pair_bf16(tmem, al, bl, IDESCW_BF, 1);
+          } else {
+            pair::mma_pair(tmem, al, bh, IDESCW, 1);
+            pair::mma_pair(tmem, ah, bl, IDESCW, 1);
+          }
         }
         pair::commit_pair(smem_u32(empty + s));
         pair::commit_pair(smem_u32(lofree + kb % LO_BUFS));
@@ -1322,9 +1499,9 @@ __global__ void __launch_bounds__(THREADS, 1)
 }
 }  // namespace wide
 
-template <bool AKF, bool BKF>
+template <bool AKF, bool BKF, bool MIX, bool W64>
 cudaError_t launch_wide_t(const TiledParams<float>& p, const TmaParams& tp, cudaStream_t s) {
-  auto k = wide::sgett_tc_wide_kernel<AKF, BKF>;
+  auto k = wide::sgett_tc_wide_kernel<AKF, BKF, MIX, W64>;
   static unsigned long long configured = 0;
   cudaError_t e = ensure_dyn_smem(k, wide::SMEMW_BYTES, configured);
   if (e != cudaSuccess) return e;
@@ -1363,13 +1540,19 @@ cudaError_t launch_sgett_tc_pair(const TiledParams<float>& p, const TmaParams& t
 }
 
 // wide CTA-pair SGETT: p.tiles_m / tiles_n in 256-row pair tiles
+template <bool MIX, bool W64>
+cudaError_t launch_wide_m(const TiledParams<float>& p, const TmaParams& tp, bool a_kf, bool b_kf, cudaStream_t s) {
+  if (a_kf && b_kf) return tc::launch_wide_t<true, true, MIX, W64>(p, tp, s);
+  if (a_kf) return tc::launch_wide_t<true, false, MIX, W64>(p, tp, s);
+  if (b_kf) return tc::launch_wide_t<false, true, MIX, W64>(p, tp, s);
+  return tc::launch_wide_t<false, false, MIX, false>(p, tp, s);
+}
+
 cudaError_t launch_sgett_tc_wide(const TiledParams<float>& p, const TmaParams& tp, bool a_kf, bool b_kf,
-                                 cudaStream_t s) {
+                                 bool mix, bool k16, cudaStream_t s) {
   cudaError_t e;
-  if (a_kf && b_kf) e = tc::launch_wide_t<true, true>(p, tp, s);
-  else if (a_kf) e = tc::launch_wide_t<true, false>(p, tp, s);
-  else if (b_kf) e = tc::launch_wide_t<false, true>(p, tp, s);
-  else e = tc::launch_wide_t<false, false>(p, tp, s);
+  if (mix) e = k16 ? launch_wide_m<true, true>(p, tp, a_kf, b_kf, s) : launch_wide_m<true, false>(p, tp, a_kf, b_kf, s);
+  else e = k16 ? launch_wide_m<false, true>(p, tp, a_kf, b_kf, s) : launch_wide_m<false, false>(p, tp, a_kf, b_kf, s);
   if (e != cudaSuccess || p.splits == 1) return e;
   return launch_splitk_reduce<float>(p, s);
 }

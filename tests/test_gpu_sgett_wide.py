@@ -34,10 +34,10 @@ def _operands(M, N, K, bkf, seed, pad_c=0):
     return args, a.view(M, K).double(), bm
 
 
-def _run(args, c0, mode, split, kernel_mode):
+def _run(args, c0, mode, split, kernel_mode, mixed=False):
     from paper_2410_06770_b200.device import sgett_device
 
-    kernel_mode("tiled", wide=mode, split=split)
+    kernel_mode("tiled", wide=mode, split=split, wide_mixed=mixed)
     c = c0.clone()
     args = args[:13] + (c,)
     assert sgett_device(*args) == []
@@ -115,7 +115,7 @@ def test_wide_strided_views(kernel_mode):
     c0 = torch.from_numpy(rng.uniform(-1, 1, N * ldc).astype(np.float32)).cuda()
     outs = []
     for mode in ("force", "off"):
-        kernel_mode("tiled", wide=mode, split=1)
+        kernel_mode("tiled", wide=mode, split=1, wide_mixed=False)
         c = c0.clone()
         assert sgett_device(2, (M, K), (K + 16, 1), a, 2, (K, N), (N + 32, 1), b, 1, (1,), (0,), (0, 1),
                             (1, ldc), c) == []
@@ -126,3 +126,41 @@ def test_wide_strided_views(kernel_mode):
     got = outs[0][0].view(N, ldc)[:, :M].double().t()
     want = c0.view(N, ldc)[:, :M].double().t() + am @ bm
     assert ((got - want).abs().max() / K).item() <= 1e-5
+
+
+@pytest.mark.parametrize("shape", SHAPES + [(1024, 1024, 2048)], ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("bkf", [False, True])
+@pytest.mark.parametrize("split", [1, 3])
+def test_wide_mixed_split(shape, bkf, split, kernel_mode):
+    """The mixed split (one tf32 MMA of the hi parts + one bf16 MMA carrying
+    both cross terms per 8 k) in the wide kernel, both B' orientations, with
+    and without split-K: within the bar of an fp64 product, as accurate as the
+    three-MMA truncation split (<= 1.5x its error; smaller for long K), padding
+    untouched, and exact on small-integer data."""
+    import torch
+
+    M, N, K = shape
+    if N < 256:
+        pytest.skip("needs two 128-row B' halves")
+    args, am, bm = _operands(M, N, K, bkf, sum(shape) + split, pad_c=5)
+    c0 = args[13].clone()
+    ldc = N + 5
+    want = c0[:M * ldc].view(M, ldc).double()
+    want[:, :N] += am @ bm.t()
+    errs = {}
+    for mixed in (True, False):
+        c, kname = _run(args, c0, "force", split, kernel_mode, mixed=mixed)
+        assert kname.startswith("sgett_tctf32bf16_wide" if mixed else "sgett_tc3xtf32_wide"), kname
+        assert ("splitk" in kname) == (split > 1), kname
+        errs[mixed] = ((c[:M * ldc].view(M, ldc).double() - want).abs().max() / K).item()
+        assert errs[mixed] <= 1e-5, (mixed, errs)
+        assert torch_equal(c[:M * ldc].view(M, ldc)[:, N:], c0[:M * ldc].view(M, ldc)[:, N:])
+        assert torch_equal(c[M * ldc:], c0[M * ldc:])
+    assert errs[True] <= 1.5 * errs[False] + 1e-9, errs
+    # integers |x| <= 8: hi parts exact, lo parts zero
+    ai = torch.round(args[3] * 8)
+    bi = torch.round(args[7] * 8)
+    ci = torch.round(c0 * 8)
+    iargs = args[:3] + (ai,) + args[4:7] + (bi,) + args[8:13] + (ci,)
+    outs = [_run(iargs, ci, "force", split, kernel_mode, mixed=m)[0] for m in (True, False)]
+    assert torch_equal(outs[0], outs[1])
