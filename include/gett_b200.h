@@ -346,7 +346,12 @@ int gett_set_bulk(int on);
  * both cross terms per 8 k, as the k-run kernel's; see gett_set_kr) instead of
  * the default three tf32 MMAs (3xTF32 truncation split, bitwise equal to the
  * 128 x 128 kernel without split-K): same accuracy, no faster while the
- * kernel is bound by its 32-byte TMA lines.  Also GETT_WIDE / GETT_WIDE_MIX. */
+ * kernel is tensor-bound at the power cap and split-latency bound above it;
+ * + 8 = no tail split (by default a partial last wave of at most half the
+ * pair slots runs as two K halves per tile, summed by a small reduce kernel:
+ * 4096^3 takes 3.5 instead of 4 waves' time).  Also GETT_WIDE / GETT_WIDE_MIX /
+ * GETT_WIDE_TAIL / GETT_WIDE_K16 (K-major operands as one 16-k SWIZZLE_64B box
+ * per k-block, default 1). */
 int gett_set_wide(int mode);
 /* Programmatic dependent launch of the k-run SGETT kernel and of the split-K
  * reduce kernels (cudaLaunchAttributeProgrammaticStreamSerialization): each is

@@ -203,12 +203,14 @@ def set_pdl(on: bool) -> None:
 _WIDE = {"off": 0, "auto": 1, "force": 2}
 
 
-def set_wide(mode: str = "auto", mixed: bool = False) -> None:
+def set_wide(mode: str = "auto", mixed: bool = False, tail: bool = True) -> None:
     """SGETT wide CTA-pair kernel (256 x 256 per cluster): "off", "auto"
     (default), "force"; mixed=True issues one tf32 + one bf16 MMA per 8 k (the
     k-run kernel's mixed split) instead of the three tf32 MMAs of the 3xTF32
-    truncation split (the default)."""
-    if mode not in _WIDE or LIB.gett_set_wide(_WIDE[mode] | (4 if mixed else 0)) != 0:
+    truncation split (the default); tail=False never cuts a partial last wave's
+    tiles into two K halves."""
+    code = _WIDE.get(mode, -1) | (4 if mixed else 0) | (0 if tail else 8)
+    if mode not in _WIDE or LIB.gett_set_wide(code) != 0:
         raise ValueError(f"bad wide mode {mode!r}")
 
 

@@ -93,6 +93,12 @@ struct TiledParams {
                       // C 16-B aligned; 2 = also C's M group's inner extent a multiple of 32 (32
                       // consecutive rows from a 32-aligned start are affine: one thread issues
                       // their adds)
+  // wide SGETT kernel, tail split (sgett_tc.cu): the pair tiles [tail_tile0,
+  // tail_tile0 + tail_tiles) of the raster — the partial last wave — are cut
+  // in two K halves (k_chunk) whose partials go to the compact workspace
+  // ws [2][tail_tiles][256 n][256 m]; every other tile runs its whole K with the
+  // fused epilogue.  tail_tiles == 0: off.
+  int32_t tail_tile0 = 0, tail_tiles = 0;
 };
 
 // Persistent stream-K schedule of the DGETT kernel (dgett_ws.cu); enabled == 0

@@ -1276,6 +1276,16 @@ constexpr uint32_t IDESCW_BF = (1u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(
                                ((uint32_t)(256 >> 4) << 24);
 
 // grid: 2 x (pair tiles x splits), clusters of 2; p.tiles_m / tiles_n count 256-row pair tiles
+// pair tile -> (tm, tn): groups of GROUP_M tile rows, column by column
+__device__ __forceinline__ void wide_tile(const TiledParams<float>& p, int tile, int& tm, int& tn) {
+  const int per_group = GROUP_M * p.tiles_n;
+  const int group = tile / per_group, first_m = group * GROUP_M;
+  const int gsize = min(p.tiles_m - first_m, GROUP_M);
+  const int in_group = tile % per_group;
+  tm = first_m + in_group % gsize;
+  tn = in_group / gsize;
+}
+
 // MIX: the mixed split (above) — 4 instead of 6 pair MMAs per k-block
 // W64: K-major operands arrive as one SWIZZLE_64B box [16 k][128 rows] per
 // k-block (half the TMA lines of two SW32 boxes)
@@ -1294,22 +1304,29 @@ __global__ void __launch_bounds__(THREADS, 1)
   asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
   const int ntiles = p.tiles_m * p.tiles_n;
   const int cl = blockIdx.x >> 1;
-  const int tile = cl % ntiles, split = cl / ntiles;
-  int tm, tn;
-  {
-    const int per_group = GROUP_M * p.tiles_n;
-    const int group = tile / per_group, first_m = group * GROUP_M;
-    const int gsize = min(p.tiles_m - first_m, GROUP_M);
-    const int in_group = tile % per_group;
-    tm = first_m + in_group % gsize;
-    tn = in_group / gsize;
+  // tail split: clusters [0, tail_tile0) run one whole tile each; the rest are
+  // the two K halves of the tail tiles (blocks are dispatched in index order,
+  // so the halves share the last wave)
+  int tile, split;
+  bool tail = false;
+  if (p.tail_tiles > 0) {
+    tail = cl >= p.tail_tile0;
+    const int t = cl - p.tail_tile0;
+    tile = tail ? p.tail_tile0 + t % p.tail_tiles : cl;
+    split = tail ? t / p.tail_tiles : 0;
+  } else {
+    tile = cl % ntiles;
+    split = cl / ntiles;
   }
+  int tm, tn;
+  wide_tile(p, tile, tm, tn);
   const int m0 = tm * 256 + 128 * (int)rank;  // this CTA's A' rows (accumulator rows)
   const int nb0 = tn * 256;                    // the pair's B' rows (accumulator columns)
   const int n0 = nb0 + 128 * (int)rank;        // this CTA's B' rows
   const bool a_live = m0 < p.M, b_live = n0 < p.N;
-  const int kbeg = split * p.k_chunk;
-  const int kend = min(p.K, kbeg + p.k_chunk);
+  const bool whole = p.tail_tiles > 0 && !tail;  // (a whole-K tile of a tail-split launch)
+  const int kbeg = whole ? 0 : split * p.k_chunk;
+  const int kend = whole ? p.K : min(p.K, kbeg + p.k_chunk);
   const int nkb = kend > kbeg ? (kend - kbeg) / BK : 0;  // K % 16 == 0 on the TMA path
   if (tid == 0) {
     asm volatile("prefetch.tensormap [%0];" ::"l"(&tp.map[0]) : "memory");
@@ -1407,6 +1424,14 @@ __global__ void __launch_bounds__(THREADS, 1)
             : "r"(taddr));
       }
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (tail) {
+        // compact partials [half][tail tile][256 n][256 m] (m fastest)
+        float* wcol = p.ws + ((int64_t)(split * p.tail_tiles + (tile - p.tail_tile0)) << 16) + 128 * (int)rank +
+                      lane_row;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) wcol[(cbeg + i) << 8] = __uint_as_float(r_or_zero(rr[i], nkb));
+        continue;
+      }
       if (p.splits > 1) {
         // partials [split][N][M] (m fastest: a warp's 32 rows are 32 consecutive floats)
         if (!mok) continue;
@@ -1497,6 +1522,30 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (warp == MMA_WARP)
     asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(TMEM_COLS));
 }
+// C += half 0 + half 1 of the tail tiles' compact partials: block (tail tile,
+// 32 m x 8 n sub-block), partials read m-fastest, staged through shared
+// memory, C read and written n-fastest (as gett_splitk_reduce_t_kernel); sums
+// from -0.0 in half order.
+__global__ void __launch_bounds__(256) wide_tail_reduce_kernel(const __grid_constant__ TiledParams<float> p) {
+  __shared__ float tl[8][33];
+  const int t = threadIdx.x;
+  const int ti = blockIdx.x >> 8, sub = blockIdx.x & 255;
+  int tm, tn;
+  wide_tile(p, p.tail_tile0 + ti, tm, tn);
+  const int ml0 = (sub & 7) * 32, nl0 = (sub >> 3) * 8;  // within the 256 x 256 tile
+  const int mw = tm * 256 + ml0 + t / 8, nw = tn * 256 + nl0 + t % 8;
+  const bool okw = mw < p.M && nw < p.N;
+  float* c = okw ? p.C + p.gm.off(1, mw) + p.gn.off(1, nw) : nullptr;
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const float c0 = okw ? *c : 0.f;
+  const int mr = ml0 + t % 32, nr = nl0 + t / 32;
+  const float* w = p.ws + ((int64_t)ti << 16) + (nr << 8) + mr;
+  const float v0 = __ldcg(w), v1 = __ldcg(w + ((int64_t)p.tail_tiles << 16));
+  tl[t / 32][t % 32] = (-0.0f + v0) + v1;
+  __syncthreads();
+  if (okw) *c = epi(c0, tl[t % 8][t / 8], p.neg);
+}
 }  // namespace wide
 
 template <bool AKF, bool BKF, bool MIX, bool W64>
@@ -1506,7 +1555,8 @@ cudaError_t launch_wide_t(const TiledParams<float>& p, const TmaParams& tp, cuda
   cudaError_t e = ensure_dyn_smem(k, wide::SMEMW_BYTES, configured);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)(2 * p.tiles_m * p.tiles_n * p.splits));
+  cfg.gridDim = p.tail_tiles > 0 ? dim3((unsigned)(2 * (p.tail_tile0 + 2 * p.tail_tiles)))
+                                 : dim3((unsigned)(2 * p.tiles_m * p.tiles_n * p.splits));
   cfg.blockDim = dim3(THREADS);
   cfg.dynamicSmemBytes = wide::SMEMW_BYTES;
   cfg.stream = s;
@@ -1553,7 +1603,20 @@ cudaError_t launch_sgett_tc_wide(const TiledParams<float>& p, const TmaParams& t
   cudaError_t e;
   if (mix) e = k16 ? launch_wide_m<true, true>(p, tp, a_kf, b_kf, s) : launch_wide_m<true, false>(p, tp, a_kf, b_kf, s);
   else e = k16 ? launch_wide_m<false, true>(p, tp, a_kf, b_kf, s) : launch_wide_m<false, false>(p, tp, a_kf, b_kf, s);
-  if (e != cudaSuccess || p.splits == 1) return e;
+  if (e != cudaSuccess) return e;
+  if (p.tail_tiles > 0) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)p.tail_tiles * 256u);
+    cfg.blockDim = dim3(256);
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = g_launch_pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, tc::wide::wide_tail_reduce_kernel, p);
+  }
+  if (p.splits == 1) return e;
   return launch_splitk_reduce<float>(p, s);
 }
 

@@ -20,10 +20,10 @@ def kernel_mode():
                                        set_pipeline, set_split_k, set_stream_k, set_tma, set_wide)
 
     def use(name, split=0, pipeline=-1, stream_k=True, tma=True, pair=False, complex_embed=True,
-            kr="auto", kr_fused=False, kr_pair=True, bulk=True, wide="auto", kr_mixed=True, wide_mixed=False):
+            kr="auto", kr_fused=False, kr_pair=True, bulk=True, wide="auto", kr_mixed=True, wide_mixed=False, wide_tail=True):
         set_kernel(name)
         set_bulk(bulk)
-        set_wide(wide, wide_mixed)
+        set_wide(wide, wide_mixed, wide_tail)
         set_split_k(split)
         set_pipeline(pipeline)
         set_stream_k(stream_k)

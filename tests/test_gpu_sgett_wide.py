@@ -34,10 +34,10 @@ def _operands(M, N, K, bkf, seed, pad_c=0):
     return args, a.view(M, K).double(), bm
 
 
-def _run(args, c0, mode, split, kernel_mode, mixed=False):
+def _run(args, c0, mode, split, kernel_mode, mixed=False, tail=True):
     from paper_2410_06770_b200.device import sgett_device
 
-    kernel_mode("tiled", wide=mode, split=split, wide_mixed=mixed)
+    kernel_mode("tiled", wide=mode, split=split, wide_mixed=mixed, wide_tail=tail)
     c = c0.clone()
     args = args[:13] + (c,)
     assert sgett_device(*args) == []
@@ -164,3 +164,38 @@ def test_wide_mixed_split(shape, bkf, split, kernel_mode):
     iargs = args[:3] + (ai,) + args[4:7] + (bi,) + args[8:13] + (ci,)
     outs = [_run(iargs, ci, "force", split, kernel_mode, mixed=m)[0] for m in (True, False)]
     assert torch_equal(outs[0], outs[1])
+
+
+@pytest.mark.parametrize("shape", [(2560, 2048, 1024), (2500, 2100, 1040), (4096, 4096, 1024)],
+                         ids=lambda s: "x".join(map(str, s)))
+@pytest.mark.parametrize("bkf", [False, True])
+@pytest.mark.parametrize("mixed", [False, True])
+def test_wide_tail_split(shape, bkf, mixed, kernel_mode):
+    """More pair tiles than pair slots (74 on 148 SMs) with a partial last wave
+    of at most half the slots (80 -> 6, 90 -> 16, 256 -> 34 tiles): those tiles
+    run as two K halves whose compact partials a small reduce adds to C.
+    Within the bar of an fp64 product; every tile the whole-K CTAs wrote is
+    bitwise what the launch without a tail split writes; padding untouched."""
+    import torch
+
+    M, N, K = shape
+    args, am, bm = _operands(M, N, K, bkf, sum(shape), pad_c=3)
+    c0 = args[13].clone()
+    ldc = N + 3
+    c, kname = _run(args, c0, "force", 0, kernel_mode, mixed=mixed)
+    assert kname.endswith("_wide_tail"), kname
+    plain, kplain = _run(args, c0, "force", 0, kernel_mode, mixed=mixed, tail=False)
+    assert kplain.endswith("_wide"), kplain
+    want = c0[:M * ldc].view(M, ldc).double()
+    want[:, :N] += am @ bm.t()
+    got = c[:M * ldc].view(M, ldc)
+    assert ((got.double() - want).abs().max() / K).item() <= 1e-5
+    assert torch_equal(got[:, N:], c0[:M * ldc].view(M, ldc)[:, N:])
+    assert torch_equal(c[M * ldc:], c0[M * ldc:])
+    same = (got == plain[:M * ldc].view(M, ldc))[:, :N]
+    tiles_m, tiles_n = -(-M // 256), -(-N // 256)
+    rem = (tiles_m * tiles_n) % 74
+    pad = torch.zeros(tiles_m * 256, tiles_n * 256, dtype=torch.bool, device=same.device)
+    pad[:M, :N] = ~same
+    differing = pad.view(tiles_m, 256, tiles_n, 256).any(dim=3).any(dim=1).sum().item()
+    assert differing <= rem, (differing, rem)
