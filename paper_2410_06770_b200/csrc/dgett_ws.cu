@@ -188,6 +188,7 @@ enum SegKind : int {
 };
 struct Seg {
   int tile, split, kbase, kend, kb0, kb1, kind;
+  int rev;  // the producer walks the k-blocks downwards (serpentine k, see seg_next)
 };
 
 // Per-CTA work list, identical in the producer and consumer roles.
@@ -226,6 +227,7 @@ __device__ __forceinline__ void seg_init(const TiledParams<double>& p, const SkP
 __device__ __forceinline__ bool seg_next(const TiledParams<double>& p, const SkParams& sk,
                                          SegIter& it, Seg& sg) {
   if (it.done) return false;
+  sg.rev = 0;
   if (!sk.enabled) {
     const int ntiles = p.tiles_m * p.tiles_n;
     sg.tile = blockIdx.x % ntiles;
@@ -255,6 +257,11 @@ __device__ __forceinline__ bool seg_next(const TiledParams<double>& p, const SkP
     sg.kb0 = 0;
     sg.kb1 = sk.nkb;
     sg.kind = SEG_FULL;
+    // serpentine k (l2hint bit 4): every other data-parallel tile of a CTA is
+    // summed from its last k-block down, so a wave starts on the k slices the
+    // previous wave (same tile rows, next columns) touched last — the part of
+    // the shared row panels still in L2
+    sg.rev = (sk.l2hint & 16) ? ((it.dp / (int)gridDim.x) & 1) : 0;
     it.dp += gridDim.x;
     return true;
   }
@@ -388,7 +395,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(fb),
                      "r"((AKF ? T_KF_BYTES : T_RF_BYTES) + (BKF ? T_KF_BYTES : T_RF_BYTES))
                      : "memory");
-        const int k0 = sg.kbase + kb * BK;
+        const int k0 = sg.kbase + (sg.rev ? sg.kb0 + sg.kb1 - 1 - kb : kb) * BK;
         int32_t c[5];
         dtma_coords(tp.op[0], m0, k0, c);
         if (hint_a) dtma_load_hint(ring + s * STAGE_ELEMS * 8, &tp.map[0], c, fb, hint_a == 1 ? pol_last : pol_first);
@@ -432,7 +439,7 @@ __global__ void __launch_bounds__(THREADS, 1)
         if (u > 0) mbar_wait(smem_u32(empty + s), (u - 1) & 1);
         double* sa = smem + s * SSTAGE;
         double* sb = sa + SOPER;
-        const int k0 = sg.kbase + kb * BK;
+        const int k0 = sg.kbase + (sg.rev ? sg.kb0 + sg.kb1 - 1 - kb : kb) * BK;
         produce<AKF, AVEC, true>(sa, p.A, rowoff_a, mvalid, p.gk, 0, k0, sg.kend, pw, lane);
         produce<BKF, BVEC, false>(sb, p.B, rowoff_b, nvalid, p.gk, 1, k0, sg.kend, pw, lane);
         mbar_arrive_cpasync(smem_u32(full + s));  // fires when this lane's copies land
