@@ -49,7 +49,7 @@ bool g_dgett_bulk = true; // DGETT: C += acc as bulk shared->global adds of 32-w
 int g_wide = 1;           // SGETT wide CTA-pair kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_WIDE)
 bool g_wide_tail = true;  // wide kernel: a partial last wave (<= half the pair slots) runs as two K halves per tile (GETT_WIDE_TAIL=0: off)
 bool g_wide_k16 = true;   // wide kernel: K-major operands as one 16-k SWIZZLE_64B box per k-block (GETT_WIDE_K16=0: two SW32 boxes)
-int g_l2hint = 0;          // DGETT TMA producer / bulk epilogue L2 policies (SkParams::l2hint; GETT_WS_L2HINT)
+int g_l2hint = 16;         // DGETT schedule / L2 policies (SkParams::l2hint; GETT_WS_L2HINT): 16 = serpentine k (c2 DRAM reads -8 %)
 bool g_wide_mix = false;  // wide kernel: mixed split, one tf32 + one bf16 MMA per 8 k (GETT_WIDE_MIX=1; 4096^3 229 vs 236 TF:
                           // the kernel is bound by the TMA line rate of its 32-byte K-major boxes, not by the MMAs)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)

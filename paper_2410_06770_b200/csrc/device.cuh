@@ -114,7 +114,8 @@ struct SkParams {
   int32_t epoch = 0;
   // L2 cache-policy hints (TMA producer, bulk-add epilogue): bit 0 A' boxes
   // evict_last, bit 1 B' boxes evict_first, bit 2 the C bulk adds evict_first,
-  // bit 3 exchanges the A' / B' policies
+  // bit 3 exchanges the A' / B' policies; bit 4 (the default): serpentine k —
+  // every other data-parallel tile of a CTA is summed from its last k-block down
   int32_t l2hint = 0;
 };
 
