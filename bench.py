@@ -408,6 +408,14 @@ def run_ours(args):
         import torch.distributed as dist
 
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # host-side barriers for the sections where one rank drives every GPU:
+        # an NCCL barrier would leave a spinning kernel on the waiting ranks'
+        # GPUs, time-slicing against rank 0's work there
+        try:
+            cpu_group = dist.new_group(backend="gloo")
+        except Exception as exc:  # noqa: BLE001  (no gloo transport: fall back to NCCL barriers)
+            print(f"bench.py: gloo side group unavailable ({exc}); NCCL barriers", file=sys.stderr)
+            cpu_group = None
     w, rows = shard(world, rank)
     a, b, c = C2.buffers()
     dev = torch.device("cuda", local)
@@ -475,7 +483,8 @@ def run_ours(args):
         # (gett_dgett_multi: slabs per GPU, B exchanged over NVLink); rank 0
         # calls, the other ranks wait
         e2e_ranks = e2e_s
-        dist.barrier()
+        torch.cuda.synchronize()
+        dist.barrier(group=cpu_group)
         if rank == 0:
             fa, fb, fc = (torch.from_numpy(x).pin_memory().numpy() for x in (a, b, c))
             fpos, fkw = C2.args(fa, fb, fc)
@@ -488,7 +497,7 @@ def run_ours(args):
             e2e_s = (time.perf_counter() - t0) / e2e_steps
             multi_sched = g.last_multi()
             del fa, fb, fc
-        dist.barrier()
+        dist.barrier(group=cpu_group)
     total_flops = C2.flops  # all ranks together process the whole c2 per step
     value = total_flops * args.steps / (ms * 1e-3) / 1e9
     e2e_value = total_flops / e2e_s / 1e9
