@@ -15,7 +15,7 @@ for cfg in c2 c3 c4; do
 done
 timeout 600 ncu --set full --clock-control none --import-source on -k regex:"sgett_kr|reduce_t" --launch-skip 6 \
   --launch-count 2 -o gpurun_out/prof/full_c5 python tools/run_one.py c5 4 > gpurun_out/prof/full_c5.log 2>&1
-timeout 600 ncu --set full --clock-control none --import-source on -k regex:wide --launch-skip 3 \
+timeout 600 ncu --set full --clock-control none --import-source on -k regex:sgett_tc_wide_kernel --launch-skip 3 \
   --launch-count 1 -o gpurun_out/prof/full_sgemm4096 python tools/run_sgemm.py 4096 4 > gpurun_out/prof/full_sgemm4096.log 2>&1
 timeout 300 python tools/tune.py c1 c2 c3 c4 c5 sgemm2048 sgemm4096 > gpurun_out/prof/tune.jsonl 2>&1
 timeout 300 python tools/debug/c5_modes.py > gpurun_out/prof/c5_modes.txt 2>&1
