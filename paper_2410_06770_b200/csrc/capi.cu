@@ -58,6 +58,8 @@ bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the t
 }  // namespace
 int g_launch_pdl = 1;     // programmatic dependent launches of the k-run SGETT kernel and the split-K reduce (GETT_PDL)
 namespace {
+int g_kr_slots = 2;       // k-run kernel: operand / TMEM ring depth wanted (GETT_KR_SLOTS)
+int g_kr_krn = 2;         // k-run kernel: most k runs per k-block for CTA pairs (GETT_KR_KRN)
 bool g_kr_mix = true;     // k-run kernel: mixed split, one tf32 + one bf16 MMA per 8 k (GETT_KR_MIX=0: three tf32 MMAs)
 bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
                           // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
@@ -102,6 +104,10 @@ void read_env_once() {
   if (krp) g_kr_pair = std::atoi(krp) != 0;
   const char* pdl = std::getenv("GETT_PDL");
   if (pdl) g_launch_pdl = std::atoi(pdl) != 0;
+  const char* krs = std::getenv("GETT_KR_SLOTS");
+  if (krs) g_kr_slots = std::max(2, std::min(8, std::atoi(krs)));
+  const char* krk = std::getenv("GETT_KR_KRN");
+  if (krk) g_kr_krn = std::atoi(krk);
   const char* krm = std::getenv("GETT_KR_MIX");
   if (krm) g_kr_mix = std::atoi(krm) != 0;
   const char* krf = std::getenv("GETT_KR_FUSED");
@@ -869,18 +875,25 @@ bool kr_decide(DevPlan& dp) {
       q.lslot_bytes = (int32_t)(xbytes + ybytes);
       q.oslot_bytes = (int32_t)(2 * up(KE * yr * 4, 1024));
       q.a_col0 = (int32_t)up(NT, 32);
-      q.aslots = 2;
-      if (q.a_col0 + 2 * 2 * KE > 512) return false;
       auto fits = [&](int l, int o) {
         return (int64_t)l * q.lslot_bytes + (int64_t)o * q.oslot_bytes + 512 <= 227 * 1024;
       };
+      // operand / TMEM ring depth: as deep as TMEM, shared memory and the load
+      // ring allow (at most g_kr_slots): the split of k-block kb starts when the
+      // MMAs of k-block kb - depth have finished, so a deeper ring keeps the
+      // tensor pipe fed across the split warps' turnaround; load slots >= depth
+      // x KRN keep the full-barrier parity waits unambiguous (sgett_kr.cu)
+      int so = g_kr_slots;
+      while (so > 2 && (q.a_col0 + so * 2 * KE > 512 || !fits(so * krn, so))) --so;
+      if (q.a_col0 + so * 2 * KE > 512) return false;
       int sl = 8;
-      while (sl > 2 * krn && !fits(sl, 2)) --sl;
-      if (!fits(sl, 2)) return false;
+      while (sl > so * krn && !fits(sl, so)) --sl;
+      if (!fits(sl, so)) return false;
       q.lslots = sl;
-      q.oslots = 2;
+      q.oslots = so;
+      q.aslots = so;
       q.o_off = sl * q.lslot_bytes;
-      q.bar_off = (int32_t)(q.o_off + 2LL * q.oslot_bytes);
+      q.bar_off = (int32_t)(q.o_off + (int64_t)so * q.oslot_bytes);
       q.nkb = (int32_t)(p.gk.G / KE);
       c.kp = q;
       c.lx = dp.kr_l[0];
@@ -893,7 +906,7 @@ bool kr_decide(DevPlan& dp) {
       return true;
     };
     if (!make(dp.krc[0], 1, false)) continue;
-    if (!make(dp.krc[1], 2, true)) make(dp.krc[1], 1, true);
+    if (g_kr_krn < 2 || !make(dp.krc[1], 2, true)) make(dp.krc[1], 1, true);
     return true;
   }
   return false;
@@ -931,8 +944,8 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
         for (int ci = 0; ci < 2; ++ci) {
           const DevPlan::KrCfg& c = dp.krc[ci];
           if (!c.valid) continue;
-          std::fprintf(stderr, "  cfg %d: pair %d runs/k-block %d nkb %d slots load %d operand 2 smem %d\n", ci,
-                       (int)c.pair, c.krn, c.kp.nkb, c.kp.lslots, c.kp.bar_off + 512);
+          std::fprintf(stderr, "  cfg %d: pair %d runs/k-block %d nkb %d slots load %d operand %d smem %d\n", ci,
+                       (int)c.pair, c.krn, c.kp.nkb, c.kp.lslots, c.kp.oslots, c.kp.bar_off + 512);
           for (int t = 0; t < 2; ++t) {
             const DevPlan::KrLayout& L = t ? c.ly : c.lx;
             std::fprintf(stderr, "    %c base_off %lld dims", t ? 'Y' : 'X', (long long)L.base_off);
@@ -1010,7 +1023,11 @@ int try_sgett_kr(DevPlan& dp, const float* A, const float* B, float* C, int neg,
   const bool mix = g_kr_mix;
   CK(launch_sgett_kr(kp, dp.kr_run, cfg.krn, pair, mix, stream));
   ++g_launches;
+#ifdef GETT_KR_NO_REDUCE  // tuning builds only: time the main kernel alone (wrong results)
+  if (false) {
+#else
   if (splits > 1 && kp.cnt == nullptr) {
+#endif
     TiledParams<float> tp{};
     tp.C = C;
     tp.gm = kp.gx;

@@ -689,9 +689,11 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_kernel(const __grid_co
   // C's element (offset tables, then its value) does not depend on the
   // partials: fetched first, so its two round trips overlap the partials'
   T* c = p.C + p.gm.off(1, m) + p.gn.off(1, n);
+  // (safe before the wait: the split-K kernel triggers this grid only after its
+  // own wait for whatever preceded it, and it never writes C)
+  const T c0 = *c;
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const T c0 = *c;
   // the slices' partials in a fixed order; loads batched 8 at a time so their
   // latencies overlap
   T s = T(-0.0);
@@ -721,11 +723,14 @@ __global__ void __launch_bounds__(256) gett_splitk_reduce_t_kernel(const __grid_
   const int mw = m0 + t / 8, nw = n0 + t % 8;
   const bool okw = mw < p.M && nw < p.N;
   T* c = okw ? p.C + p.gm.off(1, mw) + p.gn.off(1, nw) : nullptr;
-  // (a programmatic dependent of this grid may be scheduled right away: it
-  // waits for this grid's completion itself)
+  // C does not depend on the partials: fetched before the wait, so its round
+  // trip overlaps the split-K kernel's tail (that kernel never writes C, and it
+  // triggers this grid only after its own wait for whatever preceded it).  A
+  // programmatic dependent of this grid may be scheduled right away: it waits
+  // for this grid's completion itself.
+  const T c0 = okw ? *c : T(0);
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const T c0 = okw ? *c : T(0);
   const int mr = m0 + t % 32, nr = n0 + t / 32;
   if (mr < p.M && nr < p.N) {
     const int64_t idx = (int64_t)nr * p.M + mr;

@@ -784,14 +784,18 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
 #ifdef GETT_KR_TRACE
         long long c0 = clock64();
 #endif
+#ifndef GETT_KR_NOWAIT  // (tuning builds only: wrong results)
         if (PAIR) mbar_wait_cluster(smem_u32(ready + so), (kb / SO) & 1);
         else mbar_wait(smem_u32(ready + so), (kb / SO) & 1);
+#endif
 #ifdef GETT_KR_TRACE
         w_ready += clock64() - c0;
         c0 = clock64();
         if (kb == 0) g_first = globaltimer();
 #endif
+#ifndef GETT_KR_NOFENCE  // (tuning builds only)
         asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+#endif
         const uint32_t hb = sbase + p.o_off + so * p.oslot_bytes;
         const uint32_t lb = hb + p.oslot_bytes / 2;
         const uint32_t ah0 = tmem + p.a_col0 + sa * 2 * KE;
@@ -820,6 +824,16 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
             mma_tf32(tmem, al, bh, idesc, 1);
           }
         }
+#ifdef GETT_KR_PLAIN_ARRIVE  // (tuning builds only: free the slots without tracking the MMAs)
+        if (PAIR) {
+          asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(ofree + so)) : "memory");
+          uint32_t rem;
+          asm volatile("mapa.shared::cluster.u32 %0, %1, 1;" : "=r"(rem) : "r"(smem_u32(ofree + so)));
+          asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(rem) : "memory");
+        } else {
+          mbar_arrive(smem_u32(ofree + so));
+        }
+#else
         if (PAIR) {
           commit_pair(smem_u32(ofree + so));
           if (TA != SO) commit_pair(smem_u32(afree + sa));
@@ -827,6 +841,7 @@ __global__ void __launch_bounds__(THREADS, 1) sgett_kr_kernel(const __grid_const
           commit(smem_u32(ofree + so));
           if (TA != SO) commit(smem_u32(afree + sa));
         }
+#endif
 #ifdef GETT_KR_TRACE
         t_issue += clock64() - c0;
 #endif

@@ -1536,9 +1536,9 @@ __global__ void __launch_bounds__(256) wide_tail_reduce_kernel(const __grid_cons
   const int mw = tm * 256 + ml0 + t / 8, nw = tn * 256 + nl0 + t % 8;
   const bool okw = mw < p.M && nw < p.N;
   float* c = okw ? p.C + p.gm.off(1, mw) + p.gn.off(1, nw) : nullptr;
+  const float c0 = okw ? *c : 0.f;  // (before the wait: the wide kernel never writes these tiles' C)
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  const float c0 = okw ? *c : 0.f;
   const int mr = ml0 + t % 32, nr = nl0 + t / 32;
   const float* w = p.ws + ((int64_t)ti << 16) + (nr << 8) + mr;
   const float v0 = __ldcg(w), v1 = __ldcg(w + ((int64_t)p.tail_tiles << 16));

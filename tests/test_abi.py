@@ -132,6 +132,30 @@ def test_multi_device_setters():
     assert g.last_multi() == "none"
 
 
+def test_kernel_switch_setters():
+    """The tuning switches validate their argument and leave the defaults
+    restorable (no CUDA call involved)."""
+    from paper_2410_06770_b200 import _native
+
+    L = _native.LIB
+    for bad in (-1, 3, 7, 32):            # (mode & 3) == 3 or out of range
+        assert L.gett_set_kr(bad) == _native.E_INVALID_ARG
+    for bad in (-1, 3, 16):
+        assert L.gett_set_wide(bad) == _native.E_INVALID_ARG
+    for bad in (-1, 2):
+        assert L.gett_set_pdl(bad) == _native.E_INVALID_ARG
+        assert L.gett_set_bulk(bad) == _native.E_INVALID_ARG
+    for mixed in (False, True):
+        g.set_kr("force", fused=True, pair=False, mixed=mixed)
+        g.set_wide("force", mixed=mixed, tail=not mixed)
+    g.set_pdl(False)
+    g.set_pdl(True)
+    g.set_kr("auto")
+    g.set_wide("auto")
+    with pytest.raises(ValueError):
+        g.set_wide("sometimes")
+
+
 def test_derive_output_extents():
     a, b = g.TensorView.contiguous((2, 3)), g.TensorView.contiguous((3, 4))
     assert g.derive_output_extents(a, b, g.ContractionSpec(1, (1,), (0,), (1, 0))) == (4, 2)

@@ -227,3 +227,32 @@ def test_kr_mixed_split_at_least_as_accurate_as_3xtf32(kernel_mode):
         assert g.sgett(*pos[:13], c, **kw) == []
         outs.append(c)
     assert outs[0].tobytes() == outs[1].tobytes()
+
+
+def test_kr_pdl_on_off_bitwise(kernel_mode):
+    """Programmatic dependent launch only changes when the k-run kernel and the
+    reduce are scheduled: back-to-back calls on one stream (each a dependent of
+    the previous call's reduce, whose workspace it reuses) give the same bits as
+    ordinary launches, for the separate and the fused reduce."""
+    import torch
+
+    from paper_2410_06770_b200.device import sgett_device
+
+    w = C5.slice_free("A", 0, 0, 24)
+    a, b, c = w.buffers()
+    ta, tb = torch.from_numpy(a).cuda(), torch.from_numpy(b).cuda()
+    for fused in (False, True):
+        outs = []
+        for pdl in (True, False):
+            g.set_pdl(pdl)
+            try:
+                kernel_mode("tiled", kr="force", kr_fused=fused)
+                tc = torch.from_numpy(c).cuda()
+                pos, kw = w.args(ta, tb, tc)
+                for _ in range(5):  # C accumulates: 5 dependent calls
+                    assert sgett_device(*pos, **kw) == []
+                torch.cuda.synchronize()
+                outs.append(tc.cpu().numpy())
+            finally:
+                g.set_pdl(True)
+        assert outs[0].tobytes() == outs[1].tobytes(), fused
