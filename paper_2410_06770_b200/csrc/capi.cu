@@ -54,7 +54,7 @@ bool g_wide_mix = false;  // wide kernel: mixed split, one tf32 + one bf16 MMA p
                           // the kernel is bound by the TMA line rate of its 32-byte K-major boxes, not by the MMAs)
 int g_kr = 1;             // SGETT k-run kernel: 0 off, 1 automatic, 2 whenever it applies (GETT_KR)
 bool g_kr_pair = true;    // k-run kernel as CTA pairs (cta_group::2) when the tiling allows, two k runs per
-                          // k-block when they fit (c5: 46.1 vs 48.1 us; GETT_KR_PAIR=0: one CTA per tile)
+                          // k-block when they fit (c5 back to back 34.6 vs 40.2 us; GETT_KR_PAIR=0: one CTA per tile)
 }  // namespace
 int g_launch_pdl = 1;     // programmatic dependent launches of the k-run SGETT kernel and the split-K reduce (GETT_PDL)
 namespace {
@@ -62,7 +62,7 @@ int g_kr_slots = 2;       // k-run kernel: operand / TMEM ring depth wanted (GET
 int g_kr_krn = 2;         // k-run kernel: most k runs per k-block for CTA pairs (GETT_KR_KRN)
 bool g_kr_mix = true;     // k-run kernel: mixed split, one tf32 + one bf16 MMA per 8 k (GETT_KR_MIX=0: three tf32 MMAs)
 bool g_kr_fused = false;  // k-run split-K: reduce inside the kernel (GETT_KR_FUSED=1); default the
-                          // separate reduce kernel (c5: 48.1 vs 49.2 us fused, tools/kr_check.py)
+                          // separate reduce kernel (c5 from a CUDA graph: 33.2 vs 37.8 us fused)
 int g_pipeline_slabs = -1;  // -1: automatic; 0/1: off; n: n slabs (GETT_PIPELINE)
 int g_multi_stage = 0;      // multi-device split-K: 1 = stage partials by cudaMemcpyPeer instead of peer loads (GETT_MULTI_STAGE)
 std::vector<int> g_devices;  // default device list of the host entry points (gett_set_devices; empty = current device)

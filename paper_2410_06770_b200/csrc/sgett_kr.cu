@@ -15,8 +15,13 @@
 //   * Y (N = NT <= 128 columns, a multiple of 16; c5: 96, no padding): rows-
 //     major boxes [KR k][NT rows], transposed by the split warps into K-major
 //     no-swizzle core matrices (hi in place, lo in a small ring).
-//   * MMA warp: per 8-k step, tcgen05.mma.kind::tf32 hi*hi, lo*hi, hi*lo,
-//     A from TMEM, B from shared memory, M = 128, N = NT.
+//   * MMA warp: per 8-k step either the three tf32 MMAs of the 3xTF32 split
+//     (hi*hi, hi*lo, lo*hi) or — MIX, the default — one tf32 MMA hi*hi plus one
+//     bf16 MMA (K = 16) carrying both cross terms; A from TMEM, B from shared
+//     memory, M = 128 (256 for a CTA pair, cta_group::2), N = NT.
+//   * Launched as a programmatic dependent (PDL) when g_launch_pdl: the
+//     prologue overlaps the predecessor's tail, griddepcontrol.wait precedes
+//     the first global access.
 //   * Split-K (few output tiles, long K): partials [splits][NY][MX] (x
 //     fastest), then the CTAs of a tile reduce them themselves: each
 //     publishes its partial and counts in with one atomicInc on the tile's
